@@ -1,0 +1,221 @@
+"""CPU oracle for the AMGF-PCG path -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+`--impl reference` legs may import this package.  The product path
+(paper_2505_18576_b200) never imports, links or executes anything here, and
+this package never imports the product path.  See oracle/amgf_oracle.c for the
+paper citations of each function and DESIGN.md "Contract" for the arithmetic.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "amgf_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-std=c11"]
+
+
+def build(force: bool = False) -> str:
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", *CFLAGS, "-o", _LIB, _SRC, "-lm"])
+    return _LIB
+
+
+class OrcConfig(ctypes.Structure):
+    _fields_ = [("pre_sweeps", ctypes.c_int), ("post_sweeps", ctypes.c_int),
+                ("coarsest_size", ctypes.c_int), ("max_levels", ctypes.c_int),
+                ("power_iters", ctypes.c_int), ("factor_filter", ctypes.c_int),
+                ("agg_seed", ctypes.c_uint64)]
+
+
+DEFAULTS = dict(pre_sweeps=1, post_sweeps=1, coarsest_size=64, max_levels=25,
+                power_iters=10, factor_filter=1, agg_seed=0x5EED)
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = ctypes.CDLL(build())
+        P = ctypes.c_void_p
+        L.orc_create.restype = P
+        L.orc_create.argtypes = [ctypes.c_int, P, P, P, ctypes.c_int, P, P, P, P, P, ctypes.c_int, P,
+                                 ctypes.POINTER(OrcConfig), ctypes.POINTER(ctypes.c_int)]
+        L.orc_free.argtypes = [P]
+        L.orc_last_error.restype = ctypes.c_char_p
+        L.orc_dot.restype = ctypes.c_double
+        L.orc_dot.argtypes = [ctypes.c_long, ctypes.c_int, P, P]
+        L.orc_cholesky_dense.argtypes = [ctypes.c_int, P, P]
+        L.orc_trsv_dense.argtypes = [ctypes.c_int, P, P, P]
+        L.orc_priority.restype = ctypes.c_uint64
+        L.orc_priority.argtypes = [ctypes.c_int, ctypes.c_uint64]
+        L.orc_vcycle.argtypes = [P, P, P]
+        L.orc_apply.argtypes = [P, P, P]
+        L.orc_spmv.argtypes = [P, ctypes.c_int, P, P]
+        L.orc_filter_solve.argtypes = [P, P, P]
+        L.orc_pcg.argtypes = [P, P, P, ctypes.c_double, ctypes.c_int, ctypes.c_int,
+                              ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double), P]
+        L.orc_info.argtypes = [P, P]
+        L.orc_bsr_spmv.argtypes = [ctypes.c_int] * 4 + [P] * 5
+        L.orc_get.argtypes = [P, ctypes.c_int, ctypes.c_int, P]
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return a.ctypes.data_as(ctypes.c_void_p) if a is not None else None
+
+
+def _c(a, dt):
+    return np.ascontiguousarray(a, dtype=dt)
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"oracle status {code}: {msg}")
+        self.code = code
+
+
+def dot(u, v, b=3) -> float:
+    u = _c(u, np.float64); v = _c(v, np.float64)
+    return lib().orc_dot(u.size, b, _p(u), _p(v))
+
+
+def cholesky(A):
+    A = _c(A, np.float64); n = A.shape[0]
+    L = np.zeros_like(A)
+    st = lib().orc_cholesky_dense(n, _p(A), _p(L))
+    if st:
+        raise OracleError(st, lib().orc_last_error().decode())
+    return L
+
+
+def chol_solve(L, v):
+    L = _c(L, np.float64); v = _c(v, np.float64)
+    x = np.zeros_like(v)
+    lib().orc_trsv_dense(L.shape[0], _p(L), _p(v), _p(x))
+    return x
+
+
+def bsr_spmv(ptr, col, val, x, br, bc):
+    ptr = _c(ptr, np.int32); col = _c(col, np.int32); val = _c(val, np.float64); x = _c(x, np.float64)
+    nbr = len(ptr) - 1
+    y = np.zeros(nbr * br)
+    lib().orc_bsr_spmv(nbr, len(x) // bc, br, bc, _p(ptr), _p(col), _p(val), _p(x), _p(y))
+    return y
+
+
+def priority(v: int, seed: int) -> int:
+    return lib().orc_priority(v, seed)
+
+
+class Oracle:
+    """Oracle AMGF hierarchy for one system S = K + J^T D J."""
+
+    def __init__(self, nodes, K_ptr, K_col, K_val, J_ptr, J_col, J_val, D, Z, B_nns, **cfg):
+        c = dict(DEFAULTS); c.update(cfg)
+        self.cfg = c
+        self._keep = [_c(K_ptr, np.int32), _c(K_col, np.int32), _c(K_val, np.float64),
+                      _c(J_ptr, np.int32), _c(J_col, np.int32), _c(J_val, np.float64),
+                      _c(D, np.float64), None if Z is None else _c(Z, np.int32),
+                      _c(B_nns, np.float64)]
+        k = self._keep
+        m = len(k[3]) - 1
+        conf = OrcConfig(**c)
+        st = ctypes.c_int(0)
+        self.h = lib().orc_create(nodes, _p(k[0]), _p(k[1]), _p(k[2]), m, _p(k[3]), _p(k[4]), _p(k[5]),
+                                  _p(k[6]), _p(k[7]), 0 if Z is None else len(k[7]), _p(k[8]),
+                                  ctypes.byref(conf), ctypes.byref(st))
+        if not self.h:
+            raise OracleError(st.value, lib().orc_last_error().decode())
+        self.n = 3 * nodes
+        self._k = None
+        info = np.zeros(3 + 5 * 32, dtype=np.int64)
+        lib().orc_info(self.h, _p(info))
+        self.nlev, self.nc, self.nco = int(info[0]), int(info[1]), int(info[2])
+        self.levels = [dict(nodes=int(info[3 + 5 * l]), b=int(info[4 + 5 * l]), nnzb=int(info[5 + 5 * l]),
+                            nnzb_P=int(info[6 + 5 * l]), n_agg=int(info[7 + 5 * l])) for l in range(self.nlev)]
+
+    @classmethod
+    def from_problem(cls, p, D=None, Z="lattice", **cfg):
+        Zv = p.Z if isinstance(Z, str) and Z == "lattice" else Z
+        return cls(p.nodes, p.K_ptr, p.K_col, p.K_val, p.J_ptr, p.J_col, p.J_val,
+                   p.D if D is None else D, Zv, p.B_nns, **cfg)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().orc_free(self.h)
+            self.h = None
+
+    # --- getters ---
+    def get(self, which, level=0):
+        L = self.levels[level]
+        b, nodes = L["b"], L["nodes"]
+        shapes = {0: (nodes + 1, np.int32), 1: (L["nnzb"], np.int32), 2: ((L["nnzb"], b * b), np.float64),
+                  3: (nodes + 1, np.int32), 4: (L["nnzb_P"], np.int32), 5: ((L["nnzb_P"], b * 6), np.float64),
+                  6: (L["n_agg"] + 1, np.int32), 7: (L["nnzb_P"], np.int32), 8: ((L["nnzb_P"], 6 * b), np.float64),
+                  9: (nodes * b, np.float64), 10: (nodes, np.int32), 11: ((nodes * b, 6), np.float64),
+                  12: (2, np.float64), 13: ((nodes, b * 6), np.float64), 14: (nodes, np.int32), 15: (nodes, np.int32),
+                  20: (self.nc, np.int32), 21: ((self.nc, self.nc), np.float64), 22: ((self.nc, self.nc), np.float64),
+                  23: ((self.nco, self.nco), np.float64), 24: ((self.nco, self.nco), np.float64)}
+        shape, dt = shapes[which]
+        out = np.zeros(shape, dtype=dt)
+        if which == 13:
+            # Pt has one block per aggregated node
+            nz = int((self.get(10, level) >= 0).sum())
+            out = np.zeros((nz, b * 6), dtype=dt)
+        if lib().orc_get(self.h, which, level, _p(out)) != 0:
+            raise OracleError(-1, f"get {which} failed")
+        return out
+
+    def level_matrix(self, level=0, kind="A"):
+        """scipy BSR of a level operator (A, P or R)."""
+        import scipy.sparse as sp
+        L = self.levels[level]
+        b = L["b"]
+        if kind == "A":
+            ptr, col, val = self.get(0, level), self.get(1, level), self.get(2, level).reshape(-1, b, b)
+            return sp.bsr_matrix((val, col, ptr), shape=(L["nodes"] * b, L["nodes"] * b))
+        nc = L["n_agg"]
+        if kind == "P":
+            ptr, col, val = self.get(3, level), self.get(4, level), self.get(5, level).reshape(-1, b, 6)
+            return sp.bsr_matrix((val, col, ptr), shape=(L["nodes"] * b, nc * 6))
+        ptr, col, val = self.get(6, level), self.get(7, level), self.get(8, level).reshape(-1, 6, b)
+        return sp.bsr_matrix((val, col, ptr), shape=(nc * 6, L["nodes"] * b))
+
+    # --- operators ---
+    def spmv(self, x, level=0):
+        x = _c(x, np.float64); y = np.zeros_like(x)
+        lib().orc_spmv(self.h, level, _p(x), _p(y))
+        return y
+
+    def vcycle(self, b):
+        b = _c(b, np.float64); x = np.zeros_like(b)
+        lib().orc_vcycle(self.h, _p(b), _p(x))
+        return x
+
+    def apply(self, r):
+        r = _c(r, np.float64); z = np.zeros_like(r)
+        lib().orc_apply(self.h, _p(r), _p(z))
+        return z
+
+    def filter_solve(self, v):
+        v = _c(v, np.float64); y = np.zeros_like(v)
+        lib().orc_filter_solve(self.h, _p(v), _p(y))
+        return y
+
+    def pcg(self, b, rtol=1e-8, maxit=5000, precond="amgf"):
+        b = _c(b, np.float64); x = np.zeros_like(b)
+        it = ctypes.c_int(0); rr = ctypes.c_double(0)
+        hist = np.zeros(maxit + 1)
+        st = lib().orc_pcg(self.h, _p(b), _p(x), rtol, maxit, 0 if precond == "amgf" else 1,
+                           ctypes.byref(it), ctypes.byref(rr), _p(hist))
+        if st < 0:
+            raise OracleError(st, lib().orc_last_error().decode())
+        return x, dict(iterations=it.value, relres=rr.value, converged=(st == 0), history=hist[:it.value + 1])
