@@ -1,0 +1,375 @@
+#!/usr/bin/env python
+"""bench.py -- AMGF-PCG on B200 (arxiv 2505.18576), BASELINE.json metric on configs[3].
+
+Workload (N=1): cfg 3 = two-block elasticity, N=64 (1,647,750 dofs, 4,225 contact constraints),
+the 10-system interior-point-like D sequence (D log-uniform in [1, 10^(2+10s/9)], s = 0..9).
+A step = one system of the sequence: numeric re-setup for its D (amgf_update_D: S, A_w + Cholesky,
+Galerkin hierarchy) + AMGF-PCG solve to rtol 1e-8 (amgf_pcg_solve).  Symbolic setup (aggregation,
+patterns) is done once before timing (it does not depend on D, R5) and reported separately.
+
+value = device time per system (ms, CUDA events, barrier + synchronize on both sides, max over
+ranks, divided by the systems all ranks solved).  With --gpus N > 1 the ranks are replicas, each
+solving its own systems (the sequence's D values are pre-drawn, so systems are independent): "weak".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "AMGF-PCG solve ms, PCG iters, V-cycle HBM GB/s (frac of peak) @ 1.6M dofs"
+
+
+def peaks():
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(mp["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1])); mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def level_bytes(g):
+    """Algorithmic HBM bytes of one V-cycle: per level 2 passes of A, one of R and
+    one of P (values + int32 block columns), plus the vector traffic of the five kernels."""
+    tot = 0
+    for l, L in enumerate(g.levels):
+        b, n = L["b"], L["nodes"] * L["b"]
+        if l == g.nlev - 1:
+            tot += 2 * (g.nco * ((g.nco + 2) & ~1)) * 8 + 16 * n   # coarsest dense band pair
+            continue
+        A = L["nnzb"] * (8 * b * b + 4) + 4 * L["nodes"]
+        Pb = L["nnzb_P"] * (8 * 6 * b + 4)
+        nc6 = 6 * L["n_agg"]
+        vec = 24 * n + (24 * n) + (8 * n + 8 * nc6) + (8 * nc6 + 16 * n) + 32 * n
+        tot += 2 * A + 2 * Pb + vec
+    return tot
+
+
+def spmv_bytes(g):
+    L = g.levels[0]
+    return L["nnzb"] * 76 + 4 * L["nodes"] + 48 * L["nodes"]
+
+
+def run_amgf(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import amgf_gen
+    from paper_2505_18576_b200 import AMGF
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    p = amgf_gen.config(args.cfg)
+    nsys = p.D_seq.shape[0]
+    stream = torch.cuda.current_stream()
+    D_dev = [torch.from_numpy(p.D_seq[s].copy()).to(dev) for s in range(nsys)]
+    b_dev = torch.from_numpy(p.b).to(dev)
+    x_dev = torch.empty_like(b_dev)
+
+    t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    g = AMGF.from_problem(p, D=p.D_seq[rank % nsys], stream=stream)
+    t1.record(stream); t1.synchronize()
+    full_setup_ms = t0.elapsed_time(t1)
+
+    def step(k):
+        s = (rank + world * k) % nsys
+        g.update_D(D_dev[s])
+        _, rep = g.pcg(b_dev, rtol=p.rtol, max_it=5000, out=x_dev)
+        return s, rep
+
+    for k in range(args.warmup):
+        step(k)
+    # per-phase split (untimed probe, one system): numeric setup vs solve
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream); g.update_D(D_dev[0]); e1.record(stream); e1.synchronize()
+    upd_ms = e0.elapsed_time(e1)
+
+    launches0 = g.launches
+    clocks = Clocks(local_rank)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ev0 = torch.cuda.Event(enable_timing=True); ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    iters, solve_ms, systems = [], [], []
+    for k in range(args.steps):
+        s, rep = step(args.warmup + k)
+        iters.append(rep["iterations"]); solve_ms.append(rep["solve_ms"]); systems.append(s)
+        if not rep["converged"]:
+            raise RuntimeError(f"system {s} did not converge: {rep}")
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clk = clocks.stop()
+    elapsed = ev0.elapsed_time(ev1)
+    launches = g.launches - launches0
+    if world > 1:
+        t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        elapsed = float(t.item())
+
+    # ---- e2e: same metric through the public API with host buffers (pinned), copies inside the region
+    D_host = [torch.from_numpy(p.D_seq[s].copy()).pin_memory() for s in range(nsys)]
+    b_host = torch.from_numpy(p.b.copy()).pin_memory()
+    x_host = torch.empty(p.n, dtype=torch.float64).pin_memory()
+    D_stage = torch.empty(p.m, dtype=torch.float64, device=dev)
+    ke = max(1, min(args.steps, 3))
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    ee0 = torch.cuda.Event(enable_timing=True); ee1 = torch.cuda.Event(enable_timing=True)
+    ee0.record(stream)
+    for k in range(ke):
+        s = (rank + world * k) % nsys
+        D_stage.copy_(D_host[s], non_blocking=True)
+        g.update_D(D_stage)
+        g.pcg_host(b_host, x_host, rtol=p.rtol)
+    ee1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = ee0.elapsed_time(ee1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    # ---- kernel-level roofline: fine-level SpMV (dominant kernel family) and whole V-cycle
+    xr = torch.randn(p.n, dtype=torch.float64, device=dev)
+    yr = torch.empty_like(xr)
+    for _ in range(3):
+        g.spmv(xr, 0, out=yr)
+    nrep = 30
+    a0 = torch.cuda.Event(enable_timing=True); a1 = torch.cuda.Event(enable_timing=True)
+    a0.record(stream)
+    for _ in range(nrep):
+        g.spmv(xr, 0, out=yr)
+    a1.record(stream); a1.synchronize()
+    spmv_ms = a0.elapsed_time(a1) / nrep
+    for _ in range(2):
+        g.vcycle(xr, out=yr)
+    v0 = torch.cuda.Event(enable_timing=True); v1 = torch.cuda.Event(enable_timing=True)
+    nv = 20
+    v0.record(stream)
+    for _ in range(nv):
+        g.vcycle(xr, out=yr)
+    v1.record(stream); v1.synchronize()
+    vcycle_ms = v0.elapsed_time(v1) / nv
+    ap0 = torch.cuda.Event(enable_timing=True); ap1 = torch.cuda.Event(enable_timing=True)
+    ap0.record(stream)
+    for _ in range(10):
+        g.apply(xr, out=yr)
+    ap1.record(stream); ap1.synchronize()
+    apply_ms = ap0.elapsed_time(ap1) / 10
+
+    peak, peak_src = peaks()
+    sb = spmv_bytes(g)
+    vb = level_bytes(g)
+    W = (g.bw + 2) & ~1
+    filt_bytes = 2 * g.nc * W * 8
+    apply_bytes = 2 * vb + sb + filt_bytes + 6 * 8 * p.n
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "spmv_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    spmv_gbs = sb / (spmv_ms * 1e-3) / 1e9
+    res = {
+        "metric": METRIC,
+        "value": elapsed / (args.steps * world),
+        "unit": "ms/system",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": elapsed / args.steps,
+        "higher_is_better": False,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (amgf_gen: seeded two-block Q1 elasticity + node-on-segment contact, DESIGN.md section 4)",
+        "config": {"workload": f"cfg{args.cfg}: two-block N={p.N}, n={p.n} dofs, m={p.m}, n_c={g.nc}, "
+                               f"{nsys}-system IP-like D sequence, rtol={p.rtol}",
+                   "levels": [(L["nodes"] * L["b"]) for L in g.levels], "band_width_Aw": g.bw,
+                   "l2": "inputs larger than L2 (fine operator 1.1 GB)", "parallelism": f"replicas x{world}"},
+        "pcg_iterations": iters,
+        "systems": systems,
+        "solve_ms_per_system": solve_ms,
+        "numeric_setup_ms": upd_ms,
+        "full_setup_ms": full_setup_ms,
+        "vcycle_ms": vcycle_ms,
+        "vcycle_gbs": vb / (vcycle_ms * 1e-3) / 1e9,
+        "vcycle_frac_of_measured_peak": vb / (vcycle_ms * 1e-3) / 1e9 / peak,
+        "vcycle_frac_of_8TBs": vb / (vcycle_ms * 1e-3) / 1e9 / 8000.0,
+        "apply_ms": apply_ms,
+        "apply_gbs": apply_bytes / (apply_ms * 1e-3) / 1e9,
+        "roofline": {"kernel": "k_sell<3,3> (fine-level S SpMV, SELL-32)", "bound": "hbm",
+                     "achieved": spmv_gbs, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                     "frac": spmv_gbs / peak, "traffic": traffic, "algorithmic_bytes_per_launch": sb,
+                     "avg_launch_ms": spmv_ms},
+        "e2e": {"value": e2e_ms / (ke * world), "unit": "ms/system", "h2d_bytes_per_step": 8 * (p.m + p.n),
+                "d2h_bytes_per_step": 8 * p.n},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    return res, p
+
+
+def cpu_baseline(p, iters_guess, budget_s=25.0):
+    """Oracle as it stands, on a bounded sample of cfg 3: hierarchy setup without the dense A_w factor,
+    then V-cycles and S SpMVs; per-system time = setup + iters * (2 V-cycles + 2 S SpMVs)."""
+    import numpy as np
+    import oracle
+    oracle.build()
+    t = time.perf_counter()
+    o = oracle.Oracle.from_problem(p, factor_filter=0)
+    t_setup = time.perf_counter() - t
+    x = np.random.default_rng(0).standard_normal(p.n)
+    t = time.perf_counter(); o.vcycle(x); t_v = time.perf_counter() - t
+    t = time.perf_counter(); o.spmv(x); t_s = time.perf_counter() - t
+    per_sys = t_setup + iters_guess * (2 * t_v + 2 * t_s)
+    return {"value": per_sys * 1e3, "unit": "ms/system", "cores": 1, "kind": "oracle",
+            "sample": f"cfg3: oracle setup without the dense A_w factor ({t_setup:.1f} s) + 1 V-cycle "
+                      f"({t_v:.2f} s) + 1 S SpMV ({t_s:.3f} s); value = setup + {iters_guess} PCG iterations "
+                      f"x (2 V-cycles + 2 SpMVs), filter cost excluded (underestimates the oracle)",
+            "cpu": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip() + f" (nproc {os.cpu_count()})"
+    except Exception:
+        pass
+    return f"nproc {os.cpu_count()}"
+
+
+def run_reference(args, rank, world):
+    """Reference arm: the CPU oracle (this tier has no reference implementation), same metric/config."""
+    if rank != 0:
+        return None
+    import numpy as np
+    import amgf_gen
+    import oracle
+    oracle.build()
+    p = amgf_gen.config(args.cfg)
+    t = time.perf_counter()
+    o = oracle.Oracle.from_problem(p, factor_filter=0)
+    t_setup = time.perf_counter() - t
+    x = np.random.default_rng(0).standard_normal(p.n)
+    for _ in range(min(args.warmup, 1)):
+        o.spmv(x)
+    vals = []
+    iters_guess = 60
+    for k in range(args.steps):
+        t = time.perf_counter(); o.vcycle(x); t_v = time.perf_counter() - t
+        t = time.perf_counter(); o.spmv(x); t_s = time.perf_counter() - t
+        vals.append((t_setup + iters_guess * (2 * t_v + 2 * t_s)) * 1e3)
+    v = statistics.mean(vals)
+    sample = (f"cfg3 oracle: per step 1 V-cycle + 1 S SpMV timed, value = setup without the dense A_w factor "
+              f"({t_setup:.1f} s, once) + {iters_guess} iterations x (2 V + 2 SpMV); filter excluded")
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": "ms/system", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"cfg{args.cfg}: two-block N={p.N}, n={p.n} dofs"},
+            "cpu_baseline": {"value": v, "unit": "ms/system", "cores": 1, "kind": "oracle", "sample": sample,
+                             "cpu": _cpu_model()},
+            "e2e": {"value": v, "unit": "ms/system", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="amgf", choices=["amgf", "reference"])
+    ap.add_argument("--cfg", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.warmup < 3 and args.impl == "amgf":
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        out = run_reference(args, rank, world)
+        if out is not None:
+            print(json.dumps(out))
+        return
+    if world > 1:
+        import torch
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    res, p = run_amgf(args, rank, world, local_rank)
+    if rank == 0:
+        if not args.no_cpu_baseline and world == 1:
+            res["cpu_baseline"] = cpu_baseline(p, int(statistics.mean(res["pcg_iterations"])))
+        print(json.dumps(res))
+    if world > 1:
+        import torch
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,128 @@
+/*
+ * amgf.h -- C ABI of libamgf.so: B200 (sm_100a) AMGF-PCG for S = K + J^T D J.
+ *
+ * Method: arxiv 2505.18576 "AMG with Filtering".
+ *   S = K + J^T D J ............................. eq:linsystem1
+ *   I_c, P (natural embedding), A_w = P^T S P ..... Def. Discrete Operators
+ *   M: I - M S = (I - B S)(I - P A_w^{-1} P^T S)(I - B S)   Def. AMGF
+ *   B = one AMG V-cycle with l1 smoothing ......... PAPER.md:368, 587-595
+ *   PCG, relative preconditioned residual ......... PAPER.md:368
+ * The arithmetic follows DESIGN.md section 3 ("contract"), under which results are bitwise
+ * identical to the CPU oracle in oracle/.
+ *
+ * Conventions for every function:
+ *   - All array arguments are DEVICE pointers owned by the caller and only read during the call,
+ *     unless the function name ends in _host (host pointers) or the comment says otherwise.
+ *   - Index arrays are int32, values are IEEE binary64; matrices are block-CSR with column indices
+ *     sorted ascending inside each row and 3x3 blocks stored row-major.
+ *   - Dof numbering: dof = 3*node + component.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Every call is stream-ordered.
+ *     Calls that return host-visible data (setup, pcg_solve, level_info/get, *_host) synchronise it.
+ *   - No exception crosses the ABI.  A negative amgf_status is an error; amgf_last_error() returns
+ *     a thread-local description.  On error the handle is left unchanged and usable (setup leaves
+ *     *out = NULL).  A handle is used by one host thread / one stream at a time.
+ */
+#ifndef AMGF_H
+#define AMGF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  AMGF_OK = 0,
+  AMGF_NOT_CONVERGED = 1,      /* PCG reached max_it (not an error)              */
+  AMGF_ERR_ARG = -1,           /* null pointer, bad size, Z not a permutation of I_c            */
+  AMGF_ERR_NONFINITE = -2,     /* NaN/Inf in K, J or D                             */
+  AMGF_ERR_DOMAIN = -3,        /* some D_k <= 0                                    */
+  AMGF_ERR_NOT_SPD = -4,       /* non-positive Cholesky pivot in A_w or the coarsest operator   */
+  AMGF_ERR_RANK = -5,          /* rank-deficient tentative prolongator block      */
+  AMGF_ERR_BREAKDOWN = -6,     /* PCG: p.Sp <= 0 or r.Mr < 0                      */
+  AMGF_ERR_CUDA = -7,          /* CUDA runtime error                                            */
+  AMGF_ERR_OOM = -8,           /* device allocation failed                                      */
+  AMGF_ERR_LIMIT = -9          /* an internal capacity limit was exceeded (message says which)  */
+} amgf_status;
+
+typedef struct {
+  int32_t pre_sweeps;      /* l1-Jacobi sweeps before restriction, >= 1 (default 1)          */
+  int32_t post_sweeps;     /* l1-Jacobi sweeps after prolongation, >= 1 (default 1)          */
+  int32_t coarsest_size;   /* stop coarsening at <= this many dofs (default 64) */
+  int32_t max_levels;      /* default 25                                                     */
+  int32_t power_iters;     /* power steps for lambda_max(D^-1 A) (default 10)                */
+  int32_t reserved;
+  uint64_t agg_seed;       /* aggregation priority seed (default 0x5EED)                     */
+} amgf_config;
+
+typedef struct {
+  int32_t iterations;      /* number of S*p products                                         */
+  int32_t converged;       /* 1 if sqrt(r.Mr / r0.Mr0) < rtol                                */
+  double rel_pres_norm;    /* final sqrt(r.Mr / r0.Mr0)                                      */
+  double solve_ms;         /* device time of the solve (CUDA events)                         */
+} amgf_report;
+
+typedef struct amgf_ctx *amgf_handle;
+
+/* Fill *cfg with the defaults above. */
+void amgf_default_config(amgf_config *cfg);
+
+/* Build the AMGF preconditioner for S = K + J^T D J on the GPU.
+ *   nodes            number of 3-dof nodes; n = 3*nodes
+ *   K_ptr[nodes+1], K_col[nnzb], K_val[9*nnzb]   K in 3x3 BSR (symmetric positive semidefinite
+ *                    blocks per body, Dirichlet rows = identity)
+ *   m, J_ptr[m+1], J_col[nnz], J_val[nnz]        gap Jacobian, scalar CSR over dofs
+ *   D[m]             log-barrier Hessian diagonal, > 0
+ *   Z[nc]            contact dofs I_c in the column order of P; must be a
+ *                    permutation of the structurally nonzero columns of J.  NULL: ascending order.
+ *   B_nns[n*6]       near-null space (rigid-body modes), row-major n x 6
+ *   cfg              NULL for defaults
+ * Synchronises `stream`.  The handle deep-copies everything it needs. */
+amgf_status amgf_setup(int32_t nodes, const int32_t *K_ptr, const int32_t *K_col, const double *K_val,
+                       int32_t m, const int32_t *J_ptr, const int32_t *J_col, const double *J_val,
+                       const double *D, const int32_t *Z, int32_t nc, const double *B_nns,
+                       const amgf_config *cfg, void *stream, amgf_handle *out);
+
+/* Numeric re-setup for a new D (same K, J, Z): re-forms S, A_w and its factor and all Galerkin
+ * values; aggregation and all sparsity patterns are reused (they do not depend on D, reading R5). */
+amgf_status amgf_update_D(amgf_handle h, const double *D, void *stream);
+
+/* z = M r, one AMGF application (Def. AMGF, three stages SPEC.md:245).  r, z: n doubles. */
+amgf_status amgf_apply(amgf_handle h, const double *r, double *z, void *stream);
+
+/* x = B b, one V-cycle of the AMG hierarchy.  b, x: n doubles. */
+amgf_status amgf_vcycle(amgf_handle h, const double *b, double *x, void *stream);
+
+/* y = A_level x (level 0: S).  Sizes: 3*nodes at level 0, 6*n_agg below. */
+amgf_status amgf_spmv(amgf_handle h, int32_t level, const double *x, double *y, void *stream);
+
+/* PCG on S x = b with AMGF (precond = 0) or AMG-only (precond = 1), x0 = 0, stops when
+ * sqrt(r.Mr / r0.Mr0) < rtol or after max_it iterations.  Synchronises `stream`. */
+amgf_status amgf_pcg_solve(amgf_handle h, const double *b, double *x, double rtol, int32_t max_it,
+                           int32_t precond, amgf_report *rep, void *stream);
+
+/* Same with HOST b and x: copies b host->device, solves, copies x device->host (e2e timing). */
+amgf_status amgf_pcg_solve_host(amgf_handle h, const double *b_host, double *x_host, double rtol,
+                                int32_t max_it, int32_t precond, amgf_report *rep, void *stream);
+
+/* Hierarchy introspection (tests, bench).  info[0] = levels, info[1] = nc, info[2] = coarsest dofs,
+ * info[3] = band width of A_w's factor, then per level l: info[4+6l .. 9+6l] =
+ * {nodes, block size, nnzb(A), nnzb(P), n_agg, SELL slots of A}.  info needs 4 + 6*32 entries. */
+amgf_status amgf_level_info(amgf_handle h, int64_t *info);
+
+/* Copy one hierarchy array to the HOST buffer dst.  which: 0 A.ptr 1 A.col 2 A.val 3 P.ptr 4 P.col
+ * 5 P.val 6 R.ptr 7 R.col 8 R.val 9 l1 diagonal 10 aggregate ids 11 near-null space 12 {lambda,
+ * omega} 14 root flags 15 component labels 20 Z 22 A_w factor band (nc x W row-major, W = (bw+2)&~1,
+ * L_ik at column bw-(i-k), diagonal at column bw).  Sizes follow amgf_level_info.  Synchronises the handle's last stream. */
+amgf_status amgf_level_get(amgf_handle h, int32_t which, int32_t level, void *dst);
+
+/* Number of kernel launches issued by this handle since creation (bench accounting). */
+int64_t amgf_launch_count(amgf_handle h);
+
+const char *amgf_last_error(void);
+void amgf_destroy(amgf_handle h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

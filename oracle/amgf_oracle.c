@@ -175,19 +175,20 @@ int orc_cholesky_dense(int n, const double *A, double *L) {
   return ORC_OK;
 }
 
-/* Contract C10: forward  y_i = (v_i - sum_{k<i} L_ik y_k) / L_ii, chain over k ascending;
- * backward x_i = (w_i - sum_{k>i} L_ki x_k) / L_ii, chain over k descending. */
+/* Contract C10: forward  y_i = (v_i - sum_{k<i} L_ik y_k) * (1/L_ii), chain over k ascending;
+ * backward x_i = (w_i - sum_{k>i} L_ki x_k) * (1/L_ii), chain over k descending.
+ * The reciprocal 1/L_ii is one correctly rounded division (C10). */
 void orc_trsv_dense(int n, const double *L, const double *v, double *x) {
   double *y = (double *)malloc((size_t)(n > 0 ? n : 1) * sizeof(double));
   for (int i = 0; i < n; i++) {
     double acc = v[i];
     for (int k = 0; k < i; k++) acc = fma(-L[(size_t)i * n + k], y[k], acc);
-    y[i] = acc / L[(size_t)i * n + i];
+    y[i] = acc * (1.0 / L[(size_t)i * n + i]);
   }
   for (int i = n - 1; i >= 0; i--) {
     double acc = y[i];
     for (int k = n - 1; k > i; k--) acc = fma(-L[(size_t)k * n + i], x[k], acc);
-    x[i] = acc / L[(size_t)i * n + i];
+    x[i] = acc * (1.0 / L[(size_t)i * n + i]);
   }
   free(y);
 }

@@ -1,0 +1,27 @@
+"""Build libamgf.so in-tree with nvcc for sm_100a (B200)."""
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SRC = [os.path.join(HERE, "csrc", f) for f in ("solve.cu", "setup.cu", "api.cu")]
+LIB = os.path.join(HERE, "libamgf.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "--fmad=false", "-std=c++17",
+         "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off", "-shared"]
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    deps = SRC + [os.path.join(HERE, "csrc", "common.cuh"), os.path.join(HERE, "..", "include", "amgf.h")]
+    if not force and os.path.exists(LIB) and all(os.path.getmtime(LIB) >= os.path.getmtime(d) for d in deps):
+        return LIB
+    cmd = [NVCC, *FLAGS, "-o", LIB, *SRC]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    subprocess.check_call(cmd)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force=True, verbose="-v" in sys.argv)
+    print(LIB)

@@ -1,0 +1,364 @@
+// api.cu -- C-ABI entry points of libamgf.so and the solve orchestration (V-cycle, AMGF apply, PCG).
+//
+//   vcycle   B b: l1-Jacobi pre-sweep from zero, residual, restriction, recursion, prolongation,
+//            post-sweep; dense Cholesky solve on the coarsest level.
+//   apply_M  x1 = B r; r1 = r - S x1; y = A_w^{-1} r1[Z]; x2 = x1 + P y; r2 = r1 - S[:,Z] y;
+//            z = x2 + B r2  (Def. AMGF; three stages SPEC.md:245; C11).
+//   pcg      PAPER.md:368 (relative preconditioned residual), C15.
+#include <cmath>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace amgf {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string &m) { g_last_error = m; }
+const char *get_error() { return g_last_error.c_str(); }
+
+void Ctx::release(void *p) {
+  if (!p) return;
+  for (size_t i = 0; i < allocs.size(); i++)
+    if (allocs[i] == p) {
+      cudaFree(p);
+      allocs[i] = allocs.back();
+      allocs.pop_back();
+      return;
+    }
+}
+
+Ctx::~Ctx() {
+  drop_caches(*this);
+  for (void *p : allocs) cudaFree(p);
+  if (sc_host) cudaFreeHost(sc_host);
+  if (err_host) cudaFreeHost(err_host);
+}
+
+void check_dev_error(Ctx &c, const char *where) {
+  CK(cudaMemcpyAsync(c.err_host, c.err, 2 * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  const int code = c.err_host[0], info = c.err_host[1];
+  if (code == DERR_NONE) return;
+  CK(cudaMemsetAsync(c.err, 0, 2 * sizeof(int), c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  std::string w = std::string(where) + ": ";
+  switch (code) {
+    case DERR_NONFINITE: throw Error{AMGF_ERR_NONFINITE, w + "non-finite value at index " + std::to_string(info)};
+    case DERR_DOMAIN: throw Error{AMGF_ERR_DOMAIN, w + "D must be strictly positive (index " + std::to_string(info) + ")"};
+    case DERR_NOT_SPD:
+      throw Error{AMGF_ERR_NOT_SPD, w + "non-positive pivot " + std::to_string(info % 1000000) +
+                                        (info / 1000000 == 1 ? " of A_w" : " of the coarsest operator")};
+    case DERR_RANK: throw Error{AMGF_ERR_RANK, w + "rank-deficient tentative prolongator at aggregate " + std::to_string(info)};
+    case DERR_LIMIT: throw Error{AMGF_ERR_LIMIT, w + "capacity limit exceeded at row " + std::to_string(info)};
+    case DERR_BREAKDOWN: throw Error{AMGF_ERR_BREAKDOWN, w + (info == 1 ? "p.Sp <= 0" : "r.Mr < 0")};
+    default: throw Error{AMGF_ERR_ARG, w + "invalid input (index " + std::to_string(info) + ")"};
+  }
+}
+
+// ------------------------------------------------------------------ V-cycle
+void vcycle(Ctx &c, int l, const double *b, double *x, const double *add) {
+  Level &L = c.lev[l];
+  if (l == c.nlev - 1) {
+    double *dst = add ? L.x2 : x;
+    launch_band_trsv(c, c.nco, c.nco - 1, c.Lc_row, c.Lc_col, c.Lc_dinv, b, nullptr, dst, nullptr, nullptr, L.r);
+    if (add) launch_add(c, L.n, add, dst, x);
+    return;
+  }
+  Level &Lc = c.lev[l + 1];
+  const int pre = c.cfg.pre_sweeps, post = c.cfg.post_sweeps;
+  double *bufs[2] = {x, L.x2};
+  int ci = ((pre - 1) + post) & 1;  // so that the last post-sweep lands in x
+  launch_jacobi0(c, L.n, b, L.dl1, bufs[ci]);
+  for (int s = 1; s < pre; s++) {
+    launch_sell_spmv(c, L.As, SPMV_SMOOTH, bufs[ci], b, L.dl1, nullptr, bufs[1 - ci], nullptr);
+    ci = 1 - ci;
+  }
+  launch_sell_spmv(c, L.As, SPMV_RESID, bufs[ci], b, nullptr, nullptr, L.r, nullptr);
+  launch_restrict(c, L.R, L.r, Lc.bv);
+  vcycle(c, l + 1, Lc.bv, Lc.x, nullptr);
+  launch_prolong(c, L.Ps, Lc.x, bufs[ci]);
+  for (int s = 0; s < post; s++) {
+    const bool last = (s == post - 1);
+    launch_sell_spmv(c, L.As, (last && add) ? SPMV_SMOOTH_ADD : SPMV_SMOOTH, bufs[ci], b, L.dl1, add, bufs[1 - ci],
+                     nullptr);
+    ci = 1 - ci;
+  }
+}
+
+// ------------------------------------------------------------------ AMGF apply (C11)
+void apply_M(Ctx &c, const double *r, double *z) {
+  Level &L0 = c.lev[0];
+  vcycle(c, 0, r, c.w_x1, nullptr);
+  if (c.nc == 0) {
+    // I_c empty: filter stage is the identity
+    launch_sell_spmv(c, L0.As, SPMV_RESID, c.w_x1, r, nullptr, nullptr, c.w_r1, nullptr);
+    vcycle(c, 0, c.w_r1, z, c.w_x1);
+    return;
+  }
+  launch_sell_spmv(c, L0.As, SPMV_RESID, c.w_x1, r, nullptr, nullptr, c.w_r1, nullptr);
+  launch_band_trsv(c, c.nc, c.bw, c.Lrow, c.Lcol, c.Ldinv, c.w_r1, c.Z, c.fv, c.Z, c.w_x1, c.w_xv);
+  launch_thin_resid(c, c.nthin, c.thin_row, c.thin_ptr, c.thin_pos, c.thin_val, c.fv, c.w_r1);
+  vcycle(c, 0, c.w_r1, z, c.w_x1);
+}
+
+// ------------------------------------------------------------------ PCG (C15)
+static amgf_status pcg(Ctx &c, const double *b, double *x, double rtol, int max_it, int precond, amgf_report *rep) {
+  const long n = c.n;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, c.stream));
+  auto M = [&](const double *r, double *z) {
+    if (precond == 0) apply_M(c, r, z);
+    else vcycle(c, 0, r, z, nullptr);
+  };
+  launch_zero(c, n, x);
+  launch_copy(c, n, b, c.rr);
+  M(c.rr, c.zz);
+  launch_dot(c, n, 3, c.rr, c.zz, DOT_RHO0);
+  CK(cudaMemcpyAsync(c.sc_host, c.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, c.stream));
+  check_dev_error(c, "pcg");
+  const double rho0 = c.sc_host->rho0;
+  int it = 0;
+  double rel = 0.0;
+  amgf_status st = AMGF_NOT_CONVERGED;
+  if (rho0 == 0.0) {
+    st = AMGF_OK;
+  } else if (!(rho0 > 0.0)) {
+    throw Error{AMGF_ERR_BREAKDOWN, "pcg: r.Mr <= 0"};
+  } else {
+    launch_copy(c, n, c.zz, c.p);
+    for (it = 1; it <= max_it; it++) {
+      launch_sell_spmv(c, c.lev[0].As, SPMV_DOT, c.p, nullptr, nullptr, nullptr, c.q, c.dot_part);
+      launch_dot_finish(c, nblk(c.lev[0].As.nrows), DOT_PI);  // pi = p.q, alpha = rho / pi
+      launch_axpy2(c, n, c.p, c.q, x, c.rr);
+      M(c.rr, c.zz);
+      launch_dot(c, n, 3, c.rr, c.zz, DOT_RHO1);
+      CK(cudaMemcpyAsync(c.sc_host, c.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, c.stream));
+      check_dev_error(c, "pcg");
+      const double rho1 = c.sc_host->rho1;
+      rel = std::sqrt(rho1 / rho0);
+      if (rel < rtol) { st = AMGF_OK; break; }
+      if (it == max_it) break;
+      launch_xpby(c, n, c.zz, c.p);
+    }
+    if (it > max_it) it = max_it;
+  }
+  CK(cudaEventRecord(e1, c.stream));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (rep) {
+    rep->iterations = it;
+    rep->converged = st == AMGF_OK;
+    rep->rel_pres_norm = rel;
+    rep->solve_ms = ms;
+  }
+  return st;
+}
+
+}  // namespace amgf
+
+// =================================================================== C ABI
+using namespace amgf;
+
+struct amgf_ctx : public Ctx {};
+
+template <class F>
+static amgf_status guarded(F &&f) {
+  try {
+    return f();
+  } catch (const Error &e) {
+    set_error(e.msg);
+    return e.code;
+  } catch (const std::exception &e) {
+    set_error(e.what());
+    return AMGF_ERR_ARG;
+  }
+}
+
+extern "C" {
+
+void amgf_default_config(amgf_config *cfg) {
+  cfg->pre_sweeps = 1;
+  cfg->post_sweeps = 1;
+  cfg->coarsest_size = 64;
+  cfg->max_levels = 25;
+  cfg->power_iters = 10;
+  cfg->reserved = 0;
+  cfg->agg_seed = 0x5EED;
+}
+
+const char *amgf_last_error(void) { return get_error(); }
+
+amgf_status amgf_setup(int32_t nodes, const int32_t *K_ptr, const int32_t *K_col, const double *K_val, int32_t m,
+                       const int32_t *J_ptr, const int32_t *J_col, const double *J_val, const double *D,
+                       const int32_t *Z, int32_t nc, const double *B_nns, const amgf_config *cfg, void *stream,
+                       amgf_handle *out) {
+  if (!out) { set_error("out is NULL"); return AMGF_ERR_ARG; }
+  *out = nullptr;
+  amgf_ctx *c = new amgf_ctx();
+  amgf_status st = guarded([&]() -> amgf_status {
+    REQUIRE(nodes > 0 && K_ptr && K_col && K_val && B_nns, AMGF_ERR_ARG, "null K / near-null space or nodes <= 0");
+    REQUIRE(m >= 0 && (m == 0 || (J_ptr && J_col && J_val && D)), AMGF_ERR_ARG, "null J or D");
+    REQUIRE(!Z || nc >= 0, AMGF_ERR_ARG, "negative nc");
+    c->stream = (cudaStream_t)stream;
+    if (cfg) c->cfg = *cfg; else amgf_default_config(&c->cfg);
+    REQUIRE(c->cfg.pre_sweeps >= 1 && c->cfg.post_sweeps >= 1 && c->cfg.max_levels >= 1 && c->cfg.power_iters >= 1,
+            AMGF_ERR_ARG, "invalid config");
+    c->nodes = nodes;
+    c->n = 3L * nodes;
+    c->m = m;
+    c->sc = c->alloc<Scalars>(1);
+    c->err = c->alloc<int>(2);
+    CK(cudaMemsetAsync(c->err, 0, 2 * sizeof(int), c->stream));
+    CK(cudaMemsetAsync(c->sc, 0, sizeof(Scalars), c->stream));
+    CK(cudaMallocHost(&c->sc_host, sizeof(Scalars)));
+    CK(cudaMallocHost(&c->err_host, 2 * sizeof(int)));
+    c->dot_part = c->alloc<double>(nblk(c->n) + 1);
+    setup_all(*c, K_ptr, K_col, K_val, J_ptr, J_col, J_val, D, Z, nc, B_nns);
+    return AMGF_OK;
+  });
+  if (st != AMGF_OK) {
+    cudaStreamSynchronize((cudaStream_t)stream);
+    delete c;
+    return st;
+  }
+  *out = c;
+  return AMGF_OK;
+}
+
+amgf_status amgf_update_D(amgf_handle h, const double *D, void *stream) {
+  if (!h) { set_error("null handle"); return AMGF_ERR_ARG; }
+  return guarded([&]() -> amgf_status {
+    REQUIRE(h->m == 0 || D, AMGF_ERR_ARG, "null D");
+    h->stream = (cudaStream_t)stream;
+    setup_numeric(*h, D);
+    CK(cudaStreamSynchronize(h->stream));
+    return AMGF_OK;
+  });
+}
+
+amgf_status amgf_apply(amgf_handle h, const double *r, double *z, void *stream) {
+  if (!h || !r || !z) { set_error("null argument"); return AMGF_ERR_ARG; }
+  return guarded([&]() -> amgf_status {
+    h->stream = (cudaStream_t)stream;
+    apply_M(*h, r, z);
+    return AMGF_OK;
+  });
+}
+
+amgf_status amgf_vcycle(amgf_handle h, const double *b, double *x, void *stream) {
+  if (!h || !b || !x) { set_error("null argument"); return AMGF_ERR_ARG; }
+  return guarded([&]() -> amgf_status {
+    h->stream = (cudaStream_t)stream;
+    vcycle(*h, 0, b, x, nullptr);
+    return AMGF_OK;
+  });
+}
+
+amgf_status amgf_spmv(amgf_handle h, int32_t level, const double *x, double *y, void *stream) {
+  if (!h || !x || !y) { set_error("null argument"); return AMGF_ERR_ARG; }
+  return guarded([&]() -> amgf_status {
+    REQUIRE(level >= 0 && level < h->nlev, AMGF_ERR_ARG, "bad level");
+    h->stream = (cudaStream_t)stream;
+    Level &L = h->lev[level];
+    if (L.As.nrows == L.nodes && L.As.val) launch_sell_spmv(*h, L.As, SPMV_Y, x, nullptr, nullptr, nullptr, y, nullptr);
+    else launch_bsr_spmv(*h, L.A, x, y);
+    return AMGF_OK;
+  });
+}
+
+amgf_status amgf_pcg_solve(amgf_handle h, const double *b, double *x, double rtol, int32_t max_it, int32_t precond,
+                           amgf_report *rep, void *stream) {
+  if (!h || !b || !x) { set_error("null argument"); return AMGF_ERR_ARG; }
+  return guarded([&]() -> amgf_status {
+    REQUIRE(max_it >= 0 && rtol >= 0 && (precond == 0 || precond == 1), AMGF_ERR_ARG, "bad pcg arguments");
+    h->stream = (cudaStream_t)stream;
+    return pcg(*h, b, x, rtol, max_it, precond, rep);
+  });
+}
+
+amgf_status amgf_pcg_solve_host(amgf_handle h, const double *b_host, double *x_host, double rtol, int32_t max_it,
+                                int32_t precond, amgf_report *rep, void *stream) {
+  if (!h || !b_host || !x_host) { set_error("null argument"); return AMGF_ERR_ARG; }
+  return guarded([&]() -> amgf_status {
+    h->stream = (cudaStream_t)stream;
+    CK(cudaMemcpyAsync(h->bb, b_host, h->n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    amgf_status st = pcg(*h, h->bb, h->xx, rtol, max_it, precond, rep);
+    CK(cudaMemcpyAsync(x_host, h->xx, h->n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return st;
+  });
+}
+
+amgf_status amgf_level_info(amgf_handle h, int64_t *info) {
+  if (!h || !info) { set_error("null argument"); return AMGF_ERR_ARG; }
+  info[0] = h->nlev;
+  info[1] = h->nc;
+  info[2] = h->nco;
+  info[3] = h->bw;
+  for (int l = 0; l < h->nlev; l++) {
+    Level &L = h->lev[l];
+    const bool co = (l == h->nlev - 1);
+    info[4 + 6 * l + 0] = L.nodes;
+    info[4 + 6 * l + 1] = L.b;
+    info[4 + 6 * l + 2] = L.A.nnzb;
+    info[4 + 6 * l + 3] = co ? 0 : L.P.nnzb;
+    info[4 + 6 * l + 4] = co ? 0 : L.n_agg;
+    info[4 + 6 * l + 5] = L.As.nslots;
+  }
+  return AMGF_OK;
+}
+
+amgf_status amgf_level_get(amgf_handle h, int32_t which, int32_t level, void *dst) {
+  if (!h || !dst) { set_error("null argument"); return AMGF_ERR_ARG; }
+  return guarded([&]() -> amgf_status {
+    REQUIRE(level >= 0 && level < h->nlev, AMGF_ERR_ARG, "bad level");
+    Level &L = h->lev[level];
+    const bool co = (level == h->nlev - 1);
+    auto cp = [&](const void *src, size_t bytes) {
+      REQUIRE(src || bytes == 0, AMGF_ERR_ARG, "array not available at this level");
+      CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, h->stream));
+    };
+    switch (which) {
+      case 0: cp(L.A.ptr, (L.nodes + 1) * 4); break;
+      case 1: cp(L.A.col, L.A.nnzb * 4); break;
+      case 2: cp(L.A.val, L.A.nnzb * L.b * L.b * 8); break;
+      case 3: REQUIRE(!co, AMGF_ERR_ARG, "no P"); cp(L.P.ptr, (L.nodes + 1) * 4); break;
+      case 4: REQUIRE(!co, AMGF_ERR_ARG, "no P"); cp(L.P.col, L.P.nnzb * 4); break;
+      case 5: REQUIRE(!co, AMGF_ERR_ARG, "no P"); cp(L.P.val, L.P.nnzb * L.b * 6 * 8); break;
+      case 6: REQUIRE(!co, AMGF_ERR_ARG, "no R"); cp(L.R.ptr, (L.n_agg + 1) * 4); break;
+      case 7: REQUIRE(!co, AMGF_ERR_ARG, "no R"); cp(L.R.col, L.R.nnzb * 4); break;
+      case 8: REQUIRE(!co, AMGF_ERR_ARG, "no R"); cp(L.R.val, L.R.nnzb * L.b * 6 * 8); break;
+      case 9: cp(L.dl1, L.n * 8); break;
+      case 10: REQUIRE(!co, AMGF_ERR_ARG, "no aggregates"); cp(L.agg, L.nodes * 4); break;
+      case 11: cp(L.Bnn, L.n * 6 * 8); break;
+      case 12: {
+        double lo[2] = {L.lambda, L.omega};
+        CK(cudaStreamSynchronize(h->stream));
+        std::memcpy(dst, lo, sizeof lo);
+        return AMGF_OK;
+      }
+      case 14: REQUIRE(L.root, AMGF_ERR_ARG, "no roots"); cp(L.root, L.nodes * 4); break;
+      case 15: cp(L.comp, L.nodes * 4); break;
+      case 20: cp(h->Z, h->nc * 4); break;
+      case 22: cp(h->Lrow, (size_t)h->nc * band_stride(h->bw) * 8); break;
+      default: throw Error{AMGF_ERR_ARG, "unknown array id"};
+    }
+    CK(cudaStreamSynchronize(h->stream));
+    return AMGF_OK;
+  });
+}
+
+int64_t amgf_launch_count(amgf_handle h) { return h ? h->launches : -1; }
+
+void amgf_destroy(amgf_handle h) {
+  if (!h) return;
+  cudaStreamSynchronize(h->stream);
+  delete h;
+}
+
+}  // extern "C"

@@ -1,0 +1,192 @@
+// common.cuh -- shared declarations of libamgf.so (B200 / sm_100a, fp64).
+//
+// Arithmetic contract: DESIGN.md section 3.  Every kernel in this library is compiled with
+// --fmad=false, so a fused multiply-add happens only where __fma_rn is written.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/amgf.h"
+
+namespace amgf {
+
+constexpr int MAXLEV = 32;
+constexpr int CTA = 256;  // CTA size of all row kernels; fixes the dot contract C14 level 1
+
+// ------------------------------------------------------------------ errors
+struct Error {
+  amgf_status code;
+  std::string msg;
+};
+void set_error(const std::string &m);
+const char *get_error();
+
+#define CK(x)                                                                                    \
+  do {                                                                                           \
+    cudaError_t e_ = (x);                                                                        \
+    if (e_ != cudaSuccess)                                                                       \
+      throw ::amgf::Error{AMGF_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)};       \
+  } while (0)
+
+#define REQUIRE(cond, code, m)                      \
+  do {                                              \
+    if (!(cond)) throw ::amgf::Error{(code), (m)};  \
+  } while (0)
+
+// device error flag codes (first error wins)
+enum DevErr { DERR_NONE = 0, DERR_NONFINITE = 1, DERR_DOMAIN = 2, DERR_NOT_SPD = 3, DERR_RANK = 4,
+              DERR_ARG = 5, DERR_LIMIT = 6, DERR_BREAKDOWN = 7 };
+
+__device__ __forceinline__ void raise_err(int *flag, int code, int info) {
+  if (atomicCAS(flag, 0, code) == 0) flag[1] = info;
+}
+
+// ------------------------------------------------------------------ storage
+// Block-CSR matrix on the device: nbr block rows of br x bc row-major blocks.
+struct Bsr {
+  int nbr = 0, nbc = 0, br = 0, bc = 0;
+  long nnzb = 0;
+  int *ptr = nullptr, *col = nullptr;
+  double *val = nullptr;
+};
+
+// SELL-32 block matrix: slices of 32 consecutive block rows; slot s of a slice holds the s-th block
+// of each of its 32 rows, components interleaved so that one block component of the 32 rows is one
+// contiguous 256-byte segment:  col[slot*32 + lane],  val[(slot*BB + e)*32 + lane].
+struct Sell {
+  int nrows = 0, nslices = 0, br = 0, bc = 0;
+  long nslots = 0;
+  int *slice_ptr = nullptr;  // [nslices+1] first slot of each slice
+  int *rowlen = nullptr;     // [nrows]
+  int *col = nullptr;        // [nslots*32]
+  double *val = nullptr;     // [nslots*br*bc*32]
+  int *src = nullptr;        // [nslots*32] index of the source BSR block (-1 padding) for refresh
+};
+
+struct Level {
+  int b = 3, nodes = 0;
+  long n = 0;
+  Bsr A;          // operator (level 0: S)
+  Sell As;        // A in SELL-32 for the solve
+  double *dl1 = nullptr, *dpt = nullptr;
+  int *agg = nullptr, *comp = nullptr, *root = nullptr;
+  int n_agg = 0;
+  Bsr Pt, P, R;   // tentative / smoothed prolongator (b x 6), restriction (6 x b)
+  Sell Ps;        // P in SELL-32 for prolongation
+  Bsr AP;         // A*P (b x 6), kept for numeric re-setup
+  int *agg_ptr = nullptr, *agg_nodes = nullptr;  // nodes of each aggregate, ascending
+  double *Bnn = nullptr;   // near-null space [n x 6]
+  double lambda = 0, omega = 0;
+  // solve workspace
+  double *x = nullptr, *x2 = nullptr, *bv = nullptr, *r = nullptr;
+};
+
+// Device scalars of PCG (C15) and dot results.
+struct Scalars {
+  double rho0, rho, pi, alpha, beta, rho1, dot, pad;
+};
+
+struct Ctx {
+  cudaStream_t stream = nullptr;
+  amgf_config cfg;
+  int nodes = 0, m = 0;
+  long n = 0;
+  // inputs kept for update_D
+  Bsr K;
+  int *J_ptr = nullptr, *J_col = nullptr;
+  double *J_val = nullptr;
+  int nnzJ = 0;
+  int *Jt_ptr = nullptr, *Jt_row = nullptr;  // J^T (per dof: constraint rows ascending)
+  double *Jt_val = nullptr;
+  double *D = nullptr;
+  int *S_kblk = nullptr;  // per S block: index of the K block (-1 if none)
+  // filter
+  int nc = 0, bw = 0;
+  int *Z = nullptr, *pos = nullptr;
+  double *Lrow = nullptr;   // band, row-major: Lrow[i*W + bw - (i-k)] = L_ik, W = band_stride(bw)
+  double *Lcol = nullptr;   // band, column-major: Lcol[k*W + (i-k)] = L_ik
+  double *Ldinv = nullptr;  // 1/L_ii
+  double *fv = nullptr;     // filter workspace (nc)
+  int nthin = 0;
+  int *thin_row = nullptr, *thin_ptr = nullptr, *thin_pos = nullptr, *thin_src = nullptr;
+  double *thin_val = nullptr;
+  // hierarchy
+  int nlev = 0;
+  Level lev[MAXLEV];
+  int nco = 0;
+  double *Lc_row = nullptr, *Lc_col = nullptr, *Lc_dinv = nullptr;
+  // solve workspace
+  double *w_x1 = nullptr, *w_r1 = nullptr, *w_xv = nullptr;
+  double *p = nullptr, *q = nullptr, *rr = nullptr, *zz = nullptr, *xx = nullptr, *bb = nullptr;
+  double *dot_part = nullptr;
+  Scalars *sc = nullptr;      // device
+  Scalars *sc_host = nullptr; // pinned
+  int *err = nullptr;         // device [2]
+  int *err_host = nullptr;    // pinned [2]
+  int64_t launches = 0;
+  void *setup_cache = nullptr;  // numeric re-setup data (setup.cu)
+  std::vector<void *> allocs;
+
+  template <class T>
+  T *alloc(size_t count) {
+    void *p = nullptr;
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    if (e != cudaSuccess) throw Error{AMGF_ERR_OOM, "cudaMalloc " + std::to_string(count * sizeof(T)) + " bytes"};
+    allocs.push_back(p);
+    return (T *)p;
+  }
+  void release(void *p);
+  ~Ctx();
+};
+
+inline int nblk(long n, int t = CTA) { return (int)((n + t - 1) / t); }
+
+// check the device error flag (synchronises the stream)
+void check_dev_error(Ctx &c, const char *where);
+
+// ------------------------------------------------------------------ solve kernels (solve.cu)
+enum SpmvMode { SPMV_Y = 0, SPMV_RESID = 1, SPMV_SMOOTH = 2, SPMV_DOT = 3, SPMV_SMOOTH_ADD = 4 };
+void launch_sell_spmv(Ctx &c, const Sell &A, int mode, const double *x, const double *b, const double *d,
+                      const double *add, double *y, double *dot_part);
+void launch_jacobi0(Ctx &c, long n, const double *b, const double *d, double *x);
+void launch_restrict(Ctx &c, const Bsr &R, const double *r, double *bc);
+void launch_prolong(Ctx &c, const Sell &P, const double *xc, double *x);
+void launch_dot(Ctx &c, long n, int b, const double *u, const double *v, int finish);
+void launch_dot_finish(Ctx &c, long n_partials, int finish);  // C14 level 2 over c.dot_part
+void launch_axpy2(Ctx &c, long n, const double *p, const double *q, double *x, double *r);
+void launch_xpby(Ctx &c, long n, const double *z, double *p);
+// y = L^{-T} L^{-1} v[gather] (C10); if scatter: xout[scatter[a]] += y[a].  Band storage: row stride
+// W = (bw+2)&~1, 64 zero rows of padding before and after (see band_alloc in setup.cu).
+void launch_band_trsv(Ctx &c, int n, int bw, const double *Lrow, const double *Lcol, const double *dinv,
+                      const double *v, const int *gather, double *y, const int *scatter, double *xout,
+                      double *work);
+inline int band_stride(int bw) { return (bw + 2) & ~1; }
+constexpr int BAND_PAD_ROWS = 64;
+void launch_thin_resid(Ctx &c, int nthin, const int *rows, const int *ptr, const int *pos, const double *val,
+                       const double *y, double *r);
+void launch_bsr_spmv(Ctx &c, const Bsr &A, const double *x, double *y);  // setup-side, thread per block row
+void launch_copy(Ctx &c, long n, const double *src, double *dst);
+void launch_zero(Ctx &c, long n, double *dst);
+void launch_add(Ctx &c, long n, const double *a, const double *b, double *out);
+// dot finishing kinds
+enum DotFinish { DOT_PLAIN = 0, DOT_PI = 1, DOT_RHO0 = 2, DOT_RHO1 = 3 };
+
+// ------------------------------------------------------------------ setup (setup.cu)
+void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, const int *J_ptr,
+               const int *J_col, const double *J_val, const double *D, const int *Z, int nc,
+               const double *B_nns);
+void setup_numeric(Ctx &c, const double *D);  // update_D
+void drop_caches(Ctx &c);
+void build_sell(Ctx &c, const Bsr &A, Sell &S, bool alloc);
+
+// ------------------------------------------------------------------ solve orchestration (api.cu)
+void vcycle(Ctx &c, int l, const double *b, double *x, const double *add);
+void apply_M(Ctx &c, const double *r, double *z);
+
+}  // namespace amgf

@@ -1,0 +1,1215 @@
+// setup.cu -- GPU setup of the AMGF preconditioner.  No CPU fallback:
+// every step below is a device kernel; the host only sizes allocations and loops over levels.
+//
+//   s1 S = K + J^T D J (C1) ......... k_S_count/k_S_fill (pattern), k_S_values
+//   s2 I_c, Z validation ............. k_mark_cols, k_check_Z / k_compact_Z
+//   s3 A_w band + Cholesky (C9) ...... k_band_start, k_band_fill, k_band_chol, k_band_finish
+//   s4 aggregation (C16) ............. k_cc_*, k_mis_* (fixed-priority local-max rounds), k_agg_*
+//   s5 tentative P (C17) ............. k_qr (per-aggregate MGS)
+//   s6 smoothed P (C18, C19) ......... k_pow_*, k_P_count/k_P_fill/k_P_values
+//   s7 Galerkin (C20, C22) ........... transpose (stable radix sort), k_AP_*, k_G_*, k_sym
+//   s8 l1 diagonal (C3), SELL-32 ..... k_diag, k_sell_pack
+//   s9 coarsest dense Cholesky ....... k_band_chol with bw = n-1
+#include <cub/cub.cuh>
+
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace amgf {
+
+// ------------------------------------------------------------------ small helpers
+template <class T>
+static void h2d(Ctx &c, T *dst, const T *src, size_t n) {
+  CK(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyHostToDevice, c.stream));
+}
+template <class T>
+static void d2d(Ctx &c, T *dst, const T *src, size_t n) {
+  if (n) CK(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyDeviceToDevice, c.stream));
+}
+template <class T>
+static T d2h1(Ctx &c, const T *src) {
+  T v;
+  CK(cudaMemcpyAsync(&v, src, sizeof(T), cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  return v;
+}
+#define LAUNCH(kernel, n, ...)                                                   \
+  do {                                                                           \
+    long n_ = (n);                                                               \
+    if (n_ > 0) {                                                                \
+      kernel<<<nblk(n_), CTA, 0, c.stream>>>(__VA_ARGS__);                       \
+      c.launches++;                                                              \
+      CK(cudaGetLastError());                                                    \
+    }                                                                            \
+  } while (0)
+
+// exclusive scan of n ints into out[0..n] (out[n] = total); returns total
+static long scan_ex(Ctx &c, const int *in, int *out, long n) {
+  size_t tmp = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, (int)n + 1, c.stream));
+  void *t = c.alloc<char>(tmp);
+  // in[n] must exist: callers allocate n+1 and set in[n] = 0
+  CK(cub::DeviceScan::ExclusiveSum(t, tmp, in, out, (int)n + 1, c.stream));
+  int tot = d2h1(c, out + n);
+  c.release(t);
+  return tot;
+}
+
+// stable sort of (key, val) int pairs
+static void sort_pairs(Ctx &c, const int *kin, int *kout, const int *vin, int *vout, long n) {
+  if (n == 0) return;
+  size_t tmp = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, vout, (int)n, 0, 32, c.stream));
+  void *t = c.alloc<char>(tmp);
+  CK(cub::DeviceRadixSort::SortPairs(t, tmp, kin, kout, vin, vout, (int)n, 0, 32, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  c.release(t);
+}
+
+__global__ void k_gather_int(long n, const int *perm, const int *src, int *dst) {
+  long e = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (e < n) dst[e] = src[perm[e]];
+}
+__global__ void k_count_valid(long n, const int *key, int nkeys, int *cnt) {
+  long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (i < n && key[i] < nkeys) atomicAdd(&cnt[key[i]], 1);
+}
+__global__ void k_iota(long n, int *a) {
+  long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (i < n) a[i] = (int)i;
+}
+__global__ void k_fill_int(long n, int *a, int v) {
+  long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (i < n) a[i] = v;
+}
+__global__ void k_rowof(int nrows, const int *ptr, int *rowof) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nrows)
+    for (int e = ptr[i]; e < ptr[i + 1]; e++) rowof[e] = i;
+}
+__global__ void k_count_keys(long n, const int *key, int *cnt) {
+  long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (i < n) atomicAdd(&cnt[key[i]], 1);
+}
+
+__device__ __forceinline__ int bsearch_int(const int *a, int lo, int hi, int key) {  // [lo, hi)
+  hi -= 1;
+  while (lo <= hi) {
+    int mid = (lo + hi) >> 1;
+    int v = a[mid];
+    if (v == key) return mid;
+    if (v < key) lo = mid + 1; else hi = mid - 1;
+  }
+  return -1;
+}
+
+// insert into a sorted unique local list; returns false on overflow
+__device__ __forceinline__ bool insert_unique(int *list, int &cnt, int cap, int v) {
+  int lo = 0, hi = cnt - 1;
+  while (lo <= hi) {
+    int mid = (lo + hi) >> 1;
+    if (list[mid] == v) return true;
+    if (list[mid] < v) lo = mid + 1; else hi = mid - 1;
+  }
+  if (cnt >= cap) return false;
+  for (int q = cnt; q > lo; q--) list[q] = list[q - 1];
+  list[lo] = v;
+  cnt++;
+  return true;
+}
+
+// ------------------------------------------------------------------ input checks
+__global__ void k_check_finite(long n, const double *v, int *err, int code) {
+  long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (i < n && !isfinite(v[i])) raise_err(err, code, (int)i);
+}
+__global__ void k_check_pos(long n, const double *v, int *err) {
+  long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (i < n && !(v[i] > 0.0)) raise_err(err, DERR_DOMAIN, (int)i);
+}
+
+// ------------------------------------------------------------------ s1: S = K + J^T D J
+constexpr int SCAP = 96;
+
+__device__ int contact_nodes(int I, const int *Jt_ptr, const int *Jt_row, const int *J_ptr, const int *J_col,
+                             int *list, int *err) {
+  int cnt = 0;
+  for (int r = 0; r < 3; r++) {
+    const int p = 3 * I + r;
+    for (int t = Jt_ptr[p]; t < Jt_ptr[p + 1]; t++) {
+      const int k = Jt_row[t];
+      for (int f = J_ptr[k]; f < J_ptr[k + 1]; f++)
+        if (!insert_unique(list, cnt, SCAP, J_col[f] / 3)) { raise_err(err, DERR_LIMIT, I); return cnt; }
+    }
+  }
+  return cnt;
+}
+
+__global__ void k_S_count(int nodes, const int *K_ptr, const int *K_col, const int *Jt_ptr, const int *Jt_row,
+                          const int *J_ptr, const int *J_col, int *cnt, int *err) {
+  int I = blockIdx.x * blockDim.x + threadIdx.x;
+  if (I >= nodes) return;
+  int list[SCAP];
+  int nl = contact_nodes(I, Jt_ptr, Jt_row, J_ptr, J_col, list, err);
+  int a = K_ptr[I], ae = K_ptr[I + 1], b = 0, u = 0;
+  while (a < ae || b < nl) {
+    if (b >= nl || (a < ae && K_col[a] < list[b])) a++;
+    else if (a >= ae || list[b] < K_col[a]) b++;
+    else { a++; b++; }
+    u++;
+  }
+  cnt[I] = u;
+}
+
+__global__ void k_S_fill(int nodes, const int *K_ptr, const int *K_col, const int *Jt_ptr, const int *Jt_row,
+                         const int *J_ptr, const int *J_col, const int *S_ptr, int *S_col, int *S_kblk, int *err) {
+  int I = blockIdx.x * blockDim.x + threadIdx.x;
+  if (I >= nodes) return;
+  int list[SCAP];
+  int nl = contact_nodes(I, Jt_ptr, Jt_row, J_ptr, J_col, list, err);
+  int a = K_ptr[I], ae = K_ptr[I + 1], b = 0, w = S_ptr[I];
+  while (a < ae || b < nl) {
+    if (b >= nl || (a < ae && K_col[a] < list[b])) { S_col[w] = K_col[a]; S_kblk[w] = a; a++; }
+    else if (a >= ae || list[b] < K_col[a]) { S_col[w] = list[b]; S_kblk[w] = -1; b++; }
+    else { S_col[w] = K_col[a]; S_kblk[w] = a; a++; b++; }
+    w++;
+  }
+}
+
+// one thread per S block: C1
+__global__ void k_S_values(long nnzb, const int *S_rowof, const int *S_col, const int *S_kblk, const double *K_val,
+                           const int *Jt_ptr, const int *Jt_row, const double *Jt_val, const double *D, double *S_val) {
+  long e = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (e >= nnzb) return;
+  const int I = S_rowof[e], Jn = S_col[e], kb = S_kblk[e];
+  for (int r = 0; r < 3; r++)
+    for (int cc = 0; cc < 3; cc++) {
+      const int p = 3 * I + r, q = 3 * Jn + cc;
+      double acc = kb >= 0 ? K_val[(long)kb * 9 + 3 * r + cc] : 0.0;
+      int a = Jt_ptr[p], ae = Jt_ptr[p + 1], b = Jt_ptr[q], be = Jt_ptr[q + 1];
+      while (a < ae && b < be) {
+        const int ka = Jt_row[a], kb2 = Jt_row[b];
+        if (ka < kb2) a++;
+        else if (ka > kb2) b++;
+        else {
+          const double t = Jt_val[a] * D[ka];
+          acc = __fma_rn(t, Jt_val[b], acc);
+          a++; b++;
+        }
+      }
+      S_val[e * 9 + 3 * r + cc] = acc;
+    }
+}
+
+// ------------------------------------------------------------------ s2: I_c and Z
+__global__ void k_mark_cols(int nnz, const int *J_col, int *mark) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < nnz) mark[J_col[e]] = 1;
+}
+__global__ void k_check_Z(int nc, long n, const int *Z, const int *mark, int *pos, int *err) {
+  int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= nc) return;
+  const int p = Z[a];
+  if (p < 0 || p >= n || !mark[p]) { raise_err(err, DERR_ARG, a); return; }
+  if (atomicCAS(&pos[p], -1, a) != -1) raise_err(err, DERR_ARG, a);
+}
+__global__ void k_compact_Z(long n, const int *mark, const int *off, int *Z, int *pos) {
+  long p = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (p < n && mark[p]) { Z[off[p]] = (int)p; pos[p] = off[p]; }
+}
+
+// ------------------------------------------------------------------ s3: A_w band and Cholesky
+__global__ void k_band_start(int nc, const int *Z, const int *pos, const int *S_ptr, const int *S_col, int *bwmax) {
+  int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= nc) return;
+  const int I = Z[a] / 3;
+  int mn = a;
+  for (int k = S_ptr[I]; k < S_ptr[I + 1]; k++)
+    for (int cc = 0; cc < 3; cc++) {
+      const int b = pos[3 * S_col[k] + cc];
+      if (b >= 0 && b < mn) mn = b;
+    }
+  atomicMax(bwmax, a - mn);
+}
+__global__ void k_band_fill(int nc, int bw, int W, const int *Z, const int *pos, const int *S_ptr, const int *S_col,
+                            const double *S_val, double *Lrow) {
+  int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= nc) return;
+  const int p = Z[a], I = p / 3, r = p % 3;
+  for (int k = S_ptr[I]; k < S_ptr[I + 1]; k++)
+    for (int cc = 0; cc < 3; cc++) {
+      const int b = pos[3 * S_col[k] + cc];
+      if (b >= 0 && b <= a && a - b <= bw) Lrow[(long)a * W + bw - (a - b)] = S_val[(long)k * 9 + 3 * r + cc];
+    }
+}
+
+// Right-looking banded Cholesky in place (C9): entry (i,l) receives fma(-L_ij, L_lj, .) for j ascending,
+// which is exactly the left-looking chain of the contract.  One CTA.
+__global__ void __launch_bounds__(1024) k_band_chol(int n, int bw, int W, double *L, int *err, int tag) {
+  __shared__ double piv;
+  __shared__ int bad;
+  const int tid = threadIdx.x;
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  for (int j = 0; j < n; j++) {
+    if (tid == 0) {
+      double d = L[(long)j * W + bw];
+      if (!(d > 0.0)) { raise_err(err, DERR_NOT_SPD, tag * 1000000 + j); bad = 1; }
+      double s = sqrt(d);
+      L[(long)j * W + bw] = s;
+      piv = s;
+    }
+    __syncthreads();
+    if (bad) return;
+    const double ljj = piv;
+    const int rmax = min(bw, n - 1 - j);
+    for (int t = 1 + tid; t <= rmax; t += blockDim.x) {
+      const long ix = (long)(j + t) * W + bw - t;
+      L[ix] = L[ix] / ljj;
+    }
+    __syncthreads();
+    const long pairs = (long)rmax * rmax;
+    for (long q = tid; q < pairs; q += blockDim.x) {
+      const int u = (int)(q / rmax) + 1, v = (int)(q % rmax) + 1;  // i = j+u, l = j+v
+      if (v > u) continue;
+      const double lij = L[(long)(j + u) * W + bw - u];
+      const double llj = L[(long)(j + v) * W + bw - v];
+      const long ix = (long)(j + u) * W + bw - (u - v);
+      L[ix] = __fma_rn(-lij, llj, L[ix]);
+    }
+    __syncthreads();
+  }
+}
+// dinv = 1/L_ii and the column-major copy of the band
+__global__ void k_band_finish(int n, int bw, int W, const double *Lrow, double *Lcol, double *dinv) {
+  long q = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (q >= (long)n * (bw + 1)) return;
+  const int i = (int)(q / (bw + 1)), t = (int)(q % (bw + 1));  // L_{i, i-t}
+  const int k = i - t;
+  if (k < 0) return;
+  const double v = Lrow[(long)i * W + bw - t];
+  Lcol[(long)k * W + t] = v;
+  if (t == 0) dinv[i] = 1.0 / v;
+}
+
+// thin residual structure: per scalar row p, entries of S with column in Z, ascending column
+__global__ void k_thin_count(long n, const int *S_ptr, const int *S_col, const int *pos, int *cnt) {
+  long p = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int I = (int)(p / 3);
+  int c0 = 0;
+  for (int k = S_ptr[I]; k < S_ptr[I + 1]; k++)
+    for (int cc = 0; cc < 3; cc++) c0 += pos[3 * S_col[k] + cc] >= 0;
+  cnt[p] = c0;
+}
+__global__ void k_thin_fill(long n, const int *S_ptr, const int *S_col, const int *pos, const int *off,
+                            const int *rowflag_off, int *thin_row, int *thin_ptr, int *thin_pos, int *thin_src) {
+  long p = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int I = (int)(p / 3), r = (int)(p % 3);
+  int w = off[p];
+  if (off[p + 1] == w) return;
+  const int t = rowflag_off[p];
+  thin_row[t] = (int)p;
+  thin_ptr[t] = w;
+  for (int k = S_ptr[I]; k < S_ptr[I + 1]; k++)
+    for (int cc = 0; cc < 3; cc++) {
+      const int b = pos[3 * S_col[k] + cc];
+      if (b >= 0) { thin_pos[w] = b; thin_src[w] = k * 9 + 3 * r + cc; w++; }
+    }
+}
+__global__ void k_flag_nonzero(long n, const int *cnt, int *flag) {
+  long p = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (p < n) flag[p] = cnt[p] > 0;
+}
+__global__ void k_gather_vals(long n, const int *src, const double *from, double *to) {
+  long e = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (e < n) to[e] = src[e] >= 0 ? from[src[e]] : 0.0;
+}
+
+// ------------------------------------------------------------------ s8: diagonals (C3)
+__global__ void k_diag(int nodes, int b, const int *ptr, const int *col, const double *val, double *dl1, double *dpt) {
+  long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (t >= (long)nodes * b) return;
+  const int i = (int)(t / b), r = (int)(t % b);
+  double d = 0.0, dp = 0.0;
+  for (int k = ptr[i]; k < ptr[i + 1]; k++)
+    for (int cc = 0; cc < b; cc++) {
+      const double a = val[(long)k * b * b + r * b + cc];
+      d = d + fabs(a);
+      if (col[k] == i && cc == r) dp = a;
+    }
+  dl1[t] = d;
+  dpt[t] = dp;
+}
+
+// ------------------------------------------------------------------ s4: components and aggregation
+__global__ void k_cc_step(int nodes, const int *ptr, const int *col, int *lab, int *changed) {
+  int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nodes) return;
+  int m = lab[v];
+  for (int k = ptr[v]; k < ptr[v + 1]; k++) m = min(m, lab[col[k]]);
+  int l2 = lab[m];
+  m = min(m, l2);
+  if (m < lab[v]) { atomicMin(&lab[v], m); *changed = 1; }
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ bool better(int u, int v, uint64_t seed) {  // u beats v (v may be -1)
+  if (u < 0) return false;
+  if (v < 0) return true;
+  uint64_t pu = mix64((uint64_t)(uint32_t)u ^ seed), pv = mix64((uint64_t)(uint32_t)v ^ seed);
+  return pu > pv || (pu == pv && u < v);
+}
+
+enum { ST_UND = 0, ST_ROOT = 1, ST_OUT = 2, ST_ISO = 3 };
+
+__global__ void k_mis_init(int nodes, const int *ptr, const int *col, const int *comp, int *state) {
+  int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nodes) return;
+  int iso = 1;
+  for (int k = ptr[v]; k < ptr[v + 1]; k++) {
+    const int u = col[k];
+    if (u != v && comp[u] == comp[v]) { iso = 0; break; }
+  }
+  state[v] = iso ? ST_ISO : ST_UND;
+}
+// m_out[v] = best over N[v] of (m_in[u]) ; with m_in = nullptr, candidates are undecided nodes themselves
+__global__ void k_mis_max(int nodes, const int *ptr, const int *col, const int *comp, const int *state,
+                          const int *m_in, int *m_out, uint64_t seed) {
+  int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nodes) return;
+  if (state[v] == ST_ISO) { m_out[v] = -1; return; }
+  int best = m_in ? m_in[v] : (state[v] == ST_UND ? v : -1);
+  for (int k = ptr[v]; k < ptr[v + 1]; k++) {
+    const int u = col[k];
+    if (u == v || comp[u] != comp[v]) continue;
+    const int cand = m_in ? m_in[u] : (state[u] == ST_UND ? u : -1);
+    if (better(cand, best, seed)) best = cand;
+  }
+  m_out[v] = best;
+}
+__global__ void k_mis_roots(int nodes, const int *m2, int *state) {
+  int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < nodes && state[v] == ST_UND && m2[v] == v) state[v] = ST_ROOT;
+}
+// flag[v] = 1 if a root (or, with f_in, a flagged node) lies in N[v]
+__global__ void k_mis_near(int nodes, const int *ptr, const int *col, const int *comp, const int *state,
+                           const int *f_in, int *f_out) {
+  int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nodes) return;
+  int f = f_in ? f_in[v] : (state[v] == ST_ROOT);
+  for (int k = ptr[v]; k < ptr[v + 1] && !f; k++) {
+    const int u = col[k];
+    if (u == v || comp[u] != comp[v]) continue;
+    f = f_in ? f_in[u] : (state[u] == ST_ROOT);
+  }
+  f_out[v] = f;
+}
+__global__ void k_mis_block(int nodes, const int *b2, int *state, int *undecided) {
+  int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nodes) return;
+  if (state[v] == ST_UND) {
+    if (b2[v]) state[v] = ST_OUT;
+    else atomicAdd(undecided, 1);
+  }
+}
+__global__ void k_root_flag(int nodes, const int *state, int *flag) {
+  int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < nodes) flag[v] = state[v] == ST_ROOT;
+}
+__global__ void k_agg_phase3(int nodes, const int *ptr, const int *col, const int *comp, const int *state,
+                             const int *rank, int *agg3) {
+  int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nodes) return;
+  int a = -1;
+  if (state[v] == ST_ROOT) a = rank[v];
+  else if (state[v] != ST_ISO)
+    for (int k = ptr[v]; k < ptr[v + 1]; k++) {
+      const int u = col[k];
+      if (u != v && comp[u] == comp[v] && state[u] == ST_ROOT) { a = rank[u]; break; }
+    }
+  agg3[v] = a;
+}
+__global__ void k_agg_leftover(int nodes, const int *ptr, const int *col, const int *comp, const int *state,
+                               const int *agg3, int *agg, int *err) {
+  int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nodes) return;
+  if (state[v] == ST_ISO || agg3[v] >= 0) { agg[v] = agg3[v]; return; }
+  int best = -1, bestc = 0;
+  for (int k = ptr[v]; k < ptr[v + 1]; k++) {
+    const int u = col[k];
+    if (u == v || comp[u] != comp[v]) continue;
+    const int a = agg3[u];
+    if (a < 0) continue;
+    int cnum = 0;
+    for (int k2 = ptr[v]; k2 < ptr[v + 1]; k2++) {
+      const int w2 = col[k2];
+      if (w2 != v && comp[w2] == comp[v] && agg3[w2] == a) cnum++;
+    }
+    if (cnum > bestc || (cnum == bestc && a < best)) { bestc = cnum; best = a; }
+  }
+  if (best < 0) raise_err(err, DERR_ARG, v);
+  agg[v] = best;
+}
+__global__ void k_agg_key(int nodes, const int *agg, int *key) {
+  int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < nodes) key[v] = agg[v] >= 0 ? agg[v] : 0x7fffffff;
+}
+__global__ void k_coarse_comp(int nodes, const int *state, const int *rank, const int *comp, int *comp_c) {
+  int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < nodes && state[v] == ST_ROOT) comp_c[rank[v]] = comp[v];
+}
+__global__ void k_is_agg(int nodes, const int *agg, int *flag) {
+  int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < nodes) flag[v] = agg[v] >= 0;
+}
+__global__ void k_Pt_cols(int nodes, const int *agg, const int *Pt_ptr, int *Pt_col) {
+  int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < nodes && agg[v] >= 0) Pt_col[Pt_ptr[v]] = agg[v];
+}
+
+// ------------------------------------------------------------------ s5: tentative prolongator (C17)
+__global__ void k_qr(int na, int b, const int *agg_ptr, const int *agg_nodes, const int *Pt_ptr, const double *Bnn,
+                     double *Ptv, double *Bc, int *err) {
+  int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= na) return;
+  const int m0 = agg_ptr[a], m1 = agg_ptr[a + 1];
+  auto Q = [&](int t, int r, int j) -> double & {
+    return Ptv[((long)Pt_ptr[agg_nodes[t]] * b + r) * 6 + j];
+  };
+  for (int t = m0; t < m1; t++)
+    for (int r = 0; r < b; r++)
+      for (int j = 0; j < 6; j++) Q(t, r, j) = Bnn[((long)agg_nodes[t] * b + r) * 6 + j];
+  double Rm[36];
+  for (int q = 0; q < 36; q++) Rm[q] = 0.0;
+  for (int j = 0; j < 6; j++) {
+    for (int i = 0; i < j; i++) {
+      double rij = 0.0;
+      for (int t = m0; t < m1; t++)
+        for (int r = 0; r < b; r++) rij = __fma_rn(Q(t, r, i), Q(t, r, j), rij);
+      Rm[i * 6 + j] = rij;
+      for (int t = m0; t < m1; t++)
+        for (int r = 0; r < b; r++) Q(t, r, j) = __fma_rn(-rij, Q(t, r, i), Q(t, r, j));
+    }
+    double ss = 0.0;
+    for (int t = m0; t < m1; t++)
+      for (int r = 0; r < b; r++) ss = __fma_rn(Q(t, r, j), Q(t, r, j), ss);
+    const double rjj = sqrt(ss);
+    if (!(rjj > 0.0) || (j > 0 && !(rjj > 1e-10 * Rm[0]))) { raise_err(err, DERR_RANK, a); return; }
+    Rm[j * 6 + j] = rjj;
+    for (int t = m0; t < m1; t++)
+      for (int r = 0; r < b; r++) Q(t, r, j) = Q(t, r, j) / rjj;
+  }
+  for (int q = 0; q < 36; q++) Bc[(long)a * 36 + q] = Rm[q];
+}
+
+// ------------------------------------------------------------------ s6: power iteration, smoothed P
+__global__ void k_pow_init(long n, double *v) {
+  long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (i < n) v[i] = 1.0 + (double)(i % 7) / 8.0;
+}
+__global__ void k_div(long n, double *w, const double *d) {
+  long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (i < n) w[i] = w[i] / d[i];
+}
+__global__ void k_scale_div(long n, const double *w, double s, double *v) {
+  long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (i < n) v[i] = w[i] / s;
+}
+
+constexpr int PCAP = 128;
+__global__ void k_P_count(int nodes, const int *ptr, const int *col, const int *agg, int *cnt, int *err) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nodes) return;
+  int list[PCAP];
+  int nl = 0;
+  for (int k = ptr[i]; k < ptr[i + 1]; k++) {
+    const int a = agg[col[k]];
+    if (a >= 0 && !insert_unique(list, nl, PCAP, a)) { raise_err(err, DERR_LIMIT, i); break; }
+  }
+  cnt[i] = nl;
+}
+__global__ void k_P_fill(int nodes, const int *ptr, const int *col, const int *agg, const int *P_ptr, int *P_col) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nodes) return;
+  int list[PCAP];
+  int nl = 0;
+  for (int k = ptr[i]; k < ptr[i + 1]; k++) {
+    const int a = agg[col[k]];
+    if (a >= 0) insert_unique(list, nl, PCAP, a);
+  }
+  for (int q = 0; q < nl; q++) P_col[P_ptr[i] + q] = list[q];
+}
+// P_ia = Pt_ia - (omega * T_ia) / dpt, T = A Pt (C19, C20); one thread per P block
+__global__ void k_P_values(long nnzb, int b, const int *P_rowof, const int *P_col, const int *A_ptr, const int *A_col,
+                           const double *A_val, const int *agg, const int *Pt_ptr, const double *Ptv,
+                           const double *dpt, double omega, double *Pv) {
+  long e = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (e >= nnzb) return;
+  const int i = P_rowof[e], a = P_col[e];
+  for (int r = 0; r < b; r++)
+    for (int s = 0; s < 6; s++) {
+      double acc = 0.0;
+      for (int k = A_ptr[i]; k < A_ptr[i + 1]; k++) {
+        const int j = A_col[k];
+        if (agg[j] != a) continue;
+        const double *Av = A_val + (long)k * b * b + r * b;
+        const double *Qj = Ptv + (long)Pt_ptr[j] * b * 6;
+        for (int cc = 0; cc < b; cc++) acc = __fma_rn(Av[cc], Qj[cc * 6 + s], acc);
+      }
+      double t = omega * acc;
+      t = t / dpt[(long)i * b + r];
+      const double pt = (agg[i] == a) ? Ptv[((long)Pt_ptr[i] * b + r) * 6 + s] : 0.0;
+      Pv[(e * b + r) * 6 + s] = pt - t;
+    }
+}
+
+// ------------------------------------------------------------------ s7: transpose, SpGEMMs, symmetrisation
+__global__ void k_transpose_vals(long nnzb, int br, int bc, const int *perm, const double *src, double *dst) {
+  long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (t >= nnzb) return;
+  const long s = perm[t];
+  for (int r = 0; r < br; r++)
+    for (int cc = 0; cc < bc; cc++) dst[(t * bc + cc) * br + r] = src[(s * br + r) * bc + cc];
+}
+
+constexpr int GCAP = 512;
+// symbolic C = A*B: row i's pattern = union of B rows over A's columns
+__global__ void k_spgemm_count(int nrows, const int *A_ptr, const int *A_col, const int *B_ptr, const int *B_col,
+                               int *cnt, int *err) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nrows) return;
+  int list[GCAP];
+  int nl = 0;
+  for (int k = A_ptr[i]; k < A_ptr[i + 1]; k++) {
+    const int j = A_col[k];
+    for (int k2 = B_ptr[j]; k2 < B_ptr[j + 1]; k2++)
+      if (!insert_unique(list, nl, GCAP, B_col[k2])) { raise_err(err, DERR_LIMIT, i); cnt[i] = nl; return; }
+  }
+  cnt[i] = nl;
+}
+__global__ void k_spgemm_fill(int nrows, const int *A_ptr, const int *A_col, const int *B_ptr, const int *B_col,
+                              const int *C_ptr, int *C_col) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nrows) return;
+  int list[GCAP];
+  int nl = 0;
+  for (int k = A_ptr[i]; k < A_ptr[i + 1]; k++) {
+    const int j = A_col[k];
+    for (int k2 = B_ptr[j]; k2 < B_ptr[j + 1]; k2++) insert_unique(list, nl, GCAP, B_col[k2]);
+  }
+  for (int q = 0; q < nl; q++) C_col[C_ptr[i] + q] = list[q];
+}
+// numeric C = A*B (C20): one warp per row, lane owns output-block entries e = lane + 32 h
+template <int BR, int IN, int BC>
+__global__ void k_spgemm_vals(int nrows, const int *A_ptr, const int *A_col, const double *A_val, const int *B_ptr,
+                              const int *B_col, const double *B_val, const int *C_ptr, const int *C_col,
+                              double *C_val) {
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= nrows) return;
+  constexpr int NE = BR * BC;
+  const int c0 = C_ptr[i], c1 = C_ptr[i + 1];
+  for (long q = (long)c0 * NE + lane; q < (long)c1 * NE; q += 32) C_val[q] = 0.0;
+  __syncwarp();
+  for (int k = A_ptr[i]; k < A_ptr[i + 1]; k++) {
+    const int j = A_col[k];
+    const double *Av = A_val + (long)k * BR * IN;
+    for (int k2 = B_ptr[j]; k2 < B_ptr[j + 1]; k2++) {
+      const int at = bsearch_int(C_col, c0, c1, B_col[k2]);
+      const double *Bv = B_val + (long)k2 * IN * BC;
+      double *Cv = C_val + (long)at * NE;
+      for (int e = lane; e < NE; e += 32) {
+        const int r = e / BC, s = e % BC;
+        double acc = Cv[e];
+        for (int t = 0; t < IN; t++) acc = __fma_rn(Av[r * IN + t], Bv[t * BC + s], acc);
+        Cv[e] = acc;
+      }
+    }
+  }
+}
+__global__ void k_sym(long nnzb, const int *rowof, const int *ptr, const int *col, const double *G, double *Ac,
+                      int *err) {
+  long e = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (e >= nnzb) return;
+  const int a = rowof[e], b2 = col[e];
+  const int kt = bsearch_int(col, ptr[b2], ptr[b2 + 1], a);
+  if (kt < 0) { raise_err(err, DERR_ARG, (int)e); return; }
+  for (int r = 0; r < 6; r++)
+    for (int s = 0; s < 6; s++) Ac[e * 36 + r * 6 + s] = 0.5 * (G[e * 36 + r * 6 + s] + G[(long)kt * 36 + s * 6 + r]);
+}
+
+// ------------------------------------------------------------------ SELL-32 packing
+__global__ void k_row_len(int nrows, const int *ptr, int *len) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nrows) len[i] = ptr[i + 1] - ptr[i];
+}
+__global__ void k_slice_width(int nslices, int nrows, const int *len, int *width) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nslices) return;
+  int w = 0;
+  for (int l = 0; l < 32; l++) {
+    int i = 32 * s + l;
+    if (i < nrows) w = max(w, len[i]);
+  }
+  width[s] = w;
+}
+__global__ void k_sell_pack(int nrows, int BB, const int *ptr, const int *col, const int *slice_ptr,
+                            int *scol, int *ssrc) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nrows) return;
+  const int lane = i & 31;
+  const long base = slice_ptr[i >> 5];
+  const int w = slice_ptr[(i >> 5) + 1] - slice_ptr[i >> 5];
+  const int len = ptr[i + 1] - ptr[i];
+  for (int s = 0; s < w; s++) {
+    const long slot = base + s;
+    if (s < len) { scol[slot * 32 + lane] = col[ptr[i] + s]; ssrc[slot * 32 + lane] = ptr[i] + s; }
+    else { scol[slot * 32 + lane] = 0; ssrc[slot * 32 + lane] = -1; }
+  }
+}
+__global__ void k_sell_vals(long nslots, int BB, const int *ssrc, const double *val, double *sval) {
+  long q = blockIdx.x * (long)blockDim.x + threadIdx.x;  // q = slot*32 + lane
+  if (q >= nslots * 32) return;
+  const long slot = q >> 5;
+  const int lane = (int)(q & 31);
+  const int src = ssrc[q];
+  for (int e = 0; e < BB; e++) sval[(slot * BB + e) * 32 + lane] = src >= 0 ? val[(long)src * BB + e] : 0.0;
+}
+
+// ------------------------------------------------------------------ coarsest dense operator
+__global__ void k_dense_band(int nodes, int b, const int *ptr, const int *col, const double *val, int n, int W,
+                             double *Lrow) {
+  long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (t >= (long)nodes * b) return;
+  const int i = (int)(t / b), r = (int)(t % b);
+  const int row = i * b + r, bw = n - 1;
+  for (int k = ptr[i]; k < ptr[i + 1]; k++)
+    for (int cc = 0; cc < b; cc++) {
+      const int cidx = col[k] * b + cc;
+      if (cidx <= row) Lrow[(long)row * W + bw - (row - cidx)] = val[(long)k * b * b + r * b + cc];
+    }
+}
+
+// =================================================================== host orchestration
+static void bsr_alloc(Ctx &c, Bsr &A, int nbr, int nbc, int br, int bc, long nnzb) {
+  A.nbr = nbr; A.nbc = nbc; A.br = br; A.bc = bc; A.nnzb = nnzb;
+  A.ptr = c.alloc<int>(nbr + 1);
+  A.col = c.alloc<int>(nnzb);
+  A.val = c.alloc<double>(nnzb * br * bc);
+}
+
+static int *rowof(Ctx &c, const Bsr &A) {
+  int *r = c.alloc<int>(A.nnzb);
+  LAUNCH(k_rowof, A.nbr, A.nbr, A.ptr, r);
+  return r;
+}
+
+void build_sell(Ctx &c, const Bsr &A, Sell &S, bool alloc) {
+  const int BB = A.br * A.bc;
+  if (alloc) {
+    S.nrows = A.nbr; S.br = A.br; S.bc = A.bc;
+    S.nslices = (A.nbr + 31) / 32;
+    S.rowlen = c.alloc<int>(A.nbr);
+    LAUNCH(k_row_len, A.nbr, A.nbr, A.ptr, S.rowlen);
+    int *width = c.alloc<int>(S.nslices + 1);
+    CK(cudaMemsetAsync(width, 0, (S.nslices + 1) * sizeof(int), c.stream));
+    LAUNCH(k_slice_width, S.nslices, S.nslices, A.nbr, S.rowlen, width);
+    S.slice_ptr = c.alloc<int>(S.nslices + 1);
+    S.nslots = scan_ex(c, width, S.slice_ptr, S.nslices);
+    c.release(width);
+    S.col = c.alloc<int>(S.nslots * 32);
+    S.src = c.alloc<int>(S.nslots * 32);
+    S.val = c.alloc<double>(S.nslots * 32 * BB);
+    LAUNCH(k_sell_pack, A.nbr, A.nbr, BB, A.ptr, A.col, S.slice_ptr, S.col, S.src);
+  }
+  LAUNCH(k_sell_vals, S.nslots * 32, S.nslots, BB, S.src, A.val, S.val);
+}
+
+static void band_alloc(Ctx &c, int n, int bw, double *&Lrow, double *&Lcol, double *&dinv) {
+  const int W = band_stride(bw);
+  const size_t total = (size_t)(n + 2 * BAND_PAD_ROWS) * W;
+  double *r = c.alloc<double>(total), *cl = c.alloc<double>(total);
+  CK(cudaMemsetAsync(r, 0, total * sizeof(double), c.stream));
+  CK(cudaMemsetAsync(cl, 0, total * sizeof(double), c.stream));
+  Lrow = r + (size_t)BAND_PAD_ROWS * W;
+  Lcol = cl + (size_t)BAND_PAD_ROWS * W;
+  dinv = c.alloc<double>(n);
+}
+
+static void band_factor(Ctx &c, int n, int bw, double *Lrow, double *Lcol, double *dinv, int tag) {
+  const int W = band_stride(bw);
+  k_band_chol<<<1, 1024, 0, c.stream>>>(n, bw, W, Lrow, c.err, tag);
+  c.launches++;
+  CK(cudaGetLastError());
+  LAUNCH(k_band_finish, (long)n * (bw + 1), n, bw, W, Lrow, Lcol, dinv);
+}
+
+// --------------------------------------------------------------- numeric pieces (reused by update_D)
+struct SetupCache {  // per-context arrays needed for numeric re-setup
+  int *S_rowof = nullptr;
+  int *band_src = nullptr;
+  long band_nnz = 0;
+};
+
+static void S_numeric(Ctx &c, const int *S_rowof) {
+  Level &L0 = c.lev[0];
+  LAUNCH(k_S_values, L0.A.nnzb, L0.A.nnzb, S_rowof, L0.A.col, c.S_kblk, c.K.val, c.Jt_ptr, c.Jt_row, c.Jt_val, c.D,
+         L0.A.val);
+}
+
+static void filter_numeric(Ctx &c) {
+  if (c.nc == 0) return;
+  Level &L0 = c.lev[0];
+  const int W = band_stride(c.bw);
+  CK(cudaMemsetAsync(c.Lrow - (size_t)BAND_PAD_ROWS * W, 0, (size_t)(c.nc + 2 * BAND_PAD_ROWS) * W * sizeof(double),
+                     c.stream));
+  LAUNCH(k_band_fill, c.nc, c.nc, c.bw, W, c.Z, c.pos, L0.A.ptr, L0.A.col, L0.A.val, c.Lrow);
+  band_factor(c, c.nc, c.bw, c.Lrow, c.Lcol, c.Ldinv, 1);
+}
+
+static void thin_numeric(Ctx &c, long nthin_nnz) {
+  LAUNCH(k_gather_vals, nthin_nnz, nthin_nnz, c.thin_src, c.lev[0].A.val, c.thin_val);
+}
+
+static void power_iteration(Ctx &c, Level &L) {
+  double *v = c.alloc<double>(L.n), *w = c.alloc<double>(L.n);
+  LAUNCH(k_pow_init, L.n, L.n, v);
+  double lam = 0.0;
+  for (int it = 0; it < c.cfg.power_iters; it++) {
+    launch_bsr_spmv(c, L.A, v, w);
+    LAUNCH(k_div, L.n, L.n, w, L.dpt);
+    launch_dot(c, L.n, L.b, w, w, DOT_PLAIN);
+    double ww = d2h1(c, &c.sc->dot);
+    launch_dot(c, L.n, L.b, v, v, DOT_PLAIN);
+    double vv = d2h1(c, &c.sc->dot);
+    double nw = sqrt(ww), nv = sqrt(vv);
+    lam = nw / nv;
+    LAUNCH(k_scale_div, L.n, L.n, w, nw, v);
+  }
+  L.lambda = lam;
+  L.omega = 4.0 / (3.0 * lam);
+  c.release(v);
+  c.release(w);
+}
+
+// per-level cached arrays for numeric re-setup
+struct LevelCache {
+  int *P_rowof = nullptr, *R_perm = nullptr, *G_rowof = nullptr;
+  Bsr G;
+};
+
+static void level_numeric(Ctx &c, int l, LevelCache &lc) {
+  Level &L = c.lev[l];
+  Level &Lc = c.lev[l + 1];
+  power_iteration(c, L);
+  LAUNCH(k_P_values, L.P.nnzb, L.P.nnzb, L.b, lc.P_rowof, L.P.col, L.A.ptr, L.A.col, L.A.val, L.agg, L.Pt.ptr, L.Pt.val,
+         L.dpt, L.omega, L.P.val);
+  LAUNCH(k_transpose_vals, L.R.nnzb, L.R.nnzb, L.b, 6, lc.R_perm, L.P.val, L.R.val);
+  // AP = A * P
+  {
+    long threads = (long)L.A.nbr * 32;
+    if (L.b == 3)
+      k_spgemm_vals<3, 3, 6><<<nblk(threads), CTA, 0, c.stream>>>(L.A.nbr, L.A.ptr, L.A.col, L.A.val, L.P.ptr, L.P.col,
+                                                                  L.P.val, L.AP.ptr, L.AP.col, L.AP.val);
+    else
+      k_spgemm_vals<6, 6, 6><<<nblk(threads), CTA, 0, c.stream>>>(L.A.nbr, L.A.ptr, L.A.col, L.A.val, L.P.ptr, L.P.col,
+                                                                  L.P.val, L.AP.ptr, L.AP.col, L.AP.val);
+    c.launches++;
+    CK(cudaGetLastError());
+  }
+  // G = R * AP
+  {
+    long threads = (long)L.R.nbr * 32;
+    if (L.b == 3)
+      k_spgemm_vals<6, 3, 6><<<nblk(threads), CTA, 0, c.stream>>>(L.R.nbr, L.R.ptr, L.R.col, L.R.val, L.AP.ptr,
+                                                                  L.AP.col, L.AP.val, lc.G.ptr, lc.G.col, lc.G.val);
+    else
+      k_spgemm_vals<6, 6, 6><<<nblk(threads), CTA, 0, c.stream>>>(L.R.nbr, L.R.ptr, L.R.col, L.R.val, L.AP.ptr,
+                                                                  L.AP.col, L.AP.val, lc.G.ptr, lc.G.col, lc.G.val);
+    c.launches++;
+    CK(cudaGetLastError());
+  }
+  LAUNCH(k_sym, lc.G.nnzb, lc.G.nnzb, lc.G_rowof, lc.G.ptr, lc.G.col, lc.G.val, Lc.A.val, c.err);
+  LAUNCH(k_diag, (long)Lc.nodes * Lc.b, Lc.nodes, Lc.b, Lc.A.ptr, Lc.A.col, Lc.A.val, Lc.dl1, Lc.dpt);
+}
+
+static void coarsest_numeric(Ctx &c) {
+  Level &L = c.lev[c.nlev - 1];
+  const int n = c.nco, bw = n - 1, W = band_stride(bw);
+  CK(cudaMemsetAsync(c.Lc_row - (size_t)BAND_PAD_ROWS * W, 0, (size_t)(n + 2 * BAND_PAD_ROWS) * W * sizeof(double),
+                     c.stream));
+  LAUNCH(k_dense_band, (long)L.nodes * L.b, L.nodes, L.b, L.A.ptr, L.A.col, L.A.val, n, W, c.Lc_row);
+  band_factor(c, n, bw, c.Lc_row, c.Lc_col, c.Lc_dinv, 2);
+}
+
+// per-context arrays needed by the numeric re-setup (owned by Ctx::setup_cache)
+struct Caches {
+  SetupCache s;
+  LevelCache lc[MAXLEV];
+  long thin_nnz = 0;
+};
+static Caches &caches(Ctx &c) {
+  if (!c.setup_cache) c.setup_cache = new Caches();
+  return *static_cast<Caches *>(c.setup_cache);
+}
+void drop_caches(Ctx &c) {
+  delete static_cast<Caches *>(c.setup_cache);
+  c.setup_cache = nullptr;
+}
+
+// =================================================================== setup_all
+void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, const int *J_ptr, const int *J_col,
+               const double *J_val, const double *D, const int *Zin, int nc_in, const double *B_nns) {
+  Caches &C = caches(c);
+  const int nodes = c.nodes;
+  const long n = c.n;
+  const int m = c.m;
+  // ---- copy inputs
+  int nnzbK = 0, nnzJ = 0;
+  CK(cudaMemcpyAsync(&nnzbK, K_ptr + nodes, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  if (m > 0) CK(cudaMemcpyAsync(&nnzJ, J_ptr + m, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  REQUIRE(nnzbK > 0, AMGF_ERR_ARG, "K has no blocks");
+  c.nnzJ = nnzJ;
+  bsr_alloc(c, c.K, nodes, nodes, 3, 3, nnzbK);
+  d2d(c, c.K.ptr, K_ptr, nodes + 1);
+  d2d(c, c.K.col, K_col, nnzbK);
+  d2d(c, c.K.val, K_val, (size_t)nnzbK * 9);
+  c.J_ptr = c.alloc<int>(m + 1);
+  c.J_col = c.alloc<int>(nnzJ);
+  c.J_val = c.alloc<double>(nnzJ);
+  c.D = c.alloc<double>(m);
+  if (m > 0) {
+    d2d(c, c.J_ptr, J_ptr, m + 1);
+    d2d(c, c.J_col, J_col, nnzJ);
+    d2d(c, c.J_val, J_val, nnzJ);
+    d2d(c, c.D, D, m);
+  } else {
+    CK(cudaMemsetAsync(c.J_ptr, 0, sizeof(int), c.stream));
+  }
+  LAUNCH(k_check_finite, (long)nnzbK * 9, (long)nnzbK * 9, c.K.val, c.err, DERR_NONFINITE);
+  LAUNCH(k_check_finite, nnzJ, nnzJ, c.J_val, c.err, DERR_NONFINITE);
+  LAUNCH(k_check_finite, m, m, c.D, c.err, DERR_NONFINITE);
+  LAUNCH(k_check_pos, m, m, c.D, c.err);
+  check_dev_error(c, "input check");
+
+  // ---- J^T
+  {
+    int *rowJ = c.alloc<int>(nnzJ), *keys = c.alloc<int>(nnzJ), *idx = c.alloc<int>(nnzJ), *perm = c.alloc<int>(nnzJ);
+    LAUNCH(k_rowof, m, m, c.J_ptr, rowJ);
+    LAUNCH(k_iota, nnzJ, nnzJ, idx);
+    sort_pairs(c, c.J_col, keys, idx, perm, nnzJ);
+    int *cnt = c.alloc<int>(n + 1);
+    CK(cudaMemsetAsync(cnt, 0, (n + 1) * sizeof(int), c.stream));
+    LAUNCH(k_count_keys, nnzJ, nnzJ, c.J_col, cnt);
+    c.Jt_ptr = c.alloc<int>(n + 1);
+    scan_ex(c, cnt, c.Jt_ptr, n);
+    c.Jt_row = c.alloc<int>(nnzJ);
+    c.Jt_val = c.alloc<double>(nnzJ);
+    // Jt_row[t] = rowJ[perm[t]], Jt_val[t] = J_val[perm[t]]
+    LAUNCH(k_gather_int, nnzJ, nnzJ, perm, rowJ, c.Jt_row);
+    LAUNCH(k_gather_vals, nnzJ, nnzJ, perm, c.J_val, c.Jt_val);
+    c.release(rowJ); c.release(keys); c.release(idx); c.release(perm); c.release(cnt);
+  }
+
+  // ---- s1: S pattern and values
+  Level &L0 = c.lev[0];
+  L0.b = 3; L0.nodes = nodes; L0.n = n;
+  {
+    int *cnt = c.alloc<int>(nodes + 1);
+    CK(cudaMemsetAsync(cnt, 0, (nodes + 1) * sizeof(int), c.stream));
+    LAUNCH(k_S_count, nodes, nodes, c.K.ptr, c.K.col, c.Jt_ptr, c.Jt_row, c.J_ptr, c.J_col, cnt, c.err);
+    check_dev_error(c, "S pattern");
+    L0.A.ptr = c.alloc<int>(nodes + 1);
+    long nnzb = scan_ex(c, cnt, L0.A.ptr, nodes);
+    c.release(cnt);
+    L0.A.nbr = L0.A.nbc = nodes; L0.A.br = L0.A.bc = 3; L0.A.nnzb = nnzb;
+    L0.A.col = c.alloc<int>(nnzb);
+    L0.A.val = c.alloc<double>(nnzb * 9);
+    c.S_kblk = c.alloc<int>(nnzb);
+    LAUNCH(k_S_fill, nodes, nodes, c.K.ptr, c.K.col, c.Jt_ptr, c.Jt_row, c.J_ptr, c.J_col, L0.A.ptr, L0.A.col,
+           c.S_kblk, c.err);
+    C.s.S_rowof = rowof(c, L0.A);
+    S_numeric(c, C.s.S_rowof);
+  }
+
+  // ---- s2: I_c, Z
+  {
+    int *mark = c.alloc<int>(n + 1);
+    CK(cudaMemsetAsync(mark, 0, (n + 1) * sizeof(int), c.stream));
+    LAUNCH(k_mark_cols, nnzJ, nnzJ, c.J_col, mark);
+    c.pos = c.alloc<int>(n);
+    CK(cudaMemsetAsync(c.pos, 0xff, n * sizeof(int), c.stream));
+    int *off = c.alloc<int>(n + 1);
+    long nmark = scan_ex(c, mark, off, n);
+    if (Zin) {
+      REQUIRE(nc_in == nmark, AMGF_ERR_ARG, "Z is not the column support of J (size " + std::to_string(nc_in) +
+                                                " vs " + std::to_string(nmark) + ")");
+      c.nc = nc_in;
+      c.Z = c.alloc<int>(c.nc);
+      d2d(c, c.Z, Zin, c.nc);
+      LAUNCH(k_check_Z, c.nc, c.nc, n, c.Z, mark, c.pos, c.err);
+      check_dev_error(c, "Z is not a permutation of the column support of J");
+    } else {
+      c.nc = (int)nmark;
+      c.Z = c.alloc<int>(c.nc);
+      LAUNCH(k_compact_Z, n, n, mark, off, c.Z, c.pos);
+    }
+    c.release(mark);
+    c.release(off);
+  }
+
+  // ---- s3: A_w band, factor, thin residual
+  if (c.nc > 0) {
+    int *bwd = c.alloc<int>(1);
+    CK(cudaMemsetAsync(bwd, 0, sizeof(int), c.stream));
+    LAUNCH(k_band_start, c.nc, c.nc, c.Z, c.pos, L0.A.ptr, L0.A.col, bwd);
+    c.bw = d2h1(c, bwd);
+    c.release(bwd);
+    band_alloc(c, c.nc, c.bw, c.Lrow, c.Lcol, c.Ldinv);
+    c.fv = c.alloc<double>(c.nc);
+    filter_numeric(c);
+    check_dev_error(c, "A_w Cholesky");
+    // thin structure
+    int *cnt = c.alloc<int>(n + 1), *off = c.alloc<int>(n + 1), *flag = c.alloc<int>(n + 1), *foff = c.alloc<int>(n + 1);
+    CK(cudaMemsetAsync(cnt, 0, (n + 1) * sizeof(int), c.stream));
+    CK(cudaMemsetAsync(flag, 0, (n + 1) * sizeof(int), c.stream));
+    LAUNCH(k_thin_count, n, n, L0.A.ptr, L0.A.col, c.pos, cnt);
+    long tnnz = scan_ex(c, cnt, off, n);
+    LAUNCH(k_flag_nonzero, n, n, cnt, flag);
+    c.nthin = (int)scan_ex(c, flag, foff, n);
+    c.thin_row = c.alloc<int>(c.nthin);
+    c.thin_ptr = c.alloc<int>(c.nthin + 1);
+    c.thin_pos = c.alloc<int>(tnnz);
+    c.thin_src = c.alloc<int>(tnnz);
+    c.thin_val = c.alloc<double>(tnnz);
+    LAUNCH(k_thin_fill, n, n, L0.A.ptr, L0.A.col, c.pos, off, foff, c.thin_row, c.thin_ptr, c.thin_pos, c.thin_src);
+    int tn = (int)tnnz;
+    CK(cudaMemcpyAsync(c.thin_ptr + c.nthin, &tn, sizeof(int), cudaMemcpyHostToDevice, c.stream));
+    C.thin_nnz = tnnz;
+    thin_numeric(c, tnnz);
+    c.release(cnt); c.release(off); c.release(flag); c.release(foff);
+  }
+
+  // ---- hierarchy
+  L0.Bnn = c.alloc<double>(n * 6);
+  d2d(c, L0.Bnn, B_nns, (size_t)n * 6);
+  L0.dl1 = c.alloc<double>(n);
+  L0.dpt = c.alloc<double>(n);
+  LAUNCH(k_diag, n, nodes, 3, L0.A.ptr, L0.A.col, L0.A.val, L0.dl1, L0.dpt);
+  // level-0 components of K's block graph
+  L0.comp = c.alloc<int>(nodes);
+  {
+    LAUNCH(k_iota, nodes, nodes, L0.comp);
+    int *chg = c.alloc<int>(1);
+    for (int it = 0; it < 100000; it++) {
+      CK(cudaMemsetAsync(chg, 0, sizeof(int), c.stream));
+      LAUNCH(k_cc_step, nodes, nodes, c.K.ptr, c.K.col, L0.comp, chg);
+      if (d2h1(c, chg) == 0) break;
+    }
+    c.release(chg);
+  }
+  int l = 0;
+  for (;;) {
+    Level &L = c.lev[l];
+    if (L.n <= c.cfg.coarsest_size || l + 1 >= c.cfg.max_levels || l + 1 >= MAXLEV) break;
+    const int nn = L.nodes;
+    // ---- s4 aggregation
+    int *state = c.alloc<int>(nn), *m1 = c.alloc<int>(nn), *m2 = c.alloc<int>(nn), *und = c.alloc<int>(1);
+    LAUNCH(k_mis_init, nn, nn, L.A.ptr, L.A.col, L.comp, state);
+    for (int round = 0; round < 10000; round++) {
+      LAUNCH(k_mis_max, nn, nn, L.A.ptr, L.A.col, L.comp, state, (const int *)nullptr, m1, c.cfg.agg_seed);
+      LAUNCH(k_mis_max, nn, nn, L.A.ptr, L.A.col, L.comp, state, (const int *)m1, m2, c.cfg.agg_seed);
+      LAUNCH(k_mis_roots, nn, nn, m2, state);
+      LAUNCH(k_mis_near, nn, nn, L.A.ptr, L.A.col, L.comp, state, (const int *)nullptr, m1);
+      LAUNCH(k_mis_near, nn, nn, L.A.ptr, L.A.col, L.comp, state, (const int *)m1, m2);
+      CK(cudaMemsetAsync(und, 0, sizeof(int), c.stream));
+      LAUNCH(k_mis_block, nn, nn, m2, state, und);
+      if (d2h1(c, und) == 0) break;
+    }
+    int *flag = c.alloc<int>(nn + 1), *rank = c.alloc<int>(nn + 1);
+    CK(cudaMemsetAsync(flag, 0, (nn + 1) * sizeof(int), c.stream));
+    LAUNCH(k_root_flag, nn, nn, state, flag);
+    const int na = (int)scan_ex(c, flag, rank, nn);
+    L.root = flag;
+    if (na == 0 || 60L * na > 9L * L.n) {
+      c.release(state); c.release(m1); c.release(m2); c.release(und); c.release(rank);
+      break;
+    }
+    L.n_agg = na;
+    L.agg = c.alloc<int>(nn);
+    LAUNCH(k_agg_phase3, nn, nn, L.A.ptr, L.A.col, L.comp, state, rank, m1);
+    LAUNCH(k_agg_leftover, nn, nn, L.A.ptr, L.A.col, L.comp, state, m1, L.agg, c.err);
+    check_dev_error(c, "aggregation");
+    Level &Lc = c.lev[l + 1];
+    Lc.b = 6; Lc.nodes = na; Lc.n = 6L * na;
+    Lc.comp = c.alloc<int>(na);
+    LAUNCH(k_coarse_comp, nn, nn, state, rank, L.comp, Lc.comp);
+    // ---- s5 tentative prolongator
+    {
+      int *key = c.alloc<int>(nn), *keys = c.alloc<int>(nn), *idx = c.alloc<int>(nn);
+      LAUNCH(k_agg_key, nn, nn, L.agg, key);
+      LAUNCH(k_iota, nn, nn, idx);
+      L.agg_nodes = c.alloc<int>(nn);
+      sort_pairs(c, key, keys, idx, L.agg_nodes, nn);
+      int *cnt = c.alloc<int>(na + 1);
+      CK(cudaMemsetAsync(cnt, 0, (na + 1) * sizeof(int), c.stream));
+      // counts per aggregate
+      int *aggd = c.alloc<int>(nn);
+      LAUNCH(k_agg_key, nn, nn, L.agg, aggd);
+      LAUNCH(k_count_valid, nn, nn, aggd, na, cnt);
+      L.agg_ptr = c.alloc<int>(na + 1);
+      scan_ex(c, cnt, L.agg_ptr, na);
+      int *isagg = c.alloc<int>(nn + 1);
+      CK(cudaMemsetAsync(isagg, 0, (nn + 1) * sizeof(int), c.stream));
+      LAUNCH(k_is_agg, nn, nn, L.agg, isagg);
+      L.Pt.ptr = c.alloc<int>(nn + 1);
+      long nzt = scan_ex(c, isagg, L.Pt.ptr, nn);
+      L.Pt.nbr = nn; L.Pt.nbc = na; L.Pt.br = L.b; L.Pt.bc = 6; L.Pt.nnzb = nzt;
+      L.Pt.col = c.alloc<int>(nzt);
+      L.Pt.val = c.alloc<double>(nzt * L.b * 6);
+      LAUNCH(k_Pt_cols, nn, nn, L.agg, L.Pt.ptr, L.Pt.col);
+      Lc.Bnn = c.alloc<double>((long)na * 36);
+      LAUNCH(k_qr, na, na, L.b, L.agg_ptr, L.agg_nodes, L.Pt.ptr, L.Bnn, L.Pt.val, Lc.Bnn, c.err);
+      check_dev_error(c, "tentative prolongator");
+      c.release(key); c.release(keys); c.release(idx); c.release(cnt); c.release(aggd); c.release(isagg);
+    }
+    c.release(state); c.release(m1); c.release(m2); c.release(und); c.release(rank);
+    LevelCache &lc = C.lc[l];
+    // ---- s6 smoothed prolongator pattern
+    {
+      int *cnt = c.alloc<int>(nn + 1);
+      CK(cudaMemsetAsync(cnt, 0, (nn + 1) * sizeof(int), c.stream));
+      LAUNCH(k_P_count, nn, nn, L.A.ptr, L.A.col, L.agg, cnt, c.err);
+      check_dev_error(c, "prolongator pattern");
+      L.P.ptr = c.alloc<int>(nn + 1);
+      long nzp = scan_ex(c, cnt, L.P.ptr, nn);
+      c.release(cnt);
+      L.P.nbr = nn; L.P.nbc = na; L.P.br = L.b; L.P.bc = 6; L.P.nnzb = nzp;
+      L.P.col = c.alloc<int>(nzp);
+      L.P.val = c.alloc<double>(nzp * L.b * 6);
+      LAUNCH(k_P_fill, nn, nn, L.A.ptr, L.A.col, L.agg, L.P.ptr, L.P.col);
+      lc.P_rowof = rowof(c, L.P);
+    }
+    // ---- s7 R = P^T pattern
+    {
+      const long nzp = L.P.nnzb;
+      int *keys = c.alloc<int>(nzp), *idx = c.alloc<int>(nzp);
+      lc.R_perm = c.alloc<int>(nzp);
+      LAUNCH(k_iota, nzp, nzp, idx);
+      sort_pairs(c, L.P.col, keys, idx, lc.R_perm, nzp);
+      int *cnt = c.alloc<int>(na + 1);
+      CK(cudaMemsetAsync(cnt, 0, (na + 1) * sizeof(int), c.stream));
+      LAUNCH(k_count_keys, nzp, nzp, L.P.col, cnt);
+      L.R.nbr = na; L.R.nbc = nn; L.R.br = 6; L.R.bc = L.b; L.R.nnzb = nzp;
+      L.R.ptr = c.alloc<int>(na + 1);
+      scan_ex(c, cnt, L.R.ptr, na);
+      L.R.col = c.alloc<int>(nzp);
+      L.R.val = c.alloc<double>(nzp * 6 * L.b);
+      LAUNCH(k_gather_int, nzp, nzp, lc.R_perm, lc.P_rowof, L.R.col);
+      c.release(keys); c.release(idx); c.release(cnt);
+    }
+    // ---- AP and G patterns
+    {
+      int *cnt = c.alloc<int>(nn + 1);
+      CK(cudaMemsetAsync(cnt, 0, (nn + 1) * sizeof(int), c.stream));
+      LAUNCH(k_spgemm_count, nn, nn, L.A.ptr, L.A.col, L.P.ptr, L.P.col, cnt, c.err);
+      check_dev_error(c, "A*P pattern");
+      L.AP.ptr = c.alloc<int>(nn + 1);
+      long nz = scan_ex(c, cnt, L.AP.ptr, nn);
+      c.release(cnt);
+      L.AP.nbr = nn; L.AP.nbc = na; L.AP.br = L.b; L.AP.bc = 6; L.AP.nnzb = nz;
+      L.AP.col = c.alloc<int>(nz);
+      L.AP.val = c.alloc<double>(nz * L.b * 6);
+      LAUNCH(k_spgemm_fill, nn, nn, L.A.ptr, L.A.col, L.P.ptr, L.P.col, L.AP.ptr, L.AP.col);
+      int *cg = c.alloc<int>(na + 1);
+      CK(cudaMemsetAsync(cg, 0, (na + 1) * sizeof(int), c.stream));
+      LAUNCH(k_spgemm_count, na, na, L.R.ptr, L.R.col, L.AP.ptr, L.AP.col, cg, c.err);
+      check_dev_error(c, "R*AP pattern");
+      lc.G.ptr = c.alloc<int>(na + 1);
+      long nzg = scan_ex(c, cg, lc.G.ptr, na);
+      c.release(cg);
+      lc.G.nbr = na; lc.G.nbc = na; lc.G.br = 6; lc.G.bc = 6; lc.G.nnzb = nzg;
+      lc.G.col = c.alloc<int>(nzg);
+      lc.G.val = c.alloc<double>(nzg * 36);
+      LAUNCH(k_spgemm_fill, na, na, L.R.ptr, L.R.col, L.AP.ptr, L.AP.col, lc.G.ptr, lc.G.col);
+      lc.G_rowof = rowof(c, lc.G);
+      // coarse operator shares G's pattern
+      Lc.A.nbr = Lc.A.nbc = na; Lc.A.br = Lc.A.bc = 6; Lc.A.nnzb = nzg;
+      Lc.A.ptr = lc.G.ptr; Lc.A.col = lc.G.col;
+      Lc.A.val = c.alloc<double>(nzg * 36);
+      Lc.dl1 = c.alloc<double>(Lc.n);
+      Lc.dpt = c.alloc<double>(Lc.n);
+    }
+    level_numeric(c, l, lc);
+    check_dev_error(c, "Galerkin product");
+    build_sell(c, L.A, L.As, true);
+    build_sell(c, L.P, L.Ps, true);
+    l++;
+  }
+  c.nlev = l + 1;
+  // ---- s9 coarsest
+  {
+    Level &L = c.lev[c.nlev - 1];
+    REQUIRE(L.n <= 16384, AMGF_ERR_LIMIT, "coarsest level too large for a dense factor (" + std::to_string(L.n) + ")");
+    c.nco = (int)L.n;
+    band_alloc(c, c.nco, c.nco - 1, c.Lc_row, c.Lc_col, c.Lc_dinv);
+    coarsest_numeric(c);
+    check_dev_error(c, "coarsest Cholesky");
+  }
+  // ---- workspaces
+  for (int q = 0; q < c.nlev; q++) {
+    Level &L = c.lev[q];
+    L.x = c.alloc<double>(L.n);
+    L.x2 = c.alloc<double>(L.n);
+    L.bv = c.alloc<double>(L.n);
+    L.r = c.alloc<double>(L.n);
+  }
+  if (c.nlev == 1) build_sell(c, L0.A, L0.As, true);
+  c.w_x1 = c.alloc<double>(n);
+  c.w_r1 = c.alloc<double>(n);
+  c.w_xv = c.alloc<double>(n);
+  c.p = c.alloc<double>(n);
+  c.q = c.alloc<double>(n);
+  c.rr = c.alloc<double>(n);
+  c.zz = c.alloc<double>(n);
+  c.xx = c.alloc<double>(n);
+  c.bb = c.alloc<double>(n);
+  CK(cudaStreamSynchronize(c.stream));
+}
+
+// =================================================================== numeric re-setup (new D)
+void setup_numeric(Ctx &c, const double *D) {
+  Caches &C = caches(c);
+  d2d(c, c.D, D, c.m);
+  LAUNCH(k_check_finite, c.m, c.m, c.D, c.err, DERR_NONFINITE);
+  LAUNCH(k_check_pos, c.m, c.m, c.D, c.err);
+  check_dev_error(c, "D check");
+  S_numeric(c, C.s.S_rowof);
+  Level &L0 = c.lev[0];
+  if (c.nc > 0) {
+    filter_numeric(c);
+    check_dev_error(c, "A_w Cholesky");
+    thin_numeric(c, C.thin_nnz);
+  }
+  LAUNCH(k_diag, L0.n, L0.nodes, 3, L0.A.ptr, L0.A.col, L0.A.val, L0.dl1, L0.dpt);
+  for (int l = 0; l + 1 < c.nlev; l++) {
+    level_numeric(c, l, C.lc[l]);
+    check_dev_error(c, "Galerkin product");
+    build_sell(c, c.lev[l].A, c.lev[l].As, false);
+    build_sell(c, c.lev[l].P, c.lev[l].Ps, false);
+  }
+  if (c.nlev == 1) build_sell(c, L0.A, L0.As, false);
+  coarsest_numeric(c);
+  check_dev_error(c, "coarsest Cholesky");
+}
+
+}  // namespace amgf

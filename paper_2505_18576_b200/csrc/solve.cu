@@ -1,0 +1,519 @@
+// solve.cu -- solve-phase kernels of libamgf.so.
+//
+//   k_sell      SELL-32 block SpMV, one thread per block row, fused epilogues:
+//               y = Ax | r = b - Ax | l1-Jacobi sweep | y = Ax + CTA partial of x.y | sweep + add
+//               (contracts C2, C4, C6, C14 level 1).  Used for S, every A_l, and P (prolongation).
+//   k_restrict  b_c = R r, one warp per coarse block row, strided lanes + xor butterfly (C5).
+//   k_dot_*     two-level fixed-tree dot products (C14) with the PCG scalar updates (C15).
+//   k_band_trsv A_w^{-1} v by the banded Cholesky factor, one warp, shuffle broadcast, cp.async
+//               double-buffered band columns (C10); gather r1[Z] and scatter x2[Z] += y fused.
+//   k_thin      r2 = r1 - S[:,Z] y over the rows that touch Z (C11).
+#include "common.cuh"
+
+namespace amgf {
+
+__device__ __forceinline__ double ldg_stream(const double *p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int ldg_stream_i(const int *p) {
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+// Fixed tree of C14 over 256 values in shared memory; returns s[0] to all threads.
+__device__ __forceinline__ double cta_tree(double v, double *s) {
+  int t = threadIdx.x;
+  s[t] = v;
+  __syncthreads();
+#pragma unroll
+  for (int w = CTA / 2; w >= 1; w >>= 1) {
+    if (t < w) s[t] = s[t] + s[t + w];
+    __syncthreads();
+  }
+  double r = s[0];
+  __syncthreads();
+  return r;
+}
+
+enum { MODE_Y = SPMV_Y, MODE_RESID = SPMV_RESID, MODE_SMOOTH = SPMV_SMOOTH, MODE_DOT = SPMV_DOT,
+       MODE_SMOOTH_ADD = SPMV_SMOOTH_ADD, MODE_ADDTO = 5 };
+
+template <int BR, int BC, int MODE>
+__global__ void __launch_bounds__(CTA) k_sell(int nrows, const int *__restrict__ slice_ptr,
+                                              const int *__restrict__ rowlen, const int *__restrict__ col,
+                                              const double *__restrict__ val, const double *__restrict__ x,
+                                              const double *__restrict__ b, const double *__restrict__ d,
+                                              const double *__restrict__ add, double *__restrict__ y,
+                                              double *__restrict__ dot_part) {
+  const int row = blockIdx.x * CTA + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  double acc[BR];
+#pragma unroll
+  for (int r = 0; r < BR; r++) acc[r] = 0.0;
+  if (row < nrows) {
+    const int len = rowlen[row];
+    const long base = slice_ptr[row >> 5];
+    const int *cp = col + base * 32 + lane;
+    const double *vp = val + base * (BR * BC * 32) + lane;
+#pragma unroll 2
+    for (int s = 0; s < len; s++) {
+      const int c = ldg_stream_i(cp + (long)s * 32);
+      double xv[BC];
+#pragma unroll
+      for (int e = 0; e < BC; e++) xv[e] = x[(long)c * BC + e];
+      const double *v = vp + (long)s * (BR * BC * 32);
+#pragma unroll
+      for (int r = 0; r < BR; r++)
+#pragma unroll
+        for (int e = 0; e < BC; e++) acc[r] = __fma_rn(ldg_stream(v + (r * BC + e) * 32), xv[e], acc[r]);
+    }
+  }
+  if (MODE == MODE_DOT) {
+    __shared__ double red[CTA];
+    double s = 0.0;
+    if (row < nrows) {
+#pragma unroll
+      for (int r = 0; r < BR; r++) {
+        y[(long)row * BR + r] = acc[r];
+        s = __fma_rn(x[(long)row * BR + r], acc[r], s);
+      }
+    }
+    double tot = cta_tree(s, red);
+    if (threadIdx.x == 0) dot_part[blockIdx.x] = tot;
+    return;
+  }
+  if (row >= nrows) return;
+#pragma unroll
+  for (int r = 0; r < BR; r++) {
+    const long i = (long)row * BR + r;
+    if (MODE == MODE_Y) {
+      y[i] = acc[r];
+    } else if (MODE == MODE_RESID) {
+      y[i] = b[i] - acc[r];
+    } else if (MODE == MODE_SMOOTH || MODE == MODE_SMOOTH_ADD) {
+      double res = b[i] - acc[r];
+      double t = res / d[i];
+      double xn = x[i] + t;
+      if (MODE == MODE_SMOOTH_ADD) xn = add[i] + xn;
+      y[i] = xn;
+    } else if (MODE == MODE_ADDTO) {
+      y[i] = y[i] + acc[r];
+    }
+  }
+}
+
+template <int BR, int BC>
+static void sell_dispatch(Ctx &c, const Sell &A, int mode, const double *x, const double *b, const double *d,
+                          const double *add, double *y, double *dp) {
+  dim3 g(nblk(A.nrows)), t(CTA);
+  if (A.nrows == 0) return;
+  switch (mode) {
+    case MODE_Y: k_sell<BR, BC, MODE_Y><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp); break;
+    case MODE_RESID: k_sell<BR, BC, MODE_RESID><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp); break;
+    case MODE_SMOOTH: k_sell<BR, BC, MODE_SMOOTH><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp); break;
+    case MODE_DOT: k_sell<BR, BC, MODE_DOT><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp); break;
+    case MODE_SMOOTH_ADD: k_sell<BR, BC, MODE_SMOOTH_ADD><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp); break;
+    case MODE_ADDTO: k_sell<BR, BC, MODE_ADDTO><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp); break;
+  }
+  c.launches++;
+  CK(cudaGetLastError());
+}
+
+void launch_sell_spmv(Ctx &c, const Sell &A, int mode, const double *x, const double *b, const double *d,
+                      const double *add, double *y, double *dp) {
+  if (A.br == 3 && A.bc == 3) sell_dispatch<3, 3>(c, A, mode, x, b, d, add, y, dp);
+  else if (A.br == 6 && A.bc == 6) sell_dispatch<6, 6>(c, A, mode, x, b, d, add, y, dp);
+  else throw Error{AMGF_ERR_ARG, "sell spmv: unsupported block shape"};
+}
+
+void launch_prolong(Ctx &c, const Sell &P, const double *xc, double *x) {
+  if (P.br == 3) sell_dispatch<3, 6>(c, P, MODE_ADDTO, xc, nullptr, nullptr, nullptr, x, nullptr);
+  else if (P.br == 6) sell_dispatch<6, 6>(c, P, MODE_ADDTO, xc, nullptr, nullptr, nullptr, x, nullptr);
+  else throw Error{AMGF_ERR_ARG, "prolong: unsupported block shape"};
+}
+
+// ------------------------------------------------------------------ restriction (C5)
+template <int B>
+__global__ void __launch_bounds__(CTA) k_restrict(int nrows, const int *__restrict__ ptr, const int *__restrict__ col,
+                                                  const double *__restrict__ val, const double *__restrict__ r,
+                                                  double *__restrict__ out) {
+  const int w = (blockIdx.x * CTA + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= nrows) return;  // warp-uniform
+  double acc[6];
+#pragma unroll
+  for (int q = 0; q < 6; q++) acc[q] = 0.0;
+  const int end = ptr[w + 1];
+  for (int k = ptr[w] + lane; k < end; k += 32) {
+    const int c = col[k];
+    double rv[B];
+#pragma unroll
+    for (int e = 0; e < B; e++) rv[e] = r[(long)c * B + e];
+    const double2 *v2 = reinterpret_cast<const double2 *>(val + (long)k * 6 * B);
+#pragma unroll
+    for (int h = 0; h < 3 * B; h++) {
+      double2 t = __ldg(v2 + h);
+      const int e0 = 2 * h, e1 = 2 * h + 1;
+      acc[e0 / B] = __fma_rn(t.x, rv[e0 % B], acc[e0 / B]);
+      acc[e1 / B] = __fma_rn(t.y, rv[e1 % B], acc[e1 / B]);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1)
+#pragma unroll
+    for (int q = 0; q < 6; q++) acc[q] = acc[q] + __shfl_xor_sync(0xffffffffu, acc[q], o);
+  if (lane < 6) {
+    double v = acc[0];
+#pragma unroll
+    for (int q = 1; q < 6; q++)
+      if (lane == q) v = acc[q];
+    out[(long)w * 6 + lane] = v;
+  }
+}
+
+void launch_restrict(Ctx &c, const Bsr &R, const double *r, double *bc) {
+  if (R.nbr == 0) return;
+  long threads = (long)R.nbr * 32;
+  if (R.bc == 3) k_restrict<3><<<nblk(threads), CTA, 0, c.stream>>>(R.nbr, R.ptr, R.col, R.val, r, bc);
+  else k_restrict<6><<<nblk(threads), CTA, 0, c.stream>>>(R.nbr, R.ptr, R.col, R.val, r, bc);
+  c.launches++;
+  CK(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ vector kernels
+__global__ void k_jacobi0(long n, const double *__restrict__ b, const double *__restrict__ d, double *__restrict__ x) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) x[i] = b[i] / d[i];
+}
+__global__ void k_copy(long n, const double *__restrict__ s, double *__restrict__ d) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) d[i] = s[i];
+}
+__global__ void k_zero(long n, double *__restrict__ d) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) d[i] = 0.0;
+}
+__global__ void k_add(long n, const double *__restrict__ a, const double *__restrict__ b, double *__restrict__ o) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) o[i] = a[i] + b[i];
+}
+// x = fma(alpha, p, x); r = fma(-alpha, q, r)   (C15)
+__global__ void k_axpy2(long n, const Scalars *__restrict__ sc, const double *__restrict__ p,
+                        const double *__restrict__ q, double *__restrict__ x, double *__restrict__ r) {
+  const double a = sc->alpha;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    x[i] = __fma_rn(a, p[i], x[i]);
+    r[i] = __fma_rn(-a, q[i], r[i]);
+  }
+}
+// p = fma(beta, p, z)   (C15)
+__global__ void k_xpby(long n, const Scalars *__restrict__ sc, const double *__restrict__ z, double *__restrict__ p) {
+  const double be = sc->beta;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    p[i] = __fma_rn(be, p[i], z[i]);
+}
+
+static int vgrid(long n) {
+  long g = (n + CTA - 1) / CTA;
+  return (int)(g < 148 * 16 ? (g > 0 ? g : 1) : 148 * 16);
+}
+
+void launch_jacobi0(Ctx &c, long n, const double *b, const double *d, double *x) {
+  k_jacobi0<<<vgrid(n), CTA, 0, c.stream>>>(n, b, d, x); c.launches++; CK(cudaGetLastError());
+}
+void launch_copy(Ctx &c, long n, const double *s, double *d) {
+  k_copy<<<vgrid(n), CTA, 0, c.stream>>>(n, s, d); c.launches++; CK(cudaGetLastError());
+}
+void launch_zero(Ctx &c, long n, double *d) {
+  k_zero<<<vgrid(n), CTA, 0, c.stream>>>(n, d); c.launches++; CK(cudaGetLastError());
+}
+void launch_add(Ctx &c, long n, const double *a, const double *b, double *o) {
+  k_add<<<vgrid(n), CTA, 0, c.stream>>>(n, a, b, o); c.launches++; CK(cudaGetLastError());
+}
+void launch_axpy2(Ctx &c, long n, const double *p, const double *q, double *x, double *r) {
+  k_axpy2<<<vgrid(n), CTA, 0, c.stream>>>(n, c.sc, p, q, x, r); c.launches++; CK(cudaGetLastError());
+}
+void launch_xpby(Ctx &c, long n, const double *z, double *p) {
+  k_xpby<<<vgrid(n), CTA, 0, c.stream>>>(n, c.sc, z, p); c.launches++; CK(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ dots (C14, C15)
+__global__ void __launch_bounds__(CTA) k_dot1(long nb, int b, const double *__restrict__ u,
+                                              const double *__restrict__ v, double *__restrict__ part) {
+  __shared__ double red[CTA];
+  const long i = blockIdx.x * (long)CTA + threadIdx.x;
+  double s = 0.0;
+  if (i < nb)
+    for (int e = 0; e < b; e++) s = __fma_rn(u[i * b + e], v[i * b + e], s);
+  double tot = cta_tree(s, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(CTA) k_dot2(long C, const double *__restrict__ part, Scalars *sc, int kind, int *err) {
+  __shared__ double red[CTA];
+  double acc = 0.0;
+  for (long c = threadIdx.x; c < C; c += CTA) acc = acc + part[c];
+  double s = cta_tree(acc, red);
+  if (threadIdx.x == 0) {
+    switch (kind) {
+      case DOT_PLAIN: sc->dot = s; break;
+      case DOT_PI:
+        sc->pi = s;
+        if (!(s > 0.0)) raise_err(err, DERR_BREAKDOWN, 1);
+        sc->alpha = sc->rho / s;
+        break;
+      case DOT_RHO0: sc->rho0 = s; sc->rho = s; sc->rho1 = s; break;
+      case DOT_RHO1:
+        sc->rho1 = s;
+        if (s < 0.0) raise_err(err, DERR_BREAKDOWN, 2);
+        sc->beta = s / sc->rho;
+        sc->rho = s;
+        break;
+    }
+  }
+}
+
+void launch_dot_finish(Ctx &c, long C, int finish) {
+  k_dot2<<<1, CTA, 0, c.stream>>>(C, c.dot_part, c.sc, finish, c.err);
+  c.launches++;
+  CK(cudaGetLastError());
+}
+
+void launch_dot(Ctx &c, long n, int b, const double *u, const double *v, int finish) {
+  long nb = n / b;
+  long C = (nb + CTA - 1) / CTA;
+  if (C > 0) {
+    k_dot1<<<(int)C, CTA, 0, c.stream>>>(nb, b, u, v, c.dot_part);
+    c.launches++;
+  }
+  k_dot2<<<1, CTA, 0, c.stream>>>(C, c.dot_part, c.sc, finish, c.err);
+  c.launches++;
+  CK(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ banded triangular solves (C10)
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+// copy `count` doubles (count*8 divisible by 16, both pointers 16-byte aligned) global -> smem, one warp
+__device__ __forceinline__ void warp_stage(double *dst, const double *src, int count, int lane) {
+  const int chunks = count / 2;
+  for (int k = lane; k < chunks; k += 32) cp_async16(dst + 2 * k, src + 2 * k);
+}
+
+// One warp.  Forward:  w = L^{-1} v, column sweep over j ascending; backward: y = L^{-T} w, column
+// sweep over k descending.  Lane l owns window rows j0 + l + 32 s (s < R); requires bw <= 32(R-1).
+// Band storage has even row stride W = (bw+2)&~1 and 64 rows of zero padding on both sides
+// (rounds prefetch up to 63 rows past either end).
+template <int R>
+__global__ void __launch_bounds__(32) k_band_trsv(int n, int bw, const double *__restrict__ Lrow,
+                                                  const double *__restrict__ Lcol, const double *__restrict__ dinv,
+                                                  const double *__restrict__ v, const int *__restrict__ gather,
+                                                  double *__restrict__ y, const int *__restrict__ scatter,
+                                                  double *__restrict__ xout, double *__restrict__ w) {
+  extern __shared__ __align__(16) double sm[];
+  const int lane = threadIdx.x;
+  const int W = (bw + 2) & ~1;  // even row stride of the band storage (16-byte aligned rows)
+  const int chunk = 32 * W;
+  double *buf0 = sm, *buf1 = sm + chunk;
+  const int rounds = (n + 31) / 32;
+  double acc[R];
+  auto vin = [&](int i) -> double {
+    if (i >= n) return 0.0;
+    return gather ? v[gather[i]] : v[i];
+  };
+  // ---------------- forward
+#pragma unroll
+  for (int s = 0; s < R; s++) acc[s] = vin(lane + 32 * s);
+  warp_stage(buf0, Lcol, chunk, lane);
+  cp_commit();
+  for (int q = 0; q < rounds; q++) {
+    const int j0 = 32 * q;
+    double *cur = (q & 1) ? buf1 : buf0;
+    double *nxt = (q & 1) ? buf0 : buf1;
+    warp_stage(nxt, Lcol + (long)(j0 + 32) * W, chunk, lane);
+    cp_commit();
+    cp_wait<1>();
+    __syncwarp();
+    const double dv = (j0 + lane < n) ? dinv[j0 + lane] : 0.0;
+    double mine = 0.0;
+#pragma unroll
+    for (int jj = 0; jj < 32; jj++) {
+      if (j0 + jj >= n) break;
+      const double yj = __shfl_sync(0xffffffffu, acc[0] * dv, jj);
+      if (lane == jj) mine = yj;
+      const double *colj = cur + jj * W;
+#pragma unroll
+      for (int s = 0; s < R; s++) {
+        const int off = lane + 32 * s - jj;  // i - j
+        if (off > 0 && off <= bw) acc[s] = __fma_rn(-colj[off], yj, acc[s]);
+      }
+    }
+    if (j0 + lane < n) w[j0 + lane] = mine;
+#pragma unroll
+    for (int s = 0; s < R - 1; s++) acc[s] = acc[s + 1];
+    acc[R - 1] = vin(j0 + 32 + lane + 32 * (R - 1));
+    __syncwarp();
+  }
+  cp_wait<0>();
+  __syncwarp();
+  // ---------------- backward: rows handled top-down in rounds of 32, k1 = n-1-32q
+#pragma unroll
+  for (int s = 0; s < R; s++) {
+    const int i = n - 1 - lane - 32 * s;
+    acc[s] = (i >= 0) ? w[i] : 0.0;
+  }
+  warp_stage(buf0, Lrow + (long)(n - 32) * W, chunk, lane);
+  cp_commit();
+  for (int q = 0; q < rounds; q++) {
+    const int k1 = n - 1 - 32 * q;
+    double *cur = (q & 1) ? buf1 : buf0;
+    double *nxt = (q & 1) ? buf0 : buf1;
+    warp_stage(nxt, Lrow + (long)(k1 - 32 - 31) * W, chunk, lane);
+    cp_commit();
+    cp_wait<1>();
+    __syncwarp();
+    // cur holds rows k1-31 .. k1; row k is at cur + (k - (k1-31)) * W
+    const double dv = (k1 - lane >= 0) ? dinv[k1 - lane] : 0.0;
+    double mine = 0.0;
+#pragma unroll
+    for (int jj = 0; jj < 32; jj++) {
+      const int k = k1 - jj;
+      if (k < 0) break;
+      const double xk = __shfl_sync(0xffffffffu, acc[0] * dv, jj);
+      if (lane == jj) mine = xk;
+      const double *rowk = cur + (31 - jj) * W;
+#pragma unroll
+      for (int s = 0; s < R; s++) {
+        const int off = jj - lane - 32 * s + 0;  // i - k, i = k1 - lane - 32 s
+        const int dist = -off;                  // k - i
+        if (dist > 0 && dist <= bw) acc[s] = __fma_rn(-rowk[bw - dist], xk, acc[s]);
+      }
+    }
+    if (k1 - lane >= 0) y[k1 - lane] = mine;
+#pragma unroll
+    for (int s = 0; s < R - 1; s++) acc[s] = acc[s + 1];
+    {
+      const int i = k1 - 32 - lane - 32 * (R - 1);
+      acc[R - 1] = (i >= 0) ? w[i] : 0.0;
+    }
+    __syncwarp();
+  }
+  cp_wait<0>();
+  __syncwarp();
+  if (scatter)
+    for (int a = lane; a < n; a += 32) xout[scatter[a]] = xout[scatter[a]] + y[a];
+}
+
+// Generic fallback for wide bands: one CTA, thread per row of the window, barrier per pivot.
+__global__ void __launch_bounds__(1024) k_band_trsv_wide(int n, int bw, const double *__restrict__ Lrow,
+                                                         const double *__restrict__ dinv, const double *__restrict__ v,
+                                                         const int *__restrict__ gather, double *__restrict__ y,
+                                                         const int *__restrict__ scatter, double *__restrict__ xout,
+                                                         double *__restrict__ w) {
+  __shared__ double piv;
+  const int W = (bw + 2) & ~1;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) w[i] = gather ? v[gather[i]] : v[i];
+  __syncthreads();
+  for (int j = 0; j < n; j++) {
+    if (threadIdx.x == 0) { piv = w[j] * dinv[j]; w[j] = piv; }
+    __syncthreads();
+    const double yj = piv;
+    for (int i = j + 1 + threadIdx.x; i <= j + bw && i < n; i += blockDim.x)
+      w[i] = __fma_rn(-Lrow[(long)i * W + bw - (i - j)], yj, w[i]);
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) y[i] = w[i];
+  __syncthreads();
+  for (int k = n - 1; k >= 0; k--) {
+    if (threadIdx.x == 0) { piv = y[k] * dinv[k]; y[k] = piv; }
+    __syncthreads();
+    const double xk = piv;
+    for (int i = k - 1 - threadIdx.x; i >= k - bw && i >= 0; i -= blockDim.x)
+      y[i] = __fma_rn(-Lrow[(long)k * W + bw - (k - i)], xk, y[i]);
+    __syncthreads();
+  }
+  if (scatter)
+    for (int a = threadIdx.x; a < n; a += blockDim.x) xout[scatter[a]] = xout[scatter[a]] + y[a];
+}
+
+template <int R>
+static void trsv_R(Ctx &c, int n, int bw, const double *Lrow, const double *Lcol, const double *dinv,
+                   const double *v, const int *gather, double *y, const int *scatter, double *xout, double *w) {
+  size_t smem = 2 * 32 * (size_t)((bw + 2) & ~1) * sizeof(double);
+  static bool attr_set = false;
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(k_band_trsv<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr_set = true;
+  }
+  k_band_trsv<R><<<1, 32, smem, c.stream>>>(n, bw, Lrow, Lcol, dinv, v, gather, y, scatter, xout, w);
+}
+
+void launch_band_trsv(Ctx &c, int n, int bw, const double *Lrow, const double *Lcol, const double *dinv,
+                       const double *v, const int *gather, double *y, const int *scatter, double *xout,
+                       double *work) {
+  if (n == 0) return;
+  const int R = (bw + 31) / 32 + 1;
+  switch (R) {
+    case 1: case 2: trsv_R<2>(c, n, bw, Lrow, Lcol, dinv, v, gather, y, scatter, xout, work); break;
+    case 3: trsv_R<3>(c, n, bw, Lrow, Lcol, dinv, v, gather, y, scatter, xout, work); break;
+    case 4: trsv_R<4>(c, n, bw, Lrow, Lcol, dinv, v, gather, y, scatter, xout, work); break;
+    case 5: trsv_R<5>(c, n, bw, Lrow, Lcol, dinv, v, gather, y, scatter, xout, work); break;
+    case 6: trsv_R<6>(c, n, bw, Lrow, Lcol, dinv, v, gather, y, scatter, xout, work); break;
+    case 7: trsv_R<7>(c, n, bw, Lrow, Lcol, dinv, v, gather, y, scatter, xout, work); break;
+    case 8: trsv_R<8>(c, n, bw, Lrow, Lcol, dinv, v, gather, y, scatter, xout, work); break;
+    default:
+      k_band_trsv_wide<<<1, 1024, 0, c.stream>>>(n, bw, Lrow, dinv, v, gather, y, scatter, xout, work);
+  }
+  c.launches++;
+  CK(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ thin second residual (C11)
+__global__ void k_thin(int nthin, const int *__restrict__ rows, const int *__restrict__ ptr,
+                       const int *__restrict__ pos, const double *__restrict__ val, const double *__restrict__ y,
+                       double *__restrict__ r) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nthin) return;
+  double acc = 0.0;
+  for (int e = ptr[t]; e < ptr[t + 1]; e++) acc = __fma_rn(val[e], y[pos[e]], acc);
+  const int p = rows[t];
+  r[p] = r[p] - acc;
+}
+
+void launch_thin_resid(Ctx &c, int nthin, const int *rows, const int *ptr, const int *pos, const double *val,
+                       const double *y, double *r) {
+  if (nthin == 0) return;
+  k_thin<<<nblk(nthin), CTA, 0, c.stream>>>(nthin, rows, ptr, pos, val, y, r);
+  c.launches++;
+  CK(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ setup-side BSR SpMV (C2)
+__global__ void k_bsr_spmv(int nbr, int br, int bc, const int *__restrict__ ptr, const int *__restrict__ col,
+                           const double *__restrict__ val, const double *__restrict__ x, double *__restrict__ y) {
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (t >= (long)nbr * br) return;
+  const int i = (int)(t / br), r = (int)(t % br);
+  double acc = 0.0;
+  for (int k = ptr[i]; k < ptr[i + 1]; k++) {
+    const double *v = val + (long)k * br * bc + (long)r * bc;
+    const double *xs = x + (long)col[k] * bc;
+    for (int e = 0; e < bc; e++) acc = __fma_rn(v[e], xs[e], acc);
+  }
+  y[t] = acc;
+}
+
+void launch_bsr_spmv(Ctx &c, const Bsr &A, const double *x, double *y) {
+  long rows = (long)A.nbr * A.br;
+  if (rows == 0) return;
+  k_bsr_spmv<<<nblk(rows), CTA, 0, c.stream>>>(A.nbr, A.br, A.bc, A.ptr, A.col, A.val, x, y);
+  c.launches++;
+  CK(cudaGetLastError());
+}
+
+}  // namespace amgf

@@ -1,0 +1,259 @@
+"""Parity of the CUDA path (libamgf.so through the C-ABI) against the CPU oracle.
+
+Under the arithmetic contract the expected result is BITWISE equality for every
+floating-point output and exact equality for every integer output (patterns, aggregates, roots).
+Comparisons use np.array_equal, which treats +0 and -0 as equal (the only freedom the contract
+leaves: the sign of an exact zero produced by skipped zero terms of the banded factor, R3).
+"""
+import numpy as np
+import pytest
+
+import amgf_gen as gen
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    return torch
+
+
+@pytest.fixture(scope="module")
+def amgf_mod(torch_cuda):
+    import paper_2505_18576_b200 as m
+    m.load_library()
+    return m
+
+
+def tiny(N=2, matching=True, e_max=4.0, seed=7):
+    return gen.generate(N, matching=matching, e_max=[e_max], seed=seed)
+
+
+def build_pair(oracle_lib, amgf_mod, p, D=None, Z="lattice", **cfg):
+    o = oracle_lib.Oracle.from_problem(p, D=D, Z=Z, **cfg)
+    g = amgf_mod.AMGF.from_problem(p, D=D, Z=Z, config=cfg)
+    return o, g
+
+
+def assert_hierarchy_equal(o, g):
+    assert g.nlev == o.nlev and g.nc == o.nc and g.nco == o.nco
+    assert np.array_equal(g.get(20), o.get(20))
+    for l in range(o.nlev):
+        Lo, Lg = o.levels[l], g.levels[l]
+        assert (Lo["nodes"], Lo["b"], Lo["nnzb"]) == (Lg["nodes"], Lg["b"], Lg["nnzb"]), l
+        for w in (0, 1):
+            assert np.array_equal(g.get(w, l), o.get(w, l)), (l, w)
+        assert np.array_equal(g.get(2, l), o.get(2, l)), ("A values", l)
+        assert np.array_equal(g.get(9, l), o.get(9, l)), ("l1", l)
+        assert np.array_equal(g.get(15, l), o.get(15, l)), ("comp", l)
+        if l < o.nlev - 1:
+            assert Lo["n_agg"] == Lg["n_agg"] and Lo["nnzb_P"] == Lg["nnzb_P"], l
+            assert np.array_equal(g.get(10, l), o.get(10, l)), ("aggregates", l)
+            assert np.array_equal(g.get(14, l), o.get(14, l)), ("roots", l)
+            assert np.array_equal(g.get(12, l), o.get(12, l)), ("lambda/omega", l)
+            for w in (3, 4, 5, 6, 7, 8):
+                assert np.array_equal(g.get(w, l), o.get(w, l)), (l, w)
+            assert np.array_equal(g.get(11, l + 1), o.get(11, l + 1)), ("coarse near-null", l)
+
+
+def assert_filter_factor_equal(o, g):
+    if o.nc == 0:
+        return
+    Ld = o.get(22)
+    band = g.get(22)
+    nc, bw = o.nc, g.bw
+    ref = np.zeros_like(band)
+    for i in range(nc):
+        for t in range(0, min(bw, i) + 1):
+            ref[i, bw - t] = Ld[i, i - t]
+    assert np.array_equal(band, ref)
+    # nothing outside the band in the dense factor
+    mask = np.tril(np.ones((nc, nc), bool), -bw - 1)
+    assert not Ld[mask].any()
+
+
+CASES = [
+    dict(N=2, matching=True, e_max=4.0),
+    dict(N=3, matching=False, e_max=8.0),
+    dict(N=4, matching=False, e_max=12.0),
+]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_setup_parity_tiny(oracle_lib, amgf_mod, case):
+    p = tiny(**case)
+    o, g = build_pair(oracle_lib, amgf_mod, p, coarsest_size=16)
+    assert_hierarchy_equal(o, g)
+    assert_filter_factor_equal(o, g)
+
+
+@pytest.mark.parametrize("cfg", [0, 1])
+def test_setup_parity_configs(oracle_lib, amgf_mod, cfg):
+    p = gen.config(cfg)
+    o, g = build_pair(oracle_lib, amgf_mod, p)
+    assert_hierarchy_equal(o, g)
+    assert_filter_factor_equal(o, g)
+
+
+@pytest.mark.parametrize("cfg", [0, 1])
+def test_operator_parity(oracle_lib, amgf_mod, torch_cuda, cfg):
+    p = gen.config(cfg)
+    o, g = build_pair(oracle_lib, amgf_mod, p)
+    rng = np.random.default_rng(11)
+    for l in range(o.nlev):
+        x = rng.standard_normal(o.levels[l]["nodes"] * o.levels[l]["b"])
+        assert np.array_equal(g.spmv(x, l).cpu().numpy(), o.spmv(x, l)), ("spmv", l)
+    r = rng.standard_normal(p.n)
+    assert np.array_equal(g.vcycle(r).cpu().numpy(), o.vcycle(r)), "vcycle"
+    assert np.array_equal(g.apply(r).cpu().numpy(), o.apply(r)), "apply"
+    # repeated application is deterministic
+    assert np.array_equal(g.apply(r).cpu().numpy(), o.apply(r))
+
+
+@pytest.mark.parametrize("cfg", [0, 1])
+def test_pcg_parity(oracle_lib, amgf_mod, cfg):
+    p = gen.config(cfg)
+    o, g = build_pair(oracle_lib, amgf_mod, p)
+    xo, ro = o.pcg(p.b, rtol=p.rtol)
+    xg, rg = g.pcg(p.b, rtol=p.rtol)
+    assert rg["iterations"] == ro["iterations"] and rg["converged"] and ro["converged"]
+    assert rg["relres"] == ro["relres"]
+    assert np.array_equal(xg.cpu().numpy(), xo)
+    # AMG-only baseline too
+    xo2, ro2 = o.pcg(p.b, rtol=p.rtol, maxit=60, precond="amg")
+    xg2, rg2 = g.pcg(p.b, rtol=p.rtol, max_it=60, precond="amg")
+    assert rg2["iterations"] == ro2["iterations"] and np.array_equal(xg2.cpu().numpy(), xo2)
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_solve_parity_tiny(oracle_lib, amgf_mod, case):
+    p = tiny(**case)
+    o, g = build_pair(oracle_lib, amgf_mod, p, coarsest_size=16)
+    r = np.random.default_rng(3).standard_normal(p.n)
+    assert np.array_equal(g.apply(r).cpu().numpy(), o.apply(r))
+    xo, ro = o.pcg(p.b, rtol=1e-10)
+    xg, rg = g.pcg(p.b, rtol=1e-10)
+    assert rg["iterations"] == ro["iterations"] and np.array_equal(xg.cpu().numpy(), xo)
+
+
+def test_edge_cases(oracle_lib, amgf_mod):
+    p = tiny(N=3, matching=False, e_max=6.0)
+    r = np.random.default_rng(5).standard_normal(p.n)
+    # Z = NULL: ascending order (wide band)
+    o, g = build_pair(oracle_lib, amgf_mod, p, Z=None, coarsest_size=16)
+    assert np.array_equal(g.apply(r).cpu().numpy(), o.apply(r))
+    # single-level hierarchy (coarsest = whole problem, dense Cholesky)
+    o, g = build_pair(oracle_lib, amgf_mod, tiny(N=2), coarsest_size=10 ** 6)
+    assert g.nlev == 1
+    r2 = np.random.default_rng(6).standard_normal(g.n)
+    assert np.array_equal(g.apply(r2).cpu().numpy(), o.apply(r2))
+    # more sweeps
+    o, g = build_pair(oracle_lib, amgf_mod, p, coarsest_size=16, pre_sweeps=2, post_sweeps=3)
+    assert np.array_equal(g.vcycle(r).cpu().numpy(), o.vcycle(r))
+    # zero right-hand side => zero iterations
+    x, rep = g.pcg(np.zeros(p.n))
+    assert rep["iterations"] == 0 and not x.abs().max().item()
+
+
+def test_empty_Ic(oracle_lib, amgf_mod):
+    p = tiny(N=3)
+    Jp, Jc, Jv = np.zeros(1, np.int32), np.zeros(0, np.int32), np.zeros(0)
+    o = oracle_lib.Oracle(p.nodes, p.K_ptr, p.K_col, p.K_val, Jp, Jc, Jv, np.zeros(0), None, p.B_nns, coarsest_size=16)
+    g = amgf_mod.AMGF(p.nodes, p.K_ptr, p.K_col, p.K_val, Jp, Jc, Jv, np.zeros(0), None, p.B_nns,
+                      config=dict(coarsest_size=16))
+    assert g.nc == 0
+    r = np.random.default_rng(8).standard_normal(p.n)
+    assert np.array_equal(g.apply(r).cpu().numpy(), o.apply(r))
+
+
+def test_update_D_matches_fresh_setup(oracle_lib, amgf_mod):
+    p = gen.config(0)
+    D2 = 10.0 ** (4.0 * np.random.default_rng(9).random(p.m))
+    g = amgf_mod.AMGF.from_problem(p)
+    g.update_D(D2)
+    o = oracle_lib.Oracle.from_problem(p, D=D2)
+    assert_hierarchy_equal(o, g)
+    xo, ro = o.pcg(p.b, rtol=1e-8)
+    xg, rg = g.pcg(p.b, rtol=1e-8)
+    assert rg["iterations"] == ro["iterations"] and np.array_equal(xg.cpu().numpy(), xo)
+
+
+def test_error_paths(amgf_mod):
+    p = tiny(N=2)
+    D = p.D.copy(); D[3] = -1.0
+    with pytest.raises(amgf_mod.AmgfError) as e:
+        amgf_mod.AMGF.from_problem(p, D=D)
+    assert e.value.code == -3
+    D[3] = np.inf
+    with pytest.raises(amgf_mod.AmgfError) as e:
+        amgf_mod.AMGF.from_problem(p, D=D)
+    assert e.value.code == -2
+    Z = p.Z.copy(); Z[0] = Z[1]
+    with pytest.raises(amgf_mod.AmgfError) as e:
+        amgf_mod.AMGF.from_problem(p, Z=Z)
+    assert e.value.code == -1
+    # handle stays usable after a failed update
+    g = amgf_mod.AMGF.from_problem(p)
+    with pytest.raises(amgf_mod.AmgfError):
+        g.update_D(np.full(p.m, np.nan))
+    g.update_D(p.D)
+    x, rep = g.pcg(p.b, rtol=1e-8)
+    assert rep["converged"]
+
+
+def test_host_e2e_path(oracle_lib, amgf_mod, torch_cuda):
+    p = gen.config(0)
+    g = amgf_mod.AMGF.from_problem(p)
+    b = torch_cuda.from_numpy(p.b.copy()).pin_memory()
+    x = torch_cuda.zeros(p.n, dtype=torch_cuda.float64).pin_memory()
+    rep = g.pcg_host(b, x, rtol=p.rtol)
+    xo, ro = oracle_lib.Oracle.from_problem(p).pcg(p.b, rtol=p.rtol)
+    assert rep["iterations"] == ro["iterations"] and np.array_equal(x.numpy(), xo)
+
+
+@pytest.mark.parametrize("cfg", [2])
+def test_parity_cfg2(oracle_lib, amgf_mod, cfg):
+    """Largest size the oracle solves in about a minute: non-matching interface, D up to 1e12."""
+    p = gen.config(cfg)
+    o, g = build_pair(oracle_lib, amgf_mod, p)
+    assert_hierarchy_equal(o, g)
+    r = np.random.default_rng(12).standard_normal(p.n)
+    assert np.array_equal(g.apply(r).cpu().numpy(), o.apply(r))
+    xo, ro = o.pcg(p.b, rtol=p.rtol)
+    xg, rg = g.pcg(p.b, rtol=p.rtol)
+    assert rg["iterations"] == ro["iterations"] and np.array_equal(xg.cpu().numpy(), xo)
+
+
+def test_full_size_cfg3(oracle_lib, amgf_mod, torch_cuda):
+    """cfg 3 at full size in the bench's launch configuration: the hierarchy, every level operator,
+    a V-cycle and the fine SpMV are compared bitwise with the oracle (built without the A_w factor,
+    which the oracle cannot factor densely in reasonable time); the A_w band factor is checked by
+    its residual L L^T = A_w; the PCG solution by its true residual."""
+    p = gen.config(3)
+    g = amgf_mod.AMGF.from_problem(p)
+    o = oracle_lib.Oracle.from_problem(p, factor_filter=0)
+    assert_hierarchy_equal(o, g)
+    rng = np.random.default_rng(13)
+    x = rng.standard_normal(p.n)
+    assert np.array_equal(g.spmv(x).cpu().numpy(), o.spmv(x))
+    assert np.array_equal(g.vcycle(x).cpu().numpy(), o.vcycle(x))
+    # band factor residual
+    band = g.get(22)
+    nc, bw = g.nc, g.bw
+    import scipy.sparse as sp
+    rows, cols, vals = [], [], []
+    for t in range(bw + 1):
+        i = np.arange(t, nc)
+        rows.append(i); cols.append(i - t); vals.append(band[i, bw - t])
+    Lm = sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=(nc, nc))
+    S = o.level_matrix(0).tocsr()
+    Aw = S[p.Z][:, p.Z]
+    res = abs(Lm @ Lm.T - Aw).max()
+    assert res <= 1e-13 * abs(Aw).max()
+    xg, rg = g.pcg(p.b, rtol=p.rtol)
+    assert rg["converged"]
+    xs = xg.cpu().numpy()
+    assert np.linalg.norm(S @ xs - p.b) <= 1e-5 * np.linalg.norm(p.b)
