@@ -34,6 +34,22 @@ Ctx::~Ctx() {
   if (err_host) cudaFreeHost(err_host);
 }
 
+bool debug_sync() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("AMGF_DEBUG_SYNC");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+void after_launch(Ctx &c, const char *name) {
+  c.launches++;
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && debug_sync()) e = cudaStreamSynchronize(c.stream);
+  if (e != cudaSuccess) throw Error{AMGF_ERR_CUDA, std::string(name) + ": " + cudaGetErrorString(e)};
+}
+
 void check_dev_error(Ctx &c, const char *where) {
   CK(cudaMemcpyAsync(c.err_host, c.err, 2 * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
   CK(cudaStreamSynchronize(c.stream));

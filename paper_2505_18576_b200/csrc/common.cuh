@@ -147,6 +147,11 @@ struct Ctx {
 
 inline int nblk(long n, int t = CTA) { return (int)((n + t - 1) / t); }
 
+// Post-launch bookkeeping: count the launch, surface launch errors; with AMGF_DEBUG_SYNC=1 in the
+// environment also synchronise and name the kernel that faulted.
+bool debug_sync();
+void after_launch(Ctx &c, const char *name);
+
 // check the device error flag (synchronises the stream)
 void check_dev_error(Ctx &c, const char *where);
 

@@ -39,8 +39,7 @@ static T d2h1(Ctx &c, const T *src) {
     long n_ = (n);                                                               \
     if (n_ > 0) {                                                                \
       kernel<<<nblk(n_), CTA, 0, c.stream>>>(__VA_ARGS__);                       \
-      c.launches++;                                                              \
-      CK(cudaGetLastError());                                                    \
+      after_launch(c, #kernel);                                                  \
     }                                                                            \
   } while (0)
 
@@ -728,6 +727,9 @@ void build_sell(Ctx &c, const Bsr &A, Sell &S, bool alloc) {
     S.col = c.alloc<int>(S.nslots * 32);
     S.src = c.alloc<int>(S.nslots * 32);
     S.val = c.alloc<double>(S.nslots * 32 * BB);
+    // lanes of the last slice beyond nrows are never written by k_sell_pack: mark them as padding
+    CK(cudaMemsetAsync(S.col, 0, S.nslots * 32 * sizeof(int), c.stream));
+    CK(cudaMemsetAsync(S.src, 0xff, S.nslots * 32 * sizeof(int), c.stream));
     LAUNCH(k_sell_pack, A.nbr, A.nbr, BB, A.ptr, A.col, S.slice_ptr, S.col, S.src);
   }
   LAUNCH(k_sell_vals, S.nslots * 32, S.nslots, BB, S.src, A.val, S.val);
@@ -747,8 +749,7 @@ static void band_alloc(Ctx &c, int n, int bw, double *&Lrow, double *&Lcol, doub
 static void band_factor(Ctx &c, int n, int bw, double *Lrow, double *Lcol, double *dinv, int tag) {
   const int W = band_stride(bw);
   k_band_chol<<<1, 1024, 0, c.stream>>>(n, bw, W, Lrow, c.err, tag);
-  c.launches++;
-  CK(cudaGetLastError());
+  after_launch(c, "k_band_chol");
   LAUNCH(k_band_finish, (long)n * (bw + 1), n, bw, W, Lrow, Lcol, dinv);
 }
 
@@ -822,8 +823,7 @@ static void level_numeric(Ctx &c, int l, LevelCache &lc) {
     else
       k_spgemm_vals<6, 6, 6><<<nblk(threads), CTA, 0, c.stream>>>(L.A.nbr, L.A.ptr, L.A.col, L.A.val, L.P.ptr, L.P.col,
                                                                   L.P.val, L.AP.ptr, L.AP.col, L.AP.val);
-    c.launches++;
-    CK(cudaGetLastError());
+    after_launch(c, "k_spgemm_vals(AP)");
   }
   // G = R * AP
   {
@@ -834,8 +834,7 @@ static void level_numeric(Ctx &c, int l, LevelCache &lc) {
     else
       k_spgemm_vals<6, 6, 6><<<nblk(threads), CTA, 0, c.stream>>>(L.R.nbr, L.R.ptr, L.R.col, L.R.val, L.AP.ptr,
                                                                   L.AP.col, L.AP.val, lc.G.ptr, lc.G.col, lc.G.val);
-    c.launches++;
-    CK(cudaGetLastError());
+    after_launch(c, "k_spgemm_vals(G)");
   }
   LAUNCH(k_sym, lc.G.nnzb, lc.G.nnzb, lc.G_rowof, lc.G.ptr, lc.G.col, lc.G.val, Lc.A.val, c.err);
   LAUNCH(k_diag, (long)Lc.nodes * Lc.b, Lc.nodes, Lc.b, Lc.A.ptr, Lc.A.col, Lc.A.val, Lc.dl1, Lc.dpt);

@@ -118,8 +118,7 @@ static void sell_dispatch(Ctx &c, const Sell &A, int mode, const double *x, cons
     case MODE_SMOOTH_ADD: k_sell<BR, BC, MODE_SMOOTH_ADD><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp); break;
     case MODE_ADDTO: k_sell<BR, BC, MODE_ADDTO><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp); break;
   }
-  c.launches++;
-  CK(cudaGetLastError());
+  after_launch(c, __func__);
 }
 
 void launch_sell_spmv(Ctx &c, const Sell &A, int mode, const double *x, const double *b, const double *d,
@@ -179,8 +178,7 @@ void launch_restrict(Ctx &c, const Bsr &R, const double *r, double *bc) {
   long threads = (long)R.nbr * 32;
   if (R.bc == 3) k_restrict<3><<<nblk(threads), CTA, 0, c.stream>>>(R.nbr, R.ptr, R.col, R.val, r, bc);
   else k_restrict<6><<<nblk(threads), CTA, 0, c.stream>>>(R.nbr, R.ptr, R.col, R.val, r, bc);
-  c.launches++;
-  CK(cudaGetLastError());
+  after_launch(c, __func__);
 }
 
 // ------------------------------------------------------------------ vector kernels
@@ -218,22 +216,22 @@ static int vgrid(long n) {
 }
 
 void launch_jacobi0(Ctx &c, long n, const double *b, const double *d, double *x) {
-  k_jacobi0<<<vgrid(n), CTA, 0, c.stream>>>(n, b, d, x); c.launches++; CK(cudaGetLastError());
+  k_jacobi0<<<vgrid(n), CTA, 0, c.stream>>>(n, b, d, x); after_launch(c, __func__);
 }
 void launch_copy(Ctx &c, long n, const double *s, double *d) {
-  k_copy<<<vgrid(n), CTA, 0, c.stream>>>(n, s, d); c.launches++; CK(cudaGetLastError());
+  k_copy<<<vgrid(n), CTA, 0, c.stream>>>(n, s, d); after_launch(c, __func__);
 }
 void launch_zero(Ctx &c, long n, double *d) {
-  k_zero<<<vgrid(n), CTA, 0, c.stream>>>(n, d); c.launches++; CK(cudaGetLastError());
+  k_zero<<<vgrid(n), CTA, 0, c.stream>>>(n, d); after_launch(c, __func__);
 }
 void launch_add(Ctx &c, long n, const double *a, const double *b, double *o) {
-  k_add<<<vgrid(n), CTA, 0, c.stream>>>(n, a, b, o); c.launches++; CK(cudaGetLastError());
+  k_add<<<vgrid(n), CTA, 0, c.stream>>>(n, a, b, o); after_launch(c, __func__);
 }
 void launch_axpy2(Ctx &c, long n, const double *p, const double *q, double *x, double *r) {
-  k_axpy2<<<vgrid(n), CTA, 0, c.stream>>>(n, c.sc, p, q, x, r); c.launches++; CK(cudaGetLastError());
+  k_axpy2<<<vgrid(n), CTA, 0, c.stream>>>(n, c.sc, p, q, x, r); after_launch(c, __func__);
 }
 void launch_xpby(Ctx &c, long n, const double *z, double *p) {
-  k_xpby<<<vgrid(n), CTA, 0, c.stream>>>(n, c.sc, z, p); c.launches++; CK(cudaGetLastError());
+  k_xpby<<<vgrid(n), CTA, 0, c.stream>>>(n, c.sc, z, p); after_launch(c, __func__);
 }
 
 // ------------------------------------------------------------------ dots (C14, C15)
@@ -274,8 +272,7 @@ __global__ void __launch_bounds__(CTA) k_dot2(long C, const double *__restrict__
 
 void launch_dot_finish(Ctx &c, long C, int finish) {
   k_dot2<<<1, CTA, 0, c.stream>>>(C, c.dot_part, c.sc, finish, c.err);
-  c.launches++;
-  CK(cudaGetLastError());
+  after_launch(c, __func__);
 }
 
 void launch_dot(Ctx &c, long n, int b, const double *u, const double *v, int finish) {
@@ -283,11 +280,10 @@ void launch_dot(Ctx &c, long n, int b, const double *u, const double *v, int fin
   long C = (nb + CTA - 1) / CTA;
   if (C > 0) {
     k_dot1<<<(int)C, CTA, 0, c.stream>>>(nb, b, u, v, c.dot_part);
-    c.launches++;
+    after_launch(c, "k_dot1");
   }
   k_dot2<<<1, CTA, 0, c.stream>>>(C, c.dot_part, c.sc, finish, c.err);
-  c.launches++;
-  CK(cudaGetLastError());
+  after_launch(c, __func__);
 }
 
 // ------------------------------------------------------------------ banded triangular solves (C10)
@@ -469,8 +465,7 @@ void launch_band_trsv(Ctx &c, int n, int bw, const double *Lrow, const double *L
     default:
       k_band_trsv_wide<<<1, 1024, 0, c.stream>>>(n, bw, Lrow, dinv, v, gather, y, scatter, xout, work);
   }
-  c.launches++;
-  CK(cudaGetLastError());
+  after_launch(c, __func__);
 }
 
 // ------------------------------------------------------------------ thin second residual (C11)
@@ -489,8 +484,7 @@ void launch_thin_resid(Ctx &c, int nthin, const int *rows, const int *ptr, const
                        const double *y, double *r) {
   if (nthin == 0) return;
   k_thin<<<nblk(nthin), CTA, 0, c.stream>>>(nthin, rows, ptr, pos, val, y, r);
-  c.launches++;
-  CK(cudaGetLastError());
+  after_launch(c, __func__);
 }
 
 // ------------------------------------------------------------------ setup-side BSR SpMV (C2)
@@ -512,8 +506,7 @@ void launch_bsr_spmv(Ctx &c, const Bsr &A, const double *x, double *y) {
   long rows = (long)A.nbr * A.br;
   if (rows == 0) return;
   k_bsr_spmv<<<nblk(rows), CTA, 0, c.stream>>>(A.nbr, A.br, A.bc, A.ptr, A.col, A.val, x, y);
-  c.launches++;
-  CK(cudaGetLastError());
+  after_launch(c, __func__);
 }
 
 }  // namespace amgf
