@@ -94,7 +94,7 @@ def level_bytes(g):
     for l, L in enumerate(g.levels):
         b, n = L["b"], L["nodes"] * L["b"]
         if l == g.nlev - 1:
-            tot += 2 * (g.nco * ((g.nco + 2) & ~1)) * 8 + 16 * n   # coarsest dense band pair
+            tot += 2 * (g.nco * g.nco) * 8 // 2 + 16 * n   # coarsest dense factor read twice (lower half)
             continue
         A = L["nnzb"] * (8 * b * b + 4) + 4 * L["nodes"]
         Pb = L["nnzb_P"] * (8 * 6 * b + 4)
@@ -224,8 +224,7 @@ def run_amgf(args, rank, world, local_rank):
     peak, peak_src = peaks()
     sb = spmv_bytes(g)
     vb = level_bytes(g)
-    W = (g.bw + 2) & ~1
-    filt_bytes = 2 * g.nc * W * 8
+    filt_bytes = 2 * g.nc * (g.bw + 1) * 8
     apply_bytes = 2 * vb + sb + filt_bytes + 6 * 8 * p.n
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "spmv_traffic.json")

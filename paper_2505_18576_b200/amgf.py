@@ -209,7 +209,8 @@ class AMGF:
     def get(self, which, level=0):
         Lv = self.levels[level]
         b, nodes = Lv["b"], Lv["nodes"]
-        W = (self.bw + 2) & ~1
+        R = (self.bw + 31) // 32 + 1
+        W = 32 * R if R <= 8 else (self.bw + 2) & ~1
         shapes = {0: (nodes + 1, np.int32), 1: (Lv["nnzb"], np.int32), 2: ((Lv["nnzb"], b * b), np.float64),
                   3: (nodes + 1, np.int32), 4: (Lv["nnzb_P"], np.int32), 5: ((Lv["nnzb_P"], b * 6), np.float64),
                   6: (Lv["n_agg"] + 1, np.int32), 7: (Lv["nnzb_P"], np.int32),

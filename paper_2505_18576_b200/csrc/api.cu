@@ -76,7 +76,7 @@ void vcycle(Ctx &c, int l, const double *b, double *x, const double *add) {
   Level &L = c.lev[l];
   if (l == c.nlev - 1) {
     double *dst = add ? L.x2 : x;
-    launch_band_trsv(c, c.nco, c.nco - 1, c.Lc_row, c.Lc_col, c.Lc_dinv, b, nullptr, dst, nullptr, nullptr, L.r);
+    launch_band_trsv(c, c.nco, c.nco - 1, c.Lc_col, c.Lc_rev, c.Lc_dinv, b, nullptr, dst, nullptr, nullptr, L.r);
     if (add) launch_add(c, L.n, add, dst, x);
     return;
   }
@@ -112,7 +112,7 @@ void apply_M(Ctx &c, const double *r, double *z) {
     return;
   }
   launch_sell_spmv(c, L0.As, SPMV_RESID, c.w_x1, r, nullptr, nullptr, c.w_r1, nullptr);
-  launch_band_trsv(c, c.nc, c.bw, c.Lrow, c.Lcol, c.Ldinv, c.w_r1, c.Z, c.fv, c.Z, c.w_x1, c.w_xv);
+  launch_band_trsv(c, c.nc, c.bw, c.Lcol, c.Lrev, c.Ldinv, c.w_r1, c.Z, c.fv, c.Z, c.w_x1, c.w_xv);
   launch_thin_resid(c, c.nthin, c.thin_row, c.thin_ptr, c.thin_pos, c.thin_val, c.fv, c.w_r1);
   vcycle(c, 0, c.w_r1, z, c.w_x1);
 }
@@ -281,7 +281,7 @@ amgf_status amgf_spmv(amgf_handle h, int32_t level, const double *x, double *y, 
     REQUIRE(level >= 0 && level < h->nlev, AMGF_ERR_ARG, "bad level");
     h->stream = (cudaStream_t)stream;
     Level &L = h->lev[level];
-    if (L.As.nrows == L.nodes && L.As.val) launch_sell_spmv(*h, L.As, SPMV_Y, x, nullptr, nullptr, nullptr, y, nullptr);
+    if (L.As.val) launch_sell_spmv(*h, L.As, SPMV_Y, x, nullptr, nullptr, nullptr, y, nullptr);
     else launch_bsr_spmv(*h, L.A, x, y);
     return AMGF_OK;
   });

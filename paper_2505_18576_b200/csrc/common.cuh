@@ -110,6 +110,7 @@ struct Ctx {
   int *Z = nullptr, *pos = nullptr;
   double *Lrow = nullptr;   // band, row-major: Lrow[i*W + bw - (i-k)] = L_ik, W = band_stride(bw)
   double *Lcol = nullptr;   // band, column-major: Lcol[k*W + (i-k)] = L_ik
+  double *Lrev = nullptr;   // band, reversed rows: Lrev[i*W + (i-k)] = L_ik
   double *Ldinv = nullptr;  // 1/L_ii
   double *fv = nullptr;     // filter workspace (nc)
   int nthin = 0;
@@ -119,7 +120,7 @@ struct Ctx {
   int nlev = 0;
   Level lev[MAXLEV];
   int nco = 0;
-  double *Lc_row = nullptr, *Lc_col = nullptr, *Lc_dinv = nullptr;
+  double *Lc_row = nullptr, *Lc_col = nullptr, *Lc_rev = nullptr, *Lc_dinv = nullptr;
   // solve workspace
   double *w_x1 = nullptr, *w_r1 = nullptr, *w_xv = nullptr;
   double *p = nullptr, *q = nullptr, *rr = nullptr, *zz = nullptr, *xx = nullptr, *bb = nullptr;
@@ -166,12 +167,15 @@ void launch_dot(Ctx &c, long n, int b, const double *u, const double *v, int fin
 void launch_dot_finish(Ctx &c, long n_partials, int finish);  // C14 level 2 over c.dot_part
 void launch_axpy2(Ctx &c, long n, const double *p, const double *q, double *x, double *r);
 void launch_xpby(Ctx &c, long n, const double *z, double *p);
-// y = L^{-T} L^{-1} v[gather] (C10); if scatter: xout[scatter[a]] += y[a].  Band storage: row stride
-// W = (bw+2)&~1, 64 zero rows of padding before and after (see band_alloc in setup.cu).
-void launch_band_trsv(Ctx &c, int n, int bw, const double *Lrow, const double *Lcol, const double *dinv,
+// y = L^{-T} L^{-1} v[gather] (C10); if scatter: xout[scatter[a]] += y[a].  Band storage (row stride
+// W = band_stride(bw)): Lcol[j*W + t] = L_{j+t,j}, Lrev[k*W + d] = L_{k,k-d}; zero outside the band.
+void launch_band_trsv(Ctx &c, int n, int bw, const double *Lcol, const double *Lrev, const double *dinv,
                       const double *v, const int *gather, double *y, const int *scatter, double *xout,
                       double *work);
-inline int band_stride(int bw) { return (bw + 2) & ~1; }
+// Band storage row stride: 32*R (R = window registers per lane of the warp TRSV, zero padded so that a
+// round of 32 band columns is one contiguous TMA bulk copy); wider bands use the fallback kernel.
+__host__ __device__ inline int band_R(int bw) { return (bw + 31) / 32 + 1; }
+__host__ __device__ inline int band_stride(int bw) { return band_R(bw) <= 8 ? 32 * band_R(bw) : ((bw + 2) & ~1); }
 constexpr int BAND_PAD_ROWS = 64;
 void launch_thin_resid(Ctx &c, int nthin, const int *rows, const int *ptr, const int *pos, const double *val,
                        const double *y, double *r);
@@ -188,7 +192,7 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
                const double *B_nns);
 void setup_numeric(Ctx &c, const double *D);  // update_D
 void drop_caches(Ctx &c);
-void build_sell(Ctx &c, const Bsr &A, Sell &S, bool alloc);
+void build_sell(Ctx &c, const Bsr &A, Sell &S, bool alloc, bool split);
 
 // ------------------------------------------------------------------ solve orchestration (api.cu)
 void vcycle(Ctx &c, int l, const double *b, double *x, const double *add);

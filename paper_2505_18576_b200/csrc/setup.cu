@@ -280,8 +280,8 @@ __global__ void __launch_bounds__(1024) k_band_chol(int n, int bw, int W, double
     __syncthreads();
   }
 }
-// dinv = 1/L_ii and the column-major copy of the band
-__global__ void k_band_finish(int n, int bw, int W, const double *Lrow, double *Lcol, double *dinv) {
+// dinv = 1/L_ii, the column-major copy and the reversed-row copy of the band
+__global__ void k_band_finish(int n, int bw, int W, const double *Lrow, double *Lcol, double *Lrev, double *dinv) {
   long q = blockIdx.x * (long)blockDim.x + threadIdx.x;
   if (q >= (long)n * (bw + 1)) return;
   const int i = (int)(q / (bw + 1)), t = (int)(q % (bw + 1));  // L_{i, i-t}
@@ -289,6 +289,7 @@ __global__ void k_band_finish(int n, int bw, int W, const double *Lrow, double *
   if (k < 0) return;
   const double v = Lrow[(long)i * W + bw - t];
   Lcol[(long)k * W + t] = v;
+  Lrev[(long)i * W + t] = v;
   if (t == 0) dinv[i] = 1.0 / v;
 }
 
@@ -646,9 +647,10 @@ __global__ void k_sym(long nnzb, const int *rowof, const int *ptr, const int *co
 }
 
 // ------------------------------------------------------------------ SELL-32 packing
-__global__ void k_row_len(int nrows, const int *ptr, int *len) {
+// SELL rows are block rows (split = 1) or the scalar rows of the blocks (split = br, block shape 1 x bc)
+__global__ void k_row_len(int nrows, int split, const int *ptr, int *len) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < nrows) len[i] = ptr[i + 1] - ptr[i];
+  if (i < nrows) len[i] = ptr[i / split + 1] - ptr[i / split];
 }
 __global__ void k_slice_width(int nslices, int nrows, const int *len, int *width) {
   int s = blockIdx.x * blockDim.x + threadIdx.x;
@@ -660,20 +662,24 @@ __global__ void k_slice_width(int nslices, int nrows, const int *len, int *width
   }
   width[s] = w;
 }
-__global__ void k_sell_pack(int nrows, int BB, const int *ptr, const int *col, const int *slice_ptr,
+// ssrc = source BSR block index * split + scalar row within the block (or -1 for padding)
+__global__ void k_sell_pack(int nrows, int split, const int *ptr, const int *col, const int *slice_ptr,
                             int *scol, int *ssrc) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nrows) return;
   const int lane = i & 31;
+  const int ib = i / split, r = i % split;
   const long base = slice_ptr[i >> 5];
   const int w = slice_ptr[(i >> 5) + 1] - slice_ptr[i >> 5];
-  const int len = ptr[i + 1] - ptr[i];
+  const int len = ptr[ib + 1] - ptr[ib];
   for (int s = 0; s < w; s++) {
     const long slot = base + s;
-    if (s < len) { scol[slot * 32 + lane] = col[ptr[i] + s]; ssrc[slot * 32 + lane] = ptr[i] + s; }
+    if (s < len) { scol[slot * 32 + lane] = col[ptr[ib] + s]; ssrc[slot * 32 + lane] = (ptr[ib] + s) * split + r; }
     else { scol[slot * 32 + lane] = 0; ssrc[slot * 32 + lane] = -1; }
   }
 }
+// BB = values per SELL entry (br*bc, or bc when split); the source entry q of a split row is
+// row r of block q/split, i.e. the BB consecutive values at val[q*BB].
 __global__ void k_sell_vals(long nslots, int BB, const int *ssrc, const double *val, double *sval) {
   long q = blockIdx.x * (long)blockDim.x + threadIdx.x;  // q = slot*32 + lane
   if (q >= nslots * 32) return;
@@ -711,16 +717,17 @@ static int *rowof(Ctx &c, const Bsr &A) {
   return r;
 }
 
-void build_sell(Ctx &c, const Bsr &A, Sell &S, bool alloc) {
-  const int BB = A.br * A.bc;
+void build_sell(Ctx &c, const Bsr &A, Sell &S, bool alloc, bool split) {
+  const int sp = split ? A.br : 1;
+  const int BB = split ? A.bc : A.br * A.bc;
   if (alloc) {
-    S.nrows = A.nbr; S.br = A.br; S.bc = A.bc;
-    S.nslices = (A.nbr + 31) / 32;
-    S.rowlen = c.alloc<int>(A.nbr);
-    LAUNCH(k_row_len, A.nbr, A.nbr, A.ptr, S.rowlen);
+    S.nrows = A.nbr * sp; S.br = split ? 1 : A.br; S.bc = A.bc;
+    S.nslices = (S.nrows + 31) / 32;
+    S.rowlen = c.alloc<int>(S.nrows);
+    LAUNCH(k_row_len, S.nrows, S.nrows, sp, A.ptr, S.rowlen);
     int *width = c.alloc<int>(S.nslices + 1);
     CK(cudaMemsetAsync(width, 0, (S.nslices + 1) * sizeof(int), c.stream));
-    LAUNCH(k_slice_width, S.nslices, S.nslices, A.nbr, S.rowlen, width);
+    LAUNCH(k_slice_width, S.nslices, S.nslices, S.nrows, S.rowlen, width);
     S.slice_ptr = c.alloc<int>(S.nslices + 1);
     S.nslots = scan_ex(c, width, S.slice_ptr, S.nslices);
     c.release(width);
@@ -730,27 +737,29 @@ void build_sell(Ctx &c, const Bsr &A, Sell &S, bool alloc) {
     // lanes of the last slice beyond nrows are never written by k_sell_pack: mark them as padding
     CK(cudaMemsetAsync(S.col, 0, S.nslots * 32 * sizeof(int), c.stream));
     CK(cudaMemsetAsync(S.src, 0xff, S.nslots * 32 * sizeof(int), c.stream));
-    LAUNCH(k_sell_pack, A.nbr, A.nbr, BB, A.ptr, A.col, S.slice_ptr, S.col, S.src);
+    LAUNCH(k_sell_pack, S.nrows, S.nrows, sp, A.ptr, A.col, S.slice_ptr, S.col, S.src);
   }
   LAUNCH(k_sell_vals, S.nslots * 32, S.nslots, BB, S.src, A.val, S.val);
 }
 
-static void band_alloc(Ctx &c, int n, int bw, double *&Lrow, double *&Lcol, double *&dinv) {
+static void band_alloc(Ctx &c, int n, int bw, double *&Lrow, double *&Lcol, double *&Lrev, double *&dinv) {
   const int W = band_stride(bw);
   const size_t total = (size_t)(n + 2 * BAND_PAD_ROWS) * W;
-  double *r = c.alloc<double>(total), *cl = c.alloc<double>(total);
+  double *r = c.alloc<double>(total), *cl = c.alloc<double>(total), *rv = c.alloc<double>(total);
   CK(cudaMemsetAsync(r, 0, total * sizeof(double), c.stream));
   CK(cudaMemsetAsync(cl, 0, total * sizeof(double), c.stream));
+  CK(cudaMemsetAsync(rv, 0, total * sizeof(double), c.stream));
   Lrow = r + (size_t)BAND_PAD_ROWS * W;
   Lcol = cl + (size_t)BAND_PAD_ROWS * W;
+  Lrev = rv + (size_t)BAND_PAD_ROWS * W;
   dinv = c.alloc<double>(n);
 }
 
-static void band_factor(Ctx &c, int n, int bw, double *Lrow, double *Lcol, double *dinv, int tag) {
+static void band_factor(Ctx &c, int n, int bw, double *Lrow, double *Lcol, double *Lrev, double *dinv, int tag) {
   const int W = band_stride(bw);
   k_band_chol<<<1, 1024, 0, c.stream>>>(n, bw, W, Lrow, c.err, tag);
   after_launch(c, "k_band_chol");
-  LAUNCH(k_band_finish, (long)n * (bw + 1), n, bw, W, Lrow, Lcol, dinv);
+  LAUNCH(k_band_finish, (long)n * (bw + 1), n, bw, W, Lrow, Lcol, Lrev, dinv);
 }
 
 // --------------------------------------------------------------- numeric pieces (reused by update_D)
@@ -773,7 +782,7 @@ static void filter_numeric(Ctx &c) {
   CK(cudaMemsetAsync(c.Lrow - (size_t)BAND_PAD_ROWS * W, 0, (size_t)(c.nc + 2 * BAND_PAD_ROWS) * W * sizeof(double),
                      c.stream));
   LAUNCH(k_band_fill, c.nc, c.nc, c.bw, W, c.Z, c.pos, L0.A.ptr, L0.A.col, L0.A.val, c.Lrow);
-  band_factor(c, c.nc, c.bw, c.Lrow, c.Lcol, c.Ldinv, 1);
+  band_factor(c, c.nc, c.bw, c.Lrow, c.Lcol, c.Lrev, c.Ldinv, 1);
 }
 
 static void thin_numeric(Ctx &c, long nthin_nnz) {
@@ -846,7 +855,7 @@ static void coarsest_numeric(Ctx &c) {
   CK(cudaMemsetAsync(c.Lc_row - (size_t)BAND_PAD_ROWS * W, 0, (size_t)(n + 2 * BAND_PAD_ROWS) * W * sizeof(double),
                      c.stream));
   LAUNCH(k_dense_band, (long)L.nodes * L.b, L.nodes, L.b, L.A.ptr, L.A.col, L.A.val, n, W, c.Lc_row);
-  band_factor(c, n, bw, c.Lc_row, c.Lc_col, c.Lc_dinv, 2);
+  band_factor(c, n, bw, c.Lc_row, c.Lc_col, c.Lc_rev, c.Lc_dinv, 2);
 }
 
 // per-context arrays needed by the numeric re-setup (owned by Ctx::setup_cache)
@@ -973,7 +982,7 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
     LAUNCH(k_band_start, c.nc, c.nc, c.Z, c.pos, L0.A.ptr, L0.A.col, bwd);
     c.bw = d2h1(c, bwd);
     c.release(bwd);
-    band_alloc(c, c.nc, c.bw, c.Lrow, c.Lcol, c.Ldinv);
+    band_alloc(c, c.nc, c.bw, c.Lrow, c.Lcol, c.Lrev, c.Ldinv);
     c.fv = c.alloc<double>(c.nc);
     filter_numeric(c);
     check_dev_error(c, "A_w Cholesky");
@@ -1150,8 +1159,8 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
     }
     level_numeric(c, l, lc);
     check_dev_error(c, "Galerkin product");
-    build_sell(c, L.A, L.As, true);
-    build_sell(c, L.P, L.Ps, true);
+    build_sell(c, L.A, L.As, true, l > 0);   // coarse levels: one thread per scalar row (1 x 6)
+    build_sell(c, L.P, L.Ps, true, l > 0);
     l++;
   }
   c.nlev = l + 1;
@@ -1160,7 +1169,7 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
     Level &L = c.lev[c.nlev - 1];
     REQUIRE(L.n <= 16384, AMGF_ERR_LIMIT, "coarsest level too large for a dense factor (" + std::to_string(L.n) + ")");
     c.nco = (int)L.n;
-    band_alloc(c, c.nco, c.nco - 1, c.Lc_row, c.Lc_col, c.Lc_dinv);
+    band_alloc(c, c.nco, c.nco - 1, c.Lc_row, c.Lc_col, c.Lc_rev, c.Lc_dinv);
     coarsest_numeric(c);
     check_dev_error(c, "coarsest Cholesky");
   }
@@ -1172,7 +1181,7 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
     L.bv = c.alloc<double>(L.n);
     L.r = c.alloc<double>(L.n);
   }
-  if (c.nlev == 1) build_sell(c, L0.A, L0.As, true);
+  if (c.nlev == 1) build_sell(c, L0.A, L0.As, true, false);
   c.w_x1 = c.alloc<double>(n);
   c.w_r1 = c.alloc<double>(n);
   c.w_xv = c.alloc<double>(n);
@@ -1203,10 +1212,10 @@ void setup_numeric(Ctx &c, const double *D) {
   for (int l = 0; l + 1 < c.nlev; l++) {
     level_numeric(c, l, C.lc[l]);
     check_dev_error(c, "Galerkin product");
-    build_sell(c, c.lev[l].A, c.lev[l].As, false);
-    build_sell(c, c.lev[l].P, c.lev[l].Ps, false);
+    build_sell(c, c.lev[l].A, c.lev[l].As, false, l > 0);
+    build_sell(c, c.lev[l].P, c.lev[l].Ps, false, l > 0);
   }
-  if (c.nlev == 1) build_sell(c, L0.A, L0.As, false);
+  if (c.nlev == 1) build_sell(c, L0.A, L0.As, false, false);
   coarsest_numeric(c);
   check_dev_error(c, "coarsest Cholesky");
 }

@@ -14,12 +14,12 @@ namespace amgf {
 
 __device__ __forceinline__ double ldg_stream(const double *p) {
   double v;
-  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
 __device__ __forceinline__ int ldg_stream_i(const int *p) {
   int v;
-  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
 
@@ -58,17 +58,36 @@ __global__ void __launch_bounds__(CTA) k_sell(int nrows, const int *__restrict__
     const long base = slice_ptr[row >> 5];
     const int *cp = col + base * 32 + lane;
     const double *vp = val + base * (BR * BC * 32) + lane;
-#pragma unroll 2
-    for (int s = 0; s < len; s++) {
-      const int c = ldg_stream_i(cp + (long)s * 32);
-      double xv[BC];
+    // software pipeline: slot s+1's column, values and x gather are in flight while slot s is consumed
+    double vcur[BR * BC], xcur[BC];
+    int cnext = 0;
+    if (len > 0) {
+      const int c0 = ldg_stream_i(cp);
 #pragma unroll
-      for (int e = 0; e < BC; e++) xv[e] = x[(long)c * BC + e];
-      const double *v = vp + (long)s * (BR * BC * 32);
+      for (int e = 0; e < BC; e++) xcur[e] = x[(long)c0 * BC + e];
+#pragma unroll
+      for (int q = 0; q < BR * BC; q++) vcur[q] = ldg_stream(vp + q * 32);
+      cnext = ldg_stream_i(cp + (len > 1 ? 32 : 0));
+    }
+    for (int s = 0; s < len; s++) {
+      // branch-free prefetch (the last slot is re-read once at the end)
+      const int s1 = min(s + 1, len - 1), s2 = min(s + 2, len - 1);
+      const double *v = vp + (long)s1 * (BR * BC * 32);
+      double vnx[BR * BC], xnx[BC];
+#pragma unroll
+      for (int q = 0; q < BR * BC; q++) vnx[q] = ldg_stream(v + q * 32);
+#pragma unroll
+      for (int e = 0; e < BC; e++) xnx[e] = x[(long)cnext * BC + e];
+      const int cnn = ldg_stream_i(cp + (long)s2 * 32);
 #pragma unroll
       for (int r = 0; r < BR; r++)
 #pragma unroll
-        for (int e = 0; e < BC; e++) acc[r] = __fma_rn(ldg_stream(v + (r * BC + e) * 32), xv[e], acc[r]);
+        for (int e = 0; e < BC; e++) acc[r] = __fma_rn(vcur[r * BC + e], xcur[e], acc[r]);
+#pragma unroll
+      for (int q = 0; q < BR * BC; q++) vcur[q] = vnx[q];
+#pragma unroll
+      for (int e = 0; e < BC; e++) xcur[e] = xnx[e];
+      cnext = cnn;
     }
   }
   if (MODE == MODE_DOT) {
@@ -124,12 +143,14 @@ static void sell_dispatch(Ctx &c, const Sell &A, int mode, const double *x, cons
 void launch_sell_spmv(Ctx &c, const Sell &A, int mode, const double *x, const double *b, const double *d,
                       const double *add, double *y, double *dp) {
   if (A.br == 3 && A.bc == 3) sell_dispatch<3, 3>(c, A, mode, x, b, d, add, y, dp);
+  else if (A.br == 1 && A.bc == 6) sell_dispatch<1, 6>(c, A, mode, x, b, d, add, y, dp);
   else if (A.br == 6 && A.bc == 6) sell_dispatch<6, 6>(c, A, mode, x, b, d, add, y, dp);
   else throw Error{AMGF_ERR_ARG, "sell spmv: unsupported block shape"};
 }
 
 void launch_prolong(Ctx &c, const Sell &P, const double *xc, double *x) {
   if (P.br == 3) sell_dispatch<3, 6>(c, P, MODE_ADDTO, xc, nullptr, nullptr, nullptr, x, nullptr);
+  else if (P.br == 1) sell_dispatch<1, 6>(c, P, MODE_ADDTO, xc, nullptr, nullptr, nullptr, x, nullptr);
   else if (P.br == 6) sell_dispatch<6, 6>(c, P, MODE_ADDTO, xc, nullptr, nullptr, nullptr, x, nullptr);
   else throw Error{AMGF_ERR_ARG, "prolong: unsupported block shape"};
 }
@@ -146,6 +167,7 @@ __global__ void __launch_bounds__(CTA) k_restrict(int nrows, const int *__restri
 #pragma unroll
   for (int q = 0; q < 6; q++) acc[q] = 0.0;
   const int end = ptr[w + 1];
+#pragma unroll 4
   for (int k = ptr[w] + lane; k < end; k += 32) {
     const int c = col[k];
     double rv[B];
@@ -287,132 +309,176 @@ void launch_dot(Ctx &c, long n, int b, const double *u, const double *v, int fin
 }
 
 // ------------------------------------------------------------------ banded triangular solves (C10)
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
-
-// copy `count` doubles (count*8 divisible by 16, both pointers 16-byte aligned) global -> smem, one warp
-__device__ __forceinline__ void warp_stage(double *dst, const double *src, int count, int lane) {
-  const int chunks = count / 2;
-  for (int k = lane; k < chunks; k += 32) cp_async16(dst + 2 * k, src + 2 * k);
+__device__ __forceinline__ void mbar_arrive_expect(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// TMA bulk copy global -> shared (SASS UBLKCP), completion counted on an mbarrier
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// One warp.  Forward:  w = L^{-1} v, column sweep over j ascending; backward: y = L^{-T} w, column
-// sweep over k descending.  Lane l owns window rows j0 + l + 32 s (s < R); requires bw <= 32(R-1).
-// Band storage has even row stride W = (bw+2)&~1 and 64 rows of zero padding on both sides
-// (rounds prefetch up to 63 rows past either end).
-template <int R>
-__global__ void __launch_bounds__(32) k_band_trsv(int n, int bw, const double *__restrict__ Lrow,
-                                                  const double *__restrict__ Lcol, const double *__restrict__ dinv,
+// One warp solves L L^T y = v[gather] (C10).  Forward: column sweep j ascending over Lcol
+// (Lcol[j*W + t] = L_{j+t,j}); backward: row sweep k descending over Lrev (Lrev[k*W + d] = L_{k,k-d}).
+// Lane l keeps the accumulators of rows j0 + l + 32 s (s < R, 32(R-1) >= bw) in registers.  Each round of
+// 32 pivots stages its 32 band columns (rows) in shared memory with row stride Ws = 32 R, zero beyond the
+// band, so that every update is an unconditional FMA: out-of-band terms are exact zeros (fma(-0, y, a) = a)
+// and updates of already finished rows are dead.  Lane jj issues the TMA bulk copy of the round's jj-th
+// column; the next round's copies are in flight while the current round computes (double buffer).
+template <int R, int NB>
+__global__ void __launch_bounds__(32) k_band_trsv(int n, int bw, const double *__restrict__ Lcol,
+                                                  const double *__restrict__ Lrev, const double *__restrict__ dinv,
                                                   const double *__restrict__ v, const int *__restrict__ gather,
                                                   double *__restrict__ y, const int *__restrict__ scatter,
                                                   double *__restrict__ xout, double *__restrict__ w) {
-  extern __shared__ __align__(16) double sm[];
+  constexpr int Ws = 32 * R;               // = band storage stride (band_stride)
+  constexpr unsigned CHUNK = 32u * Ws * 8u; // one round = 32 consecutive band columns / rows
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t bar[NB];
   const int lane = threadIdx.x;
-  const int W = (bw + 2) & ~1;  // even row stride of the band storage (16-byte aligned rows)
-  const int chunk = 32 * W;
-  double *buf0 = sm, *buf1 = sm + chunk;
-  const int rounds = (n + 31) / 32;
-  double acc[R];
-  auto vin = [&](int i) -> double {
-    if (i >= n) return 0.0;
-    return gather ? v[gather[i]] : v[i];
-  };
-  // ---------------- forward
+  const int F = (n + 31) / 32;  // rounds per sweep
+  if (lane == 0) {
 #pragma unroll
-  for (int s = 0; s < R; s++) acc[s] = vin(lane + 32 * s);
-  warp_stage(buf0, Lcol, chunk, lane);
-  cp_commit();
-  for (int q = 0; q < rounds; q++) {
+    for (int b = 0; b < NB; b++) mbar_init(&bar[b], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  // stage global round g (forward g < F: columns 32g..32g+31; backward: rows k1-31..k1) into buffer g % NB
+  auto issue = [&](int g) {
+    if (g >= 2 * F || lane != 0) return;
+    const double *src = (g < F) ? Lcol + (long)(32 * g) * Ws : Lrev + (long)(n - 1 - 32 * (g - F) - 31) * Ws;
+    uint64_t *br = &bar[g % NB];
+    mbar_arrive_expect(br, CHUNK);
+    bulk_g2s(sm + (g % NB) * 32 * Ws, src, CHUNK, br);
+  };
+#pragma unroll
+  for (int g = 0; g < NB - 1; g++) issue(g);
+#pragma unroll 8
+  for (int a = lane; a < n; a += 32) y[a] = gather ? v[gather[a]] : v[a];
+  __syncwarp();
+  double acc[R];
+  // ---------------- forward: w = L^{-1} y (column sweep)
+#pragma unroll
+  for (int s = 0; s < R; s++) acc[s] = (lane + 32 * s < n) ? y[lane + 32 * s] : 0.0;
+  double dv = (lane < n) ? dinv[lane] : 0.0;
+  double vq1, dq1;  // operands of the next round, loaded one round ahead
+  {
+    const int i1 = 32 + lane + 32 * (R - 1);
+    vq1 = (i1 < n) ? y[i1] : 0.0;
+    dq1 = (32 + lane < n) ? dinv[32 + lane] : 0.0;
+  }
+  for (int q = 0; q < F; q++) {
     const int j0 = 32 * q;
-    double *cur = (q & 1) ? buf1 : buf0;
-    double *nxt = (q & 1) ? buf0 : buf1;
-    warp_stage(nxt, Lcol + (long)(j0 + 32) * W, chunk, lane);
-    cp_commit();
-    cp_wait<1>();
     __syncwarp();
-    const double dv = (j0 + lane < n) ? dinv[j0 + lane] : 0.0;
-    double mine = 0.0;
+    fence_proxy_async();
+    issue(q + NB - 1);
+    const int i2 = j0 + 64 + lane + 32 * (R - 1);
+    const double vq2 = (i2 < n) ? y[i2] : 0.0;
+    const double dq2 = (j0 + 64 + lane < n) ? dinv[j0 + 64 + lane] : 0.0;
+    mbar_wait(&bar[q % NB], (q / NB) & 1);
+    // column jj of the round at cur + jj*Ws; row i = j0+lane+32s is at offset t = lane + 32s - jj
+    const double *cur = sm + (q % NB) * 32 * Ws + lane;
+    double lc[R], mine = 0.0;
+#pragma unroll
+    for (int s = 0; s < R; s++) lc[s] = cur[32 * s];
 #pragma unroll
     for (int jj = 0; jj < 32; jj++) {
       if (j0 + jj >= n) break;
-      const double yj = __shfl_sync(0xffffffffu, acc[0] * dv, jj);
-      if (lane == jj) mine = yj;
-      const double *colj = cur + jj * W;
+      double ln[R];  // band values of the next pivot, loaded before this pivot's broadcast
 #pragma unroll
-      for (int s = 0; s < R; s++) {
-        const int off = lane + 32 * s - jj;  // i - j
-        if (off > 0 && off <= bw) acc[s] = __fma_rn(-colj[off], yj, acc[s]);
-      }
+      for (int s = 0; s < R; s++) ln[s] = cur[((jj + 1) & 31) * (Ws - 1) + 32 * s];
+      const double yj = __shfl_sync(0xffffffffu, acc[0] * dv, jj);
+      mine = (lane == jj) ? yj : mine;
+#pragma unroll
+      for (int s = 0; s < R; s++) acc[s] = __fma_rn(-lc[s], yj, acc[s]);
+#pragma unroll
+      for (int s = 0; s < R; s++) lc[s] = ln[s];
     }
     if (j0 + lane < n) w[j0 + lane] = mine;
 #pragma unroll
     for (int s = 0; s < R - 1; s++) acc[s] = acc[s + 1];
-    acc[R - 1] = vin(j0 + 32 + lane + 32 * (R - 1));
-    __syncwarp();
+    acc[R - 1] = vq1;
+    dv = dq1;
+    vq1 = vq2;
+    dq1 = dq2;
   }
-  cp_wait<0>();
   __syncwarp();
-  // ---------------- backward: rows handled top-down in rounds of 32, k1 = n-1-32q
+  // ---------------- backward: y = L^{-T} w (row sweep), pivots k = k1 - jj, k1 = n-1-32q
 #pragma unroll
   for (int s = 0; s < R; s++) {
     const int i = n - 1 - lane - 32 * s;
     acc[s] = (i >= 0) ? w[i] : 0.0;
   }
-  warp_stage(buf0, Lrow + (long)(n - 32) * W, chunk, lane);
-  cp_commit();
-  for (int q = 0; q < rounds; q++) {
+  dv = (n - 1 - lane >= 0) ? dinv[n - 1 - lane] : 0.0;
+  {
+    const int i1 = n - 1 - 32 - lane - 32 * (R - 1);
+    vq1 = (i1 >= 0) ? w[i1] : 0.0;
+    dq1 = (n - 1 - 32 - lane >= 0) ? dinv[n - 1 - 32 - lane] : 0.0;
+  }
+  for (int q = 0; q < F; q++) {
+    const int g = F + q;
     const int k1 = n - 1 - 32 * q;
-    double *cur = (q & 1) ? buf1 : buf0;
-    double *nxt = (q & 1) ? buf0 : buf1;
-    warp_stage(nxt, Lrow + (long)(k1 - 32 - 31) * W, chunk, lane);
-    cp_commit();
-    cp_wait<1>();
     __syncwarp();
-    // cur holds rows k1-31 .. k1; row k is at cur + (k - (k1-31)) * W
-    const double dv = (k1 - lane >= 0) ? dinv[k1 - lane] : 0.0;
-    double mine = 0.0;
+    fence_proxy_async();
+    issue(g + NB - 1);
+    const int i2 = k1 - 64 - lane - 32 * (R - 1);
+    const double wnew = (i2 >= 0) ? w[i2] : 0.0;
+    const double dq2 = (k1 - 64 - lane >= 0) ? dinv[k1 - 64 - lane] : 0.0;
+    mbar_wait(&bar[g % NB], (g / NB) & 1);
+    // row k = k1 - jj of the round at cur + (31 - jj)*Ws; row i = k1-lane-32s at offset d = lane + 32s - jj
+    const double *cur = sm + (g % NB) * 32 * Ws + lane;
+    double lc[R], mine = 0.0;
+#pragma unroll
+    for (int s = 0; s < R; s++) lc[s] = cur[31 * Ws + 32 * s];
 #pragma unroll
     for (int jj = 0; jj < 32; jj++) {
-      const int k = k1 - jj;
-      if (k < 0) break;
-      const double xk = __shfl_sync(0xffffffffu, acc[0] * dv, jj);
-      if (lane == jj) mine = xk;
-      const double *rowk = cur + (31 - jj) * W;
+      if (k1 - jj < 0) break;
+      double ln[R];
 #pragma unroll
-      for (int s = 0; s < R; s++) {
-        const int off = jj - lane - 32 * s + 0;  // i - k, i = k1 - lane - 32 s
-        const int dist = -off;                  // k - i
-        if (dist > 0 && dist <= bw) acc[s] = __fma_rn(-rowk[bw - dist], xk, acc[s]);
-      }
+      for (int s = 0; s < R; s++) ln[s] = cur[(31 - ((jj + 1) & 31)) * Ws - ((jj + 1) & 31) + 32 * s];
+      const double xk = __shfl_sync(0xffffffffu, acc[0] * dv, jj);
+      mine = (lane == jj) ? xk : mine;
+#pragma unroll
+      for (int s = 0; s < R; s++) acc[s] = __fma_rn(-lc[s], xk, acc[s]);
+#pragma unroll
+      for (int s = 0; s < R; s++) lc[s] = ln[s];
     }
     if (k1 - lane >= 0) y[k1 - lane] = mine;
 #pragma unroll
     for (int s = 0; s < R - 1; s++) acc[s] = acc[s + 1];
-    {
-      const int i = k1 - 32 - lane - 32 * (R - 1);
-      acc[R - 1] = (i >= 0) ? w[i] : 0.0;
-    }
-    __syncwarp();
+    acc[R - 1] = vq1;
+    dv = dq1;
+    vq1 = wnew;
+    dq1 = dq2;
   }
-  cp_wait<0>();
   __syncwarp();
   if (scatter)
     for (int a = lane; a < n; a += 32) xout[scatter[a]] = xout[scatter[a]] + y[a];
 }
 
 // Generic fallback for wide bands: one CTA, thread per row of the window, barrier per pivot.
-__global__ void __launch_bounds__(1024) k_band_trsv_wide(int n, int bw, const double *__restrict__ Lrow,
+__global__ void __launch_bounds__(1024) k_band_trsv_wide(int n, int bw, const double *__restrict__ Lcol,
+                                                         const double *__restrict__ Lrev,
                                                          const double *__restrict__ dinv, const double *__restrict__ v,
                                                          const int *__restrict__ gather, double *__restrict__ y,
                                                          const int *__restrict__ scatter, double *__restrict__ xout,
                                                          double *__restrict__ w) {
   __shared__ double piv;
-  const int W = (bw + 2) & ~1;
+  const int W = band_stride(bw);
   for (int i = threadIdx.x; i < n; i += blockDim.x) w[i] = gather ? v[gather[i]] : v[i];
   __syncthreads();
   for (int j = 0; j < n; j++) {
@@ -420,7 +486,7 @@ __global__ void __launch_bounds__(1024) k_band_trsv_wide(int n, int bw, const do
     __syncthreads();
     const double yj = piv;
     for (int i = j + 1 + threadIdx.x; i <= j + bw && i < n; i += blockDim.x)
-      w[i] = __fma_rn(-Lrow[(long)i * W + bw - (i - j)], yj, w[i]);
+      w[i] = __fma_rn(-Lcol[(long)j * W + (i - j)], yj, w[i]);
     __syncthreads();
   }
   for (int i = threadIdx.x; i < n; i += blockDim.x) y[i] = w[i];
@@ -430,7 +496,7 @@ __global__ void __launch_bounds__(1024) k_band_trsv_wide(int n, int bw, const do
     __syncthreads();
     const double xk = piv;
     for (int i = k - 1 - threadIdx.x; i >= k - bw && i >= 0; i -= blockDim.x)
-      y[i] = __fma_rn(-Lrow[(long)k * W + bw - (k - i)], xk, y[i]);
+      y[i] = __fma_rn(-Lrev[(long)k * W + (k - i)], xk, y[i]);
     __syncthreads();
   }
   if (scatter)
@@ -438,34 +504,36 @@ __global__ void __launch_bounds__(1024) k_band_trsv_wide(int n, int bw, const do
 }
 
 template <int R>
-static void trsv_R(Ctx &c, int n, int bw, const double *Lrow, const double *Lcol, const double *dinv,
+static void trsv_R(Ctx &c, int n, int bw, const double *Lcol, const double *Lrev, const double *dinv,
                    const double *v, const int *gather, double *y, const int *scatter, double *xout, double *w) {
-  size_t smem = 2 * 32 * (size_t)((bw + 2) & ~1) * sizeof(double);
+  // as many rounds in flight as 220 KB of shared memory allow (TMA latency > one round of 32 pivots)
+  constexpr int NB = (220 * 1024) / (32 * 32 * R * 8) >= 4 ? 4 : 3;
+  const size_t smem = (size_t)NB * 32 * (32 * R) * sizeof(double);
   static bool attr_set = false;
   if (!attr_set) {
-    CK(cudaFuncSetAttribute(k_band_trsv<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    CK(cudaFuncSetAttribute(k_band_trsv<R, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_set = true;
   }
-  k_band_trsv<R><<<1, 32, smem, c.stream>>>(n, bw, Lrow, Lcol, dinv, v, gather, y, scatter, xout, w);
+  k_band_trsv<R, NB><<<1, 32, smem, c.stream>>>(n, bw, Lcol, Lrev, dinv, v, gather, y, scatter, xout, w);
 }
 
-void launch_band_trsv(Ctx &c, int n, int bw, const double *Lrow, const double *Lcol, const double *dinv,
-                       const double *v, const int *gather, double *y, const int *scatter, double *xout,
-                       double *work) {
+void launch_band_trsv(Ctx &c, int n, int bw, const double *Lcol, const double *Lrev, const double *dinv,
+                      const double *v, const int *gather, double *y, const int *scatter, double *xout,
+                      double *work) {
   if (n == 0) return;
   const int R = (bw + 31) / 32 + 1;
   switch (R) {
-    case 1: case 2: trsv_R<2>(c, n, bw, Lrow, Lcol, dinv, v, gather, y, scatter, xout, work); break;
-    case 3: trsv_R<3>(c, n, bw, Lrow, Lcol, dinv, v, gather, y, scatter, xout, work); break;
-    case 4: trsv_R<4>(c, n, bw, Lrow, Lcol, dinv, v, gather, y, scatter, xout, work); break;
-    case 5: trsv_R<5>(c, n, bw, Lrow, Lcol, dinv, v, gather, y, scatter, xout, work); break;
-    case 6: trsv_R<6>(c, n, bw, Lrow, Lcol, dinv, v, gather, y, scatter, xout, work); break;
-    case 7: trsv_R<7>(c, n, bw, Lrow, Lcol, dinv, v, gather, y, scatter, xout, work); break;
-    case 8: trsv_R<8>(c, n, bw, Lrow, Lcol, dinv, v, gather, y, scatter, xout, work); break;
+    case 1: case 2: trsv_R<2>(c, n, bw, Lcol, Lrev, dinv, v, gather, y, scatter, xout, work); break;
+    case 3: trsv_R<3>(c, n, bw, Lcol, Lrev, dinv, v, gather, y, scatter, xout, work); break;
+    case 4: trsv_R<4>(c, n, bw, Lcol, Lrev, dinv, v, gather, y, scatter, xout, work); break;
+    case 5: trsv_R<5>(c, n, bw, Lcol, Lrev, dinv, v, gather, y, scatter, xout, work); break;
+    case 6: trsv_R<6>(c, n, bw, Lcol, Lrev, dinv, v, gather, y, scatter, xout, work); break;
+    case 7: trsv_R<7>(c, n, bw, Lcol, Lrev, dinv, v, gather, y, scatter, xout, work); break;
+    case 8: trsv_R<8>(c, n, bw, Lcol, Lrev, dinv, v, gather, y, scatter, xout, work); break;
     default:
-      k_band_trsv_wide<<<1, 1024, 0, c.stream>>>(n, bw, Lrow, dinv, v, gather, y, scatter, xout, work);
+      k_band_trsv_wide<<<1, 1024, 0, c.stream>>>(n, bw, Lcol, Lrev, dinv, v, gather, y, scatter, xout, work);
   }
-  after_launch(c, __func__);
+  after_launch(c, "k_band_trsv");
 }
 
 // ------------------------------------------------------------------ thin second residual (C11)
