@@ -339,6 +339,44 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 // band, so that every update is an unconditional FMA: out-of-band terms are exact zeros (fma(-0, y, a) = a)
 // and updates of already finished rows are dead.  Lane jj issues the TMA bulk copy of the round's jj-th
 // column; the next round's copies are in flight while the current round computes (double buffer).
+// x[idx[a]] += y[a] for a < n by one warp, 8 independent elements per lane in flight
+__device__ __forceinline__ void scatter_add_warp(int n, const int *__restrict__ idx, const double *__restrict__ y,
+                                                 double *__restrict__ x, int lane) {
+  for (int a0 = 0; a0 < n; a0 += 32 * 8) {
+    int id[8];
+    double yv[8], xv[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const int a = a0 + 32 * u + lane;
+      id[u] = a < n ? idx[a] : -1;
+      yv[u] = a < n ? y[a] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; u++) xv[u] = id[u] >= 0 ? x[id[u]] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; u++)
+      if (id[u] >= 0) x[id[u]] = xv[u] + yv[u];
+  }
+}
+// y[a] = v[idx[a]] (or v[a]) by one warp, batched
+__device__ __forceinline__ void gather_warp(int n, const int *__restrict__ idx, const double *__restrict__ v,
+                                            double *__restrict__ y, int lane) {
+  for (int a0 = 0; a0 < n; a0 += 32 * 8) {
+    int id[8];
+    double vv[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      const int a = a0 + 32 * u + lane;
+      id[u] = a < n ? (idx ? idx[a] : a) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; u++) vv[u] = id[u] >= 0 ? v[id[u]] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; u++)
+      if (a0 + 32 * u + lane < n) y[a0 + 32 * u + lane] = vv[u];
+  }
+}
+
 template <int R, int NB>
 __global__ void __launch_bounds__(32) k_band_trsv(int n, int bw, const double *__restrict__ Lcol,
                                                   const double *__restrict__ Lrev, const double *__restrict__ dinv,
@@ -367,8 +405,7 @@ __global__ void __launch_bounds__(32) k_band_trsv(int n, int bw, const double *_
   };
 #pragma unroll
   for (int g = 0; g < NB - 1; g++) issue(g);
-#pragma unroll 8
-  for (int a = lane; a < n; a += 32) y[a] = gather ? v[gather[a]] : v[a];
+  gather_warp(n, gather, v, y, lane);
   __syncwarp();
   double acc[R];
   // ---------------- forward: w = L^{-1} y (column sweep)
@@ -466,8 +503,7 @@ __global__ void __launch_bounds__(32) k_band_trsv(int n, int bw, const double *_
     dq1 = dq2;
   }
   __syncwarp();
-  if (scatter)
-    for (int a = lane; a < n; a += 32) xout[scatter[a]] = xout[scatter[a]] + y[a];
+  if (scatter) scatter_add_warp(n, scatter, y, xout, lane);
 }
 
 // Generic fallback for wide bands: one CTA, thread per row of the window, barrier per pivot.
