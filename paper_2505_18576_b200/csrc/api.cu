@@ -29,6 +29,9 @@ void Ctx::release(void *p) {
 
 Ctx::~Ctx() {
   drop_caches(*this);
+  if (side) cudaStreamDestroy(side);
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
   for (void *p : allocs) cudaFree(p);
   if (sc_host) cudaFreeHost(sc_host);
   if (err_host) cudaFreeHost(err_host);

@@ -93,6 +93,8 @@ struct Scalars {
 
 struct Ctx {
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;        // A_w factorization overlaps the hierarchy's numeric setup
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   amgf_config cfg;
   int nodes = 0, m = 0;
   long n = 0;

@@ -243,9 +243,84 @@ __global__ void k_band_fill(int nc, int bw, int W, const int *Z, const int *pos,
     }
 }
 
-// Right-looking banded Cholesky in place (C9): entry (i,l) receives fma(-L_ij, L_lj, .) for j ascending,
-// which is exactly the left-looking chain of the contract.  One CTA.
-__global__ void __launch_bounds__(1024) k_band_chol(int n, int bw, int W, double *L, int *err, int tag) {
+// Banded Cholesky in place (C9), blocked left-looking over panels of 32 columns, one CTA.  Entry (i,l)
+// receives fma(-L_ik, L_lk, .) for k ascending, exactly the contract's chain: phase A applies the terms of
+// all previous panels (one independent chain per entry, all threads), phase B the terms inside the panel
+// (right-looking over its 32 columns on a shared-memory copy of the panel).
+constexpr int CHOL_THREADS = 1024;
+constexpr int CHOL_EPT = 8;  // entries per thread in phase A: (32 + bw) * 32 <= 1024 * 8  =>  bw <= 224
+constexpr int PLD = 33;      // padded row stride of the panel arrays
+__global__ void __launch_bounds__(CHOL_THREADS) k_band_chol(int n, int bw, int W, double *L, int *err, int tag) {
+  extern __shared__ double sh[];
+  const int rows = 32 + bw;          // rows i = c0 + r of the panel's band
+  const int ldk = rows + 1;          // k-major staging AT[kk][r], padded
+  double *PA = sh;                   // [rows][PLD] panel accumulators
+  double *PL = sh + rows * PLD;      // [rows][PLD] final panel values of L
+  double *AT = sh + 2 * rows * PLD;  // [32][ldk]  L_{c0+r, kc+kk}, zero outside the band / k >= c0
+  const int tid = threadIdx.x;
+  for (int c0 = 0; c0 < n; c0 += 32) {
+    // ---- phase A: acc(i,l) = a_il - sum_{k < c0} L_ik L_lk in ascending k (chunks of 32 k's staged in smem)
+    double acc[CHOL_EPT];
+#pragma unroll
+    for (int q = 0; q < CHOL_EPT; q++) {
+      const int e = tid + q * CHOL_THREADS;
+      const int r = e >> 5, cc = e & 31;
+      const int i = c0 + r, l = c0 + cc;
+      acc[q] = (r < rows && i < n && l < n && i >= l && i - l <= bw) ? L[(long)i * W + bw - (i - l)] : 0.0;
+    }
+    for (int kc = max(0, c0 - bw); kc < c0; kc += 32) {
+      __syncthreads();
+      for (int t = tid; t < rows * 32; t += CHOL_THREADS) {
+        const int r = t >> 5, kk = t & 31;
+        const int i = c0 + r, k = kc + kk;
+        AT[kk * ldk + r] = (i < n && k < c0 && i - k <= bw) ? L[(long)i * W + bw - (i - k)] : 0.0;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < CHOL_EPT; q++) {
+        const int e = tid + q * CHOL_THREADS;
+        const int r = e >> 5, cc = e & 31;
+        if (r >= rows || cc > r) continue;
+        double a = acc[q];
+#pragma unroll 8
+        for (int kk = 0; kk < 32; kk++) a = __fma_rn(-AT[kk * ldk + r], AT[kk * ldk + cc], a);
+        acc[q] = a;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < CHOL_EPT; q++) {
+      const int e = tid + q * CHOL_THREADS;
+      if (e < rows * 32) PA[(e >> 5) * PLD + (e & 31)] = acc[q];
+    }
+    __syncthreads();
+    // ---- phase B: factor the panel, one thread per panel row r (right-looking over its 32 columns)
+    const int cmax = min(32, n - c0);
+    const int rend = min(rows, n - c0);
+    for (int c = 0; c < cmax; c++) {
+      const double ljj = sqrt(PA[c * PLD + c]);  // every thread: identical correctly rounded value
+      if (tid == 0 && !(PA[c * PLD + c] > 0.0)) raise_err(err, DERR_NOT_SPD, tag * 1000000 + c0 + c);
+      const int r = tid;
+      if (r < rend && r >= c && r - c <= bw) PL[r * PLD + c] = (r == c) ? ljj : PA[r * PLD + c] / ljj;
+      __syncthreads();
+      if (r < rend && r > c && r - c <= bw) {
+        const double lrc = PL[r * PLD + c];
+        for (int cp = c + 1; cp < cmax && cp <= r; cp++)
+          if (r - cp <= bw) PA[r * PLD + cp] = __fma_rn(-lrc, PL[cp * PLD + c], PA[r * PLD + cp]);
+      }
+      __syncthreads();
+    }
+    // ---- write the panel back
+    for (int e = tid; e < rows * 32; e += CHOL_THREADS) {
+      const int r = e >> 5, cc = e & 31;
+      const int i = c0 + r, l = c0 + cc;
+      if (l >= n || i >= n || i < l || i - l > bw) continue;
+      L[(long)i * W + bw - (i - l)] = PL[r * PLD + cc];
+    }
+    __syncthreads();
+  }
+}
+// Fallback for wide bands (e.g. Z = NULL ordering): right-looking on global memory, one CTA (same chains).
+__global__ void __launch_bounds__(1024) k_band_chol_wide(int n, int bw, int W, double *L, int *err, int tag) {
   __shared__ double piv;
   __shared__ int bad;
   const int tid = threadIdx.x;
@@ -270,7 +345,7 @@ __global__ void __launch_bounds__(1024) k_band_chol(int n, int bw, int W, double
     __syncthreads();
     const long pairs = (long)rmax * rmax;
     for (long q = tid; q < pairs; q += blockDim.x) {
-      const int u = (int)(q / rmax) + 1, v = (int)(q % rmax) + 1;  // i = j+u, l = j+v
+      const int u = (int)(q / rmax) + 1, v = (int)(q % rmax) + 1;
       if (v > u) continue;
       const double lij = L[(long)(j + u) * W + bw - u];
       const double llj = L[(long)(j + v) * W + bw - v];
@@ -280,6 +355,7 @@ __global__ void __launch_bounds__(1024) k_band_chol(int n, int bw, int W, double
     __syncthreads();
   }
 }
+
 // dinv = 1/L_ii, the column-major copy and the reversed-row copy of the band
 __global__ void k_band_finish(int n, int bw, int W, const double *Lrow, double *Lcol, double *Lrev, double *dinv) {
   long q = blockIdx.x * (long)blockDim.x + threadIdx.x;
@@ -547,27 +623,39 @@ __global__ void k_P_fill(int nodes, const int *ptr, const int *col, const int *a
   }
   for (int q = 0; q < nl; q++) P_col[P_ptr[i] + q] = list[q];
 }
-// P_ia = Pt_ia - (omega * T_ia) / dpt, T = A Pt (C19, C20); one thread per P block
-__global__ void k_P_values(long nnzb, int b, const int *P_rowof, const int *P_col, const int *A_ptr, const int *A_col,
+// P_ia = Pt_ia - (omega * T_ia) / dpt, T = A Pt (C19, C20); one thread per P block, the b x 6 entries
+// accumulate in registers over one pass of A's row (per entry: j ascending, then cc ascending)
+template <int B>
+__global__ void k_P_values(long nnzb, const int *P_rowof, const int *P_col, const int *A_ptr, const int *A_col,
                            const double *A_val, const int *agg, const int *Pt_ptr, const double *Ptv,
                            const double *dpt, double omega, double *Pv) {
   long e = blockIdx.x * (long)blockDim.x + threadIdx.x;
   if (e >= nnzb) return;
   const int i = P_rowof[e], a = P_col[e];
-  for (int r = 0; r < b; r++)
+  double acc[B * 6];
+#pragma unroll
+  for (int q = 0; q < B * 6; q++) acc[q] = 0.0;
+  for (int k = A_ptr[i]; k < A_ptr[i + 1]; k++) {
+    const int j = A_col[k];
+    if (agg[j] != a) continue;
+    const double *Av = A_val + (long)k * B * B;
+    const double *Qj = Ptv + (long)Pt_ptr[j] * B * 6;
+#pragma unroll
+    for (int r = 0; r < B; r++)
+#pragma unroll
+      for (int s = 0; s < 6; s++)
+#pragma unroll
+        for (int cc = 0; cc < B; cc++) acc[r * 6 + s] = __fma_rn(Av[r * B + cc], Qj[cc * 6 + s], acc[r * 6 + s]);
+  }
+  const bool own = agg[i] == a;
+#pragma unroll
+  for (int r = 0; r < B; r++)
+#pragma unroll
     for (int s = 0; s < 6; s++) {
-      double acc = 0.0;
-      for (int k = A_ptr[i]; k < A_ptr[i + 1]; k++) {
-        const int j = A_col[k];
-        if (agg[j] != a) continue;
-        const double *Av = A_val + (long)k * b * b + r * b;
-        const double *Qj = Ptv + (long)Pt_ptr[j] * b * 6;
-        for (int cc = 0; cc < b; cc++) acc = __fma_rn(Av[cc], Qj[cc * 6 + s], acc);
-      }
-      double t = omega * acc;
-      t = t / dpt[(long)i * b + r];
-      const double pt = (agg[i] == a) ? Ptv[((long)Pt_ptr[i] * b + r) * 6 + s] : 0.0;
-      Pv[(e * b + r) * 6 + s] = pt - t;
+      double t = omega * acc[r * 6 + s];
+      t = t / dpt[(long)i * B + r];
+      const double pt = own ? Ptv[((long)Pt_ptr[i] * B + r) * 6 + s] : 0.0;
+      Pv[(e * B + r) * 6 + s] = pt - t;
     }
 }
 
@@ -607,33 +695,33 @@ __global__ void k_spgemm_fill(int nrows, const int *A_ptr, const int *A_col, con
   }
   for (int q = 0; q < nl; q++) C_col[C_ptr[i] + q] = list[q];
 }
-// numeric C = A*B (C20): one warp per row, lane owns output-block entries e = lane + 32 h
+// numeric C = A*B (C20): one thread per output block C_ib; walks A's row i (ascending j), finds B_jb by
+// binary search in B's row j, accumulates the BR x BC entries in registers (per entry: j asc, t asc).
 template <int BR, int IN, int BC>
-__global__ void k_spgemm_vals(int nrows, const int *A_ptr, const int *A_col, const double *A_val, const int *B_ptr,
-                              const int *B_col, const double *B_val, const int *C_ptr, const int *C_col,
+__global__ void k_spgemm_vals(long nnzc, const int *C_rowof, const int *C_col, const int *A_ptr, const int *A_col,
+                              const double *A_val, const int *B_ptr, const int *B_col, const double *B_val,
                               double *C_val) {
-  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (i >= nrows) return;
-  constexpr int NE = BR * BC;
-  const int c0 = C_ptr[i], c1 = C_ptr[i + 1];
-  for (long q = (long)c0 * NE + lane; q < (long)c1 * NE; q += 32) C_val[q] = 0.0;
-  __syncwarp();
+  const long e = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (e >= nnzc) return;
+  const int i = C_rowof[e], bcol = C_col[e];
+  double acc[BR * BC];
+#pragma unroll
+  for (int q = 0; q < BR * BC; q++) acc[q] = 0.0;
   for (int k = A_ptr[i]; k < A_ptr[i + 1]; k++) {
     const int j = A_col[k];
+    const int k2 = bsearch_int(B_col, B_ptr[j], B_ptr[j + 1], bcol);
+    if (k2 < 0) continue;
     const double *Av = A_val + (long)k * BR * IN;
-    for (int k2 = B_ptr[j]; k2 < B_ptr[j + 1]; k2++) {
-      const int at = bsearch_int(C_col, c0, c1, B_col[k2]);
-      const double *Bv = B_val + (long)k2 * IN * BC;
-      double *Cv = C_val + (long)at * NE;
-      for (int e = lane; e < NE; e += 32) {
-        const int r = e / BC, s = e % BC;
-        double acc = Cv[e];
-        for (int t = 0; t < IN; t++) acc = __fma_rn(Av[r * IN + t], Bv[t * BC + s], acc);
-        Cv[e] = acc;
-      }
-    }
+    const double *Bv = B_val + (long)k2 * IN * BC;
+#pragma unroll
+    for (int r = 0; r < BR; r++)
+#pragma unroll
+      for (int s = 0; s < BC; s++)
+#pragma unroll
+        for (int t = 0; t < IN; t++) acc[r * BC + s] = __fma_rn(Av[r * IN + t], Bv[t * BC + s], acc[r * BC + s]);
   }
+#pragma unroll
+  for (int q = 0; q < BR * BC; q++) C_val[e * BR * BC + q] = acc[q];
 }
 __global__ void k_sym(long nnzb, const int *rowof, const int *ptr, const int *col, const double *G, double *Ac,
                       int *err) {
@@ -757,7 +845,13 @@ static void band_alloc(Ctx &c, int n, int bw, double *&Lrow, double *&Lcol, doub
 
 static void band_factor(Ctx &c, int n, int bw, double *Lrow, double *Lcol, double *Lrev, double *dinv, int tag) {
   const int W = band_stride(bw);
-  k_band_chol<<<1, 1024, 0, c.stream>>>(n, bw, W, Lrow, c.err, tag);
+  const size_t smem = (2 * (size_t)(32 + bw) * PLD + 32 * (size_t)(33 + bw)) * sizeof(double);
+  if ((32 + bw) * 32 <= CHOL_THREADS * CHOL_EPT && 32 + bw <= CHOL_THREADS && smem <= 220 * 1024) {
+    CK(cudaFuncSetAttribute(k_band_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_band_chol<<<1, CHOL_THREADS, smem, c.stream>>>(n, bw, W, Lrow, c.err, tag);
+  } else {
+    k_band_chol_wide<<<1, 1024, 0, c.stream>>>(n, bw, W, Lrow, c.err, tag);
+  }
   after_launch(c, "k_band_chol");
   LAUNCH(k_band_finish, (long)n * (bw + 1), n, bw, W, Lrow, Lcol, Lrev, dinv);
 }
@@ -785,6 +879,33 @@ static void filter_numeric(Ctx &c) {
   band_factor(c, c.nc, c.bw, c.Lrow, c.Lcol, c.Lrev, c.Ldinv, 1);
 }
 
+// Run the A_w band fill + Cholesky (single-SM kernel) on the side stream, concurrently with the
+// hierarchy's numeric setup on the main stream; join_filter() makes the main stream wait for it.
+static void fork_filter(Ctx &c) {
+  if (c.nc == 0) return;
+  if (!c.side) {
+    CK(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming));
+  }
+  cudaStream_t main = c.stream;
+  CK(cudaEventRecord(c.ev_fork, main));
+  CK(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
+  c.stream = c.side;
+  try {
+    filter_numeric(c);
+  } catch (...) {
+    c.stream = main;
+    throw;
+  }
+  c.stream = main;
+  CK(cudaEventRecord(c.ev_join, c.side));
+}
+static void join_filter(Ctx &c) {
+  if (c.nc == 0) return;
+  CK(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
+}
+
 static void thin_numeric(Ctx &c, long nthin_nnz) {
   LAUNCH(k_gather_vals, nthin_nnz, nthin_nnz, c.thin_src, c.lev[0].A.val, c.thin_val);
 }
@@ -794,7 +915,8 @@ static void power_iteration(Ctx &c, Level &L) {
   LAUNCH(k_pow_init, L.n, L.n, v);
   double lam = 0.0;
   for (int it = 0; it < c.cfg.power_iters; it++) {
-    launch_bsr_spmv(c, L.A, v, w);
+    if (L.As.val) launch_sell_spmv(c, L.As, SPMV_Y, v, nullptr, nullptr, nullptr, w, nullptr);
+    else launch_bsr_spmv(c, L.A, v, w);
     LAUNCH(k_div, L.n, L.n, w, L.dpt);
     launch_dot(c, L.n, L.b, w, w, DOT_PLAIN);
     double ww = d2h1(c, &c.sc->dot);
@@ -812,7 +934,7 @@ static void power_iteration(Ctx &c, Level &L) {
 
 // per-level cached arrays for numeric re-setup
 struct LevelCache {
-  int *P_rowof = nullptr, *R_perm = nullptr, *G_rowof = nullptr;
+  int *P_rowof = nullptr, *R_perm = nullptr, *G_rowof = nullptr, *AP_rowof = nullptr;
   Bsr G;
 };
 
@@ -820,30 +942,21 @@ static void level_numeric(Ctx &c, int l, LevelCache &lc) {
   Level &L = c.lev[l];
   Level &Lc = c.lev[l + 1];
   power_iteration(c, L);
-  LAUNCH(k_P_values, L.P.nnzb, L.P.nnzb, L.b, lc.P_rowof, L.P.col, L.A.ptr, L.A.col, L.A.val, L.agg, L.Pt.ptr, L.Pt.val,
-         L.dpt, L.omega, L.P.val);
+  if (L.b == 3)
+    LAUNCH(k_P_values<3>, L.P.nnzb, L.P.nnzb, lc.P_rowof, L.P.col, L.A.ptr, L.A.col, L.A.val, L.agg, L.Pt.ptr,
+           L.Pt.val, L.dpt, L.omega, L.P.val);
+  else
+    LAUNCH(k_P_values<6>, L.P.nnzb, L.P.nnzb, lc.P_rowof, L.P.col, L.A.ptr, L.A.col, L.A.val, L.agg, L.Pt.ptr,
+           L.Pt.val, L.dpt, L.omega, L.P.val);
   LAUNCH(k_transpose_vals, L.R.nnzb, L.R.nnzb, L.b, 6, lc.R_perm, L.P.val, L.R.val);
-  // AP = A * P
+  // AP = A * P, G = R * AP
   {
-    long threads = (long)L.A.nbr * 32;
-    if (L.b == 3)
-      k_spgemm_vals<3, 3, 6><<<nblk(threads), CTA, 0, c.stream>>>(L.A.nbr, L.A.ptr, L.A.col, L.A.val, L.P.ptr, L.P.col,
-                                                                  L.P.val, L.AP.ptr, L.AP.col, L.AP.val);
-    else
-      k_spgemm_vals<6, 6, 6><<<nblk(threads), CTA, 0, c.stream>>>(L.A.nbr, L.A.ptr, L.A.col, L.A.val, L.P.ptr, L.P.col,
-                                                                  L.P.val, L.AP.ptr, L.AP.col, L.AP.val);
-    after_launch(c, "k_spgemm_vals(AP)");
-  }
-  // G = R * AP
-  {
-    long threads = (long)L.R.nbr * 32;
-    if (L.b == 3)
-      k_spgemm_vals<6, 3, 6><<<nblk(threads), CTA, 0, c.stream>>>(L.R.nbr, L.R.ptr, L.R.col, L.R.val, L.AP.ptr,
-                                                                  L.AP.col, L.AP.val, lc.G.ptr, lc.G.col, lc.G.val);
-    else
-      k_spgemm_vals<6, 6, 6><<<nblk(threads), CTA, 0, c.stream>>>(L.R.nbr, L.R.ptr, L.R.col, L.R.val, L.AP.ptr,
-                                                                  L.AP.col, L.AP.val, lc.G.ptr, lc.G.col, lc.G.val);
-    after_launch(c, "k_spgemm_vals(G)");
+    auto kap = (L.b == 3) ? k_spgemm_vals<3, 3, 6> : k_spgemm_vals<6, 6, 6>;
+    auto kg = (L.b == 3) ? k_spgemm_vals<6, 3, 6> : k_spgemm_vals<6, 6, 6>;
+    LAUNCH(kap, L.AP.nnzb, L.AP.nnzb, lc.AP_rowof, L.AP.col, L.A.ptr, L.A.col, L.A.val, L.P.ptr, L.P.col, L.P.val,
+           L.AP.val);
+    LAUNCH(kg, lc.G.nnzb, lc.G.nnzb, lc.G_rowof, lc.G.col, L.R.ptr, L.R.col, L.R.val, L.AP.ptr, L.AP.col, L.AP.val,
+           lc.G.val);
   }
   LAUNCH(k_sym, lc.G.nnzb, lc.G.nnzb, lc.G_rowof, lc.G.ptr, lc.G.col, lc.G.val, Lc.A.val, c.err);
   LAUNCH(k_diag, (long)Lc.nodes * Lc.b, Lc.nodes, Lc.b, Lc.A.ptr, Lc.A.col, Lc.A.val, Lc.dl1, Lc.dpt);
@@ -1138,6 +1251,7 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
       L.AP.col = c.alloc<int>(nz);
       L.AP.val = c.alloc<double>(nz * L.b * 6);
       LAUNCH(k_spgemm_fill, nn, nn, L.A.ptr, L.A.col, L.P.ptr, L.P.col, L.AP.ptr, L.AP.col);
+      lc.AP_rowof = rowof(c, L.AP);
       int *cg = c.alloc<int>(na + 1);
       CK(cudaMemsetAsync(cg, 0, (na + 1) * sizeof(int), c.stream));
       LAUNCH(k_spgemm_count, na, na, L.R.ptr, L.R.col, L.AP.ptr, L.AP.col, cg, c.err);
@@ -1157,9 +1271,9 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
       Lc.dl1 = c.alloc<double>(Lc.n);
       Lc.dpt = c.alloc<double>(Lc.n);
     }
+    build_sell(c, L.A, L.As, true, l > 0);   // coarse levels: one thread per scalar row (1 x 6)
     level_numeric(c, l, lc);
     check_dev_error(c, "Galerkin product");
-    build_sell(c, L.A, L.As, true, l > 0);   // coarse levels: one thread per scalar row (1 x 6)
     build_sell(c, L.P, L.Ps, true, l > 0);
     l++;
   }
@@ -1204,20 +1318,20 @@ void setup_numeric(Ctx &c, const double *D) {
   S_numeric(c, C.s.S_rowof);
   Level &L0 = c.lev[0];
   if (c.nc > 0) {
-    filter_numeric(c);
-    check_dev_error(c, "A_w Cholesky");
+    fork_filter(c);
     thin_numeric(c, C.thin_nnz);
   }
   LAUNCH(k_diag, L0.n, L0.nodes, 3, L0.A.ptr, L0.A.col, L0.A.val, L0.dl1, L0.dpt);
   for (int l = 0; l + 1 < c.nlev; l++) {
+    build_sell(c, c.lev[l].A, c.lev[l].As, false, l > 0);
     level_numeric(c, l, C.lc[l]);
     check_dev_error(c, "Galerkin product");
-    build_sell(c, c.lev[l].A, c.lev[l].As, false, l > 0);
     build_sell(c, c.lev[l].P, c.lev[l].Ps, false, l > 0);
   }
   if (c.nlev == 1) build_sell(c, L0.A, L0.As, false, false);
   coarsest_numeric(c);
-  check_dev_error(c, "coarsest Cholesky");
+  join_filter(c);
+  check_dev_error(c, "numeric setup (A_w / coarsest Cholesky)");
 }
 
 }  // namespace amgf

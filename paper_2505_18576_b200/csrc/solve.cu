@@ -124,11 +124,88 @@ __global__ void __launch_bounds__(CTA) k_sell(int nrows, const int *__restrict__
   }
 }
 
+// Latency-oriented variant for scalar-row (1 x BC) SELL of the small coarse levels: D slots of values and
+// x in flight (register ring, fully unrolled), column indices 2D slots ahead.  Same chain as k_sell (C2).
+template <int BC, int MODE, int D>
+__global__ void __launch_bounds__(CTA) k_sell_r1(int nrows, const int *__restrict__ slice_ptr,
+                                                 const int *__restrict__ rowlen, const int *__restrict__ col,
+                                                 const double *__restrict__ val, const double *__restrict__ x,
+                                                 const double *__restrict__ b, const double *__restrict__ d,
+                                                 const double *__restrict__ add, double *__restrict__ y) {
+  const int row = blockIdx.x * CTA + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  if (row >= nrows) return;
+  const int len = rowlen[row];
+  const long base = slice_ptr[row >> 5];
+  const int *cp = col + base * 32 + lane;
+  const double *vp = val + base * (BC * 32) + lane;
+  double acc = 0.0;
+  double rv[D][BC], rx[D][BC];
+  int rc[D];
+  const int last = len - 1;
+  if (len > 0) {
+  // prologue: columns of slots D..2D-1, values + x of slots 0..D-1
+#pragma unroll
+  for (int q = 0; q < D; q++) rc[q] = ldg_stream_i(cp + (long)min(q, last) * 32);
+#pragma unroll
+  for (int q = 0; q < D; q++) {
+    const int sq = min(q, last);
+#pragma unroll
+    for (int e = 0; e < BC; e++) rv[q][e] = ldg_stream(vp + ((long)sq * BC + e) * 32);
+#pragma unroll
+    for (int e = 0; e < BC; e++) rx[q][e] = x[(long)rc[q] * BC + e];
+    rc[q] = ldg_stream_i(cp + (long)min(q + D, last) * 32);
+  }
+  for (int s0 = 0; s0 < len; s0 += D) {
+#pragma unroll
+    for (int q = 0; q < D; q++) {
+      const int sl = s0 + q;
+      if (sl < len) {
+#pragma unroll
+        for (int e = 0; e < BC; e++) acc = __fma_rn(rv[q][e], rx[q][e], acc);
+      }
+      // refill stage q with slot sl + D (column already loaded), and fetch the column of slot sl + 2D
+      const int sn = min(sl + D, last), sc = min(sl + 2 * D, last);
+#pragma unroll
+      for (int e = 0; e < BC; e++) rv[q][e] = ldg_stream(vp + ((long)sn * BC + e) * 32);
+#pragma unroll
+      for (int e = 0; e < BC; e++) rx[q][e] = x[(long)rc[q] * BC + e];
+      rc[q] = ldg_stream_i(cp + (long)sc * 32);
+    }
+  }
+  }
+  const long i = row;
+  if (MODE == MODE_Y) {
+    y[i] = acc;
+  } else if (MODE == MODE_RESID) {
+    y[i] = b[i] - acc;
+  } else if (MODE == MODE_SMOOTH || MODE == MODE_SMOOTH_ADD) {
+    double res = b[i] - acc;
+    double t = res / d[i];
+    double xn = x[i] + t;
+    if (MODE == MODE_SMOOTH_ADD) xn = add[i] + xn;
+    y[i] = xn;
+  } else if (MODE == MODE_ADDTO) {
+    y[i] = y[i] + acc;
+  }
+}
+
 template <int BR, int BC>
 static void sell_dispatch(Ctx &c, const Sell &A, int mode, const double *x, const double *b, const double *d,
                           const double *add, double *y, double *dp) {
   dim3 g(nblk(A.nrows)), t(CTA);
   if (A.nrows == 0) return;
+  if (BR == 1 && mode != MODE_DOT) {
+    switch (mode) {
+      case MODE_Y: k_sell_r1<BC, MODE_Y, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y); break;
+      case MODE_RESID: k_sell_r1<BC, MODE_RESID, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y); break;
+      case MODE_SMOOTH: k_sell_r1<BC, MODE_SMOOTH, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y); break;
+      case MODE_SMOOTH_ADD: k_sell_r1<BC, MODE_SMOOTH_ADD, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y); break;
+      case MODE_ADDTO: k_sell_r1<BC, MODE_ADDTO, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y); break;
+    }
+    after_launch(c, "k_sell_r1");
+    return;
+  }
   switch (mode) {
     case MODE_Y: k_sell<BR, BC, MODE_Y><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp); break;
     case MODE_RESID: k_sell<BR, BC, MODE_RESID><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp); break;
@@ -166,32 +243,48 @@ __global__ void __launch_bounds__(CTA) k_restrict(int nrows, const int *__restri
   double acc[6];
 #pragma unroll
   for (int q = 0; q < 6; q++) acc[q] = 0.0;
-  const int end = ptr[w + 1];
-#pragma unroll 4
-  for (int k = ptr[w] + lane; k < end; k += 32) {
+  const int beg = ptr[w], end = ptr[w + 1];
+  // lane-strided blocks k = beg + lane + 32 t; the next block's values and r are prefetched (C5 order kept)
+  int k = beg + lane;
+  double2 v[3 * B];
+  double rv[B];
+  if (k < end) {
     const int c = col[k];
-    double rv[B];
+#pragma unroll
+    for (int h = 0; h < 3 * B; h++) v[h] = __ldg(reinterpret_cast<const double2 *>(val + (long)k * 6 * B) + h);
 #pragma unroll
     for (int e = 0; e < B; e++) rv[e] = r[(long)c * B + e];
-    const double2 *v2 = reinterpret_cast<const double2 *>(val + (long)k * 6 * B);
+  }
+  for (; k < end; k += 32) {
+    const int kn = k + 32 < end ? k + 32 : k;
+    const int cn = col[kn];
+    double2 vn[3 * B];
+    double rn[B];
+#pragma unroll
+    for (int h = 0; h < 3 * B; h++) vn[h] = __ldg(reinterpret_cast<const double2 *>(val + (long)kn * 6 * B) + h);
+#pragma unroll
+    for (int e = 0; e < B; e++) rn[e] = r[(long)cn * B + e];
 #pragma unroll
     for (int h = 0; h < 3 * B; h++) {
-      double2 t = __ldg(v2 + h);
       const int e0 = 2 * h, e1 = 2 * h + 1;
-      acc[e0 / B] = __fma_rn(t.x, rv[e0 % B], acc[e0 / B]);
-      acc[e1 / B] = __fma_rn(t.y, rv[e1 % B], acc[e1 / B]);
+      acc[e0 / B] = __fma_rn(v[h].x, rv[e0 % B], acc[e0 / B]);
+      acc[e1 / B] = __fma_rn(v[h].y, rv[e1 % B], acc[e1 / B]);
     }
+#pragma unroll
+    for (int h = 0; h < 3 * B; h++) v[h] = vn[h];
+#pragma unroll
+    for (int e = 0; e < B; e++) rv[e] = rn[e];
   }
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1)
 #pragma unroll
     for (int q = 0; q < 6; q++) acc[q] = acc[q] + __shfl_xor_sync(0xffffffffu, acc[q], o);
   if (lane < 6) {
-    double v = acc[0];
+    double vv = acc[0];
 #pragma unroll
     for (int q = 1; q < 6; q++)
-      if (lane == q) v = acc[q];
-    out[(long)w * 6 + lane] = v;
+      if (lane == q) vv = acc[q];
+    out[(long)w * 6 + lane] = vv;
   }
 }
 
