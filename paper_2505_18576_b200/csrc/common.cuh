@@ -127,6 +127,7 @@ struct Ctx {
   double *w_x1 = nullptr, *w_r1 = nullptr, *w_xv = nullptr;
   double *p = nullptr, *q = nullptr, *rr = nullptr, *zz = nullptr, *xx = nullptr, *bb = nullptr;
   double *dot_part = nullptr;
+  double *pw_v = nullptr, *pw_w = nullptr;  // power-iteration work vectors (allocated once)
   Scalars *sc = nullptr;      // device
   Scalars *sc_host = nullptr; // pinned
   int *err = nullptr;         // device [2]

@@ -911,7 +911,11 @@ static void thin_numeric(Ctx &c, long nthin_nnz) {
 }
 
 static void power_iteration(Ctx &c, Level &L) {
-  double *v = c.alloc<double>(L.n), *w = c.alloc<double>(L.n);
+  if (!c.pw_v) {  // once per handle: no allocation on the numeric re-setup path
+    c.pw_v = c.alloc<double>(c.n);
+    c.pw_w = c.alloc<double>(c.n);
+  }
+  double *v = c.pw_v, *w = c.pw_w;
   LAUNCH(k_pow_init, L.n, L.n, v);
   double lam = 0.0;
   for (int it = 0; it < c.cfg.power_iters; it++) {
@@ -928,8 +932,6 @@ static void power_iteration(Ctx &c, Level &L) {
   }
   L.lambda = lam;
   L.omega = 4.0 / (3.0 * lam);
-  c.release(v);
-  c.release(w);
 }
 
 // per-level cached arrays for numeric re-setup
