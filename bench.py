@@ -104,6 +104,21 @@ def level_bytes(g):
     return tot
 
 
+def system_of(rank: int, world: int, k: int, nsys: int) -> int:
+    """Replica schedule: rank r solves systems r, r+N, r+2N, ... of the sequence (mod its length)."""
+    return (rank + world * k) % nsys
+
+
+def max_over_ranks(value: float, world: int, device=None) -> float:
+    """Max of a timing over all ranks (identity for one rank)."""
+    if world <= 1:
+        return float(value)
+    import torch
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
 def spmv_bytes(g):
     L = g.levels[0]
     return L["nnzb"] * 76 + 4 * L["nodes"] + 48 * L["nodes"]
@@ -131,7 +146,7 @@ def run_amgf(args, rank, world, local_rank):
     full_setup_ms = t0.elapsed_time(t1)
 
     def step(k):
-        s = (rank + world * k) % nsys
+        s = system_of(rank, world, k, nsys)
         g.update_D(D_dev[s])
         _, rep = g.pcg(b_dev, rtol=p.rtol, max_it=5000, out=x_dev)
         return s, rep
@@ -164,10 +179,7 @@ def run_amgf(args, rank, world, local_rank):
     clk = clocks.stop()
     elapsed = ev0.elapsed_time(ev1)
     launches = g.launches - launches0
-    if world > 1:
-        t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        elapsed = float(t.item())
+    elapsed = max_over_ranks(elapsed, world, dev)
 
     # ---- e2e: same metric through the public API with host buffers (pinned), copies inside the region
     D_host = [torch.from_numpy(p.D_seq[s].copy()).pin_memory() for s in range(nsys)]
@@ -181,17 +193,14 @@ def run_amgf(args, rank, world, local_rank):
     ee0 = torch.cuda.Event(enable_timing=True); ee1 = torch.cuda.Event(enable_timing=True)
     ee0.record(stream)
     for k in range(ke):
-        s = (rank + world * k) % nsys
+        s = system_of(rank, world, k, nsys)
         D_stage.copy_(D_host[s], non_blocking=True)
         g.update_D(D_stage)
         g.pcg_host(b_host, x_host, rtol=p.rtol)
     ee1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = ee0.elapsed_time(ee1)
-    if world > 1:
-        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = max_over_ranks(e2e_ms, world, dev)
 
     # ---- kernel-level roofline: fine-level SpMV (dominant kernel family) and whole V-cycle
     xr = torch.randn(p.n, dtype=torch.float64, device=dev)
