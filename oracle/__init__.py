@@ -30,11 +30,11 @@ class OrcConfig(ctypes.Structure):
     _fields_ = [("pre_sweeps", ctypes.c_int), ("post_sweeps", ctypes.c_int),
                 ("coarsest_size", ctypes.c_int), ("max_levels", ctypes.c_int),
                 ("power_iters", ctypes.c_int), ("factor_filter", ctypes.c_int),
-                ("agg_seed", ctypes.c_uint64)]
+                ("agg_seed", ctypes.c_uint64), ("nd_levels", ctypes.c_int), ("pad_", ctypes.c_int)]
 
 
 DEFAULTS = dict(pre_sweeps=1, post_sweeps=1, coarsest_size=64, max_levels=25,
-                power_iters=10, factor_filter=1, agg_seed=0x5EED)
+                power_iters=10, factor_filter=1, agg_seed=0x5EED, nd_levels=3)
 
 _lib = None
 
@@ -53,6 +53,7 @@ def lib():
         L.orc_dot.argtypes = [ctypes.c_long, ctypes.c_int, P, P]
         L.orc_cholesky_dense.argtypes = [ctypes.c_int, P, P]
         L.orc_trsv_dense.argtypes = [ctypes.c_int, P, P, P]
+        L.orc_nd_order.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
         L.orc_priority.restype = ctypes.c_uint64
         L.orc_priority.argtypes = [ctypes.c_int, ctypes.c_uint64]
         L.orc_vcycle.argtypes = [P, P, P]
@@ -111,6 +112,12 @@ def bsr_spmv(ptr, col, val, x, br, bc):
     return y
 
 
+def nd_order(nc: int, bw: int, levels: int):
+    out = np.zeros(max(nc, 1), np.int32)
+    lib().orc_nd_order(nc, bw, levels, _p(out))
+    return out[:nc]
+
+
 def priority(v: int, seed: int) -> int:
     return lib().orc_priority(v, seed)
 
@@ -163,7 +170,8 @@ class Oracle:
                   9: (nodes * b, np.float64), 10: (nodes, np.int32), 11: ((nodes * b, 6), np.float64),
                   12: (2, np.float64), 13: ((nodes, b * 6), np.float64), 14: (nodes, np.int32), 15: (nodes, np.int32),
                   20: (self.nc, np.int32), 21: ((self.nc, self.nc), np.float64), 22: ((self.nc, self.nc), np.float64),
-                  23: ((self.nco, self.nco), np.float64), 24: ((self.nco, self.nco), np.float64)}
+                  23: ((self.nco, self.nco), np.float64), 24: ((self.nco, self.nco), np.float64),
+                  25: (self.nc, np.int32), 26: (1, np.int32)}
         shape, dt = shapes[which]
         out = np.zeros(shape, dtype=dt)
         if which == 13:

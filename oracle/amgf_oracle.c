@@ -206,6 +206,8 @@ uint64_t orc_priority(int v, uint64_t seed) { return mix64((uint64_t)(uint32_t)v
 typedef struct {
   int pre_sweeps, post_sweeps, coarsest_size, max_levels, power_iters, factor_filter;
   uint64_t agg_seed;
+  int nd_levels;  /* nested-dissection depth of A_w's elimination order (contract C9/C10, reading R16) */
+  int pad_;
 } orc_config;
 
 typedef struct {
@@ -232,10 +234,12 @@ typedef struct {
   int m;
   bsr_t S;
   int nc;
-  int *Z;        /* contact dofs in elimination order */
+  int *Z;        /* contact dofs, the column order of P */
   int *pos;      /* dof -> position in Z or -1 */
-  double *Aw;    /* dense n_c x n_c */
-  double *Lw;    /* Cholesky factor of Aw */
+  int bw;        /* structural lower band width of A_w in Z order */
+  int *pi;       /* elimination order: pi[i] = position in Z of the i-th eliminated dof */
+  double *Aw;    /* dense n_c x n_c, Z order */
+  double *Lw;    /* Cholesky factor of Aw[pi, pi] */
   int nlev;
   level_t lev[MAXLEV];
   double *Ac, *Lc; /* coarsest dense operator and factor */
@@ -332,6 +336,25 @@ static int form_S(orc_ctx *cx, const int *Kptr, const int *Kcol, const double *K
   return ORC_OK;
 }
 
+/* Elimination order of A_w (reading R16): one-dimensional nested dissection of the band.  The interval
+ * [a, b) of Z positions is a leaf if depth == 0 or b - a < 4 bw + 64; otherwise it is split by the
+ * separator [m, m + bw), m = a + (b - a - bw)/2, which decouples [a, m) from [m + bw, b) because A_w has
+ * no entries farther than bw from the diagonal.  Postorder: left subtree, right subtree, separator. */
+static void nd_rec(int a, int b, int depth, int bw, int *out, int *cnt) {
+  if (depth == 0 || b - a < 4 * bw + 64) {
+    for (int i = a; i < b; i++) out[(*cnt)++] = i;
+    return;
+  }
+  int m = a + (b - a - bw) / 2;
+  nd_rec(a, m, depth - 1, bw, out, cnt);
+  nd_rec(m + bw, b, depth - 1, bw, out, cnt);
+  for (int i = m; i < m + bw; i++) out[(*cnt)++] = i;
+}
+void orc_nd_order(int nc, int bw, int levels, int *out) {
+  int cnt = 0;
+  nd_rec(0, nc, levels, bw, out, &cnt);
+}
+
 /* ---------- I_c and A_w = P^T S P ---------- */
 static int setup_filter(orc_ctx *cx, int m, const int *Jptr, const int *Jcol, const int *Z, int nc) {
   long n = cx->n;
@@ -363,10 +386,25 @@ static int setup_filter(orc_ctx *cx, int m, const int *Jptr, const int *Jcol, co
   }
   free(mark);
   cx->nc = nc;
+  /* structural band width in Z order: bw = max_a (a - min{b <= a : S[Z_a, Z_b] stored}) */
+  int bw = 0;
+  for (int a = 0; a < nc; a++) {
+    int p = cx->Z[a], I = p / 3, mn = a;
+    for (int k = cx->S.ptr[I]; k < cx->S.ptr[I + 1]; k++)
+      for (int c = 0; c < 3; c++) {
+        int b = cx->pos[3 * cx->S.col[k] + c];
+        if (b >= 0 && b < mn) mn = b;
+      }
+    if (a - mn > bw) bw = a - mn;
+  }
+  cx->bw = bw;
+  cx->pi = (int *)malloc((size_t)(nc > 0 ? nc : 1) * sizeof(int));
+  orc_nd_order(nc, bw, cx->cfg.nd_levels, cx->pi);
   if (!cx->cfg.factor_filter || nc == 0) return ORC_OK;
   cx->Aw = (double *)calloc((size_t)nc * nc, sizeof(double));
   cx->Lw = (double *)malloc((size_t)nc * nc * sizeof(double));
-  if (!cx->Aw || !cx->Lw) return fail(ORC_ERR_OOM, "oom A_w");
+  double *Ap = (double *)malloc((size_t)nc * nc * sizeof(double));
+  if (!cx->Aw || !cx->Lw || !Ap) return fail(ORC_ERR_OOM, "oom A_w");
   for (int a = 0; a < nc; a++) {
     int p = cx->Z[a], I = p / 3, r = p % 3;
     for (int k = cx->S.ptr[I]; k < cx->S.ptr[I + 1]; k++)
@@ -375,7 +413,10 @@ static int setup_filter(orc_ctx *cx, int m, const int *Jptr, const int *Jcol, co
         if (cx->pos[q] >= 0) cx->Aw[(size_t)a * nc + cx->pos[q]] = cx->S.val[9L * k + 3 * r + c];
       }
   }
-  int st = orc_cholesky_dense(nc, cx->Aw, cx->Lw);
+  for (int i = 0; i < nc; i++)
+    for (int j = 0; j < nc; j++) Ap[(size_t)i * nc + j] = cx->Aw[(size_t)cx->pi[i] * nc + cx->pi[j]];
+  int st = orc_cholesky_dense(nc, Ap, cx->Lw);
+  free(Ap);
   if (st) {
     char buf[512];
     snprintf(buf, sizeof buf, "A_w: %.480s", g_err);
@@ -799,7 +840,7 @@ void orc_free(orc_ctx *cx) {
     for (int t = 0; t < 4; t++) free(cx->work[l][t]);
   }
   bsr_free(&cx->S);
-  free(cx->Z); free(cx->pos); free(cx->Aw); free(cx->Lw); free(cx->Ac); free(cx->Lc);
+  free(cx->Z); free(cx->pos); free(cx->pi); free(cx->Aw); free(cx->Lw); free(cx->Ac); free(cx->Lc);
   free(cx);
 }
 
@@ -873,10 +914,17 @@ void orc_spmv(orc_ctx *cx, int level, const double *x, double *y) {
   bsr_spmv(&cx->lev[level].A, x, NULL, y, 0);
 }
 
-/* y = A_w^{-1} v  (filter solve, contract C10) */
-void orc_filter_solve(orc_ctx *cx, const double *v, double *y) {
-  orc_trsv_dense(cx->nc, cx->Lw, v, y);
+/* y = A_w^{-1} v (filter solve, contract C10): A_w[pi,pi] = L L^T, so y[pi] = L^{-T} L^{-1} v[pi]. */
+static void filter_solve(orc_ctx *cx, const double *v, double *y) {
+  int nc = cx->nc;
+  double *vp = (double *)malloc((size_t)(nc > 0 ? nc : 1) * sizeof(double));
+  double *yp = (double *)malloc((size_t)(nc > 0 ? nc : 1) * sizeof(double));
+  for (int i = 0; i < nc; i++) vp[i] = v[cx->pi[i]];
+  orc_trsv_dense(nc, cx->Lw, vp, yp);
+  for (int i = 0; i < nc; i++) y[cx->pi[i]] = yp[i];
+  free(vp); free(yp);
 }
+void orc_filter_solve(orc_ctx *cx, const double *v, double *y) { filter_solve(cx, v, y); }
 
 /* AMGF apply (Def. AMGF eq:M_itmat PAPER.md:426; three stages SPEC.md:245,
  * thin second residual = reading R11):
@@ -893,7 +941,7 @@ void orc_apply(orc_ctx *cx, const double *r, double *z) {
   vcycle(cx, 0, r, x1);
   bsr_spmv(&cx->S, x1, r, r1, 1);
   for (int a = 0; a < nc; a++) v[a] = r1[cx->Z[a]];
-  if (nc > 0) orc_trsv_dense(nc, cx->Lw, v, y);
+  if (nc > 0) filter_solve(cx, v, y);
   /* x2 (stored in x1) and thin r2 (stored in r1) */
   const bsr_t *S = &cx->S;
   for (int I = 0; I < cx->nodes; I++)
@@ -981,7 +1029,7 @@ void orc_info(orc_ctx *cx, long *out) {
 
 /* which: 0 A.ptr 1 A.col 2 A.val 3 P.ptr 4 P.col 5 P.val 6 R.ptr 7 R.col 8 R.val
  *        9 dl1 10 agg 11 Bnn 12 [lambda, omega] 13 Pt.val 14 root 15 comp
- *        20 Z 21 Aw(dense) 22 Lw(dense) 23 Ac(dense) 24 Lc(dense) */
+ *        20 Z 21 Aw(dense, Z order) 22 Lw(dense, pi order) 23 Ac(dense) 24 Lc(dense) 25 pi 26 bw */
 int orc_get(orc_ctx *cx, int which, int level, void *dst) {
   level_t *L = &cx->lev[level];
   long nzA = bsr_nnzb(&L->A);
@@ -1007,6 +1055,8 @@ int orc_get(orc_ctx *cx, int which, int level, void *dst) {
     case 22: if (!cx->Lw) return -1; memcpy(dst, cx->Lw, (size_t)cx->nc * cx->nc * sizeof(double)); return 0;
     case 23: memcpy(dst, cx->Ac, (size_t)cx->nco * cx->nco * sizeof(double)); return 0;
     case 24: memcpy(dst, cx->Lc, (size_t)cx->nco * cx->nco * sizeof(double)); return 0;
+    case 25: memcpy(dst, cx->pi, (size_t)cx->nc * sizeof(int)); return 0;
+    case 26: ((int *)dst)[0] = cx->bw; return 0;
   }
   return -1;
 }

@@ -211,12 +211,53 @@ def test_Aw_is_principal_submatrix_and_factor(oracle_lib):
     Aw = o.get(21)
     assert np.array_equal(Aw, S[np.ix_(p.Z, p.Z)])
     Lw = o.get(22)
-    assert np.abs(Lw @ Lw.T - Aw).max() <= 1e-13 * np.abs(Aw).max()
+    pi = o.get(25)
+    assert sorted(pi.tolist()) == list(range(len(p.Z)))
+    Awp = Aw[np.ix_(pi, pi)]
+    assert np.abs(Lw @ Lw.T - Awp).max() <= 1e-13 * np.abs(Aw).max()
     # filter solves A_w exactly: residual in span(Z) is corrected exactly (north_star)
     w = np.random.default_rng(3).standard_normal(len(p.Z))
     y = o.filter_solve(Aw @ w)
     assert np.abs(y - w).max() <= 1e-6 * np.abs(w).max()
     assert np.abs(Aw @ y - Aw @ w).max() <= 1e-12 * np.abs(Aw @ w).max()
+
+
+@pytest.mark.parametrize("levels", [0, 1, 3])
+def test_nd_order_structure(oracle_lib, levels):
+    """Reading R16: the nested-dissection order is a permutation; a separator of width bw decouples its two
+    sides (no A_w entry across it), so the dense factor of A_w[pi,pi] has no fill outside the profile:
+    leaf rows within bw of the diagonal inside their leaf, separator rows from their subtree start."""
+    p = gen.config(1)
+    o = oracle_lib.Oracle.from_problem(p, nd_levels=levels)
+    bw = int(o.get(26)[0])
+    pi = o.get(25)
+    assert sorted(pi.tolist()) == list(range(o.nc))
+    S = o.level_matrix(0).toarray()
+    Aw = S[np.ix_(p.Z, p.Z)]
+    ii, jj = np.nonzero(Aw)
+    assert np.abs(ii - jj).max() == bw
+    L = o.get(22)
+    # block structure from pi: maximal runs of consecutive Z positions
+    starts = [0] + [i for i in range(1, o.nc) if pi[i] != pi[i - 1] + 1]
+    nblocks = len(starts)
+    assert nblocks % 2 == 1 and nblocks <= 2 ** (levels + 1) - 1 and (levels == 0) == (nblocks == 1)
+    env = np.zeros(o.nc, int)
+    # reconstruct subtrees recursively from the postorder (leaf, leaf, sep) pattern: a block of length bw
+    # preceded by two subtrees is a separator
+    stack = []
+    bounds = starts + [o.nc]
+    for b in range(nblocks):
+        b0, b1 = bounds[b], bounds[b + 1]
+        is_sep = levels > 0 and (b1 - b0) == bw and len(stack) >= 2
+        if is_sep:
+            r = stack.pop(); l = stack.pop()
+            env[b0:b1] = l[0]
+            stack.append((l[0], b1))
+        else:
+            env[b0:b1] = np.maximum(np.arange(b0, b1) - bw, b0)
+            stack.append((b0, b1))
+    for i in range(o.nc):
+        assert not L[i, :env[i]].any()
 
 
 def test_Z_validation(oracle_lib):
