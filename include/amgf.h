@@ -51,7 +51,7 @@ typedef struct {
   int32_t coarsest_size;   /* stop coarsening at <= this many dofs (default 64) */
   int32_t max_levels;      /* default 25                                                     */
   int32_t power_iters;     /* power steps for lambda_max(D^-1 A) (default 10)                */
-  int32_t reserved;
+  int32_t nd_levels;       /* nested-dissection depth of A_w's elimination order (default 3, DESIGN R16) */
   uint64_t agg_seed;       /* aggregation priority seed (default 0x5EED)                     */
 } amgf_config;
 
@@ -107,13 +107,16 @@ amgf_status amgf_pcg_solve_host(amgf_handle h, const double *b_host, double *x_h
 
 /* Hierarchy introspection (tests, bench).  info[0] = levels, info[1] = nc, info[2] = coarsest dofs,
  * info[3] = band width of A_w's factor, then per level l: info[4+6l .. 9+6l] =
- * {nodes, block size, nnzb(A), nnzb(P), n_agg, SELL slots of A}.  info needs 4 + 6*32 entries. */
+ * {nodes, block size, nnzb(A), nnzb(P), n_agg, SELL slots of A}; info[196] = size of the separator
+ * off-block factor, info[197] = number of nested-dissection blocks.  info needs 4 + 6*32 + 2 entries. */
 amgf_status amgf_level_info(amgf_handle h, int64_t *info);
 
 /* Copy one hierarchy array to the HOST buffer dst.  which: 0 A.ptr 1 A.col 2 A.val 3 P.ptr 4 P.col
  * 5 P.val 6 R.ptr 7 R.col 8 R.val 9 l1 diagonal 10 aggregate ids 11 near-null space 12 {lambda,
- * omega} 14 root flags 15 component labels 20 Z 22 A_w factor band (nc x W row-major, W = (bw+2)&~1,
- * L_ik at column bw-(i-k), diagonal at column bw).  Sizes follow amgf_level_info.  Synchronises the handle's last stream. */
+ * omega} 14 root flags 15 component labels 20 Z 22 in-block band of the factor of A_w[pi,pi] (nc x W
+ * row-major over pi positions, W = band stride, L_ik at column bw-(i-k), diagonal at column bw)
+ * 23 separator-vs-subtree factor entries 25 pi (elimination order as Z positions) 27 block table
+ * {int p0, len, kind, t0; int64 off; int level, pad}.  Sizes follow amgf_level_info.  Synchronises the handle's last stream. */
 amgf_status amgf_level_get(amgf_handle h, int32_t which, int32_t level, void *dst);
 
 /* Number of kernel launches issued by this handle since creation (bench accounting). */

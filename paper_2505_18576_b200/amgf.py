@@ -28,7 +28,7 @@ def lib_path() -> str:
 class Config(ctypes.Structure):
     _fields_ = [("pre_sweeps", ctypes.c_int32), ("post_sweeps", ctypes.c_int32),
                 ("coarsest_size", ctypes.c_int32), ("max_levels", ctypes.c_int32),
-                ("power_iters", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("power_iters", ctypes.c_int32), ("nd_levels", ctypes.c_int32),
                 ("agg_seed", ctypes.c_uint64)]
 
 
@@ -125,12 +125,13 @@ class AMGF:
                           ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(h))
         _check(st)
         self.h = h
-        info = np.zeros(4 + 6 * 32, dtype=np.int64)
+        info = np.zeros(4 + 6 * 32 + 2, dtype=np.int64)
         _check(L.amgf_level_info(self.h, info.ctypes.data_as(ctypes.c_void_p)))
         self.nlev, self.nc, self.nco, self.bw = (int(v) for v in info[:4])
         self.levels = [dict(nodes=int(info[4 + 6 * l]), b=int(info[5 + 6 * l]), nnzb=int(info[6 + 6 * l]),
                             nnzb_P=int(info[7 + 6 * l]), n_agg=int(info[8 + 6 * l]), slots=int(info[9 + 6 * l]))
                        for l in range(self.nlev)]
+        self.loff_size, self.nd_nblocks = int(info[4 + 6 * 32]), int(info[5 + 6 * 32])
 
     @classmethod
     def from_problem(cls, p, D=None, Z="lattice", config=None, stream=None):
@@ -157,33 +158,35 @@ class AMGF:
             return T.empty(n if n is not None else self.n, dtype=T.float64, device="cuda")
         if isinstance(x, np.ndarray):
             x = T.from_numpy(np.ascontiguousarray(x))
+        if n is not None and x.numel() != n:
+            raise ValueError(f"vector of {x.numel()} entries, expected {n}")
         return x if (x.is_cuda and x.dtype == T.float64 and x.is_contiguous()) else x.to("cuda", T.float64).contiguous()
 
     def update_D(self, D):
-        D = self._vec(D)
+        D = self._vec(D, self.m)
         self._in["D_upd"] = D
         _check(load_library().amgf_update_D(self.h, _ptr(D), self._s))
 
     def apply(self, r, out=None):
-        r = self._vec(r)
+        r = self._vec(r, self.n)
         z = out if out is not None else self._vec(n=self.n)
         _check(load_library().amgf_apply(self.h, _ptr(r), _ptr(z), self._s))
         return z
 
     def vcycle(self, b, out=None):
-        b = self._vec(b)
+        b = self._vec(b, self.n)
         x = out if out is not None else self._vec(n=self.n)
         _check(load_library().amgf_vcycle(self.h, _ptr(b), _ptr(x), self._s))
         return x
 
     def spmv(self, x, level=0, out=None):
-        x = self._vec(x)
+        x = self._vec(x, self.levels[level]["nodes"] * self.levels[level]["b"])
         y = out if out is not None else self._vec(n=x.numel())
         _check(load_library().amgf_spmv(self.h, level, _ptr(x), _ptr(y), self._s))
         return y
 
     def pcg(self, b, rtol=1e-8, max_it=5000, precond="amgf", out=None):
-        b = self._vec(b)
+        b = self._vec(b, self.n)
         x = out if out is not None else self._vec(n=self.n)
         rep = Report()
         st = load_library().amgf_pcg_solve(self.h, _ptr(b), _ptr(x), rtol, max_it, 0 if precond == "amgf" else 1,
@@ -194,6 +197,8 @@ class AMGF:
 
     def pcg_host(self, b_host, x_host, rtol=1e-8, max_it=5000, precond="amgf"):
         """b_host, x_host: CPU float64 tensors (pinned for async copies)."""
+        if b_host.numel() != self.n or x_host.numel() != self.n or b_host.is_cuda or x_host.is_cuda:
+            raise ValueError("pcg_host needs host (CPU) float64 tensors of n entries")
         rep = Report()
         st = load_library().amgf_pcg_solve_host(self.h, ctypes.c_void_p(b_host.data_ptr()),
                                                 ctypes.c_void_p(x_host.data_ptr()), rtol, max_it,
@@ -216,7 +221,14 @@ class AMGF:
                   6: (Lv["n_agg"] + 1, np.int32), 7: (Lv["nnzb_P"], np.int32),
                   8: ((Lv["nnzb_P"], 6 * b), np.float64), 9: (nodes * b, np.float64), 10: (nodes, np.int32),
                   11: ((nodes * b, 6), np.float64), 12: (2, np.float64), 14: (nodes, np.int32),
-                  15: (nodes, np.int32), 20: (self.nc, np.int32), 22: ((self.nc, W), np.float64)}
+                  15: (nodes, np.int32), 20: (self.nc, np.int32), 22: ((self.nc, W), np.float64),
+                  23: (self.loff_size, np.float64), 25: (self.nc, np.int32)}
+        if which == 27:
+            dt = np.dtype([("p0", np.int32), ("len", np.int32), ("kind", np.int32), ("t0", np.int32),
+                           ("off", np.int64), ("level", np.int32), ("pad", np.int32)])
+            out = np.zeros(self.nd_nblocks, dtype=dt)
+            _check(load_library().amgf_level_get(self.h, which, level, out.ctypes.data_as(ctypes.c_void_p)))
+            return out
         shape, dt = shapes[which]
         out = np.zeros(shape, dtype=dt)
         _check(load_library().amgf_level_get(self.h, which, level, out.ctypes.data_as(ctypes.c_void_p)))

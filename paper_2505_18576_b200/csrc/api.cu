@@ -115,7 +115,7 @@ void apply_M(Ctx &c, const double *r, double *z) {
     return;
   }
   launch_sell_spmv(c, L0.As, SPMV_RESID, c.w_x1, r, nullptr, nullptr, c.w_r1, nullptr);
-  launch_band_trsv(c, c.nc, c.bw, c.Lcol, c.Lrev, c.Ldinv, c.w_r1, c.Z, c.fv, c.Z, c.w_x1, c.w_xv);
+  nd_solve(c, c.w_r1, c.w_x1);  // y = A_w^{-1} r1[Z] (pi order, c.fv), x2 = x1 + P y
   launch_thin_resid(c, c.nthin, c.thin_row, c.thin_ptr, c.thin_pos, c.thin_val, c.fv, c.w_r1);
   vcycle(c, 0, c.w_r1, z, c.w_x1);
 }
@@ -206,7 +206,7 @@ void amgf_default_config(amgf_config *cfg) {
   cfg->coarsest_size = 64;
   cfg->max_levels = 25;
   cfg->power_iters = 10;
-  cfg->reserved = 0;
+  cfg->nd_levels = 3;
   cfg->agg_seed = 0x5EED;
 }
 
@@ -329,6 +329,8 @@ amgf_status amgf_level_info(amgf_handle h, int64_t *info) {
     info[4 + 6 * l + 4] = co ? 0 : L.n_agg;
     info[4 + 6 * l + 5] = L.As.nslots;
   }
+  info[4 + 6 * MAXLEV + 0] = h->loff_size;
+  info[4 + 6 * MAXLEV + 1] = h->nd_nblocks;
   return AMGF_OK;
 }
 
@@ -365,6 +367,9 @@ amgf_status amgf_level_get(amgf_handle h, int32_t which, int32_t level, void *ds
       case 15: cp(L.comp, L.nodes * 4); break;
       case 20: cp(h->Z, h->nc * 4); break;
       case 22: cp(h->Lrow, (size_t)h->nc * band_stride(h->bw) * 8); break;
+      case 23: cp(h->Loff, (size_t)h->loff_size * 8); break;
+      case 25: cp(h->pi_z, (size_t)h->nc * 4); break;
+      case 27: cp(h->nd_blk, (size_t)h->nd_nblocks * 32); break;
       default: throw Error{AMGF_ERR_ARG, "unknown array id"};
     }
     CK(cudaStreamSynchronize(h->stream));

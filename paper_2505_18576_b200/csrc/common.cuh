@@ -107,7 +107,18 @@ struct Ctx {
   double *Jt_val = nullptr;
   double *D = nullptr;
   int *S_kblk = nullptr;  // per S block: index of the K block (-1 if none)
-  // filter
+  // filter (A_w factor in nested-dissection order, filter.cu)
+  struct NdLevel { int count = 0; int *ids = nullptr, *p0 = nullptr, *len = nullptr, *sub_ptr = nullptr, *sub_list = nullptr; };
+  int nd_nblocks = 0, nd_nleaves = 0, nd_depth = 0, nd_npairs = 0;
+  void *nd_blk = nullptr;                 // device NdBlk[nd_nblocks]
+  int *nd_leaf_p0 = nullptr, *nd_leaf_len = nullptr, *nd_pairs = nullptr;
+  NdLevel nd_lev[16];                     // separators by depth (0 = root)
+  int *nd_sspairs[16][16] = {};           // (S at level l, S' at depth d) pairs
+  int nd_sspairs_n[16][16] = {};
+  int *pi_z = nullptr, *zpi = nullptr, *dof = nullptr, *block_of = nullptr;
+  double *Loff = nullptr;
+  long loff_size = 0;
+  double *fw = nullptr;                   // filter workspace (pi order)
   int nc = 0, bw = 0;
   int *Z = nullptr, *pos = nullptr;
   double *Lrow = nullptr;   // band, row-major: Lrow[i*W + bw - (i-k)] = L_ik, W = band_stride(bw)
@@ -194,6 +205,16 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
                const int *J_col, const double *J_val, const double *D, const int *Z, int nc,
                const double *B_nns);
 void setup_numeric(Ctx &c, const double *D);  // update_D
+// filter.cu
+void nd_symbolic(Ctx &c);
+void nd_numeric(Ctx &c);
+void nd_solve(Ctx &c, const double *r1, double *x2);  // c.fv <- A_w^{-1} r1[Z] (pi order), x2[Z] += y
+void nd_remap_positions(Ctx &c, int *pos_z, long n);  // Z positions -> pi positions
+void band_factor_blocks(Ctx &c, int n, int nblocks, const int *d_p0, const int *d_len, int bw, double *Lrow, int tag);
+void band_finish(Ctx &c, int n, int bw, const double *Lrow, double *Lcol, double *Lrev, double *dinv);
+void launch_band_sweep(Ctx &c, int nblocks, const int *d_p0, const int *d_len, int max_len, int bw, bool forward,
+                       const double *Lcol, const double *Lrev, const double *dinv, const double *in, const int *gather,
+                       double *out);
 void drop_caches(Ctx &c);
 void build_sell(Ctx &c, const Bsr &A, Sell &S, bool alloc, bool split);
 

@@ -1,0 +1,469 @@
+// filter.cu -- the AMGF filter y = A_w^{-1} r1[Z] (Def. AMGF; A_w = P^T S P)
+// with A_w factored in a nested-dissection elimination order (R16, contracts C9/C10).
+//
+// pi = ND(n_c, bw, levels) is a one-dimensional nested dissection of A_w's band (Z order): an interval is a
+// leaf or is split by a separator of bw consecutive positions, which decouples its two halves; blocks are
+// emitted in postorder.  The oracle factors the dense A_w[pi,pi]; here the factor is stored by structure:
+//   - in-block entries (leaf rows within the band, separator rows inside their separator): band arrays
+//     over pi positions (Lrow / Lcol / Lrev, stride band_stride(bw)), zero across blocks;
+//   - separator rows against their subtree (dense by fill): Loff, row-major per separator
+//     (Loff[off + s * (p0 - t0) + (k - t0)] = L_{p0+s, k}).
+// Every entry keeps the contract's chain (ascending k for the factor and the forward solve, descending k for
+// the backward solve); terms skipped here are exact zeros of the dense factor.  Parallelism: leaves are
+// independent (one CTA / warp each); separators of one level are independent.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+namespace amgf {
+
+struct NdBlk {
+  int p0, len, kind;  // kind 0 = leaf, 1 = separator
+  int t0;             // separator: first pi position of its subtree
+  long off;           // separator: offset of its rows in Loff (row-major: s * (p0 - t0) + (k - t0))
+  int level;          // separator depth (root 0)
+};
+
+namespace {
+
+struct Node {
+  int z0, z1;  // Z interval
+  bool leaf;
+  int left = -1, right = -1;
+  int depth;
+};
+
+// Same recursion as orc_nd_order (oracle/amgf_oracle.c): leaf if depth == 0 or b - a < 4 bw + 64.
+int build(std::vector<Node> &nodes, int a, int b, int depth, int bw, int d) {
+  Node nd;
+  nd.z0 = a; nd.z1 = b; nd.depth = d;
+  if (depth == 0 || b - a < 4 * bw + 64) {
+    nd.leaf = true;
+    nodes.push_back(nd);
+    return (int)nodes.size() - 1;
+  }
+  nd.leaf = false;
+  const int m = a + (b - a - bw) / 2;
+  nodes.push_back(nd);
+  const int id = (int)nodes.size() - 1;
+  const int l = build(nodes, a, m, depth - 1, bw, d + 1);
+  const int r = build(nodes, m + bw, b, depth - 1, bw, d + 1);
+  nodes[id].left = l;
+  nodes[id].right = r;
+  nodes[id].z0 = m;  // separator interval [m, m + bw)
+  nodes[id].z1 = m + bw;
+  return id;
+}
+
+struct Emit {
+  std::vector<NdBlk> blk;
+  std::vector<int> pi;  // pi position -> Z position
+  std::vector<std::vector<int>> sub_leaves, sub_seps;  // per block (separators): blocks in its subtree
+};
+
+// postorder emission; returns (first block id, subtree start pi)
+int emit(const std::vector<Node> &nodes, int id, Emit &E, std::vector<int> &leaves, std::vector<int> &seps) {
+  const Node &nd = nodes[id];
+  if (nd.leaf) {
+    NdBlk b{(int)E.pi.size(), nd.z1 - nd.z0, 0, (int)E.pi.size(), 0, nd.depth};
+    for (int z = nd.z0; z < nd.z1; z++) E.pi.push_back(z);
+    E.blk.push_back(b);
+    E.sub_leaves.emplace_back();
+    E.sub_seps.emplace_back();
+    leaves.push_back((int)E.blk.size() - 1);
+    return b.t0;
+  }
+  std::vector<int> ll, ls, rl, rs;
+  const int t0 = emit(nodes, nd.left, E, ll, ls);
+  emit(nodes, nd.right, E, rl, rs);
+  NdBlk b{(int)E.pi.size(), nd.z1 - nd.z0, 1, t0, 0, nd.depth};
+  for (int z = nd.z0; z < nd.z1; z++) E.pi.push_back(z);
+  E.blk.push_back(b);
+  std::vector<int> sl = ll, ss = ls;  // subtree blocks in pi order: left subtree, then right subtree
+  sl.insert(sl.end(), rl.begin(), rl.end());
+  ss.insert(ss.end(), rs.begin(), rs.end());
+  E.sub_leaves.push_back(sl);
+  E.sub_seps.push_back(ss);
+  leaves.insert(leaves.end(), sl.begin(), sl.end());
+  seps.insert(seps.end(), ss.begin(), ss.end());
+  seps.push_back((int)E.blk.size() - 1);
+  return t0;
+}
+
+template <class T>
+T *upload(Ctx &c, const std::vector<T> &v) {
+  T *d = c.alloc<T>(v.size());
+  if (!v.empty()) CK(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, c.stream));
+  return d;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ kernels
+// acc - sum_{t < n} a[t*sa] * b[t*sb] as one fma chain in ascending t (contract order), with the loads of
+// the next 8 terms in flight while the current 8 are consumed (register double buffer).
+__device__ __forceinline__ double chain_sub(double acc, const double *__restrict__ a, long sa,
+                                            const double *__restrict__ b, long sb, int n) {
+  int t = 0;
+  double ra[8], rb[8];
+  if (n >= 8) {
+#pragma unroll
+    for (int u = 0; u < 8; u++) { ra[u] = a[u * sa]; rb[u] = b[u * sb]; }
+    for (; t + 16 <= n; t += 8) {
+      double na[8], nb[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) { na[u] = a[(t + 8 + u) * sa]; nb[u] = b[(t + 8 + u) * sb]; }
+#pragma unroll
+      for (int u = 0; u < 8; u++) acc = __fma_rn(-ra[u], rb[u], acc);
+#pragma unroll
+      for (int u = 0; u < 8; u++) { ra[u] = na[u]; rb[u] = nb[u]; }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; u++) acc = __fma_rn(-ra[u], rb[u], acc);
+    t += 8;
+  }
+  for (; t < n; t++) acc = __fma_rn(-a[t * sa], b[t * sb], acc);
+  return acc;
+}
+
+__global__ void k_nd_maps(int nc, const int *pi_z, const int *Z, int *zpi, int *dof) {
+  int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= nc) return;
+  zpi[pi_z[p]] = p;
+  dof[p] = Z[pi_z[p]];
+}
+__global__ void k_nd_block_of(int nblk, const NdBlk *blk, int *block_of) {
+  int b = blockIdx.x;
+  if (b >= nblk) return;
+  for (int t = threadIdx.x; t < blk[b].len; t += blockDim.x) block_of[blk[b].p0 + t] = b;
+}
+__global__ void k_remap(long n, const int *zpi, int *pos) {
+  long e = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (e < n) pos[e] = zpi[pos[e]];
+}
+
+// A_w[pi,pi] entries of S: in-block lower entries into the band, separator-vs-subtree entries into Loff.
+__global__ void k_nd_fill(int nc, int bw, int W, const NdBlk *blk, const int *block_of, const int *dof,
+                          const int *pos, const int *zpi, const int *S_ptr, const int *S_col, const double *S_val,
+                          double *Lrow, double *Loff) {
+  int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= nc) return;
+  const NdBlk B = blk[block_of[p]];
+  const int d = dof[p], I = d / 3, r = d % 3;
+  for (int k = S_ptr[I]; k < S_ptr[I + 1]; k++)
+    for (int cc = 0; cc < 3; cc++) {
+      const int zq = pos[3 * S_col[k] + cc];
+      if (zq < 0) continue;
+      const int q = zpi[zq];
+      const double v = S_val[(long)k * 9 + 3 * r + cc];
+      if (q >= B.p0 && q <= p) Lrow[(long)p * W + bw - (p - q)] = v;
+      else if (B.kind == 1 && q >= B.t0 && q < B.p0) Loff[B.off + (long)(p - B.p0) * (B.p0 - B.t0) + (q - B.t0)] = v;
+    }
+}
+
+// Separator rows against leaf columns (C9): for j in leaf Lf, L_sj = (a_sj - sum_k L_sk L_jk) / L_jj with
+// k ascending over [max(p0(Lf), j - bw), j) (the only nonzero terms).  One thread per (separator, leaf, s).
+__global__ void k_nd_off_leaf(const int2 *pairs, const NdBlk *blk, int bw, int W, const double *Lrow, double *Loff) {
+  const NdBlk S = blk[pairs[blockIdx.x].x], Lf = blk[pairs[blockIdx.x].y];
+  const int ncol = S.p0 - S.t0;
+  for (int s = threadIdx.x; s < S.len; s += blockDim.x) {
+    double *Ls = Loff + S.off + (long)s * ncol - S.t0;  // Ls[k] = L_sk
+    for (int j = Lf.p0; j < Lf.p0 + Lf.len; j++) {
+      const double *Lj = Lrow + (long)j * W + bw - j;  // Lj[k] = L_jk
+      const int k0 = max(Lf.p0, j - bw);
+      const double acc = chain_sub(Ls[j], Ls + k0, 1, Lj + k0, 1, j - k0);
+      Ls[j] = acc / Lj[j];
+    }
+  }
+}
+
+// Separator rows against the columns j of a lower separator S' (in S's subtree), part 1: the subtree terms
+// acc(s, j) = a_sj - sum_{k in [t0(S'), p0(S'))} L_sk L_jk, all (s, j) in parallel (they do not depend on
+// each other); part 2 (k_nd_off_sep_blk) continues each chain with S'-internal columns.
+// grid.x = (S, S') pair, threads over the len(S) * len(S') entries.
+__global__ void k_nd_off_sep_dot(const int2 *pairs, const NdBlk *blk, double *Loff) {
+  const NdBlk S = blk[pairs[blockIdx.x].x], Sp = blk[pairs[blockIdx.x].y];
+  const int ncol = S.p0 - S.t0, ncolp = Sp.p0 - Sp.t0;
+  const int ne = S.len * Sp.len;
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < ne; e += gridDim.y * blockDim.x) {
+    const int s = e / Sp.len, jj = e % Sp.len;
+    double *Ls = Loff + S.off + (long)s * ncol - S.t0;
+    const double *Lj = Loff + Sp.off + (long)jj * ncolp - Sp.t0;
+    Ls[Sp.p0 + jj] = chain_sub(Ls[Sp.p0 + jj], Ls + Sp.t0, 1, Lj + Sp.t0, 1, Sp.p0 - Sp.t0);
+  }
+}
+// part 2: for j in S' ascending: acc -= sum_{k in [p0', j)} L_sk L_jk; L_sj = acc / L_jj.  Thread per (pair, s).
+__global__ void k_nd_off_sep_blk(const int2 *pairs, const NdBlk *blk, int bw, int W, const double *Lrow,
+                                 double *Loff) {
+  const NdBlk S = blk[pairs[blockIdx.x].x], Sp = blk[pairs[blockIdx.x].y];
+  const int ncol = S.p0 - S.t0;
+  for (int s = threadIdx.x; s < S.len; s += blockDim.x) {
+    double *Ls = Loff + S.off + (long)s * ncol - S.t0;
+    for (int j = Sp.p0; j < Sp.p0 + Sp.len; j++) {
+      const double *Lj = Lrow + (long)j * W + bw - j;
+      const double acc = chain_sub(Ls[j], Ls + Sp.p0, 1, Lj + Sp.p0, 1, j - Sp.p0);
+      Ls[j] = acc / Lj[j];
+    }
+  }
+}
+
+// Schur complement of a separator's own block: acc(s, j) = a_sj - sum_{k in [t0, p0)} L_sk L_jk, j <= s,
+// written into the band; the in-block Cholesky continues the chains (k in [p0, j)).
+__global__ void k_nd_schur(const int *ids, const NdBlk *blk, int bw, int W, double *Lrow, const double *Loff) {
+  const NdBlk S = blk[ids[blockIdx.x]];
+  const int ncol = S.p0 - S.t0;
+  const int ne = S.len * S.len;
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < ne; e += gridDim.y * blockDim.x) {
+    const int s = e / S.len, j = e % S.len;
+    if (j > s) continue;
+    const long ix = (long)(S.p0 + s) * W + bw - (s - j);
+    const double *Ls = Loff + S.off + (long)s * ncol, *Lj = Loff + S.off + (long)j * ncol;
+    Lrow[ix] = chain_sub(Lrow[ix], Ls, 1, Lj, 1, ncol);
+  }
+}
+
+// Forward, separator rows: acc_s = v_s - sum_{k in [t0, p0)} L_sk w_k (ascending k), into accbuf.
+// One CTA per separator, thread s owns row s.  The rows' 32-column chunks and the matching w values are
+// staged in shared memory by cp.async (8-byte copies, transposed to [kk][s] so the chain reads are
+// conflict-free) in an NS-deep ring, so each chain runs at FMA latency instead of memory latency.
+constexpr int SF_KC = 32, SF_NS = 4, SF_THREADS = 256;
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem));
+}
+__global__ void __launch_bounds__(SF_THREADS) k_nd_sep_fwd(const int *ids, const NdBlk *blk, const double *Loff,
+                                                           const double *r1, const int *dof, const double *w,
+                                                           double *accbuf) {
+  extern __shared__ double sfb[];  // [SF_NS][SF_KC][len] rows, then [SF_NS][SF_KC] w
+  const NdBlk S = blk[ids[blockIdx.x]];
+  const int len = S.len, ncol = S.p0 - S.t0;
+  const int nch = (ncol + SF_KC - 1) / SF_KC;
+  double *sw = sfb + SF_NS * SF_KC * len;
+  const double *L0 = Loff + S.off;
+  auto issue = [&](int c) {
+    if (c < nch) {
+      double *dst = sfb + (c % SF_NS) * SF_KC * len;
+      const int k0 = c * SF_KC;
+      const int kn = min(SF_KC, ncol - k0);
+      for (int e = threadIdx.x; e < len * SF_KC; e += SF_THREADS) {
+        const int sr = e / SF_KC, kk = e % SF_KC;  // consecutive threads: consecutive kk of one row
+        if (kk < kn) cp_async8(dst + kk * len + sr, L0 + (long)sr * ncol + k0 + kk);
+      }
+      if (threadIdx.x < kn) cp_async8(sw + (c % SF_NS) * SF_KC + threadIdx.x, w + S.t0 + k0 + threadIdx.x);
+    }
+    asm volatile("cp.async.commit_group;");
+  };
+#pragma unroll
+  for (int c = 0; c < SF_NS - 1; c++) issue(c);
+  const int sr = threadIdx.x;
+  double acc = (sr < len) ? r1[dof[S.p0 + sr]] : 0.0;
+  for (int c = 0; c < nch; c++) {
+    issue(c + SF_NS - 1);
+    asm volatile("cp.async.wait_group %0;" ::"n"(SF_NS - 1));
+    __syncthreads();
+    const double *buf = sfb + (c % SF_NS) * SF_KC * len;
+    const double *wb = sw + (c % SF_NS) * SF_KC;
+    const int kn = min(SF_KC, ncol - c * SF_KC);
+    if (sr < len) {
+      if (kn == SF_KC) {
+#pragma unroll
+        for (int kk = 0; kk < SF_KC; kk++) acc = __fma_rn(-buf[kk * len + sr], wb[kk], acc);
+      } else {
+        for (int kk = 0; kk < kn; kk++) acc = __fma_rn(-buf[kk * len + sr], wb[kk], acc);
+      }
+    }
+    __syncthreads();  // buffer (c % NS) is refilled by the issue of iteration c + 1
+  }
+  asm volatile("cp.async.wait_group 0;");
+  if (sr < len) accbuf[S.p0 + sr] = acc;
+}
+
+// Backward, subtree rows of a separator: acc_k -= sum_{s descending} L_sk x_s (chain continues in w).
+__global__ void k_nd_sep_bwd(const int *ids, const NdBlk *blk, const double *Loff, const double *x, double *w) {
+  const NdBlk S = blk[ids[blockIdx.y]];
+  const int k = S.t0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= S.p0) return;
+  const int ncol = S.p0 - S.t0;
+  const double *Lk = Loff + S.off + (k - S.t0);  // Lk[s * ncol] = L_{p0+s, k}
+  // s descending: start at the last row and step backwards
+  w[k] = chain_sub(w[k], Lk + (long)(S.len - 1) * ncol, -(long)ncol, x + S.p0 + S.len - 1, -1, S.len);
+}
+
+__global__ void k_nd_scatter(int nc, const int *dof, const double *y, double *x2) {
+  int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < nc) x2[dof[p]] = x2[dof[p]] + y[p];
+}
+
+// ------------------------------------------------------------------ host
+void nd_remap_positions(Ctx &c, int *pos_z, long n) {
+  if (n <= 0) return;
+  k_remap<<<nblk(n), CTA, 0, c.stream>>>(n, c.zpi, pos_z);
+  after_launch(c, "k_remap");
+}
+
+void nd_symbolic(Ctx &c) {
+  const int nc = c.nc, bw = c.bw;
+  std::vector<Node> nodes;
+  build(nodes, 0, nc, std::max(0, c.cfg.nd_levels), bw, 0);
+  Emit E;
+  std::vector<int> leaves, seps;
+  emit(nodes, 0, E, leaves, seps);
+  REQUIRE((int)E.pi.size() == nc, AMGF_ERR_ARG, "nd order size mismatch");
+  // Loff offsets
+  long off = 0;
+  int depth = 0;
+  for (auto &b : E.blk)
+    if (b.kind == 1) {
+      b.off = off;
+      off += (long)(b.p0 - b.t0) * b.len;
+      depth = std::max(depth, b.level + 1);
+    }
+  REQUIRE(depth <= 16, AMGF_ERR_LIMIT, "nested dissection deeper than 16 levels");
+  c.nd_nblocks = (int)E.blk.size();
+  c.nd_depth = depth;
+  c.loff_size = off;
+  c.nd_blk = upload(c, E.blk);
+  c.pi_z = upload(c, E.pi);
+  c.zpi = c.alloc<int>(nc);
+  c.dof = c.alloc<int>(nc);
+  c.block_of = c.alloc<int>(nc);
+  k_nd_maps<<<nblk(nc), CTA, 0, c.stream>>>(nc, c.pi_z, c.Z, c.zpi, c.dof);
+  after_launch(c, "k_nd_maps");
+  k_nd_block_of<<<c.nd_nblocks, CTA, 0, c.stream>>>(c.nd_nblocks, (const NdBlk *)c.nd_blk, c.block_of);
+  after_launch(c, "k_nd_block_of");
+  // leaves
+  std::vector<int> lp0, llen, pairs;
+  for (int b = 0; b < (int)E.blk.size(); b++)
+    if (E.blk[b].kind == 0) { lp0.push_back(E.blk[b].p0); llen.push_back(E.blk[b].len); }
+  c.nd_nleaves = (int)lp0.size();
+  c.nd_leaf_p0 = upload(c, lp0);
+  c.nd_leaf_len = upload(c, llen);
+  // separators by level, their lower separators, and (separator, leaf) pairs
+  for (int l = 0; l < depth; l++) {
+    std::vector<int> ids, p0, len, sptr{0}, slist;
+    for (int b = 0; b < (int)E.blk.size(); b++)
+      if (E.blk[b].kind == 1 && E.blk[b].level == l) {
+        ids.push_back(b);
+        p0.push_back(E.blk[b].p0);
+        len.push_back(E.blk[b].len);
+        for (int q : E.sub_seps[b]) slist.push_back(q);  // pi (post)order: deeper first
+        sptr.push_back((int)slist.size());
+      }
+    Ctx::NdLevel &Lv = c.nd_lev[l];
+    Lv.count = (int)ids.size();
+    Lv.ids = upload(c, ids);
+    Lv.p0 = upload(c, p0);
+    Lv.len = upload(c, len);
+    Lv.sub_ptr = upload(c, sptr);
+    Lv.sub_list = upload(c, slist);
+  }
+  for (int b = 0; b < (int)E.blk.size(); b++)
+    if (E.blk[b].kind == 1)
+      for (int lf : E.sub_leaves[b]) { pairs.push_back(b); pairs.push_back(lf); }
+  c.nd_npairs = (int)pairs.size() / 2;
+  c.nd_pairs = upload(c, pairs);
+  // (S, S') pairs: S at level l, S' a separator in S's subtree at depth d > l; one list per (l, d)
+  for (int l = 0; l < depth; l++)
+    for (int d = l + 1; d < depth; d++) {
+      std::vector<int> pr;
+      for (int b = 0; b < (int)E.blk.size(); b++)
+        if (E.blk[b].kind == 1 && E.blk[b].level == l)
+          for (int q : E.sub_seps[b])
+            if (E.blk[q].level == d) { pr.push_back(b); pr.push_back(q); }
+      c.nd_sspairs_n[l][d] = (int)pr.size() / 2;
+      c.nd_sspairs[l][d] = pr.empty() ? nullptr : upload(c, pr);
+    }
+  // storage
+  const int W = band_stride(bw);
+  const size_t total = (size_t)(nc + 2 * BAND_PAD_ROWS) * W;
+  double *r = c.alloc<double>(total), *cl = c.alloc<double>(total), *rv = c.alloc<double>(total);
+  CK(cudaMemsetAsync(cl, 0, total * sizeof(double), c.stream));
+  CK(cudaMemsetAsync(rv, 0, total * sizeof(double), c.stream));
+  CK(cudaMemsetAsync(r, 0, total * sizeof(double), c.stream));
+  c.Lrow = r + (size_t)BAND_PAD_ROWS * W;
+  c.Lcol = cl + (size_t)BAND_PAD_ROWS * W;
+  c.Lrev = rv + (size_t)BAND_PAD_ROWS * W;
+  c.Ldinv = c.alloc<double>(nc);
+  c.Loff = c.alloc<double>(std::max(off, 1L));
+  c.fv = c.alloc<double>(nc);
+  c.fw = c.alloc<double>(nc);
+}
+
+void nd_numeric(Ctx &c) {
+  const int nc = c.nc, bw = c.bw, W = band_stride(bw);
+  const NdBlk *blk = (const NdBlk *)c.nd_blk;
+  Level &L0 = c.lev[0];
+  CK(cudaMemsetAsync(c.Lrow - (size_t)BAND_PAD_ROWS * W, 0, (size_t)(nc + 2 * BAND_PAD_ROWS) * W * sizeof(double),
+                     c.stream));
+  if (c.loff_size) CK(cudaMemsetAsync(c.Loff, 0, c.loff_size * sizeof(double), c.stream));
+  k_nd_fill<<<nblk(nc), CTA, 0, c.stream>>>(nc, bw, W, blk, c.block_of, c.dof, c.pos, c.zpi, L0.A.ptr, L0.A.col,
+                                            L0.A.val, c.Lrow, c.Loff);
+  after_launch(c, "k_nd_fill");
+  // leaves (independent), then separator-vs-leaf columns (independent given the leaves)
+  band_factor_blocks(c, nc, c.nd_nleaves, c.nd_leaf_p0, c.nd_leaf_len, bw, c.Lrow, 1);
+  if (c.nd_npairs) {
+    k_nd_off_leaf<<<c.nd_npairs, 128, 0, c.stream>>>((const int2 *)c.nd_pairs, blk, bw, W, c.Lrow, c.Loff);
+    after_launch(c, "k_nd_off_leaf");
+  }
+  // separators bottom-up; for a separator S at level l, its lower separators S' (depth d > l) in postorder
+  // (deepest first), each in two parts (subtree terms in parallel, then the S'-internal chain)
+  for (int l = c.nd_depth - 1; l >= 0; l--) {
+    Ctx::NdLevel &Lv = c.nd_lev[l];
+    if (!Lv.count) continue;
+    for (int d = c.nd_depth - 1; d > l; d--) {
+      const int np = c.nd_sspairs_n[l][d];
+      if (!np) continue;
+      dim3 g1(np, 16);
+      k_nd_off_sep_dot<<<g1, 256, 0, c.stream>>>((const int2 *)c.nd_sspairs[l][d], blk, c.Loff);
+      after_launch(c, "k_nd_off_sep_dot");
+      k_nd_off_sep_blk<<<np, 256, 0, c.stream>>>((const int2 *)c.nd_sspairs[l][d], blk, bw, W, c.Lrow, c.Loff);
+      after_launch(c, "k_nd_off_sep_blk");
+    }
+    dim3 g2(Lv.count, 16);
+    k_nd_schur<<<g2, 256, 0, c.stream>>>(Lv.ids, blk, bw, W, c.Lrow, c.Loff);
+    after_launch(c, "k_nd_schur");
+    band_factor_blocks(c, nc, Lv.count, Lv.p0, Lv.len, bw, c.Lrow, 1);
+  }
+  band_finish(c, nc, bw, c.Lrow, c.Lcol, c.Lrev, c.Ldinv);
+}
+
+void nd_solve(Ctx &c, const double *r1, double *x2) {
+  const int nc = c.nc, bw = c.bw;
+  const NdBlk *blk = (const NdBlk *)c.nd_blk;
+  double *w = c.fw, *y = c.fv;
+  // forward: leaves (gathered r1), then separators bottom-up
+  launch_band_sweep(c, c.nd_nleaves, c.nd_leaf_p0, c.nd_leaf_len, nc, bw, true, c.Lcol, c.Lrev, c.Ldinv, r1, c.dof,
+                    w);
+  for (int l = c.nd_depth - 1; l >= 0; l--) {
+    Ctx::NdLevel &Lv = c.nd_lev[l];
+    if (!Lv.count) continue;
+    {
+      const size_t smem = (size_t)SF_NS * SF_KC * (bw + 1) * sizeof(double);
+      static bool attr = false;
+      if (!attr) {
+        CK(cudaFuncSetAttribute(k_nd_sep_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        attr = true;
+      }
+      REQUIRE(bw <= SF_THREADS && smem <= 220 * 1024, AMGF_ERR_LIMIT, "separator too wide for k_nd_sep_fwd");
+      k_nd_sep_fwd<<<Lv.count, SF_THREADS, smem, c.stream>>>(Lv.ids, blk, c.Loff, r1, c.dof, w, y);
+    }
+    after_launch(c, "k_nd_sep_fwd");
+    launch_band_sweep(c, Lv.count, Lv.p0, Lv.len, nc, bw, true, c.Lcol, c.Lrev, c.Ldinv, y, nullptr, w);
+  }
+  // backward: separators top-down (then their subtree rows), then leaves
+  for (int l = 0; l < c.nd_depth; l++) {
+    Ctx::NdLevel &Lv = c.nd_lev[l];
+    if (!Lv.count) continue;
+    launch_band_sweep(c, Lv.count, Lv.p0, Lv.len, nc, bw, false, c.Lcol, c.Lrev, c.Ldinv, w, nullptr, y);
+    dim3 grid((nc + 127) / 128, Lv.count);
+    k_nd_sep_bwd<<<grid, 128, 0, c.stream>>>(Lv.ids, blk, c.Loff, y, w);
+    after_launch(c, "k_nd_sep_bwd");
+  }
+  launch_band_sweep(c, c.nd_nleaves, c.nd_leaf_p0, c.nd_leaf_len, nc, bw, false, c.Lcol, c.Lrev, c.Ldinv, w, nullptr,
+                    y);
+  k_nd_scatter<<<nblk(nc), CTA, 0, c.stream>>>(nc, c.dof, y, x2);
+  after_launch(c, "k_nd_scatter");
+}
+
+}  // namespace amgf

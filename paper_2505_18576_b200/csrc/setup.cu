@@ -250,7 +250,12 @@ __global__ void k_band_fill(int nc, int bw, int W, const int *Z, const int *pos,
 constexpr int CHOL_THREADS = 1024;
 constexpr int CHOL_EPT = 8;  // entries per thread in phase A: (32 + bw) * 32 <= 1024 * 8  =>  bw <= 224
 constexpr int PLD = 33;      // padded row stride of the panel arrays
-__global__ void __launch_bounds__(CHOL_THREADS) k_band_chol(int n, int bw, int W, double *L, int *err, int tag) {
+__global__ void __launch_bounds__(CHOL_THREADS) k_band_chol(int n_all, const int *blk_p0, const int *blk_len, int bw,
+                                                             int W, double *L, int *err, int tag) {
+  // one CTA per diagonal block [p0, p0+n) of the band (the whole band if blk_p0 == nullptr)
+  const int p0 = blk_p0 ? blk_p0[blockIdx.x] : 0;
+  const int n = blk_p0 ? blk_len[blockIdx.x] : n_all;
+  L += (long)p0 * W;
   extern __shared__ double sh[];
   const int rows = 32 + bw;          // rows i = c0 + r of the panel's band
   const int ldk = rows + 1;          // k-major staging AT[kk][r], padded
@@ -298,7 +303,7 @@ __global__ void __launch_bounds__(CHOL_THREADS) k_band_chol(int n, int bw, int W
     const int rend = min(rows, n - c0);
     for (int c = 0; c < cmax; c++) {
       const double ljj = sqrt(PA[c * PLD + c]);  // every thread: identical correctly rounded value
-      if (tid == 0 && !(PA[c * PLD + c] > 0.0)) raise_err(err, DERR_NOT_SPD, tag * 1000000 + c0 + c);
+      if (tid == 0 && !(PA[c * PLD + c] > 0.0)) raise_err(err, DERR_NOT_SPD, tag * 1000000 + p0 + c0 + c);
       const int r = tid;
       if (r < rend && r >= c && r - c <= bw) PL[r * PLD + c] = (r == c) ? ljj : PA[r * PLD + c] / ljj;
       __syncthreads();
@@ -320,7 +325,11 @@ __global__ void __launch_bounds__(CHOL_THREADS) k_band_chol(int n, int bw, int W
   }
 }
 // Fallback for wide bands (e.g. Z = NULL ordering): right-looking on global memory, one CTA (same chains).
-__global__ void __launch_bounds__(1024) k_band_chol_wide(int n, int bw, int W, double *L, int *err, int tag) {
+__global__ void __launch_bounds__(1024) k_band_chol_wide(int n_all, const int *blk_p0, const int *blk_len, int bw,
+                                                         int W, double *L, int *err, int tag) {
+  const int p0 = blk_p0 ? blk_p0[blockIdx.x] : 0;
+  const int n = blk_p0 ? blk_len[blockIdx.x] : n_all;
+  L += (long)p0 * W;
   __shared__ double piv;
   __shared__ int bad;
   const int tid = threadIdx.x;
@@ -329,7 +338,7 @@ __global__ void __launch_bounds__(1024) k_band_chol_wide(int n, int bw, int W, d
   for (int j = 0; j < n; j++) {
     if (tid == 0) {
       double d = L[(long)j * W + bw];
-      if (!(d > 0.0)) { raise_err(err, DERR_NOT_SPD, tag * 1000000 + j); bad = 1; }
+      if (!(d > 0.0)) { raise_err(err, DERR_NOT_SPD, tag * 1000000 + p0 + j); bad = 1; }
       double s = sqrt(d);
       L[(long)j * W + bw] = s;
       piv = s;
@@ -843,17 +852,26 @@ static void band_alloc(Ctx &c, int n, int bw, double *&Lrow, double *&Lcol, doub
   dinv = c.alloc<double>(n);
 }
 
-static void band_factor(Ctx &c, int n, int bw, double *Lrow, double *Lcol, double *Lrev, double *dinv, int tag) {
+// Cholesky of diagonal blocks of a band (nblocks > 0: block lists p0/len on the device; else one block [0,n))
+void band_factor_blocks(Ctx &c, int n, int nblocks, const int *d_p0, const int *d_len, int bw, double *Lrow, int tag) {
   const int W = band_stride(bw);
+  const int grid = nblocks > 0 ? nblocks : 1;
   const size_t smem = (2 * (size_t)(32 + bw) * PLD + 32 * (size_t)(33 + bw)) * sizeof(double);
   if ((32 + bw) * 32 <= CHOL_THREADS * CHOL_EPT && 32 + bw <= CHOL_THREADS && smem <= 220 * 1024) {
     CK(cudaFuncSetAttribute(k_band_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_band_chol<<<1, CHOL_THREADS, smem, c.stream>>>(n, bw, W, Lrow, c.err, tag);
+    k_band_chol<<<grid, CHOL_THREADS, smem, c.stream>>>(n, d_p0, d_len, bw, W, Lrow, c.err, tag);
   } else {
-    k_band_chol_wide<<<1, 1024, 0, c.stream>>>(n, bw, W, Lrow, c.err, tag);
+    k_band_chol_wide<<<grid, 1024, 0, c.stream>>>(n, d_p0, d_len, bw, W, Lrow, c.err, tag);
   }
   after_launch(c, "k_band_chol");
+}
+void band_finish(Ctx &c, int n, int bw, const double *Lrow, double *Lcol, double *Lrev, double *dinv) {
+  const int W = band_stride(bw);
   LAUNCH(k_band_finish, (long)n * (bw + 1), n, bw, W, Lrow, Lcol, Lrev, dinv);
+}
+static void band_factor(Ctx &c, int n, int bw, double *Lrow, double *Lcol, double *Lrev, double *dinv, int tag) {
+  band_factor_blocks(c, n, 0, nullptr, nullptr, bw, Lrow, tag);
+  band_finish(c, n, bw, Lrow, Lcol, Lrev, dinv);
 }
 
 // --------------------------------------------------------------- numeric pieces (reused by update_D)
@@ -871,12 +889,7 @@ static void S_numeric(Ctx &c, const int *S_rowof) {
 
 static void filter_numeric(Ctx &c) {
   if (c.nc == 0) return;
-  Level &L0 = c.lev[0];
-  const int W = band_stride(c.bw);
-  CK(cudaMemsetAsync(c.Lrow - (size_t)BAND_PAD_ROWS * W, 0, (size_t)(c.nc + 2 * BAND_PAD_ROWS) * W * sizeof(double),
-                     c.stream));
-  LAUNCH(k_band_fill, c.nc, c.nc, c.bw, W, c.Z, c.pos, L0.A.ptr, L0.A.col, L0.A.val, c.Lrow);
-  band_factor(c, c.nc, c.bw, c.Lrow, c.Lcol, c.Lrev, c.Ldinv, 1);
+  nd_numeric(c);  // filter.cu: A_w[pi,pi] fill + nested-dissection Cholesky
 }
 
 // Run the A_w band fill + Cholesky (single-SM kernel) on the side stream, concurrently with the
@@ -1097,8 +1110,7 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
     LAUNCH(k_band_start, c.nc, c.nc, c.Z, c.pos, L0.A.ptr, L0.A.col, bwd);
     c.bw = d2h1(c, bwd);
     c.release(bwd);
-    band_alloc(c, c.nc, c.bw, c.Lrow, c.Lcol, c.Lrev, c.Ldinv);
-    c.fv = c.alloc<double>(c.nc);
+    nd_symbolic(c);
     filter_numeric(c);
     check_dev_error(c, "A_w Cholesky");
     // thin structure
@@ -1115,6 +1127,7 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
     c.thin_src = c.alloc<int>(tnnz);
     c.thin_val = c.alloc<double>(tnnz);
     LAUNCH(k_thin_fill, n, n, L0.A.ptr, L0.A.col, c.pos, off, foff, c.thin_row, c.thin_ptr, c.thin_pos, c.thin_src);
+    nd_remap_positions(c, c.thin_pos, tnnz);  // thin entries address y in elimination (pi) order
     int tn = (int)tnnz;
     CK(cudaMemcpyAsync(c.thin_ptr + c.nthin, &tn, sizeof(int), cudaMemcpyHostToDevice, c.stream));
     C.thin_nnz = tnnz;

@@ -599,6 +599,156 @@ __global__ void __launch_bounds__(32) k_band_trsv(int n, int bw, const double *_
   if (scatter) scatter_add_warp(n, scatter, y, xout, lane);
 }
 
+// Block sweep (nested-dissection filter, filter.cu): one warp per diagonal block [p0, p0+len) of a band,
+// forward (w = L_B^{-1} in, column sweep over Lcol) or backward (out = L_B^{-T} in, row sweep over Lrev),
+// starting from the accumulators in[] (gathered through gather[] if given).  Same round structure, TMA ring
+// and chain order as k_band_trsv; entries outside the block are zero in the band storage.
+template <int R, int NB, bool FWD>
+__global__ void __launch_bounds__(32) k_band_sweep(const int *__restrict__ blk_p0, const int *__restrict__ blk_len,
+                                                   int bw, const double *__restrict__ Lcol,
+                                                   const double *__restrict__ Lrev, const double *__restrict__ dinv,
+                                                   const double *__restrict__ in, const int *__restrict__ gather,
+                                                   double *__restrict__ out) {
+  constexpr int Ws = 32 * R;
+  constexpr unsigned CHUNK = 32u * Ws * 8u;
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t bar[NB];
+  const int lane = threadIdx.x;
+  const int p0 = blk_p0[blockIdx.x], n = blk_len[blockIdx.x];
+  const int F = (n + 31) / 32;
+  if (lane == 0) {
+#pragma unroll
+    for (int b = 0; b < NB; b++) mbar_init(&bar[b], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  auto issue = [&](int g) {
+    if (g >= F || lane != 0) return;
+    const double *src = FWD ? Lcol + (long)(p0 + 32 * g) * Ws : Lrev + (long)(p0 + n - 1 - 32 * g - 31) * Ws;
+    uint64_t *br = &bar[g % NB];
+    mbar_arrive_expect(br, CHUNK);
+    bulk_g2s(sm + (g % NB) * 32 * Ws, src, CHUNK, br);
+  };
+#pragma unroll
+  for (int g = 0; g < NB - 1; g++) issue(g);
+  // local row index t in [0, n): forward row p0 + t, backward row p0 + n - 1 - t
+  auto row = [&](int t) { return FWD ? p0 + t : p0 + n - 1 - t; };
+  auto ld_in = [&](int t) -> double {
+    if (t >= n) return 0.0;
+    const int r = row(t);
+    return gather ? in[gather[r]] : in[r];
+  };
+  double acc[R];
+#pragma unroll
+  for (int s = 0; s < R; s++) acc[s] = ld_in(lane + 32 * s);
+  double dv = (lane < n) ? dinv[row(lane)] : 0.0;
+  double vq1 = ld_in(32 + lane + 32 * (R - 1));
+  double dq1 = (32 + lane < n) ? dinv[row(32 + lane)] : 0.0;
+  for (int q = 0; q < F; q++) {
+    const int t0 = 32 * q;
+    __syncwarp();
+    fence_proxy_async();
+    issue(q + NB - 1);
+    const double vq2 = ld_in(t0 + 64 + lane + 32 * (R - 1));
+    const double dq2 = (t0 + 64 + lane < n) ? dinv[row(t0 + 64 + lane)] : 0.0;
+    mbar_wait(&bar[q % NB], (q / NB) & 1);
+    // forward: column jj of the round at jj*Ws, row offset lane + 32s - jj
+    // backward: row k = k1 - jj at (31 - jj)*Ws, distance lane + 32s - jj
+    const double *cur = sm + (q % NB) * 32 * Ws + lane;
+    double lc[R], mine = 0.0;
+#pragma unroll
+    for (int s = 0; s < R; s++) lc[s] = FWD ? cur[32 * s] : cur[31 * Ws + 32 * s];
+#pragma unroll
+    for (int jj = 0; jj < 32; jj++) {
+      if (t0 + jj >= n) break;
+      double ln[R];
+      const int jn = (jj + 1) & 31;
+#pragma unroll
+      for (int s = 0; s < R; s++) ln[s] = FWD ? cur[jn * (Ws - 1) + 32 * s] : cur[(31 - jn) * Ws - jn + 32 * s];
+      const double yj = __shfl_sync(0xffffffffu, acc[0] * dv, jj);
+      mine = (lane == jj) ? yj : mine;
+#pragma unroll
+      for (int s = 0; s < R; s++) acc[s] = __fma_rn(-lc[s], yj, acc[s]);
+#pragma unroll
+      for (int s = 0; s < R; s++) lc[s] = ln[s];
+    }
+    if (t0 + lane < n) out[row(t0 + lane)] = mine;
+#pragma unroll
+    for (int s = 0; s < R - 1; s++) acc[s] = acc[s + 1];
+    acc[R - 1] = vq1;
+    dv = dq1;
+    vq1 = vq2;
+    dq1 = dq2;
+  }
+}
+
+template <int R>
+static void sweep_R(Ctx &c, int nblocks, const int *p0, const int *len, int bw, bool fwd, const double *Lcol,
+                    const double *Lrev, const double *dinv, const double *in, const int *gather, double *out) {
+  constexpr int NB = (220 * 1024) / (32 * 32 * R * 8) >= 4 ? 4 : 3;
+  const size_t smem = (size_t)NB * 32 * (32 * R) * sizeof(double);
+  static bool attr_f = false, attr_b = false;
+  if (fwd) {
+    if (!attr_f) {
+      CK(cudaFuncSetAttribute(k_band_sweep<R, NB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr_f = true;
+    }
+    k_band_sweep<R, NB, true><<<nblocks, 32, smem, c.stream>>>(p0, len, bw, Lcol, Lrev, dinv, in, gather, out);
+  } else {
+    if (!attr_b) {
+      CK(cudaFuncSetAttribute(k_band_sweep<R, NB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr_b = true;
+    }
+    k_band_sweep<R, NB, false><<<nblocks, 32, smem, c.stream>>>(p0, len, bw, Lcol, Lrev, dinv, in, gather, out);
+  }
+}
+
+// Generic fallback sweep for wide bands: one CTA per block, barrier per pivot.
+__global__ void __launch_bounds__(1024) k_band_sweep_wide(const int *blk_p0, const int *blk_len, int bw, int W, bool fwd,
+                                                          const double *__restrict__ Lcol,
+                                                          const double *__restrict__ Lrev,
+                                                          const double *__restrict__ dinv,
+                                                          const double *__restrict__ in, const int *__restrict__ gather,
+                                                          double *__restrict__ out) {
+  __shared__ double piv;
+  const int p0 = blk_p0[blockIdx.x], n = blk_len[blockIdx.x];
+  for (int t = threadIdx.x; t < n; t += blockDim.x) out[p0 + t] = gather ? in[gather[p0 + t]] : in[p0 + t];
+  __syncthreads();
+  for (int u = 0; u < n; u++) {
+    const int j = fwd ? p0 + u : p0 + n - 1 - u;
+    if (threadIdx.x == 0) { piv = out[j] * dinv[j]; out[j] = piv; }
+    __syncthreads();
+    const double yj = piv;
+    for (int d = 1 + threadIdx.x; d <= bw; d += blockDim.x) {
+      const int i = fwd ? j + d : j - d;
+      if (i < p0 || i >= p0 + n) continue;
+      const double l = fwd ? Lcol[(long)j * W + d] : Lrev[(long)j * W + d];
+      out[i] = __fma_rn(-l, yj, out[i]);
+    }
+    __syncthreads();
+  }
+}
+
+void launch_band_sweep(Ctx &c, int nblocks, const int *d_p0, const int *d_len, int max_len, int bw, bool forward,
+                       const double *Lcol, const double *Lrev, const double *dinv, const double *in, const int *gather,
+                       double *out) {
+  if (nblocks == 0 || max_len == 0) return;
+  const int R = (bw + 31) / 32 + 1;
+  switch (R) {
+    case 1: case 2: sweep_R<2>(c, nblocks, d_p0, d_len, bw, forward, Lcol, Lrev, dinv, in, gather, out); break;
+    case 3: sweep_R<3>(c, nblocks, d_p0, d_len, bw, forward, Lcol, Lrev, dinv, in, gather, out); break;
+    case 4: sweep_R<4>(c, nblocks, d_p0, d_len, bw, forward, Lcol, Lrev, dinv, in, gather, out); break;
+    case 5: sweep_R<5>(c, nblocks, d_p0, d_len, bw, forward, Lcol, Lrev, dinv, in, gather, out); break;
+    case 6: sweep_R<6>(c, nblocks, d_p0, d_len, bw, forward, Lcol, Lrev, dinv, in, gather, out); break;
+    case 7: sweep_R<7>(c, nblocks, d_p0, d_len, bw, forward, Lcol, Lrev, dinv, in, gather, out); break;
+    case 8: sweep_R<8>(c, nblocks, d_p0, d_len, bw, forward, Lcol, Lrev, dinv, in, gather, out); break;
+    default:
+      k_band_sweep_wide<<<nblocks, 1024, 0, c.stream>>>(d_p0, d_len, bw, band_stride(bw), forward, Lcol, Lrev, dinv,
+                                                        in, gather, out);
+  }
+  after_launch(c, "k_band_sweep");
+}
+
 // Generic fallback for wide bands: one CTA, thread per row of the window, barrier per pivot.
 __global__ void __launch_bounds__(1024) k_band_trsv_wide(int n, int bw, const double *__restrict__ Lcol,
                                                          const double *__restrict__ Lrev,
