@@ -12,7 +12,7 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "--fm
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    deps = SRC + [os.path.join(HERE, "csrc", "common.cuh"), os.path.join(HERE, "..", "include", "amgf.h")]
+    deps = SRC + [os.path.join(HERE, "csrc", "common.cuh"), os.path.join(HERE, "csrc", "devutil.cuh"), os.path.join(HERE, "..", "include", "amgf.h")]
     if not force and os.path.exists(LIB) and all(os.path.getmtime(LIB) >= os.path.getmtime(d) for d in deps):
         return LIB
     cmd = [NVCC, *FLAGS, "-o", LIB, *SRC]

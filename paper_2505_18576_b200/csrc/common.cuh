@@ -109,14 +109,17 @@ struct Ctx {
   int *S_kblk = nullptr;  // per S block: index of the K block (-1 if none)
   // filter (A_w factor in nested-dissection order, filter.cu)
   struct NdLevel { int count = 0; int *ids = nullptr, *p0 = nullptr, *len = nullptr, *sub_ptr = nullptr, *sub_list = nullptr; };
-  int nd_nblocks = 0, nd_nleaves = 0, nd_depth = 0, nd_npairs = 0;
+  int nd_nblocks = 0, nd_nleaves = 0, nd_depth = 0, nd_npairs = 0, nd_nsep = 0;
+  int *nd_sep_blocks = nullptr;
   void *nd_blk = nullptr;                 // device NdBlk[nd_nblocks]
   int *nd_leaf_p0 = nullptr, *nd_leaf_len = nullptr, *nd_pairs = nullptr;
   NdLevel nd_lev[16];                     // separators by depth (0 = root)
   int *nd_sspairs[16][16] = {};           // (S at level l, S' at depth d) pairs
   int nd_sspairs_n[16][16] = {};
   int *pi_z = nullptr, *zpi = nullptr, *dof = nullptr, *block_of = nullptr;
-  double *Loff = nullptr;
+  double *Loff = nullptr;                 // separator rows, row-major (factorization)
+  double *LoffT = nullptr;                // the same, k-major (solve: one TMA bulk copy per chunk)
+  double *fw2 = nullptr;                  // forward results shifted by one position (TMA alignment)
   long loff_size = 0;
   double *fw = nullptr;                   // filter workspace (pi order)
   int nc = 0, bw = 0;
@@ -214,7 +217,7 @@ void band_factor_blocks(Ctx &c, int n, int nblocks, const int *d_p0, const int *
 void band_finish(Ctx &c, int n, int bw, const double *Lrow, double *Lcol, double *Lrev, double *dinv);
 void launch_band_sweep(Ctx &c, int nblocks, const int *d_p0, const int *d_len, int max_len, int bw, bool forward,
                        const double *Lcol, const double *Lrev, const double *dinv, const double *in, const int *gather,
-                       double *out);
+                       double *out, double *out_shift = nullptr);
 void drop_caches(Ctx &c);
 void build_sell(Ctx &c, const Bsr &A, Sell &S, bool alloc, bool split);
 

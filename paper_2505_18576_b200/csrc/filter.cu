@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "devutil.cuh"
 
 namespace amgf {
 
@@ -224,59 +225,74 @@ __global__ void k_nd_schur(const int *ids, const NdBlk *blk, int bw, int W, doub
 }
 
 // Forward, separator rows: acc_s = v_s - sum_{k in [t0, p0)} L_sk w_k (ascending k), into accbuf.
-// One CTA per separator, thread s owns row s.  The rows' 32-column chunks and the matching w values are
-// staged in shared memory by cp.async (8-byte copies, transposed to [kk][s] so the chain reads are
-// conflict-free) in an NS-deep ring, so each chain runs at FMA latency instead of memory latency.
+// One CTA per separator, thread s owns row s.  Chunks of SF_KC columns of the k-major copy LoffT (one
+// contiguous block per chunk) and the matching w values are brought into shared memory by TMA bulk copies
+// in an SF_NS-deep ring (full/empty mbarriers, thread 0 produces), so each chain runs at FMA latency.
 constexpr int SF_KC = 32, SF_NS = 4, SF_THREADS = 256;
-__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
-  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem));
-}
-__global__ void __launch_bounds__(SF_THREADS) k_nd_sep_fwd(const int *ids, const NdBlk *blk, const double *Loff,
+__global__ void __launch_bounds__(SF_THREADS) k_nd_sep_fwd(const int *ids, const NdBlk *blk, const double *LoffT,
                                                            const double *r1, const int *dof, const double *w,
-                                                           double *accbuf) {
-  extern __shared__ double sfb[];  // [SF_NS][SF_KC][len] rows, then [SF_NS][SF_KC] w
+                                                           const double *w2, double *accbuf) {
+  extern __shared__ __align__(128) double sfb[];  // [SF_NS][SF_KC * len] rows, then [SF_NS][SF_KC] w
+  __shared__ __align__(8) uint64_t full[SF_NS], empty[SF_NS];
   const NdBlk S = blk[ids[blockIdx.x]];
   const int len = S.len, ncol = S.p0 - S.t0;
   const int nch = (ncol + SF_KC - 1) / SF_KC;
-  double *sw = sfb + SF_NS * SF_KC * len;
-  const double *L0 = Loff + S.off;
-  auto issue = [&](int c) {
-    if (c < nch) {
-      double *dst = sfb + (c % SF_NS) * SF_KC * len;
-      const int k0 = c * SF_KC;
-      const int kn = min(SF_KC, ncol - k0);
-      for (int e = threadIdx.x; e < len * SF_KC; e += SF_THREADS) {
-        const int sr = e / SF_KC, kk = e % SF_KC;  // consecutive threads: consecutive kk of one row
-        if (kk < kn) cp_async8(dst + kk * len + sr, L0 + (long)sr * ncol + k0 + kk);
-      }
-      if (threadIdx.x < kn) cp_async8(sw + (c % SF_NS) * SF_KC + threadIdx.x, w + S.t0 + k0 + threadIdx.x);
-    }
-    asm volatile("cp.async.commit_group;");
-  };
+  const int tid = threadIdx.x;
+  double *sL = sfb, *sW = sfb + SF_NS * SF_KC * len;
+  // w[t0 + k] 16-byte aligned: from w itself (t0 even) or from the copy shifted by one (t0 odd)
+  const double *wsrc = (S.t0 & 1) ? w2 + S.t0 + 1 : w + S.t0;
+  const unsigned bytesL = (unsigned)(SF_KC * len * 8), bytesW = SF_KC * 8;
+  if (tid == 0) {
 #pragma unroll
-  for (int c = 0; c < SF_NS - 1; c++) issue(c);
-  const int sr = threadIdx.x;
-  double acc = (sr < len) ? r1[dof[S.p0 + sr]] : 0.0;
+    for (int b = 0; b < SF_NS; b++) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], SF_THREADS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto produce = [&](int c) {  // thread 0
+    if (c >= nch) return;
+    const int st = c % SF_NS;
+    if (c >= SF_NS) mbar_wait(&empty[st], ((c / SF_NS) - 1) & 1);
+    mbar_arrive_expect(&full[st], bytesL + bytesW);
+    bulk_g2s(sL + st * SF_KC * len, LoffT + S.off + (long)c * SF_KC * len, bytesL, &full[st]);
+    bulk_g2s(sW + st * SF_KC, wsrc + (long)c * SF_KC, bytesW, &full[st]);
+  };
+  if (tid == 0)
+    for (int c = 0; c < SF_NS; c++) produce(c);
+  double acc = (tid < len) ? r1[dof[S.p0 + tid]] : 0.0;
   for (int c = 0; c < nch; c++) {
-    issue(c + SF_NS - 1);
-    asm volatile("cp.async.wait_group %0;" ::"n"(SF_NS - 1));
-    __syncthreads();
-    const double *buf = sfb + (c % SF_NS) * SF_KC * len;
-    const double *wb = sw + (c % SF_NS) * SF_KC;
+    const int st = c % SF_NS;
+    mbar_wait(&full[st], (c / SF_NS) & 1);
+    const double *buf = sL + st * SF_KC * len + tid;
+    const double *wb = sW + st * SF_KC;
     const int kn = min(SF_KC, ncol - c * SF_KC);
-    if (sr < len) {
+    if (tid < len) {
       if (kn == SF_KC) {
 #pragma unroll
-        for (int kk = 0; kk < SF_KC; kk++) acc = __fma_rn(-buf[kk * len + sr], wb[kk], acc);
+        for (int kk = 0; kk < SF_KC; kk++) acc = __fma_rn(-buf[kk * len], wb[kk], acc);
       } else {
-        for (int kk = 0; kk < kn; kk++) acc = __fma_rn(-buf[kk * len + sr], wb[kk], acc);
+        for (int kk = 0; kk < kn; kk++) acc = __fma_rn(-buf[kk * len], wb[kk], acc);
       }
     }
-    __syncthreads();  // buffer (c % NS) is refilled by the issue of iteration c + 1
+    mbar_arrive(&empty[st]);
+    if (tid == 0) produce(c + SF_NS);
   }
-  asm volatile("cp.async.wait_group 0;");
-  if (sr < len) accbuf[S.p0 + sr] = acc;
+  if (tid < len) accbuf[S.p0 + tid] = acc;
+}
+
+// k-major copy of the separator rows for the forward solve: LoffT[off + (k - t0) * len + s]
+__global__ void k_nd_transpose(int nsep_blocks, const int *sep_block_ids, const NdBlk *blk, const double *Loff,
+                               double *LoffT) {
+  const NdBlk S = blk[sep_block_ids[blockIdx.y]];
+  const int ncol = S.p0 - S.t0;
+  const long ne = (long)ncol * S.len;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < ne; e += (long)gridDim.x * blockDim.x) {
+    const int s = (int)(e % S.len);
+    const long k = e / S.len;
+    LoffT[S.off + e] = Loff[S.off + (long)s * ncol + k];
+  }
 }
 
 // Backward, subtree rows of a separator: acc_k -= sum_{s descending} L_sk x_s (chain continues in w).
@@ -313,12 +329,17 @@ void nd_symbolic(Ctx &c) {
   // Loff offsets
   long off = 0;
   int depth = 0;
-  for (auto &b : E.blk)
+  std::vector<int> sep_blocks;
+  for (int bi = 0; bi < (int)E.blk.size(); bi++) {
+    NdBlk &b = E.blk[bi];
     if (b.kind == 1) {
       b.off = off;
       off += (long)(b.p0 - b.t0) * b.len;
+      off = (off + 1) & ~1L;  // even offsets: 16-byte aligned TMA sources
       depth = std::max(depth, b.level + 1);
+      sep_blocks.push_back(bi);
     }
+  }
   REQUIRE(depth <= 16, AMGF_ERR_LIMIT, "nested dissection deeper than 16 levels");
   c.nd_nblocks = (int)E.blk.size();
   c.nd_depth = depth;
@@ -386,8 +407,12 @@ void nd_symbolic(Ctx &c) {
   c.Lrev = rv + (size_t)BAND_PAD_ROWS * W;
   c.Ldinv = c.alloc<double>(nc);
   c.Loff = c.alloc<double>(std::max(off, 1L));
+  c.LoffT = c.alloc<double>(off + (long)SF_KC * (bw + 2) + 2);  // chunks may read past the last separator
   c.fv = c.alloc<double>(nc);
-  c.fw = c.alloc<double>(nc);
+  c.fw = c.alloc<double>(nc + SF_KC + 2);
+  c.fw2 = c.alloc<double>(nc + SF_KC + 2);
+  c.nd_nsep = (int)sep_blocks.size();
+  c.nd_sep_blocks = upload(c, sep_blocks);
 }
 
 void nd_numeric(Ctx &c) {
@@ -426,6 +451,11 @@ void nd_numeric(Ctx &c) {
     band_factor_blocks(c, nc, Lv.count, Lv.p0, Lv.len, bw, c.Lrow, 1);
   }
   band_finish(c, nc, bw, c.Lrow, c.Lcol, c.Lrev, c.Ldinv);
+  if (c.nd_nsep) {
+    dim3 g(64, c.nd_nsep);
+    k_nd_transpose<<<g, CTA, 0, c.stream>>>(c.nd_nsep, c.nd_sep_blocks, blk, c.Loff, c.LoffT);
+    after_launch(c, "k_nd_transpose");
+  }
 }
 
 void nd_solve(Ctx &c, const double *r1, double *x2) {
@@ -434,7 +464,7 @@ void nd_solve(Ctx &c, const double *r1, double *x2) {
   double *w = c.fw, *y = c.fv;
   // forward: leaves (gathered r1), then separators bottom-up
   launch_band_sweep(c, c.nd_nleaves, c.nd_leaf_p0, c.nd_leaf_len, nc, bw, true, c.Lcol, c.Lrev, c.Ldinv, r1, c.dof,
-                    w);
+                    w, c.fw2);
   for (int l = c.nd_depth - 1; l >= 0; l--) {
     Ctx::NdLevel &Lv = c.nd_lev[l];
     if (!Lv.count) continue;
@@ -446,10 +476,10 @@ void nd_solve(Ctx &c, const double *r1, double *x2) {
         attr = true;
       }
       REQUIRE(bw <= SF_THREADS && smem <= 220 * 1024, AMGF_ERR_LIMIT, "separator too wide for k_nd_sep_fwd");
-      k_nd_sep_fwd<<<Lv.count, SF_THREADS, smem, c.stream>>>(Lv.ids, blk, c.Loff, r1, c.dof, w, y);
+      k_nd_sep_fwd<<<Lv.count, SF_THREADS, smem, c.stream>>>(Lv.ids, blk, c.LoffT, r1, c.dof, w, c.fw2, y);
+      after_launch(c, "k_nd_sep_fwd");
     }
-    after_launch(c, "k_nd_sep_fwd");
-    launch_band_sweep(c, Lv.count, Lv.p0, Lv.len, nc, bw, true, c.Lcol, c.Lrev, c.Ldinv, y, nullptr, w);
+    launch_band_sweep(c, Lv.count, Lv.p0, Lv.len, nc, bw, true, c.Lcol, c.Lrev, c.Ldinv, y, nullptr, w, c.fw2);
   }
   // backward: separators top-down (then their subtree rows), then leaves
   for (int l = 0; l < c.nd_depth; l++) {

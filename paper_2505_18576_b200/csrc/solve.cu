@@ -9,6 +9,7 @@
 //               double-buffered band columns (C10); gather r1[Z] and scatter x2[Z] += y fused.
 //   k_thin      r2 = r1 - S[:,Z] y over the rows that touch Z (C11).
 #include "common.cuh"
+#include "devutil.cuh"
 
 namespace amgf {
 
@@ -402,28 +403,7 @@ void launch_dot(Ctx &c, long n, int b, const double *u, const double *v, int fin
 }
 
 // ------------------------------------------------------------------ banded triangular solves (C10)
-__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive_expect(uint64_t *bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
-          smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-// TMA bulk copy global -> shared (SASS UBLKCP), completion counted on an mbarrier
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 
 // One warp solves L L^T y = v[gather] (C10).  Forward: column sweep j ascending over Lcol
 // (Lcol[j*W + t] = L_{j+t,j}); backward: row sweep k descending over Lrev (Lrev[k*W + d] = L_{k,k-d}).
@@ -608,7 +588,7 @@ __global__ void __launch_bounds__(32) k_band_sweep(const int *__restrict__ blk_p
                                                    int bw, const double *__restrict__ Lcol,
                                                    const double *__restrict__ Lrev, const double *__restrict__ dinv,
                                                    const double *__restrict__ in, const int *__restrict__ gather,
-                                                   double *__restrict__ out) {
+                                                   double *__restrict__ out, double *__restrict__ out_shift) {
   constexpr int Ws = 32 * R;
   constexpr unsigned CHUNK = 32u * Ws * 8u;
   extern __shared__ __align__(128) double sm[];
@@ -672,7 +652,10 @@ __global__ void __launch_bounds__(32) k_band_sweep(const int *__restrict__ blk_p
 #pragma unroll
       for (int s = 0; s < R; s++) lc[s] = ln[s];
     }
-    if (t0 + lane < n) out[row(t0 + lane)] = mine;
+    if (t0 + lane < n) {
+      out[row(t0 + lane)] = mine;
+      if (out_shift) out_shift[row(t0 + lane) + 1] = mine;  // copy shifted by one (TMA alignment, filter.cu)
+    }
 #pragma unroll
     for (int s = 0; s < R - 1; s++) acc[s] = acc[s + 1];
     acc[R - 1] = vq1;
@@ -684,7 +667,8 @@ __global__ void __launch_bounds__(32) k_band_sweep(const int *__restrict__ blk_p
 
 template <int R>
 static void sweep_R(Ctx &c, int nblocks, const int *p0, const int *len, int bw, bool fwd, const double *Lcol,
-                    const double *Lrev, const double *dinv, const double *in, const int *gather, double *out) {
+                    const double *Lrev, const double *dinv, const double *in, const int *gather, double *out,
+                    double *out_shift) {
   constexpr int NB = (220 * 1024) / (32 * 32 * R * 8) >= 4 ? 4 : 3;
   const size_t smem = (size_t)NB * 32 * (32 * R) * sizeof(double);
   static bool attr_f = false, attr_b = false;
@@ -693,13 +677,15 @@ static void sweep_R(Ctx &c, int nblocks, const int *p0, const int *len, int bw, 
       CK(cudaFuncSetAttribute(k_band_sweep<R, NB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       attr_f = true;
     }
-    k_band_sweep<R, NB, true><<<nblocks, 32, smem, c.stream>>>(p0, len, bw, Lcol, Lrev, dinv, in, gather, out);
+    k_band_sweep<R, NB, true><<<nblocks, 32, smem, c.stream>>>(p0, len, bw, Lcol, Lrev, dinv, in, gather, out,
+                                                                out_shift);
   } else {
     if (!attr_b) {
       CK(cudaFuncSetAttribute(k_band_sweep<R, NB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       attr_b = true;
     }
-    k_band_sweep<R, NB, false><<<nblocks, 32, smem, c.stream>>>(p0, len, bw, Lcol, Lrev, dinv, in, gather, out);
+    k_band_sweep<R, NB, false><<<nblocks, 32, smem, c.stream>>>(p0, len, bw, Lcol, Lrev, dinv, in, gather, out,
+                                                                 out_shift);
   }
 }
 
@@ -709,7 +695,7 @@ __global__ void __launch_bounds__(1024) k_band_sweep_wide(const int *blk_p0, con
                                                           const double *__restrict__ Lrev,
                                                           const double *__restrict__ dinv,
                                                           const double *__restrict__ in, const int *__restrict__ gather,
-                                                          double *__restrict__ out) {
+                                                          double *__restrict__ out, double *__restrict__ out_shift) {
   __shared__ double piv;
   const int p0 = blk_p0[blockIdx.x], n = blk_len[blockIdx.x];
   for (int t = threadIdx.x; t < n; t += blockDim.x) out[p0 + t] = gather ? in[gather[p0 + t]] : in[p0 + t];
@@ -727,24 +713,26 @@ __global__ void __launch_bounds__(1024) k_band_sweep_wide(const int *blk_p0, con
     }
     __syncthreads();
   }
+  if (out_shift)
+    for (int t = threadIdx.x; t < n; t += blockDim.x) out_shift[p0 + t + 1] = out[p0 + t];
 }
 
 void launch_band_sweep(Ctx &c, int nblocks, const int *d_p0, const int *d_len, int max_len, int bw, bool forward,
                        const double *Lcol, const double *Lrev, const double *dinv, const double *in, const int *gather,
-                       double *out) {
+                       double *out, double *out_shift) {
   if (nblocks == 0 || max_len == 0) return;
   const int R = (bw + 31) / 32 + 1;
   switch (R) {
-    case 1: case 2: sweep_R<2>(c, nblocks, d_p0, d_len, bw, forward, Lcol, Lrev, dinv, in, gather, out); break;
-    case 3: sweep_R<3>(c, nblocks, d_p0, d_len, bw, forward, Lcol, Lrev, dinv, in, gather, out); break;
-    case 4: sweep_R<4>(c, nblocks, d_p0, d_len, bw, forward, Lcol, Lrev, dinv, in, gather, out); break;
-    case 5: sweep_R<5>(c, nblocks, d_p0, d_len, bw, forward, Lcol, Lrev, dinv, in, gather, out); break;
-    case 6: sweep_R<6>(c, nblocks, d_p0, d_len, bw, forward, Lcol, Lrev, dinv, in, gather, out); break;
-    case 7: sweep_R<7>(c, nblocks, d_p0, d_len, bw, forward, Lcol, Lrev, dinv, in, gather, out); break;
-    case 8: sweep_R<8>(c, nblocks, d_p0, d_len, bw, forward, Lcol, Lrev, dinv, in, gather, out); break;
+    case 1: case 2: sweep_R<2>(c, nblocks, d_p0, d_len, bw, forward, Lcol, Lrev, dinv, in, gather, out, out_shift); break;
+    case 3: sweep_R<3>(c, nblocks, d_p0, d_len, bw, forward, Lcol, Lrev, dinv, in, gather, out, out_shift); break;
+    case 4: sweep_R<4>(c, nblocks, d_p0, d_len, bw, forward, Lcol, Lrev, dinv, in, gather, out, out_shift); break;
+    case 5: sweep_R<5>(c, nblocks, d_p0, d_len, bw, forward, Lcol, Lrev, dinv, in, gather, out, out_shift); break;
+    case 6: sweep_R<6>(c, nblocks, d_p0, d_len, bw, forward, Lcol, Lrev, dinv, in, gather, out, out_shift); break;
+    case 7: sweep_R<7>(c, nblocks, d_p0, d_len, bw, forward, Lcol, Lrev, dinv, in, gather, out, out_shift); break;
+    case 8: sweep_R<8>(c, nblocks, d_p0, d_len, bw, forward, Lcol, Lrev, dinv, in, gather, out, out_shift); break;
     default:
       k_band_sweep_wide<<<nblocks, 1024, 0, c.stream>>>(d_p0, d_len, bw, band_stride(bw), forward, Lcol, Lrev, dinv,
-                                                        in, gather, out);
+                                                        in, gather, out, out_shift);
   }
   after_launch(c, "k_band_sweep");
 }
