@@ -289,11 +289,48 @@ __global__ void __launch_bounds__(CTA) k_restrict(int nrows, const int *__restri
   }
 }
 
+// One warp per SCALAR row of R (6 per coarse block row): the same lane-strided chain and butterfly per
+// scalar row as k_restrict (C5), with 6x more warps for the latency-bound coarse levels.
+template <int B>
+__global__ void __launch_bounds__(CTA) k_restrict_row(int nrows6, const int *__restrict__ ptr,
+                                                      const int *__restrict__ col, const double *__restrict__ val,
+                                                      const double *__restrict__ r, double *__restrict__ out) {
+  const int w = (blockIdx.x * CTA + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= nrows6) return;  // warp-uniform
+  const int a = w / 6, rr = w % 6;
+  const int beg = ptr[a], end = ptr[a + 1];
+  double acc = 0.0;
+  int k = beg + lane;
+  double v[B], rv[B];
+  if (k < end) {
+    const int c = col[k];
+#pragma unroll
+    for (int e = 0; e < B; e++) { v[e] = __ldg(val + (long)k * 6 * B + rr * B + e); rv[e] = r[(long)c * B + e]; }
+  }
+  for (; k < end; k += 32) {
+    const int kn = k + 32 < end ? k + 32 : k;
+    const int cn = col[kn];
+    double vn[B], rn[B];
+#pragma unroll
+    for (int e = 0; e < B; e++) { vn[e] = __ldg(val + (long)kn * 6 * B + rr * B + e); rn[e] = r[(long)cn * B + e]; }
+#pragma unroll
+    for (int e = 0; e < B; e++) acc = __fma_rn(v[e], rv[e], acc);
+#pragma unroll
+    for (int e = 0; e < B; e++) { v[e] = vn[e]; rv[e] = rn[e]; }
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) acc = acc + __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) out[w] = acc;
+}
+
 void launch_restrict(Ctx &c, const Bsr &R, const double *r, double *bc) {
   if (R.nbr == 0) return;
   long threads = (long)R.nbr * 32;
+  // level 0 (3 x 3 -> 6 x 3 blocks): one warp per coarse block row moves full blocks (measured 69 us at cfg 3
+  // vs 112 us split by scalar row); coarse levels are latency-bound: one warp per scalar row (23 vs 31 us)
   if (R.bc == 3) k_restrict<3><<<nblk(threads), CTA, 0, c.stream>>>(R.nbr, R.ptr, R.col, R.val, r, bc);
-  else k_restrict<6><<<nblk(threads), CTA, 0, c.stream>>>(R.nbr, R.ptr, R.col, R.val, r, bc);
+  else k_restrict_row<6><<<nblk(threads * 6), CTA, 0, c.stream>>>(R.nbr * 6, R.ptr, R.col, R.val, r, bc);
   after_launch(c, __func__);
 }
 
