@@ -73,8 +73,9 @@ void amgf_default_config(amgf_config *cfg);
  *                    blocks per body, Dirichlet rows = identity)
  *   m, J_ptr[m+1], J_col[nnz], J_val[nnz]        gap Jacobian, scalar CSR over dofs
  *   D[m]             log-barrier Hessian diagonal, > 0
- *   Z[nc]            contact dofs I_c in the column order of P; must be a
- *                    permutation of the structurally nonzero columns of J.  NULL: ascending order.
+ *   Z[nc]            contact dofs I_c in the column order of P: duplicate-free and
+ *                    containing every structurally nonzero column of J (e.g. exactly those columns, or
+ *                    all components of the interface nodes).  NULL: J's columns in ascending order.
  *   B_nns[n*6]       near-null space (rigid-body modes), row-major n x 6
  *   cfg              NULL for defaults
  * Synchronises `stream`.  The handle deep-copies everything it needs. */

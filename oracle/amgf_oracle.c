@@ -366,17 +366,22 @@ static int setup_filter(orc_ctx *cx, int m, const int *Jptr, const int *Jcol, co
   cx->pos = (int *)malloc((size_t)n * sizeof(int));
   for (long p = 0; p < n; p++) cx->pos[p] = -1;
   if (Z) {
-    if (nc != nmark) { free(mark); return fail(ORC_ERR_ARG, "Z is not the column support of J (size)"); }
+    /* Z must be duplicate-free and contain every structurally nonzero column of J (reading R1/R17:
+     * I_c = dofs whose basis support touches the contact surface, PAPER.md:384 - a superset of J's
+     * column support, e.g. all components of the interface nodes). */
     cx->Z = (int *)malloc((size_t)(nc > 0 ? nc : 1) * sizeof(int));
+    long covered = 0;
     for (int a = 0; a < nc; a++) {
       int p = Z[a];
-      if (p < 0 || p >= n || !mark[p] || cx->pos[p] >= 0) {
+      if (p < 0 || p >= n || cx->pos[p] >= 0) {
         free(mark);
-        return fail(ORC_ERR_ARG, "Z is not a permutation of the column support of J");
+        return fail(ORC_ERR_ARG, "Z has an out-of-range or duplicate dof");
       }
       cx->Z[a] = p;
       cx->pos[p] = a;
+      covered += mark[p];
     }
+    if (covered != nmark) { free(mark); return fail(ORC_ERR_ARG, "Z does not contain every column of J"); }
   } else {
     nc = (int)nmark;
     cx->Z = (int *)malloc((size_t)(nc > 0 ? nc : 1) * sizeof(int));

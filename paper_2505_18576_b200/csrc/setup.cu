@@ -206,12 +206,15 @@ __global__ void k_mark_cols(int nnz, const int *J_col, int *mark) {
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e < nnz) mark[J_col[e]] = 1;
 }
-__global__ void k_check_Z(int nc, long n, const int *Z, const int *mark, int *pos, int *err) {
+// Z must be duplicate-free and contain every structurally nonzero column of J (I_c: every dof
+// whose basis support touches the contact surface, reading R17); covered counts the columns of J it holds.
+__global__ void k_check_Z(int nc, long n, const int *Z, const int *mark, int *pos, int *covered, int *err) {
   int a = blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= nc) return;
   const int p = Z[a];
-  if (p < 0 || p >= n || !mark[p]) { raise_err(err, DERR_ARG, a); return; }
-  if (atomicCAS(&pos[p], -1, a) != -1) raise_err(err, DERR_ARG, a);
+  if (p < 0 || p >= n) { raise_err(err, DERR_ARG, a); return; }
+  if (atomicCAS(&pos[p], -1, a) != -1) { raise_err(err, DERR_ARG, a); return; }
+  if (mark[p]) atomicAdd(covered, 1);
 }
 __global__ void k_compact_Z(long n, const int *mark, const int *off, int *Z, int *pos) {
   long p = blockIdx.x * (long)blockDim.x + threadIdx.x;
@@ -1087,13 +1090,17 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
     int *off = c.alloc<int>(n + 1);
     long nmark = scan_ex(c, mark, off, n);
     if (Zin) {
-      REQUIRE(nc_in == nmark, AMGF_ERR_ARG, "Z is not the column support of J (size " + std::to_string(nc_in) +
-                                                " vs " + std::to_string(nmark) + ")");
       c.nc = nc_in;
       c.Z = c.alloc<int>(c.nc);
       d2d(c, c.Z, Zin, c.nc);
-      LAUNCH(k_check_Z, c.nc, c.nc, n, c.Z, mark, c.pos, c.err);
-      check_dev_error(c, "Z is not a permutation of the column support of J");
+      int *cov = c.alloc<int>(1);
+      CK(cudaMemsetAsync(cov, 0, sizeof(int), c.stream));
+      LAUNCH(k_check_Z, c.nc, c.nc, n, c.Z, mark, c.pos, cov, c.err);
+      check_dev_error(c, "Z has an out-of-range or duplicate dof");
+      const int covered = d2h1(c, cov);
+      c.release(cov);
+      REQUIRE(covered == nmark, AMGF_ERR_ARG, "Z does not contain every column of J (" + std::to_string(covered) +
+                                                  " of " + std::to_string(nmark) + ")");
     } else {
       c.nc = (int)nmark;
       c.Z = c.alloc<int>(c.nc);

@@ -177,6 +177,20 @@ def test_edge_cases(oracle_lib, amgf_mod):
     assert rep["iterations"] == 0 and not x.abs().max().item()
 
 
+def test_superset_Ic(oracle_lib, amgf_mod):
+    """I_c with all three components of the interface nodes, a superset of J's columns."""
+    p = tiny(N=3, matching=False, e_max=8.0)
+    n1, nn = p.N + 1, (p.N + 1) ** 3
+    fj, fi = np.meshgrid(np.arange(n1), np.arange(n1), indexing="ij")
+    low, up = (p.N * n1 + fj.ravel()) * n1 + fi.ravel(), nn + fj.ravel() * n1 + fi.ravel()
+    Z3 = np.stack([3 * low, 3 * low + 1, 3 * low + 2, 3 * up, 3 * up + 1, 3 * up + 2], axis=1).ravel().astype(np.int32)
+    o, g = build_pair(oracle_lib, amgf_mod, p, Z=Z3, coarsest_size=16)
+    assert g.nc == 3 * len(p.Z)
+    assert_filter_factor_equal(o, g)
+    r = np.random.default_rng(4).standard_normal(p.n)
+    assert np.array_equal(g.apply(r).cpu().numpy(), o.apply(r))
+
+
 def test_empty_Ic(oracle_lib, amgf_mod):
     p = tiny(N=3)
     Jp, Jc, Jv = np.zeros(1, np.int32), np.zeros(0, np.int32), np.zeros(0)
@@ -222,6 +236,9 @@ def test_error_paths(amgf_mod):
     Z = p.Z.copy(); Z[0] = Z[1]
     with pytest.raises(amgf_mod.AmgfError) as e:
         amgf_mod.AMGF.from_problem(p, Z=Z)
+    assert e.value.code == -1
+    with pytest.raises(amgf_mod.AmgfError) as e:      # misses a column of J
+        amgf_mod.AMGF.from_problem(p, Z=p.Z[1:])
     assert e.value.code == -1
     # handle stays usable after a failed update
     g = amgf_mod.AMGF.from_problem(p)

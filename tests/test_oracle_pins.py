@@ -267,6 +267,10 @@ def test_Z_validation(oracle_lib):
         oracle_lib.Oracle.from_problem(p, Z=bad)
     o = oracle_lib.Oracle.from_problem(p, Z=None)
     assert np.array_equal(o.get(20), np.sort(p.Z))
+    with pytest.raises(oracle_lib.OracleError):          # must contain every column of J
+        oracle_lib.Oracle.from_problem(p, Z=p.Z[1:])
+    extra = np.concatenate([p.Z, [0]]).astype(np.int32)  # supersets are allowed
+    assert oracle_lib.Oracle.from_problem(p, Z=extra).nc == len(p.Z) + 1
 
 
 def test_domain_errors(oracle_lib):
