@@ -29,6 +29,11 @@ void Ctx::release(void *p) {
 
 Ctx::~Ctx() {
   drop_caches(*this);
+  for (auto &g : pcg_graph)
+    if (g) cudaGraphExecDestroy(g);
+  if (gstream) cudaStreamDestroy(gstream);
+  if (ev_in) cudaEventDestroy(ev_in);
+  if (ev_out) cudaEventDestroy(ev_out);
   if (side) cudaStreamDestroy(side);
   if (ev_fork) cudaEventDestroy(ev_fork);
   if (ev_join) cudaEventDestroy(ev_join);
@@ -49,7 +54,7 @@ bool debug_sync() {
 void after_launch(Ctx &c, const char *name) {
   c.launches++;
   cudaError_t e = cudaGetLastError();
-  if (e == cudaSuccess && debug_sync()) e = cudaStreamSynchronize(c.stream);
+  if (e == cudaSuccess && debug_sync() && !c.capturing) e = cudaStreamSynchronize(c.stream);
   if (e != cudaSuccess) throw Error{AMGF_ERR_CUDA, std::string(name) + ": " + cudaGetErrorString(e)};
 }
 
@@ -121,19 +126,34 @@ void apply_M(Ctx &c, const double *r, double *z) {
 }
 
 // ------------------------------------------------------------------ PCG (C15)
-static amgf_status pcg(Ctx &c, const double *b, double *x, double rtol, int max_it, int precond, amgf_report *rep) {
+// One PCG iteration (C15): q = S p (+ p.q partials), pi and alpha, x += alpha p, r -= alpha q, z = M r,
+// rho' = r.z and beta, p = z + beta p, then the scalars and the error flag to pinned host memory.  The
+// p update of the final iteration is harmless (p is not used afterwards).  All pointers are the handle's
+// own buffers, so the body is captured once into a CUDA graph and replayed (values change, pointers do not).
+static void pcg_body(Ctx &c, int precond) {
+  const long n = c.n;
+  launch_sell_spmv(c, c.lev[0].As, SPMV_DOT, c.p, nullptr, nullptr, nullptr, c.q, c.dot_part);
+  launch_dot_finish(c, nblk(c.lev[0].As.nrows), DOT_PI);  // pi = p.q, alpha = rho / pi
+  launch_axpy2(c, n, c.p, c.q, c.xx, c.rr);
+  if (precond == 0) apply_M(c, c.rr, c.zz);
+  else vcycle(c, 0, c.rr, c.zz, nullptr);
+  launch_dot(c, n, 3, c.rr, c.zz, DOT_RHO1);             // rho' = r.z, beta = rho'/rho, rho = rho'
+  launch_xpby(c, n, c.zz, c.p);
+  CK(cudaMemcpyAsync(c.sc_host, c.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaMemcpyAsync(c.err_host, c.err, 2 * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+}
+
+static amgf_status pcg_impl(Ctx &c, const double *b, double *x, double rtol, int max_it, int precond,
+                            amgf_report *rep) {
   const long n = c.n;
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   CK(cudaEventRecord(e0, c.stream));
-  auto M = [&](const double *r, double *z) {
-    if (precond == 0) apply_M(c, r, z);
-    else vcycle(c, 0, r, z, nullptr);
-  };
-  launch_zero(c, n, x);
+  launch_zero(c, n, c.xx);
   launch_copy(c, n, b, c.rr);
-  M(c.rr, c.zz);
+  if (precond == 0) apply_M(c, c.rr, c.zz);
+  else vcycle(c, 0, c.rr, c.zz, nullptr);
   launch_dot(c, n, 3, c.rr, c.zz, DOT_RHO0);
   CK(cudaMemcpyAsync(c.sc_host, c.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, c.stream));
   check_dev_error(c, "pcg");
@@ -147,22 +167,38 @@ static amgf_status pcg(Ctx &c, const double *b, double *x, double rtol, int max_
     throw Error{AMGF_ERR_BREAKDOWN, "pcg: r.Mr <= 0"};
   } else {
     launch_copy(c, n, c.zz, c.p);
+    if (!c.pcg_graph[precond] && max_it > 0) {
+      cudaGraph_t g;
+      const int64_t l0 = c.launches;
+      c.capturing = true;
+      CK(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+      try {
+        pcg_body(c, precond);
+      } catch (...) {
+        cudaStreamEndCapture(c.stream, &g);
+        c.capturing = false;
+        throw;
+      }
+      CK(cudaStreamEndCapture(c.stream, &g));
+      c.capturing = false;
+      CK(cudaGraphInstantiate(&c.pcg_graph[precond], g, 0));
+      CK(cudaGraphDestroy(g));
+      c.graph_launches[precond] = c.launches - l0;
+      c.launches = l0;
+    }
     for (it = 1; it <= max_it; it++) {
-      launch_sell_spmv(c, c.lev[0].As, SPMV_DOT, c.p, nullptr, nullptr, nullptr, c.q, c.dot_part);
-      launch_dot_finish(c, nblk(c.lev[0].As.nrows), DOT_PI);  // pi = p.q, alpha = rho / pi
-      launch_axpy2(c, n, c.p, c.q, x, c.rr);
-      M(c.rr, c.zz);
-      launch_dot(c, n, 3, c.rr, c.zz, DOT_RHO1);
-      CK(cudaMemcpyAsync(c.sc_host, c.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, c.stream));
-      check_dev_error(c, "pcg");
+      CK(cudaGraphLaunch(c.pcg_graph[precond], c.stream));
+      c.launches += c.graph_launches[precond];
+      CK(cudaStreamSynchronize(c.stream));
+      if (c.err_host[0]) check_dev_error(c, "pcg");
       const double rho1 = c.sc_host->rho1;
       rel = std::sqrt(rho1 / rho0);
       if (rel < rtol) { st = AMGF_OK; break; }
       if (it == max_it) break;
-      launch_xpby(c, n, c.zz, c.p);
     }
     if (it > max_it) it = max_it;
   }
+  if (x != c.xx) launch_copy(c, n, c.xx, x);
   CK(cudaEventRecord(e1, c.stream));
   CK(cudaEventSynchronize(e1));
   float ms = 0;
@@ -175,6 +211,31 @@ static amgf_status pcg(Ctx &c, const double *b, double *x, double rtol, int max_
     rep->rel_pres_norm = rel;
     rep->solve_ms = ms;
   }
+  return st;
+}
+
+// The solve runs on the handle's own (capturable, non-default) stream, ordered after and before the
+// caller's stream by events.
+static amgf_status pcg(Ctx &c, const double *b, double *x, double rtol, int max_it, int precond, amgf_report *rep) {
+  if (!c.gstream) {
+    CK(cudaStreamCreateWithFlags(&c.gstream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c.ev_in, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c.ev_out, cudaEventDisableTiming));
+  }
+  cudaStream_t user = c.stream;
+  CK(cudaEventRecord(c.ev_in, user));
+  CK(cudaStreamWaitEvent(c.gstream, c.ev_in, 0));
+  c.stream = c.gstream;
+  amgf_status st;
+  try {
+    st = pcg_impl(c, b, x, rtol, max_it, precond, rep);
+  } catch (...) {
+    c.stream = user;
+    throw;
+  }
+  c.stream = user;
+  CK(cudaEventRecord(c.ev_out, c.gstream));
+  CK(cudaStreamWaitEvent(user, c.ev_out, 0));
   return st;
 }
 

@@ -148,6 +148,12 @@ struct Ctx {
   int *err_host = nullptr;    // pinned [2]
   int64_t launches = 0;
   void *setup_cache = nullptr;  // numeric re-setup data (setup.cu)
+  // PCG iteration body captured once per preconditioner (0 AMGF, 1 AMG) and replayed as one graph launch
+  cudaStream_t gstream = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  cudaGraphExec_t pcg_graph[2] = {nullptr, nullptr};
+  int64_t graph_launches[2] = {0, 0};
+  bool capturing = false;
   std::vector<void *> allocs;
 
   template <class T>
