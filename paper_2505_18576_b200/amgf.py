@@ -225,7 +225,7 @@ class AMGF:
                   23: (self.loff_size, np.float64), 25: (self.nc, np.int32)}
         if which == 27:
             dt = np.dtype([("p0", np.int32), ("len", np.int32), ("kind", np.int32), ("t0", np.int32),
-                           ("off", np.int64), ("level", np.int32), ("pad", np.int32)])
+                           ("off", np.int64), ("level", np.int32), ("rs", np.int32)])
             out = np.zeros(self.nd_nblocks, dtype=dt)
             _check(load_library().amgf_level_get(self.h, which, level, out.ctypes.data_as(ctypes.c_void_p)))
             return out

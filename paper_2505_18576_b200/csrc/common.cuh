@@ -108,7 +108,7 @@ struct Ctx {
   double *D = nullptr;
   int *S_kblk = nullptr;  // per S block: index of the K block (-1 if none)
   // filter (A_w factor in nested-dissection order, filter.cu)
-  struct NdLevel { int count = 0; int *ids = nullptr, *p0 = nullptr, *len = nullptr, *sub_ptr = nullptr, *sub_list = nullptr; };
+  struct NdLevel { int count = 0, ngroups = 0; int *ids = nullptr, *p0 = nullptr, *len = nullptr, *sub_ptr = nullptr, *sub_list = nullptr, *groups = nullptr; };
   int nd_nblocks = 0, nd_nleaves = 0, nd_depth = 0, nd_npairs = 0, nd_nsep = 0;
   int *nd_sep_blocks = nullptr;
   void *nd_blk = nullptr;                 // device NdBlk[nd_nblocks]
@@ -118,7 +118,6 @@ struct Ctx {
   int nd_sspairs_n[16][16] = {};
   int *pi_z = nullptr, *zpi = nullptr, *dof = nullptr, *block_of = nullptr;
   double *Loff = nullptr;                 // separator rows, row-major (factorization)
-  double *LoffT = nullptr;                // the same, k-major (solve: one TMA bulk copy per chunk)
   double *fw2 = nullptr;                  // forward results shifted by one position (TMA alignment)
   long loff_size = 0;
   double *fw = nullptr;                   // filter workspace (pi order)

@@ -7,7 +7,7 @@
 //   - in-block entries (leaf rows within the band, separator rows inside their separator): band arrays
 //     over pi positions (Lrow / Lcol / Lrev, stride band_stride(bw)), zero across blocks;
 //   - separator rows against their subtree (dense by fill): Loff, row-major per separator
-//     (Loff[off + s * (p0 - t0) + (k - t0)] = L_{p0+s, k}).
+//     (Loff[off + s * rs + (k - t0)] = L_{p0+s, k}, rs = p0 - t0 rounded up to even).
 // Every entry keeps the contract's chain (ascending k for the factor and the forward solve, descending k for
 // the backward solve); terms skipped here are exact zeros of the dense factor.  Parallelism: leaves are
 // independent (one CTA / warp each); separators of one level are independent.
@@ -22,8 +22,9 @@ namespace amgf {
 struct NdBlk {
   int p0, len, kind;  // kind 0 = leaf, 1 = separator
   int t0;             // separator: first pi position of its subtree
-  long off;           // separator: offset of its rows in Loff (row-major: s * (p0 - t0) + (k - t0))
+  long off;           // separator: offset of its rows in Loff (row-major: s * rs + (k - t0))
   int level;          // separator depth (root 0)
+  int rs;             // separator: row stride of its rows in Loff (p0 - t0 rounded up to even)
 };
 
 namespace {
@@ -67,7 +68,7 @@ struct Emit {
 int emit(const std::vector<Node> &nodes, int id, Emit &E, std::vector<int> &leaves, std::vector<int> &seps) {
   const Node &nd = nodes[id];
   if (nd.leaf) {
-    NdBlk b{(int)E.pi.size(), nd.z1 - nd.z0, 0, (int)E.pi.size(), 0, nd.depth};
+    NdBlk b{(int)E.pi.size(), nd.z1 - nd.z0, 0, (int)E.pi.size(), 0, nd.depth, 0};
     for (int z = nd.z0; z < nd.z1; z++) E.pi.push_back(z);
     E.blk.push_back(b);
     E.sub_leaves.emplace_back();
@@ -78,7 +79,7 @@ int emit(const std::vector<Node> &nodes, int id, Emit &E, std::vector<int> &leav
   std::vector<int> ll, ls, rl, rs;
   const int t0 = emit(nodes, nd.left, E, ll, ls);
   emit(nodes, nd.right, E, rl, rs);
-  NdBlk b{(int)E.pi.size(), nd.z1 - nd.z0, 1, t0, 0, nd.depth};
+  NdBlk b{(int)E.pi.size(), nd.z1 - nd.z0, 1, t0, 0, nd.depth, 0};
   for (int z = nd.z0; z < nd.z1; z++) E.pi.push_back(z);
   E.blk.push_back(b);
   std::vector<int> sl = ll, ss = ls;  // subtree blocks in pi order: left subtree, then right subtree
@@ -159,7 +160,7 @@ __global__ void k_nd_fill(int nc, int bw, int W, const NdBlk *blk, const int *bl
       const int q = zpi[zq];
       const double v = S_val[(long)k * 9 + 3 * r + cc];
       if (q >= B.p0 && q <= p) Lrow[(long)p * W + bw - (p - q)] = v;
-      else if (B.kind == 1 && q >= B.t0 && q < B.p0) Loff[B.off + (long)(p - B.p0) * (B.p0 - B.t0) + (q - B.t0)] = v;
+      else if (B.kind == 1 && q >= B.t0 && q < B.p0) Loff[B.off + (long)(p - B.p0) * B.rs + (q - B.t0)] = v;
     }
 }
 
@@ -167,9 +168,8 @@ __global__ void k_nd_fill(int nc, int bw, int W, const NdBlk *blk, const int *bl
 // k ascending over [max(p0(Lf), j - bw), j) (the only nonzero terms).  One thread per (separator, leaf, s).
 __global__ void k_nd_off_leaf(const int2 *pairs, const NdBlk *blk, int bw, int W, const double *Lrow, double *Loff) {
   const NdBlk S = blk[pairs[blockIdx.x].x], Lf = blk[pairs[blockIdx.x].y];
-  const int ncol = S.p0 - S.t0;
   for (int s = threadIdx.x; s < S.len; s += blockDim.x) {
-    double *Ls = Loff + S.off + (long)s * ncol - S.t0;  // Ls[k] = L_sk
+    double *Ls = Loff + S.off + (long)s * S.rs - S.t0;  // Ls[k] = L_sk
     for (int j = Lf.p0; j < Lf.p0 + Lf.len; j++) {
       const double *Lj = Lrow + (long)j * W + bw - j;  // Lj[k] = L_jk
       const int k0 = max(Lf.p0, j - bw);
@@ -185,12 +185,11 @@ __global__ void k_nd_off_leaf(const int2 *pairs, const NdBlk *blk, int bw, int W
 // grid.x = (S, S') pair, threads over the len(S) * len(S') entries.
 __global__ void k_nd_off_sep_dot(const int2 *pairs, const NdBlk *blk, double *Loff) {
   const NdBlk S = blk[pairs[blockIdx.x].x], Sp = blk[pairs[blockIdx.x].y];
-  const int ncol = S.p0 - S.t0, ncolp = Sp.p0 - Sp.t0;
   const int ne = S.len * Sp.len;
   for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < ne; e += gridDim.y * blockDim.x) {
     const int s = e / Sp.len, jj = e % Sp.len;
-    double *Ls = Loff + S.off + (long)s * ncol - S.t0;
-    const double *Lj = Loff + Sp.off + (long)jj * ncolp - Sp.t0;
+    double *Ls = Loff + S.off + (long)s * S.rs - S.t0;
+    const double *Lj = Loff + Sp.off + (long)jj * Sp.rs - Sp.t0;
     Ls[Sp.p0 + jj] = chain_sub(Ls[Sp.p0 + jj], Ls + Sp.t0, 1, Lj + Sp.t0, 1, Sp.p0 - Sp.t0);
   }
 }
@@ -198,9 +197,8 @@ __global__ void k_nd_off_sep_dot(const int2 *pairs, const NdBlk *blk, double *Lo
 __global__ void k_nd_off_sep_blk(const int2 *pairs, const NdBlk *blk, int bw, int W, const double *Lrow,
                                  double *Loff) {
   const NdBlk S = blk[pairs[blockIdx.x].x], Sp = blk[pairs[blockIdx.x].y];
-  const int ncol = S.p0 - S.t0;
   for (int s = threadIdx.x; s < S.len; s += blockDim.x) {
-    double *Ls = Loff + S.off + (long)s * ncol - S.t0;
+    double *Ls = Loff + S.off + (long)s * S.rs - S.t0;
     for (int j = Sp.p0; j < Sp.p0 + Sp.len; j++) {
       const double *Lj = Lrow + (long)j * W + bw - j;
       const double acc = chain_sub(Ls[j], Ls + Sp.p0, 1, Lj + Sp.p0, 1, j - Sp.p0);
@@ -219,80 +217,67 @@ __global__ void k_nd_schur(const int *ids, const NdBlk *blk, int bw, int W, doub
     const int s = e / S.len, j = e % S.len;
     if (j > s) continue;
     const long ix = (long)(S.p0 + s) * W + bw - (s - j);
-    const double *Ls = Loff + S.off + (long)s * ncol, *Lj = Loff + S.off + (long)j * ncol;
+    const double *Ls = Loff + S.off + (long)s * S.rs, *Lj = Loff + S.off + (long)j * S.rs;
     Lrow[ix] = chain_sub(Lrow[ix], Ls, 1, Lj, 1, ncol);
   }
 }
 
 // Forward, separator rows: acc_s = v_s - sum_{k in [t0, p0)} L_sk w_k (ascending k), into accbuf.
-// One CTA per separator, thread s owns row s.  Chunks of SF_KC columns of the k-major copy LoffT (one
-// contiguous block per chunk) and the matching w values are brought into shared memory by TMA bulk copies
-// in an SF_NS-deep ring (full/empty mbarriers, thread 0 produces), so each chain runs at FMA latency.
-constexpr int SF_KC = 32, SF_NS = 4, SF_THREADS = 256;
-__global__ void __launch_bounds__(SF_THREADS) k_nd_sep_fwd(const int *ids, const NdBlk *blk, const double *LoffT,
-                                                           const double *r1, const int *dof, const double *w,
-                                                           const double *w2, double *accbuf) {
-  extern __shared__ __align__(128) double sfb[];  // [SF_NS][SF_KC * len] rows, then [SF_NS][SF_KC] w
-  __shared__ __align__(8) uint64_t full[SF_NS], empty[SF_NS];
-  const NdBlk S = blk[ids[blockIdx.x]];
-  const int len = S.len, ncol = S.p0 - S.t0;
+// One warp per group of 32 rows of a separator (so a separator's rows stream through several SMs); lane l
+// owns row row0 + l.  Chunks of SF_KC columns of the 32 rows (row-major; lane q copies the q-th 16-byte piece
+// of every row) and the matching w values go through an SF_NS-deep cp.async ring (padded smem rows).
+constexpr int SF_KC = 64, SF_NS = 4, SF_LD = SF_KC + 2;
+constexpr size_t SF_SMEM = (size_t)SF_NS * (32 * SF_LD + SF_KC) * sizeof(double);
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem));
+}
+__global__ void __launch_bounds__(32) k_nd_sep_fwd(const int2 *groups, const NdBlk *blk, const double *Loff,
+                                                   const double *r1, const int *dof, const double *w,
+                                                   const double *w2, double *accbuf) {
+  extern __shared__ __align__(16) double sfm[];  // [SF_NS][32 * SF_LD] rows, then [SF_NS][SF_KC] w
+  const NdBlk S = blk[groups[blockIdx.x].x];
+  const int row0 = groups[blockIdx.x].y;
+  const int lane = threadIdx.x;
+  const int nrow = min(32, S.len - row0);
+  const int ncol = S.p0 - S.t0;
   const int nch = (ncol + SF_KC - 1) / SF_KC;
-  const int tid = threadIdx.x;
-  double *sL = sfb, *sW = sfb + SF_NS * SF_KC * len;
-  // w[t0 + k] 16-byte aligned: from w itself (t0 even) or from the copy shifted by one (t0 odd)
-  const double *wsrc = (S.t0 & 1) ? w2 + S.t0 + 1 : w + S.t0;
-  const unsigned bytesL = (unsigned)(SF_KC * len * 8), bytesW = SF_KC * 8;
-  if (tid == 0) {
-#pragma unroll
-    for (int b = 0; b < SF_NS; b++) {
-      mbar_init(&full[b], 1);
-      mbar_init(&empty[b], SF_THREADS);
+  double *sW = sfm + SF_NS * 32 * SF_LD;
+  const double *wsrc = (S.t0 & 1) ? w2 + S.t0 + 1 : w + S.t0;  // 16-byte aligned view of w[t0 + k]
+  const double *Lq = Loff + S.off + (long)row0 * S.rs + 2 * lane;  // this lane's piece of row 0
+  auto issue = [&](int c) {
+    if (c < nch) {
+      const int k0 = c * SF_KC, st = c % SF_NS;
+      if (2 * lane < ncol - k0) {  // the even row stride covers an odd tail element
+        const double *src = Lq + k0;
+        double *dst = sfm + st * 32 * SF_LD + 2 * lane;
+        for (int r = 0; r < nrow; r++) cp_async16(dst + r * SF_LD, src + (long)r * S.rs);
+      }
+      cp_async16(sW + st * SF_KC + 2 * lane, wsrc + k0 + 2 * lane);
     }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  auto produce = [&](int c) {  // thread 0
-    if (c >= nch) return;
-    const int st = c % SF_NS;
-    if (c >= SF_NS) mbar_wait(&empty[st], ((c / SF_NS) - 1) & 1);
-    mbar_arrive_expect(&full[st], bytesL + bytesW);
-    bulk_g2s(sL + st * SF_KC * len, LoffT + S.off + (long)c * SF_KC * len, bytesL, &full[st]);
-    bulk_g2s(sW + st * SF_KC, wsrc + (long)c * SF_KC, bytesW, &full[st]);
+    asm volatile("cp.async.commit_group;");
   };
-  if (tid == 0)
-    for (int c = 0; c < SF_NS; c++) produce(c);
-  double acc = (tid < len) ? r1[dof[S.p0 + tid]] : 0.0;
+#pragma unroll
+  for (int c = 0; c < SF_NS - 1; c++) issue(c);
+  double acc = (lane < nrow) ? r1[dof[S.p0 + row0 + lane]] : 0.0;
   for (int c = 0; c < nch; c++) {
+    issue(c + SF_NS - 1);
+    asm volatile("cp.async.wait_group %0;" ::"n"(SF_NS - 1));
+    __syncwarp();
     const int st = c % SF_NS;
-    mbar_wait(&full[st], (c / SF_NS) & 1);
-    const double *buf = sL + st * SF_KC * len + tid;
+    const double *buf = sfm + st * 32 * SF_LD + lane * SF_LD;
     const double *wb = sW + st * SF_KC;
     const int kn = min(SF_KC, ncol - c * SF_KC);
-    if (tid < len) {
-      if (kn == SF_KC) {
+    if (kn == SF_KC) {
 #pragma unroll
-        for (int kk = 0; kk < SF_KC; kk++) acc = __fma_rn(-buf[kk * len], wb[kk], acc);
-      } else {
-        for (int kk = 0; kk < kn; kk++) acc = __fma_rn(-buf[kk * len], wb[kk], acc);
-      }
+      for (int kk = 0; kk < SF_KC; kk++) acc = __fma_rn(-buf[kk], wb[kk], acc);
+    } else {
+      for (int kk = 0; kk < kn; kk++) acc = __fma_rn(-buf[kk], wb[kk], acc);
     }
-    mbar_arrive(&empty[st]);
-    if (tid == 0) produce(c + SF_NS);
+    __syncwarp();  // stage st is refilled by the issue of iteration c + 1
   }
-  if (tid < len) accbuf[S.p0 + tid] = acc;
-}
-
-// k-major copy of the separator rows for the forward solve: LoffT[off + (k - t0) * len + s]
-__global__ void k_nd_transpose(int nsep_blocks, const int *sep_block_ids, const NdBlk *blk, const double *Loff,
-                               double *LoffT) {
-  const NdBlk S = blk[sep_block_ids[blockIdx.y]];
-  const int ncol = S.p0 - S.t0;
-  const long ne = (long)ncol * S.len;
-  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < ne; e += (long)gridDim.x * blockDim.x) {
-    const int s = (int)(e % S.len);
-    const long k = e / S.len;
-    LoffT[S.off + e] = Loff[S.off + (long)s * ncol + k];
-  }
+  asm volatile("cp.async.wait_group 0;");
+  if (lane < nrow) accbuf[S.p0 + row0 + lane] = acc;
 }
 
 // Backward, subtree rows of a separator: acc_k -= sum_{s descending} L_sk x_s (chain continues in w).
@@ -300,10 +285,9 @@ __global__ void k_nd_sep_bwd(const int *ids, const NdBlk *blk, const double *Lof
   const NdBlk S = blk[ids[blockIdx.y]];
   const int k = S.t0 + blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= S.p0) return;
-  const int ncol = S.p0 - S.t0;
-  const double *Lk = Loff + S.off + (k - S.t0);  // Lk[s * ncol] = L_{p0+s, k}
+  const double *Lk = Loff + S.off + (k - S.t0);  // Lk[s * rs] = L_{p0+s, k}
   // s descending: start at the last row and step backwards
-  w[k] = chain_sub(w[k], Lk + (long)(S.len - 1) * ncol, -(long)ncol, x + S.p0 + S.len - 1, -1, S.len);
+  w[k] = chain_sub(w[k], Lk + (long)(S.len - 1) * S.rs, -(long)S.rs, x + S.p0 + S.len - 1, -1, S.len);
 }
 
 __global__ void k_nd_scatter(int nc, const int *dof, const double *y, double *x2) {
@@ -333,9 +317,9 @@ void nd_symbolic(Ctx &c) {
   for (int bi = 0; bi < (int)E.blk.size(); bi++) {
     NdBlk &b = E.blk[bi];
     if (b.kind == 1) {
+      b.rs = (b.p0 - b.t0 + 1) & ~1;  // even row stride: 16-byte aligned rows
       b.off = off;
-      off += (long)(b.p0 - b.t0) * b.len;
-      off = (off + 1) & ~1L;  // even offsets: 16-byte aligned TMA sources
+      off += (long)b.rs * b.len;
       depth = std::max(depth, b.level + 1);
       sep_blocks.push_back(bi);
     }
@@ -372,6 +356,11 @@ void nd_symbolic(Ctx &c) {
         sptr.push_back((int)slist.size());
       }
     Ctx::NdLevel &Lv = c.nd_lev[l];
+    std::vector<int> groups;  // (separator block, first row) per warp of the forward dot kernel
+    for (int b : ids)
+      for (int r0 = 0; r0 < E.blk[b].len; r0 += 32) { groups.push_back(b); groups.push_back(r0); }
+    Lv.ngroups = (int)groups.size() / 2;
+    Lv.groups = upload(c, groups);
     Lv.count = (int)ids.size();
     Lv.ids = upload(c, ids);
     Lv.p0 = upload(c, p0);
@@ -407,10 +396,9 @@ void nd_symbolic(Ctx &c) {
   c.Lrev = rv + (size_t)BAND_PAD_ROWS * W;
   c.Ldinv = c.alloc<double>(nc);
   c.Loff = c.alloc<double>(std::max(off, 1L));
-  c.LoffT = c.alloc<double>(off + (long)SF_KC * (bw + 2) + 2);  // chunks may read past the last separator
   c.fv = c.alloc<double>(nc);
-  c.fw = c.alloc<double>(nc + SF_KC + 2);
-  c.fw2 = c.alloc<double>(nc + SF_KC + 2);
+  c.fw = c.alloc<double>(nc + SF_KC + 4);
+  c.fw2 = c.alloc<double>(nc + SF_KC + 4);
   c.nd_nsep = (int)sep_blocks.size();
   c.nd_sep_blocks = upload(c, sep_blocks);
 }
@@ -451,11 +439,6 @@ void nd_numeric(Ctx &c) {
     band_factor_blocks(c, nc, Lv.count, Lv.p0, Lv.len, bw, c.Lrow, 1);
   }
   band_finish(c, nc, bw, c.Lrow, c.Lcol, c.Lrev, c.Ldinv);
-  if (c.nd_nsep) {
-    dim3 g(64, c.nd_nsep);
-    k_nd_transpose<<<g, CTA, 0, c.stream>>>(c.nd_nsep, c.nd_sep_blocks, blk, c.Loff, c.LoffT);
-    after_launch(c, "k_nd_transpose");
-  }
 }
 
 void nd_solve(Ctx &c, const double *r1, double *x2) {
@@ -469,16 +452,15 @@ void nd_solve(Ctx &c, const double *r1, double *x2) {
     Ctx::NdLevel &Lv = c.nd_lev[l];
     if (!Lv.count) continue;
     {
-      const size_t smem = (size_t)SF_NS * SF_KC * (bw + 1) * sizeof(double);
       static bool attr = false;
       if (!attr) {
-        CK(cudaFuncSetAttribute(k_nd_sep_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        CK(cudaFuncSetAttribute(k_nd_sep_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SF_SMEM));
         attr = true;
       }
-      REQUIRE(bw <= SF_THREADS && smem <= 220 * 1024, AMGF_ERR_LIMIT, "separator too wide for k_nd_sep_fwd");
-      k_nd_sep_fwd<<<Lv.count, SF_THREADS, smem, c.stream>>>(Lv.ids, blk, c.LoffT, r1, c.dof, w, c.fw2, y);
-      after_launch(c, "k_nd_sep_fwd");
     }
+    k_nd_sep_fwd<<<Lv.ngroups, 32, SF_SMEM, c.stream>>>((const int2 *)Lv.groups, blk, c.Loff, r1, c.dof, w, c.fw2,
+                                                        y);
+    after_launch(c, "k_nd_sep_fwd");
     launch_band_sweep(c, Lv.count, Lv.p0, Lv.len, nc, bw, true, c.Lcol, c.Lrev, c.Ldinv, y, nullptr, w, c.fw2);
   }
   // backward: separators top-down (then their subtree rows), then leaves

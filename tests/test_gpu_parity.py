@@ -72,8 +72,8 @@ def gpu_dense_factor(g):
         off = g.get(23)
         for b in blk:
             if b["kind"] == 1:
-                p0, ln, t0, o = int(b["p0"]), int(b["len"]), int(b["t0"]), int(b["off"])
-                seg = off[o:o + (p0 - t0) * ln].reshape(ln, p0 - t0)   # [s][k - t0] (row-major)
+                p0, ln, t0, o, rs = int(b["p0"]), int(b["len"]), int(b["t0"]), int(b["off"]), int(b["rs"])
+                seg = off[o:o + rs * ln].reshape(ln, rs)[:, :p0 - t0]   # [s][k - t0] (row-major, stride rs)
                 L[p0:p0 + ln, t0:p0] = seg
     return L
 
