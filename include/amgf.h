@@ -109,7 +109,8 @@ amgf_status amgf_pcg_solve_host(amgf_handle h, const double *b_host, double *x_h
 /* Hierarchy introspection (tests, bench).  info[0] = levels, info[1] = nc, info[2] = coarsest dofs,
  * info[3] = band width of A_w's factor, then per level l: info[4+6l .. 9+6l] =
  * {nodes, block size, nnzb(A), nnzb(P), n_agg, SELL slots of A}; info[196] = size of the separator
- * off-block factor, info[197] = number of nested-dissection blocks.  info needs 4 + 6*32 + 2 entries. */
+ * off-block factor, info[197] = number of nested-dissection blocks, info[198] = first level of the fused
+ * coarse-tail kernel (-1: none), info[199] = its cluster size in CTAs.  info needs 4 + 6*32 + 4 entries. */
 amgf_status amgf_level_info(amgf_handle h, int64_t *info);
 
 /* Copy one hierarchy array to the HOST buffer dst.  which: 0 A.ptr 1 A.col 2 A.val 3 P.ptr 4 P.col

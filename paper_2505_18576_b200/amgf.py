@@ -125,13 +125,14 @@ class AMGF:
                           ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(h))
         _check(st)
         self.h = h
-        info = np.zeros(4 + 6 * 32 + 2, dtype=np.int64)
+        info = np.zeros(4 + 6 * 32 + 4, dtype=np.int64)
         _check(L.amgf_level_info(self.h, info.ctypes.data_as(ctypes.c_void_p)))
         self.nlev, self.nc, self.nco, self.bw = (int(v) for v in info[:4])
         self.levels = [dict(nodes=int(info[4 + 6 * l]), b=int(info[5 + 6 * l]), nnzb=int(info[6 + 6 * l]),
                             nnzb_P=int(info[7 + 6 * l]), n_agg=int(info[8 + 6 * l]), slots=int(info[9 + 6 * l]))
                        for l in range(self.nlev)]
         self.loff_size, self.nd_nblocks = int(info[4 + 6 * 32]), int(info[5 + 6 * 32])
+        self.tail_level, self.tail_ncta = int(info[6 + 6 * 32]), int(info[7 + 6 * 32])
 
     @classmethod
     def from_problem(cls, p, D=None, Z="lattice", config=None, stream=None):

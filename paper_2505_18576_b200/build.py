@@ -4,7 +4,7 @@ import subprocess
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SRC = [os.path.join(HERE, "csrc", f) for f in ("solve.cu", "setup.cu", "filter.cu", "api.cu")]
+SRC = [os.path.join(HERE, "csrc", f) for f in ("solve.cu", "setup.cu", "filter.cu", "tail.cu", "api.cu")]
 LIB = os.path.join(HERE, "libamgf.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "--fmad=false", "-std=c++17",

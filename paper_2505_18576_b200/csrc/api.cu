@@ -88,6 +88,10 @@ void vcycle(Ctx &c, int l, const double *b, double *x, const double *add) {
     if (add) launch_add(c, L.n, add, dst, x);
     return;
   }
+  if (l == c.tail_level && !add) {
+    tail_vcycle(c, b, x);
+    return;
+  }
   Level &Lc = c.lev[l + 1];
   const int pre = c.cfg.pre_sweeps, post = c.cfg.post_sweeps;
   double *bufs[2] = {x, L.x2};
@@ -392,6 +396,8 @@ amgf_status amgf_level_info(amgf_handle h, int64_t *info) {
   }
   info[4 + 6 * MAXLEV + 0] = h->loff_size;
   info[4 + 6 * MAXLEV + 1] = h->nd_nblocks;
+  info[4 + 6 * MAXLEV + 2] = h->tail_level;
+  info[4 + 6 * MAXLEV + 3] = h->tail_ncta;
   return AMGF_OK;
 }
 

@@ -135,6 +135,10 @@ struct Ctx {
   int nlev = 0;
   Level lev[MAXLEV];
   int nco = 0;
+  // fused coarse tail (tail.cu): the V-cycle below level tail_level in one thread-block cluster
+  int tail_level = -1, tail_ncta = 0, tail_xs = 0, tail_maxv = 0, tail_maxc = 0, tail_maxpv = 0, tail_maxpc = 0;
+  size_t tail_smem = 0;
+  int *tail_cta_s = nullptr;
   double *Lc_row = nullptr, *Lc_col = nullptr, *Lc_rev = nullptr, *Lc_dinv = nullptr;
   // solve workspace
   double *w_x1 = nullptr, *w_r1 = nullptr, *w_xv = nullptr;
@@ -228,6 +232,8 @@ void build_sell(Ctx &c, const Bsr &A, Sell &S, bool alloc, bool split);
 
 // ------------------------------------------------------------------ solve orchestration (api.cu)
 void vcycle(Ctx &c, int l, const double *b, double *x, const double *add);
+void tail_plan(Ctx &c);                                   // after setup_all: enable the fused coarse tail
+void tail_vcycle(Ctx &c, const double *b, double *x);    // V-cycle from level c.tail_level down, one launch
 void apply_M(Ctx &c, const double *r, double *z);
 
 }  // namespace amgf

@@ -12,6 +12,7 @@
 // the backward solve); terms skipped here are exact zeros of the dense factor.  Parallelism: leaves are
 // independent (one CTA / warp each); separators of one level are independent.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -225,32 +226,34 @@ __global__ void k_nd_schur(const int *ids, const NdBlk *blk, int bw, int W, doub
 // Forward, separator rows: acc_s = v_s - sum_{k in [t0, p0)} L_sk w_k (ascending k), into accbuf.
 // One warp per group of 32 rows of a separator (so a separator's rows stream through several SMs); lane l
 // owns row row0 + l.  Chunks of SF_KC columns of the 32 rows (row-major; lane q copies the q-th 16-byte piece
-// of every row) and the matching w values go through an SF_NS-deep cp.async ring (padded smem rows).
-constexpr int SF_KC = 64, SF_NS = 4, SF_LD = SF_KC + 2;
-constexpr size_t SF_SMEM = (size_t)SF_NS * (32 * SF_LD + SF_KC) * sizeof(double);
+// of every row) and the matching w values go through an NS-deep cp.async ring (padded smem rows).
+constexpr int SF_KC = 64, SF_LD = SF_KC + 2;
+constexpr size_t sf_smem(int G, int NS) { return (size_t)NS * (G * SF_LD + SF_KC) * sizeof(double); }
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
   unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem));
 }
+
+template <int G, int NS>
 __global__ void __launch_bounds__(32) k_nd_sep_fwd(const int2 *groups, const NdBlk *blk, const double *Loff,
                                                    const double *r1, const int *dof, const double *w,
                                                    const double *w2, double *accbuf) {
-  extern __shared__ __align__(16) double sfm[];  // [SF_NS][32 * SF_LD] rows, then [SF_NS][SF_KC] w
+  extern __shared__ __align__(16) double sfm[];  // [NS][G * SF_LD] rows, then [NS][SF_KC] w
   const NdBlk S = blk[groups[blockIdx.x].x];
   const int row0 = groups[blockIdx.x].y;
   const int lane = threadIdx.x;
-  const int nrow = min(32, S.len - row0);
+  const int nrow = min(G, S.len - row0);
   const int ncol = S.p0 - S.t0;
   const int nch = (ncol + SF_KC - 1) / SF_KC;
-  double *sW = sfm + SF_NS * 32 * SF_LD;
+  double *sW = sfm + NS * G * SF_LD;
   const double *wsrc = (S.t0 & 1) ? w2 + S.t0 + 1 : w + S.t0;  // 16-byte aligned view of w[t0 + k]
   const double *Lq = Loff + S.off + (long)row0 * S.rs + 2 * lane;  // this lane's piece of row 0
   auto issue = [&](int c) {
     if (c < nch) {
-      const int k0 = c * SF_KC, st = c % SF_NS;
+      const int k0 = c * SF_KC, st = c % NS;
       if (2 * lane < ncol - k0) {  // the even row stride covers an odd tail element
         const double *src = Lq + k0;
-        double *dst = sfm + st * 32 * SF_LD + 2 * lane;
+        double *dst = sfm + st * G * SF_LD + 2 * lane;
         for (int r = 0; r < nrow; r++) cp_async16(dst + r * SF_LD, src + (long)r * S.rs);
       }
       cp_async16(sW + st * SF_KC + 2 * lane, wsrc + k0 + 2 * lane);
@@ -258,19 +261,24 @@ __global__ void __launch_bounds__(32) k_nd_sep_fwd(const int2 *groups, const NdB
     asm volatile("cp.async.commit_group;");
   };
 #pragma unroll
-  for (int c = 0; c < SF_NS - 1; c++) issue(c);
+  for (int c = 0; c < NS - 1; c++) issue(c);
   double acc = (lane < nrow) ? r1[dof[S.p0 + row0 + lane]] : 0.0;
+  const int me = min(lane, G - 1);
   for (int c = 0; c < nch; c++) {
-    issue(c + SF_NS - 1);
-    asm volatile("cp.async.wait_group %0;" ::"n"(SF_NS - 1));
+    issue(c + NS - 1);
+    asm volatile("cp.async.wait_group %0;" ::"n"(NS - 1));
     __syncwarp();
-    const int st = c % SF_NS;
-    const double *buf = sfm + st * 32 * SF_LD + lane * SF_LD;
+    const int st = c % NS;
+    const double *buf = sfm + st * G * SF_LD + me * SF_LD;
     const double *wb = sW + st * SF_KC;
     const int kn = min(SF_KC, ncol - c * SF_KC);
     if (kn == SF_KC) {
 #pragma unroll
-      for (int kk = 0; kk < SF_KC; kk++) acc = __fma_rn(-buf[kk], wb[kk], acc);
+      for (int kk = 0; kk < SF_KC; kk += 2) {
+        const double2 a = *(const double2 *)(buf + kk), b = *(const double2 *)(wb + kk);
+        acc = __fma_rn(-a.x, b.x, acc);
+        acc = __fma_rn(-a.y, b.y, acc);
+      }
     } else {
       for (int kk = 0; kk < kn; kk++) acc = __fma_rn(-buf[kk], wb[kk], acc);
     }
@@ -278,6 +286,34 @@ __global__ void __launch_bounds__(32) k_nd_sep_fwd(const int2 *groups, const NdB
   }
   asm volatile("cp.async.wait_group 0;");
   if (lane < nrow) accbuf[S.p0 + row0 + lane] = acc;
+}
+
+typedef void (*SepFwdFn)(const int2 *, const NdBlk *, const double *, const double *, const int *, const double *,
+                         const double *, double *);
+struct SepFwdVariant {
+  int G, NS;
+  SepFwdFn fn;
+};
+static const SepFwdVariant kSepFwd[] = {{32, 4, k_nd_sep_fwd<32, 4>},  {32, 8, k_nd_sep_fwd<32, 8>},
+                                        {32, 12, k_nd_sep_fwd<32, 12>}, {16, 8, k_nd_sep_fwd<16, 8>},
+                                        {16, 16, k_nd_sep_fwd<16, 16>}, {8, 8, k_nd_sep_fwd<8, 8>},
+                                        {8, 16, k_nd_sep_fwd<8, 16>},   {4, 16, k_nd_sep_fwd<4, 16>},
+                                        {4, 24, k_nd_sep_fwd<4, 24>},   {2, 16, k_nd_sep_fwd<2, 16>}};
+constexpr int kSepFwdDefault = 7;  // G = 4, NS = 16: measured best with 5 and 9 (tools/time_apply.py)
+
+static int sep_fwd_variant() {
+  static int v = -1;
+  if (v < 0) {
+    v = kSepFwdDefault;
+    if (const char *e = getenv("AMGF_SF_VARIANT")) {  // tuning experiments only
+      int i = atoi(e);
+      if (i >= 0 && i < (int)(sizeof(kSepFwd) / sizeof(kSepFwd[0]))) v = i;
+    }
+    const SepFwdVariant &V = kSepFwd[v];
+    CK(cudaFuncSetAttribute((const void *)V.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)sf_smem(V.G, V.NS)));
+  }
+  return v;
 }
 
 // Backward, subtree rows of a separator: acc_k -= sum_{s descending} L_sk x_s (chain continues in w).
@@ -358,7 +394,10 @@ void nd_symbolic(Ctx &c) {
     Ctx::NdLevel &Lv = c.nd_lev[l];
     std::vector<int> groups;  // (separator block, first row) per warp of the forward dot kernel
     for (int b : ids)
-      for (int r0 = 0; r0 < E.blk[b].len; r0 += 32) { groups.push_back(b); groups.push_back(r0); }
+      for (int r0 = 0; r0 < E.blk[b].len; r0 += kSepFwd[sep_fwd_variant()].G) {
+        groups.push_back(b);
+        groups.push_back(r0);
+      }
     Lv.ngroups = (int)groups.size() / 2;
     Lv.groups = upload(c, groups);
     Lv.count = (int)ids.size();
@@ -451,15 +490,9 @@ void nd_solve(Ctx &c, const double *r1, double *x2) {
   for (int l = c.nd_depth - 1; l >= 0; l--) {
     Ctx::NdLevel &Lv = c.nd_lev[l];
     if (!Lv.count) continue;
-    {
-      static bool attr = false;
-      if (!attr) {
-        CK(cudaFuncSetAttribute(k_nd_sep_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SF_SMEM));
-        attr = true;
-      }
-    }
-    k_nd_sep_fwd<<<Lv.ngroups, 32, SF_SMEM, c.stream>>>((const int2 *)Lv.groups, blk, c.Loff, r1, c.dof, w, c.fw2,
-                                                        y);
+    const SepFwdVariant &V = kSepFwd[sep_fwd_variant()];
+    V.fn<<<Lv.ngroups, 32, sf_smem(V.G, V.NS), c.stream>>>((const int2 *)Lv.groups, blk, c.Loff, r1, c.dof, w,
+                                                           c.fw2, y);
     after_launch(c, "k_nd_sep_fwd");
     launch_band_sweep(c, Lv.count, Lv.p0, Lv.len, nc, bw, true, c.Lcol, c.Lrev, c.Ldinv, y, nullptr, w, c.fw2);
   }

@@ -1328,6 +1328,7 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
   c.xx = c.alloc<double>(n);
   c.bb = c.alloc<double>(n);
   CK(cudaStreamSynchronize(c.stream));
+  tail_plan(c);
 }
 
 // =================================================================== numeric re-setup (new D)

@@ -301,23 +301,29 @@ __global__ void __launch_bounds__(CTA) k_restrict_row(int nrows6, const int *__r
   const int a = w / 6, rr = w % 6;
   const int beg = ptr[a], end = ptr[a + 1];
   double acc = 0.0;
-  int k = beg + lane;
-  double v[B], rv[B];
-  if (k < end) {
-    const int c = col[k];
+  // batches of U lane-strided blocks (k, k+32, ...): all their columns, values and r entries in flight
+  // at once; the chain still runs over the lane's blocks in ascending order (C5)
+  constexpr int U = 4;
+  for (int k0 = beg + lane; k0 < end; k0 += U * 32) {
+    int cc[U];
+    double v[U][B], rv[U][B];
+    int kk[U];  // clamped (loads unconditional, so that they are all issued before the chain)
 #pragma unroll
-    for (int e = 0; e < B; e++) { v[e] = __ldg(val + (long)k * 6 * B + rr * B + e); rv[e] = r[(long)c * B + e]; }
-  }
-  for (; k < end; k += 32) {
-    const int kn = k + 32 < end ? k + 32 : k;
-    const int cn = col[kn];
-    double vn[B], rn[B];
+    for (int u = 0; u < U; u++) kk[u] = min(k0 + 32 * u, end - 1);
 #pragma unroll
-    for (int e = 0; e < B; e++) { vn[e] = __ldg(val + (long)kn * 6 * B + rr * B + e); rn[e] = r[(long)cn * B + e]; }
+    for (int u = 0; u < U; u++) cc[u] = col[kk[u]];
 #pragma unroll
-    for (int e = 0; e < B; e++) acc = __fma_rn(v[e], rv[e], acc);
+    for (int u = 0; u < U; u++)
 #pragma unroll
-    for (int e = 0; e < B; e++) { v[e] = vn[e]; rv[e] = rn[e]; }
+      for (int e = 0; e < B; e++) {
+        v[u][e] = __ldg(val + (long)kk[u] * 6 * B + rr * B + e);
+        rv[u][e] = r[(long)cc[u] * B + e];
+      }
+#pragma unroll
+    for (int u = 0; u < U; u++)
+      if (k0 + 32 * u < end)
+#pragma unroll
+        for (int e = 0; e < B; e++) acc = __fma_rn(v[u][e], rv[u][e], acc);
   }
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) acc = acc + __shfl_xor_sync(0xffffffffu, acc, o);

@@ -297,3 +297,23 @@ def test_full_size_cfg3(oracle_lib, amgf_mod, torch_cuda):
     assert rg["converged"]
     xs = xg.cpu().numpy()
     assert np.linalg.norm(S @ xs - p.b) <= 1e-5 * np.linalg.norm(p.b)
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_fused_tail_matches_level_kernels(oracle_lib, amgf_mod, torch_cuda, cfg, monkeypatch):
+    """The fused coarse-tail kernel (tail.cu: one cluster launch for the two coarsest levels) gives the
+    same bits as the separate level kernels (AMGF_NO_TAIL=1), and at cfg 2 as the oracle."""
+    p = gen.config(cfg)
+    g = amgf_mod.AMGF.from_problem(p)
+    monkeypatch.setenv("AMGF_NO_TAIL", "1")
+    h = amgf_mod.AMGF.from_problem(p)
+    monkeypatch.delenv("AMGF_NO_TAIL")
+    assert h.tail_level == -1
+    if cfg == 3:
+        assert g.tail_level == g.nlev - 2 and g.tail_ncta >= 1
+    rng = np.random.default_rng(21)
+    r = rng.standard_normal(p.n)
+    assert np.array_equal(g.vcycle(r).cpu().numpy(), h.vcycle(r).cpu().numpy())
+    assert np.array_equal(g.apply(r).cpu().numpy(), h.apply(r).cpu().numpy())
+    if cfg == 2:
+        assert np.array_equal(g.vcycle(r).cpu().numpy(), oracle_lib.Oracle.from_problem(p).vcycle(r))
