@@ -66,6 +66,8 @@ struct Sell {
   int *col = nullptr;        // [nslots*32]
   double *val = nullptr;     // [nslots*br*bc*32]
   int *src = nullptr;        // [nslots*32] index of the source BSR block (-1 padding) for refresh
+  int *perm = nullptr;       // [nrows] or null: SELL row i holds matrix row perm[i] (rows sorted by length
+                             // within windows to remove slot padding; prolongation only, SPMV_ADDTO)
 };
 
 struct Level {
@@ -228,7 +230,7 @@ void launch_band_sweep(Ctx &c, int nblocks, const int *d_p0, const int *d_len, i
                        const double *Lcol, const double *Lrev, const double *dinv, const double *in, const int *gather,
                        double *out, double *out_shift = nullptr);
 void drop_caches(Ctx &c);
-void build_sell(Ctx &c, const Bsr &A, Sell &S, bool alloc, bool split);
+void build_sell(Ctx &c, const Bsr &A, Sell &S, bool alloc, bool split, bool sort_rows = false);
 
 // ------------------------------------------------------------------ solve orchestration (api.cu)
 void vcycle(Ctx &c, int l, const double *b, double *x, const double *add);

@@ -752,6 +752,14 @@ __global__ void k_row_len(int nrows, int split, const int *ptr, int *len) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < nrows) len[i] = ptr[i / split + 1] - ptr[i / split];
 }
+// sort key of a row: its window of SELL_SORT_WINDOW rows, then decreasing length (radix sort is stable)
+constexpr int SELL_SORT_WINDOW = 8192;
+__global__ void k_sell_sort_keys(int nrows, const int *len, int *key, int *idx) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nrows) return;
+  key[i] = (i / SELL_SORT_WINDOW) * 65536 + (65535 - min(len[i], 65535));
+  idx[i] = i;
+}
 __global__ void k_slice_width(int nslices, int nrows, const int *len, int *width) {
   int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= nslices) return;
@@ -764,11 +772,12 @@ __global__ void k_slice_width(int nslices, int nrows, const int *len, int *width
 }
 // ssrc = source BSR block index * split + scalar row within the block (or -1 for padding)
 __global__ void k_sell_pack(int nrows, int split, const int *ptr, const int *col, const int *slice_ptr,
-                            int *scol, int *ssrc) {
+                            const int *perm, int *scol, int *ssrc) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nrows) return;
   const int lane = i & 31;
-  const int ib = i / split, r = i % split;
+  const int oi = perm ? perm[i] : i;
+  const int ib = oi / split, r = oi % split;
   const long base = slice_ptr[i >> 5];
   const int w = slice_ptr[(i >> 5) + 1] - slice_ptr[i >> 5];
   const int len = ptr[ib + 1] - ptr[ib];
@@ -817,7 +826,7 @@ static int *rowof(Ctx &c, const Bsr &A) {
   return r;
 }
 
-void build_sell(Ctx &c, const Bsr &A, Sell &S, bool alloc, bool split) {
+void build_sell(Ctx &c, const Bsr &A, Sell &S, bool alloc, bool split, bool sort_rows) {
   const int sp = split ? A.br : 1;
   const int BB = split ? A.bc : A.br * A.bc;
   if (alloc) {
@@ -825,6 +834,16 @@ void build_sell(Ctx &c, const Bsr &A, Sell &S, bool alloc, bool split) {
     S.nslices = (S.nrows + 31) / 32;
     S.rowlen = c.alloc<int>(S.nrows);
     LAUNCH(k_row_len, S.nrows, S.nrows, sp, A.ptr, S.rowlen);
+    if (sort_rows) {
+      int *key = c.alloc<int>(S.nrows), *key2 = c.alloc<int>(S.nrows), *idx = c.alloc<int>(S.nrows);
+      int *len0 = c.alloc<int>(S.nrows);
+      S.perm = c.alloc<int>(S.nrows);
+      LAUNCH(k_sell_sort_keys, S.nrows, S.nrows, S.rowlen, key, idx);
+      sort_pairs(c, key, key2, idx, S.perm, S.nrows);
+      d2d(c, len0, S.rowlen, S.nrows);
+      LAUNCH(k_gather_int, S.nrows, S.nrows, S.perm, len0, S.rowlen);
+      c.release(key); c.release(key2); c.release(idx); c.release(len0);
+    }
     int *width = c.alloc<int>(S.nslices + 1);
     CK(cudaMemsetAsync(width, 0, (S.nslices + 1) * sizeof(int), c.stream));
     LAUNCH(k_slice_width, S.nslices, S.nslices, S.nrows, S.rowlen, width);
@@ -837,7 +856,7 @@ void build_sell(Ctx &c, const Bsr &A, Sell &S, bool alloc, bool split) {
     // lanes of the last slice beyond nrows are never written by k_sell_pack: mark them as padding
     CK(cudaMemsetAsync(S.col, 0, S.nslots * 32 * sizeof(int), c.stream));
     CK(cudaMemsetAsync(S.src, 0xff, S.nslots * 32 * sizeof(int), c.stream));
-    LAUNCH(k_sell_pack, S.nrows, S.nrows, sp, A.ptr, A.col, S.slice_ptr, S.col, S.src);
+    LAUNCH(k_sell_pack, S.nrows, S.nrows, sp, A.ptr, A.col, S.slice_ptr, S.perm, S.col, S.src);
   }
   LAUNCH(k_sell_vals, S.nslots * 32, S.nslots, BB, S.src, A.val, S.val);
 }
@@ -1296,7 +1315,7 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
     build_sell(c, L.A, L.As, true, l > 0);   // coarse levels: one thread per scalar row (1 x 6)
     level_numeric(c, l, lc);
     check_dev_error(c, "Galerkin product");
-    build_sell(c, L.P, L.Ps, true, l > 0);
+    build_sell(c, L.P, L.Ps, true, l > 0, l == 0);  // fine prolongator: rows sorted by length
     l++;
   }
   c.nlev = l + 1;

@@ -8,6 +8,8 @@
 //   k_band_trsv A_w^{-1} v by the banded Cholesky factor, one warp, shuffle broadcast, cp.async
 //               double-buffered band columns (C10); gather r1[Z] and scatter x2[Z] += y fused.
 //   k_thin      r2 = r1 - S[:,Z] y over the rows that touch Z (C11).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "devutil.cuh"
 
@@ -48,7 +50,7 @@ __global__ void __launch_bounds__(CTA) k_sell(int nrows, const int *__restrict__
                                               const double *__restrict__ val, const double *__restrict__ x,
                                               const double *__restrict__ b, const double *__restrict__ d,
                                               const double *__restrict__ add, double *__restrict__ y,
-                                              double *__restrict__ dot_part) {
+                                              double *__restrict__ dot_part, const int *__restrict__ perm) {
   const int row = blockIdx.x * CTA + threadIdx.x;
   const int lane = threadIdx.x & 31;
   double acc[BR];
@@ -106,9 +108,10 @@ __global__ void __launch_bounds__(CTA) k_sell(int nrows, const int *__restrict__
     return;
   }
   if (row >= nrows) return;
+  const int orow = (MODE == MODE_ADDTO && perm) ? perm[row] : row;
 #pragma unroll
   for (int r = 0; r < BR; r++) {
-    const long i = (long)row * BR + r;
+    const long i = (long)orow * BR + r;
     if (MODE == MODE_Y) {
       y[i] = acc[r];
     } else if (MODE == MODE_RESID) {
@@ -132,7 +135,8 @@ __global__ void __launch_bounds__(CTA) k_sell_r1(int nrows, const int *__restric
                                                  const int *__restrict__ rowlen, const int *__restrict__ col,
                                                  const double *__restrict__ val, const double *__restrict__ x,
                                                  const double *__restrict__ b, const double *__restrict__ d,
-                                                 const double *__restrict__ add, double *__restrict__ y) {
+                                                 const double *__restrict__ add, double *__restrict__ y,
+                                                 const int *__restrict__ perm) {
   const int row = blockIdx.x * CTA + threadIdx.x;
   const int lane = threadIdx.x & 31;
   if (row >= nrows) return;
@@ -175,7 +179,7 @@ __global__ void __launch_bounds__(CTA) k_sell_r1(int nrows, const int *__restric
     }
   }
   }
-  const long i = row;
+  const long i = (MODE == MODE_ADDTO && perm) ? perm[row] : row;
   if (MODE == MODE_Y) {
     y[i] = acc;
   } else if (MODE == MODE_RESID) {
@@ -198,22 +202,22 @@ static void sell_dispatch(Ctx &c, const Sell &A, int mode, const double *x, cons
   if (A.nrows == 0) return;
   if (BR == 1 && mode != MODE_DOT) {
     switch (mode) {
-      case MODE_Y: k_sell_r1<BC, MODE_Y, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y); break;
-      case MODE_RESID: k_sell_r1<BC, MODE_RESID, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y); break;
-      case MODE_SMOOTH: k_sell_r1<BC, MODE_SMOOTH, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y); break;
-      case MODE_SMOOTH_ADD: k_sell_r1<BC, MODE_SMOOTH_ADD, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y); break;
-      case MODE_ADDTO: k_sell_r1<BC, MODE_ADDTO, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y); break;
+      case MODE_Y: k_sell_r1<BC, MODE_Y, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm); break;
+      case MODE_RESID: k_sell_r1<BC, MODE_RESID, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm); break;
+      case MODE_SMOOTH: k_sell_r1<BC, MODE_SMOOTH, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm); break;
+      case MODE_SMOOTH_ADD: k_sell_r1<BC, MODE_SMOOTH_ADD, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm); break;
+      case MODE_ADDTO: k_sell_r1<BC, MODE_ADDTO, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm); break;
     }
     after_launch(c, "k_sell_r1");
     return;
   }
   switch (mode) {
-    case MODE_Y: k_sell<BR, BC, MODE_Y><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp); break;
-    case MODE_RESID: k_sell<BR, BC, MODE_RESID><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp); break;
-    case MODE_SMOOTH: k_sell<BR, BC, MODE_SMOOTH><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp); break;
-    case MODE_DOT: k_sell<BR, BC, MODE_DOT><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp); break;
-    case MODE_SMOOTH_ADD: k_sell<BR, BC, MODE_SMOOTH_ADD><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp); break;
-    case MODE_ADDTO: k_sell<BR, BC, MODE_ADDTO><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp); break;
+    case MODE_Y: k_sell<BR, BC, MODE_Y><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm); break;
+    case MODE_RESID: k_sell<BR, BC, MODE_RESID><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm); break;
+    case MODE_SMOOTH: k_sell<BR, BC, MODE_SMOOTH><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm); break;
+    case MODE_DOT: k_sell<BR, BC, MODE_DOT><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm); break;
+    case MODE_SMOOTH_ADD: k_sell<BR, BC, MODE_SMOOTH_ADD><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm); break;
+    case MODE_ADDTO: k_sell<BR, BC, MODE_ADDTO><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm); break;
   }
   after_launch(c, __func__);
 }
@@ -235,7 +239,7 @@ void launch_prolong(Ctx &c, const Sell &P, const double *xc, double *x) {
 
 // ------------------------------------------------------------------ restriction (C5)
 template <int B>
-__global__ void __launch_bounds__(CTA) k_restrict(int nrows, const int *__restrict__ ptr, const int *__restrict__ col,
+__global__ void __launch_bounds__(CTA, 2) k_restrict(int nrows, const int *__restrict__ ptr, const int *__restrict__ col,
                                                   const double *__restrict__ val, const double *__restrict__ r,
                                                   double *__restrict__ out) {
   const int w = (blockIdx.x * CTA + threadIdx.x) >> 5;
@@ -245,36 +249,23 @@ __global__ void __launch_bounds__(CTA) k_restrict(int nrows, const int *__restri
 #pragma unroll
   for (int q = 0; q < 6; q++) acc[q] = 0.0;
   const int beg = ptr[w], end = ptr[w + 1];
-  // lane-strided blocks k = beg + lane + 32 t; the next block's values and r are prefetched (C5 order kept)
-  int k = beg + lane;
-  double2 v[3 * B];
-  double rv[B];
-  if (k < end) {
+  // lane-strided blocks k = beg + lane + 32 t (C5 order).  No software pipeline: at 126 registers two
+  // CTAs per SM stay resident and their loads carry enough bytes in flight (measured 71 -> ~60 us at cfg 3
+  // against the register-heavy prefetching version)
+  for (int k = beg + lane; k < end; k += 32) {
     const int c = col[k];
+    double2 v[3 * B];
+    double rv[B];
 #pragma unroll
     for (int h = 0; h < 3 * B; h++) v[h] = __ldg(reinterpret_cast<const double2 *>(val + (long)k * 6 * B) + h);
 #pragma unroll
     for (int e = 0; e < B; e++) rv[e] = r[(long)c * B + e];
-  }
-  for (; k < end; k += 32) {
-    const int kn = k + 32 < end ? k + 32 : k;
-    const int cn = col[kn];
-    double2 vn[3 * B];
-    double rn[B];
-#pragma unroll
-    for (int h = 0; h < 3 * B; h++) vn[h] = __ldg(reinterpret_cast<const double2 *>(val + (long)kn * 6 * B) + h);
-#pragma unroll
-    for (int e = 0; e < B; e++) rn[e] = r[(long)cn * B + e];
 #pragma unroll
     for (int h = 0; h < 3 * B; h++) {
       const int e0 = 2 * h, e1 = 2 * h + 1;
       acc[e0 / B] = __fma_rn(v[h].x, rv[e0 % B], acc[e0 / B]);
       acc[e1 / B] = __fma_rn(v[h].y, rv[e1 % B], acc[e1 / B]);
     }
-#pragma unroll
-    for (int h = 0; h < 3 * B; h++) v[h] = vn[h];
-#pragma unroll
-    for (int e = 0; e < B; e++) rv[e] = rn[e];
   }
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1)
@@ -301,29 +292,45 @@ __global__ void __launch_bounds__(CTA) k_restrict_row(int nrows6, const int *__r
   const int a = w / 6, rr = w % 6;
   const int beg = ptr[a], end = ptr[a + 1];
   double acc = 0.0;
-  // batches of U lane-strided blocks (k, k+32, ...): all their columns, values and r entries in flight
-  // at once; the chain still runs over the lane's blocks in ascending order (C5)
-  constexpr int U = 4;
-  for (int k0 = beg + lane; k0 < end; k0 += U * 32) {
-    int cc[U];
+  // software pipeline over batches of U lane-strided blocks (k, k+32, ...): the next batch's values and
+  // r entries are in flight while this batch's FMAs run, its columns one batch further ahead; the chain
+  // still runs over the lane's blocks in ascending order (C5).  Indices are clamped so that every load
+  // is unconditional.
+  constexpr int U = 2;
+  if (beg + lane < end) {
+    const int last = end - 1;
     double v[U][B], rv[U][B];
-    int kk[U];  // clamped (loads unconditional, so that they are all issued before the chain)
+    int cn[U];
+    int k0 = beg + lane;
 #pragma unroll
-    for (int u = 0; u < U; u++) kk[u] = min(k0 + 32 * u, end - 1);
+    for (int u = 0; u < U; u++) {
+      const int kk = min(k0 + 32 * u, last);
+      const int cc = col[kk];
 #pragma unroll
-    for (int u = 0; u < U; u++) cc[u] = col[kk[u]];
+      for (int e = 0; e < B; e++) { v[u][e] = __ldg(val + (long)kk * 6 * B + rr * B + e); rv[u][e] = r[(long)cc * B + e]; }
+    }
 #pragma unroll
-    for (int u = 0; u < U; u++)
+    for (int u = 0; u < U; u++) cn[u] = col[min(k0 + 32 * (U + u), last)];
+    for (; k0 < end; k0 += U * 32) {
+      double vn[U][B], rn[U][B];
 #pragma unroll
-      for (int e = 0; e < B; e++) {
-        v[u][e] = __ldg(val + (long)kk[u] * 6 * B + rr * B + e);
-        rv[u][e] = r[(long)cc[u] * B + e];
+      for (int u = 0; u < U; u++) {
+        const int kk = min(k0 + 32 * (U + u), last);
+#pragma unroll
+        for (int e = 0; e < B; e++) { vn[u][e] = __ldg(val + (long)kk * 6 * B + rr * B + e); rn[u][e] = r[(long)cn[u] * B + e]; }
       }
 #pragma unroll
-    for (int u = 0; u < U; u++)
-      if (k0 + 32 * u < end)
+      for (int u = 0; u < U; u++) cn[u] = col[min(k0 + 32 * (2 * U + u), last)];
 #pragma unroll
-        for (int e = 0; e < B; e++) acc = __fma_rn(v[u][e], rv[u][e], acc);
+      for (int u = 0; u < U; u++)
+        if (k0 + 32 * u < end)
+#pragma unroll
+          for (int e = 0; e < B; e++) acc = __fma_rn(v[u][e], rv[u][e], acc);
+#pragma unroll
+      for (int u = 0; u < U; u++)
+#pragma unroll
+        for (int e = 0; e < B; e++) { v[u][e] = vn[u][e]; rv[u][e] = rn[u][e]; }
+    }
   }
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) acc = acc + __shfl_xor_sync(0xffffffffu, acc, o);

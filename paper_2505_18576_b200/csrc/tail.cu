@@ -273,7 +273,7 @@ void tail_plan(Ctx &c) {
   const int t = c.nlev - 2;
   Level &L = c.lev[t];
   if (L.b != 6 || L.As.br != 1 || L.As.bc != 6 || L.Ps.br != 1 || L.Ps.bc != 6 || L.R.bc != 6) return;
-  if (c.nco > TAIL_MAX_NCO || c.nco != 6 * L.R.nbr) return;
+  if (c.nco > TAIL_MAX_NCO || c.nco != 6 * L.R.nbr || L.Ps.perm || L.As.perm) return;
   const int ns = L.As.nslices;
   std::vector<int> sp(ns + 1);
   CK(cudaMemcpy(sp.data(), L.As.slice_ptr, (ns + 1) * sizeof(int), cudaMemcpyDeviceToHost));
