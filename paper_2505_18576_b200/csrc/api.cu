@@ -36,6 +36,9 @@ Ctx::~Ctx() {
   if (ev_out) cudaEventDestroy(ev_out);
   if (side) cudaStreamDestroy(side);
   if (ev_fork) cudaEventDestroy(ev_fork);
+  if (fstream) cudaStreamDestroy(fstream);
+  if (ev_f0) cudaEventDestroy(ev_f0);
+  if (ev_f1) cudaEventDestroy(ev_f1);
   if (ev_join) cudaEventDestroy(ev_join);
   for (void *p : allocs) cudaFree(p);
   if (sc_host) cudaFreeHost(sc_host);
@@ -123,8 +126,46 @@ void apply_M(Ctx &c, const double *r, double *z) {
     vcycle(c, 0, c.w_r1, z, c.w_x1);
     return;
   }
+  // r1 at the Z rows first (pi order), then the A_w solve on the high-priority filter stream while the
+  // full residual r1 = r - S x1 runs here; x2 = x1 + P y and the thin r2 after the join.  Same kernels
+  // and arithmetic as the serial order, so the result is unchanged bitwise.
+  if (!c.fstream) {
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(&c.fstream, cudaStreamNonBlocking, hi));
+    CK(cudaEventCreateWithFlags(&c.ev_f0, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c.ev_f1, cudaEventDisableTiming));
+  }
+  static const bool trace = getenv("AMGF_TRACE_FILTER") != nullptr;  // tools only: overlap timeline
+  cudaEvent_t te[5] = {};
+  if (trace && !c.capturing) {
+    for (auto &e : te) CK(cudaEventCreate(&e));
+    CK(cudaEventRecord(te[0], c.stream));
+  }
+  launch_resid_dofs(c, L0.As, c.nc, c.dof, c.w_x1, r, c.rz);
+  CK(cudaEventRecord(c.ev_f0, c.stream));
+  CK(cudaStreamWaitEvent(c.fstream, c.ev_f0, 0));
+  {
+    cudaStream_t main = c.stream;
+    c.stream = c.fstream;
+    nd_solve(c, c.rz, nullptr);  // y = A_w^{-1} r1[Z] (pi order, c.fv)
+    c.stream = main;
+  }
+  CK(cudaEventRecord(c.ev_f1, c.fstream));
+  if (te[0]) CK(cudaEventRecord(te[1], c.fstream));
   launch_sell_spmv(c, L0.As, SPMV_RESID, c.w_x1, r, nullptr, nullptr, c.w_r1, nullptr);
-  nd_solve(c, c.w_r1, c.w_x1);  // y = A_w^{-1} r1[Z] (pi order, c.fv), x2 = x1 + P y
+  if (te[0]) CK(cudaEventRecord(te[2], c.stream));
+  CK(cudaStreamWaitEvent(c.stream, c.ev_f1, 0));
+  if (te[0]) {
+    CK(cudaEventSynchronize(te[1]));
+    CK(cudaEventSynchronize(te[2]));
+    float a = 0, b = 0;
+    CK(cudaEventElapsedTime(&a, te[0], te[1]));
+    CK(cudaEventElapsedTime(&b, te[0], te[2]));
+    fprintf(stderr, "filter overlap: filter done at %.1f us, residual SpMV done at %.1f us\n", a * 1e3, b * 1e3);
+    for (auto &e : te) cudaEventDestroy(e);
+  }
+  nd_scatter(c, c.w_x1);  // x2 = x1 + P y
   launch_thin_resid(c, c.nthin, c.thin_row, c.thin_ptr, c.thin_pos, c.thin_val, c.fv, c.w_r1);
   vcycle(c, 0, c.w_r1, z, c.w_x1);
 }

@@ -67,7 +67,7 @@ struct Sell {
   double *val = nullptr;     // [nslots*br*bc*32]
   int *src = nullptr;        // [nslots*32] index of the source BSR block (-1 padding) for refresh
   int *perm = nullptr;       // [nrows] or null: SELL row i holds matrix row perm[i] (rows sorted by length
-                             // within windows to remove slot padding; prolongation only, SPMV_ADDTO)
+                             // within windows to remove slot padding; prolongators and large coarse levels)
 };
 
 struct Level {
@@ -97,6 +97,11 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;        // A_w factorization overlaps the hierarchy's numeric setup
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // filter overlap (apply_M): the A_w solve runs on fstream (high priority) while the full residual
+  // SpMV runs on the main stream; rz = r1 at the Z rows in pi order, computed first by k_resid_dofs
+  cudaStream_t fstream = nullptr;
+  cudaEvent_t ev_f0 = nullptr, ev_f1 = nullptr;
+  double *rz = nullptr;
   amgf_config cfg;
   int nodes = 0, m = 0;
   long n = 0;
@@ -222,7 +227,9 @@ void setup_numeric(Ctx &c, const double *D);  // update_D
 // filter.cu
 void nd_symbolic(Ctx &c);
 void nd_numeric(Ctx &c);
-void nd_solve(Ctx &c, const double *r1, double *x2);  // c.fv <- A_w^{-1} r1[Z] (pi order), x2[Z] += y
+void nd_solve(Ctx &c, const double *r1, const int *gather);  // c.fv <- A_w^{-1} r1 (pi order; r1[gather[p]])
+void nd_scatter(Ctx &c, double *x2);                          // x2[Z] += y (c.fv)
+void launch_resid_dofs(Ctx &c, const Sell &A, int n, const int *dof, const double *x, const double *b, double *out);
 void nd_remap_positions(Ctx &c, int *pos_z, long n);  // Z positions -> pi positions
 void band_factor_blocks(Ctx &c, int n, int nblocks, const int *d_p0, const int *d_len, int bw, double *Lrow, int tag);
 void band_finish(Ctx &c, int n, int bw, const double *Lrow, double *Lcol, double *Lrev, double *dinv);

@@ -262,7 +262,8 @@ __global__ void __launch_bounds__(32) k_nd_sep_fwd(const int2 *groups, const NdB
   };
 #pragma unroll
   for (int c = 0; c < NS - 1; c++) issue(c);
-  double acc = (lane < nrow) ? r1[dof[S.p0 + row0 + lane]] : 0.0;
+  const int prow = S.p0 + row0 + lane;
+  double acc = (lane < nrow) ? r1[dof ? dof[prow] : prow] : 0.0;
   const int me = min(lane, G - 1);
   for (int c = 0; c < nch; c++) {
     issue(c + NS - 1);
@@ -436,6 +437,7 @@ void nd_symbolic(Ctx &c) {
   c.Ldinv = c.alloc<double>(nc);
   c.Loff = c.alloc<double>(std::max(off, 1L));
   c.fv = c.alloc<double>(nc);
+  c.rz = c.alloc<double>(nc);
   c.fw = c.alloc<double>(nc + SF_KC + 4);
   c.fw2 = c.alloc<double>(nc + SF_KC + 4);
   c.nd_nsep = (int)sep_blocks.size();
@@ -480,18 +482,23 @@ void nd_numeric(Ctx &c) {
   band_finish(c, nc, bw, c.Lrow, c.Lcol, c.Lrev, c.Ldinv);
 }
 
-void nd_solve(Ctx &c, const double *r1, double *x2) {
+void nd_scatter(Ctx &c, double *x2) {
+  k_nd_scatter<<<nblk(c.nc), CTA, 0, c.stream>>>(c.nc, c.dof, c.fv, x2);
+  after_launch(c, "k_nd_scatter");
+}
+
+void nd_solve(Ctx &c, const double *r1, const int *gather) {
   const int nc = c.nc, bw = c.bw;
   const NdBlk *blk = (const NdBlk *)c.nd_blk;
   double *w = c.fw, *y = c.fv;
   // forward: leaves (gathered r1), then separators bottom-up
-  launch_band_sweep(c, c.nd_nleaves, c.nd_leaf_p0, c.nd_leaf_len, nc, bw, true, c.Lcol, c.Lrev, c.Ldinv, r1, c.dof,
+  launch_band_sweep(c, c.nd_nleaves, c.nd_leaf_p0, c.nd_leaf_len, nc, bw, true, c.Lcol, c.Lrev, c.Ldinv, r1, gather,
                     w, c.fw2);
   for (int l = c.nd_depth - 1; l >= 0; l--) {
     Ctx::NdLevel &Lv = c.nd_lev[l];
     if (!Lv.count) continue;
     const SepFwdVariant &V = kSepFwd[sep_fwd_variant()];
-    V.fn<<<Lv.ngroups, 32, sf_smem(V.G, V.NS), c.stream>>>((const int2 *)Lv.groups, blk, c.Loff, r1, c.dof, w,
+    V.fn<<<Lv.ngroups, 32, sf_smem(V.G, V.NS), c.stream>>>((const int2 *)Lv.groups, blk, c.Loff, r1, gather, w,
                                                            c.fw2, y);
     after_launch(c, "k_nd_sep_fwd");
     launch_band_sweep(c, Lv.count, Lv.p0, Lv.len, nc, bw, true, c.Lcol, c.Lrev, c.Ldinv, y, nullptr, w, c.fw2);
@@ -507,8 +514,6 @@ void nd_solve(Ctx &c, const double *r1, double *x2) {
   }
   launch_band_sweep(c, c.nd_nleaves, c.nd_leaf_p0, c.nd_leaf_len, nc, bw, false, c.Lcol, c.Lrev, c.Ldinv, w, nullptr,
                     y);
-  k_nd_scatter<<<nblk(nc), CTA, 0, c.stream>>>(nc, c.dof, y, x2);
-  after_launch(c, "k_nd_scatter");
 }
 
 }  // namespace amgf

@@ -1312,10 +1312,14 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
       Lc.dl1 = c.alloc<double>(Lc.n);
       Lc.dpt = c.alloc<double>(Lc.n);
     }
-    build_sell(c, L.A, L.As, true, l > 0);   // coarse levels: one thread per scalar row (1 x 6)
+    // coarse levels: one thread per scalar row (1 x 6).  Rows sorted by length (less slot padding) on the
+    // large levels: the fine operator keeps its order (the PCG dot partials and the Z-row residual read
+    // it by row), small levels may become the fused tail (tail.cu), which needs the natural order
+    const bool sort_level = l > 0 && L.n > 16384;
+    build_sell(c, L.A, L.As, true, l > 0, sort_level);
     level_numeric(c, l, lc);
     check_dev_error(c, "Galerkin product");
-    build_sell(c, L.P, L.Ps, true, l > 0, l == 0);  // fine prolongator: rows sorted by length
+    build_sell(c, L.P, L.Ps, true, l > 0, l == 0 || sort_level);  // prolongators: rows sorted by length
     l++;
   }
   c.nlev = l + 1;

@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(CTA) k_sell_r1(int nrows, const int *__restric
     }
   }
   }
-  const long i = (MODE == MODE_ADDTO && perm) ? perm[row] : row;
+  const long i = perm ? perm[row] : row;  // rows sorted by length (SELL packing), any mode
   if (MODE == MODE_Y) {
     y[i] = acc;
   } else if (MODE == MODE_RESID) {
@@ -200,6 +200,16 @@ static void sell_dispatch(Ctx &c, const Sell &A, int mode, const double *x, cons
                           const double *add, double *y, double *dp) {
   dim3 g(nblk(A.nrows)), t(CTA);
   if (A.nrows == 0) return;
+  {
+    // An explicit carveout preference for the residual SpMV lets the A_w solve, which runs concurrently on
+    // the filter stream (apply_M), get SMs while the SpMV is resident: the driver default cost ~50 us per
+    // AMGF apply at cfg 3; any value in 0..60 % gave the same time, above that the SpMV loses L1.
+    static bool once = false;
+    if (!once) {
+      once = true;
+      CK(cudaFuncSetAttribute(k_sell<BR, BC, MODE_RESID>, cudaFuncAttributePreferredSharedMemoryCarveout, 50));
+    }
+  }
   if (BR == 1 && mode != MODE_DOT) {
     switch (mode) {
       case MODE_Y: k_sell_r1<BC, MODE_Y, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm); break;
@@ -235,6 +245,51 @@ void launch_prolong(Ctx &c, const Sell &P, const double *xc, double *x) {
   else if (P.br == 1) sell_dispatch<1, 6>(c, P, MODE_ADDTO, xc, nullptr, nullptr, nullptr, x, nullptr);
   else if (P.br == 6) sell_dispatch<6, 6>(c, P, MODE_ADDTO, xc, nullptr, nullptr, nullptr, x, nullptr);
   else throw Error{AMGF_ERR_ARG, "prolong: unsupported block shape"};
+}
+
+// Residual b - S x at the dofs dof[p] only (p < n), into out[p]: the same SELL chain as k_sell<3,3> for
+// that scalar row (C2), so the values equal the full residual's at those rows bitwise.  One warp per dof:
+// lane s loads slot s (column, the row's 3 values, the 3 x entries), all in flight at once, then every
+// lane runs the row's chain over shuffled operands (slots ascending, components ascending) and lane 0
+// writes.  Used to start the A_w solve before the full residual SpMV (apply_M).
+__global__ void __launch_bounds__(CTA) k_resid_dofs(int n, const int *__restrict__ dof,
+                                                    const int *__restrict__ slice_ptr, const int *__restrict__ rowlen,
+                                                    const int *__restrict__ col, const double *__restrict__ val,
+                                                    const double *__restrict__ x, const double *__restrict__ b,
+                                                    double *__restrict__ out) {
+  const int p = (blockIdx.x * CTA + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (p >= n) return;  // warp-uniform
+  const int d = dof[p], i = d / 3, r = d % 3, il = i & 31;
+  const long base = slice_ptr[i >> 5];
+  const int len = rowlen[i];
+  double acc = 0.0;
+  for (int s0 = 0; s0 < len; s0 += 32) {
+    const int s = s0 + lane;
+    double v[3] = {0.0, 0.0, 0.0}, xv[3] = {0.0, 0.0, 0.0};
+    if (s < len) {
+      const long slot = base + s;
+      const int c = col[slot * 32 + il];
+#pragma unroll
+      for (int e = 0; e < 3; e++) {
+        v[e] = val[(slot * 9 + r * 3 + e) * 32 + il];
+        xv[e] = x[(long)c * 3 + e];
+      }
+    }
+    const int m = min(32, len - s0);
+    for (int q = 0; q < m; q++)
+#pragma unroll
+      for (int e = 0; e < 3; e++)
+        acc = __fma_rn(__shfl_sync(0xffffffffu, v[e], q), __shfl_sync(0xffffffffu, xv[e], q), acc);
+  }
+  if (lane == 0) out[p] = b[d] - acc;
+}
+
+void launch_resid_dofs(Ctx &c, const Sell &A, int n, const int *dof, const double *x, const double *b, double *out) {
+  if (n == 0) return;
+  REQUIRE(A.br == 3 && A.bc == 3 && !A.perm, AMGF_ERR_ARG, "resid_dofs: fine-level 3x3 SELL expected");
+  k_resid_dofs<<<nblk((long)n * 32), CTA, 0, c.stream>>>(n, dof, A.slice_ptr, A.rowlen, A.col, A.val, x, b, out);
+  after_launch(c, "k_resid_dofs");
 }
 
 // ------------------------------------------------------------------ restriction (C5)
@@ -629,89 +684,32 @@ __global__ void __launch_bounds__(32) k_band_trsv(int n, int bw, const double *_
   if (scatter) scatter_add_warp(n, scatter, y, xout, lane);
 }
 
-// Block sweep (nested-dissection filter, filter.cu): one warp per diagonal block [p0, p0+len) of a band,
-// forward (w = L_B^{-1} in, column sweep over Lcol) or backward (out = L_B^{-T} in, row sweep over Lrev),
-// starting from the accumulators in[] (gathered through gather[] if given).  Same round structure, TMA ring
-// and chain order as k_band_trsv; entries outside the block are zero in the band storage.
-template <int R, int NB, bool FWD>
-__global__ void __launch_bounds__(32) k_band_sweep(const int *__restrict__ blk_p0, const int *__restrict__ blk_len,
-                                                   int bw, const double *__restrict__ Lcol,
-                                                   const double *__restrict__ Lrev, const double *__restrict__ dinv,
-                                                   const double *__restrict__ in, const int *__restrict__ gather,
-                                                   double *__restrict__ out, double *__restrict__ out_shift) {
-  constexpr int Ws = 32 * R;
-  constexpr unsigned CHUNK = 32u * Ws * 8u;
-  extern __shared__ __align__(128) double sm[];
-  __shared__ __align__(8) uint64_t bar[NB];
-  const int lane = threadIdx.x;
-  const int p0 = blk_p0[blockIdx.x], n = blk_len[blockIdx.x];
-  const int F = (n + 31) / 32;
-  if (lane == 0) {
-#pragma unroll
-    for (int b = 0; b < NB; b++) mbar_init(&bar[b], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
-  auto issue = [&](int g) {
-    if (g >= F || lane != 0) return;
-    const double *src = FWD ? Lcol + (long)(p0 + 32 * g) * Ws : Lrev + (long)(p0 + n - 1 - 32 * g - 31) * Ws;
-    uint64_t *br = &bar[g % NB];
-    mbar_arrive_expect(br, CHUNK);
-    bulk_g2s(sm + (g % NB) * 32 * Ws, src, CHUNK, br);
-  };
-#pragma unroll
-  for (int g = 0; g < NB - 1; g++) issue(g);
-  // local row index t in [0, n): forward row p0 + t, backward row p0 + n - 1 - t
-  auto row = [&](int t) { return FWD ? p0 + t : p0 + n - 1 - t; };
-  auto ld_in = [&](int t) -> double {
-    if (t >= n) return 0.0;
-    const int r = row(t);
-    return gather ? in[gather[r]] : in[r];
-  };
-  double acc[R];
-#pragma unroll
-  for (int s = 0; s < R; s++) acc[s] = ld_in(lane + 32 * s);
-  double dv = (lane < n) ? dinv[row(lane)] : 0.0;
-  double vq1 = ld_in(32 + lane + 32 * (R - 1));
-  double dq1 = (32 + lane < n) ? dinv[row(32 + lane)] : 0.0;
-  for (int q = 0; q < F; q++) {
-    const int t0 = 32 * q;
-    __syncwarp();
-    fence_proxy_async();
-    issue(q + NB - 1);
-    const double vq2 = ld_in(t0 + 64 + lane + 32 * (R - 1));
-    const double dq2 = (t0 + 64 + lane < n) ? dinv[row(t0 + 64 + lane)] : 0.0;
-    mbar_wait(&bar[q % NB], (q / NB) & 1);
-    // forward: column jj of the round at jj*Ws, row offset lane + 32s - jj
-    // backward: row k = k1 - jj at (31 - jj)*Ws, distance lane + 32s - jj
-    const double *cur = sm + (q % NB) * 32 * Ws + lane;
-    double lc[R], mine = 0.0;
-#pragma unroll
-    for (int s = 0; s < R; s++) lc[s] = FWD ? cur[32 * s] : cur[31 * Ws + 32 * s];
-#pragma unroll
-    for (int jj = 0; jj < 32; jj++) {
-      if (t0 + jj >= n) break;
-      double ln[R];
-      const int jn = (jj + 1) & 31;
-#pragma unroll
-      for (int s = 0; s < R; s++) ln[s] = FWD ? cur[jn * (Ws - 1) + 32 * s] : cur[(31 - jn) * Ws - jn + 32 * s];
-      const double yj = __shfl_sync(0xffffffffu, acc[0] * dv, jj);
-      mine = (lane == jj) ? yj : mine;
-#pragma unroll
-      for (int s = 0; s < R; s++) acc[s] = __fma_rn(-lc[s], yj, acc[s]);
-#pragma unroll
-      for (int s = 0; s < R; s++) lc[s] = ln[s];
+}  // namespace amgf
+#include "band_sweep.cuh"
+namespace amgf {
+
+template <int R, int NB, bool BLOCKED>
+static void sweep_RN(Ctx &c, int nblocks, const int *p0, const int *len, int bw, bool fwd, const double *Lcol,
+                     const double *Lrev, const double *dinv, const double *in, const int *gather, double *out,
+                     double *out_shift) {
+  const size_t smem = (size_t)NB * 32 * (32 * R) * sizeof(double);
+  static bool attr_f = false, attr_b = false;
+  if (fwd) {
+    if (!attr_f) {
+      CK(cudaFuncSetAttribute(k_band_sweep<R, NB, true, BLOCKED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)smem));
+      attr_f = true;
     }
-    if (t0 + lane < n) {
-      out[row(t0 + lane)] = mine;
-      if (out_shift) out_shift[row(t0 + lane) + 1] = mine;  // copy shifted by one (TMA alignment, filter.cu)
+    k_band_sweep<R, NB, true, BLOCKED><<<nblocks, 32, smem, c.stream>>>(p0, len, bw, Lcol, Lrev, dinv, in, gather,
+                                                                         out, out_shift);
+  } else {
+    if (!attr_b) {
+      CK(cudaFuncSetAttribute(k_band_sweep<R, NB, false, BLOCKED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)smem));
+      attr_b = true;
     }
-#pragma unroll
-    for (int s = 0; s < R - 1; s++) acc[s] = acc[s + 1];
-    acc[R - 1] = vq1;
-    dv = dq1;
-    vq1 = vq2;
-    dq1 = dq2;
+    k_band_sweep<R, NB, false, BLOCKED><<<nblocks, 32, smem, c.stream>>>(p0, len, bw, Lcol, Lrev, dinv, in, gather,
+                                                                          out, out_shift);
   }
 }
 
@@ -719,24 +717,11 @@ template <int R>
 static void sweep_R(Ctx &c, int nblocks, const int *p0, const int *len, int bw, bool fwd, const double *Lcol,
                     const double *Lrev, const double *dinv, const double *in, const int *gather, double *out,
                     double *out_shift) {
+  // as many rounds in flight as 220 KB of shared memory allow (2 stages measured slower at cfg 3)
   constexpr int NB = (220 * 1024) / (32 * 32 * R * 8) >= 4 ? 4 : 3;
-  const size_t smem = (size_t)NB * 32 * (32 * R) * sizeof(double);
-  static bool attr_f = false, attr_b = false;
-  if (fwd) {
-    if (!attr_f) {
-      CK(cudaFuncSetAttribute(k_band_sweep<R, NB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr_f = true;
-    }
-    k_band_sweep<R, NB, true><<<nblocks, 32, smem, c.stream>>>(p0, len, bw, Lcol, Lrev, dinv, in, gather, out,
-                                                                out_shift);
-  } else {
-    if (!attr_b) {
-      CK(cudaFuncSetAttribute(k_band_sweep<R, NB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr_b = true;
-    }
-    k_band_sweep<R, NB, false><<<nblocks, 32, smem, c.stream>>>(p0, len, bw, Lcol, Lrev, dinv, in, gather, out,
-                                                                 out_shift);
-  }
+  // per-pivot form: the blocked form (triangle, then the rows below) measured 150 vs 99 cycles per pivot
+  // (tools/mb_sweep.cu), so it is kept only as a microbenchmark variant
+  sweep_RN<R, NB, false>(c, nblocks, p0, len, bw, fwd, Lcol, Lrev, dinv, in, gather, out, out_shift);
 }
 
 // Generic fallback sweep for wide bands: one CTA per block, barrier per pivot.

@@ -8,7 +8,9 @@ ci = {k: i for i, k in enumerate(h)}
 key = "Warp Stall Sampling (All Samples)"
 data = []
 for idx, r in enumerate(rows[2:]):
-    if len(r) <= ci[key]:
+    if r and r[0] == "Kernel Name":
+        break  # first kernel of the export only
+    if len(r) <= ci[key] or not r[ci[key]].replace(".", "").isdigit():
         continue
     data.append((float(r[ci[key]] or 0), idx, r[ci["Source"]].strip()))
 tot = sum(d[0] for d in data)
