@@ -115,8 +115,8 @@ struct Ctx {
   double *D = nullptr;
   int *S_kblk = nullptr;  // per S block: index of the K block (-1 if none)
   // filter (A_w factor in nested-dissection order, filter.cu)
-  struct NdLevel { int count = 0, ngroups = 0; int *ids = nullptr, *p0 = nullptr, *len = nullptr, *sub_ptr = nullptr, *sub_list = nullptr, *groups = nullptr; };
-  int nd_nblocks = 0, nd_nleaves = 0, nd_depth = 0, nd_npairs = 0, nd_nsep = 0;
+  struct NdLevel { int count = 0, ngroups = 0; int *ids = nullptr, *p0 = nullptr, *len = nullptr, *sub_ptr = nullptr, *sub_list = nullptr, *groups = nullptr, *selfpairs = nullptr; };
+  int nd_nblocks = 0, nd_nleaves = 0, nd_depth = 0, nd_npairs = 0, nd_nsep = 0, nd_maxsep = 0;
   int *nd_sep_blocks = nullptr;
   void *nd_blk = nullptr;                 // device NdBlk[nd_nblocks]
   int *nd_leaf_p0 = nullptr, *nd_leaf_len = nullptr, *nd_pairs = nullptr;

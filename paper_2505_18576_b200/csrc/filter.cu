@@ -165,62 +165,118 @@ __global__ void k_nd_fill(int nc, int bw, int W, const NdBlk *blk, const int *bl
     }
 }
 
-// Separator rows against leaf columns (C9): for j in leaf Lf, L_sj = (a_sj - sum_k L_sk L_jk) / L_jj with
-// k ascending over [max(p0(Lf), j - bw), j) (the only nonzero terms).  One thread per (separator, leaf, s).
-__global__ void k_nd_off_leaf(const int2 *pairs, const NdBlk *blk, int bw, int W, const double *Lrow, double *Loff) {
-  const NdBlk S = blk[pairs[blockIdx.x].x], Lf = blk[pairs[blockIdx.x].y];
-  for (int s = threadIdx.x; s < S.len; s += blockDim.x) {
-    double *Ls = Loff + S.off + (long)s * S.rs - S.t0;  // Ls[k] = L_sk
-    for (int j = Lf.p0; j < Lf.p0 + Lf.len; j++) {
-      const double *Lj = Lrow + (long)j * W + bw - j;  // Lj[k] = L_jk
-      const int k0 = max(Lf.p0, j - bw);
-      const double acc = chain_sub(Ls[j], Ls + k0, 1, Lj + k0, 1, j - k0);
-      Ls[j] = acc / Lj[j];
-    }
+// Separator rows against the columns of a diagonal block B (a leaf, or a lower separator S' after its
+// subtree terms): for j in B ascending, L_sj = (acc_sj - sum_k L_sk L_jk) / L_jj with k ascending over
+// [max(p0(B), j - bw), j) (C9; the only nonzero terms of the band row j).  One thread per separator row s;
+// its last bw values L_sk live in a shared-memory ring (M = bw rounded up to odd: conflict-free), so each
+// chain runs from shared memory (L_jk is the same band row for all threads: a broadcast load).
+constexpr int OB_RC = 16, OB_NS = 3;  // band rows per staged chunk, chunks in flight
+__global__ void __launch_bounds__(1024) k_nd_off_band(const int2 *pairs, const NdBlk *blk, int bw, int W, int M,
+                                                      const double *Lrow, double *Loff) {
+  extern __shared__ __align__(128) double ring[];  // [S.len][M] rings, then [OB_NS][OB_RC][W] band rows
+  __shared__ __align__(8) uint64_t bar[OB_NS];
+  const NdBlk S = blk[pairs[blockIdx.x].x], B = blk[pairs[blockIdx.x].y];
+  const int s = threadIdx.x;
+  const bool act = s < S.len;
+  double *Lbuf = ring + (((long)S.len * M + 15) & ~15L);
+  const int nch = (B.len + OB_RC - 1) / OB_RC;
+  if (s == 0) {
+    for (int q = 0; q < OB_NS; q++) mbar_init(&bar[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int ch) {  // band rows B.p0 + ch*RC .. (contiguous in Lrow) into stage ch % NS
+    if (ch >= nch) return;
+    const int r0 = B.p0 + ch * OB_RC, nr = min(OB_RC, B.p0 + B.len - r0);
+    const unsigned bytes = (unsigned)nr * W * 8u;
+    mbar_arrive_expect(&bar[ch % OB_NS], bytes);
+    bulk_g2s(Lbuf + (long)(ch % OB_NS) * OB_RC * W, Lrow + (long)r0 * W, bytes, &bar[ch % OB_NS]);
+  };
+  if (s == 0)
+    for (int ch = 0; ch < OB_NS - 1; ch++) issue(ch);
+  double *rs = ring + (long)min(s, S.len - 1) * M;
+  double *Ls = Loff + S.off + (long)min(s, S.len - 1) * S.rs - S.t0;  // Ls[k] = L_sk
+  double init = act ? Ls[B.p0] : 0.0;
+  for (int ch = 0; ch < nch; ch++) {
+    if (s == 0) issue(ch + OB_NS - 1);
+    mbar_wait(&bar[ch % OB_NS], (ch / OB_NS) & 1);
+    const double *stage = Lbuf + (long)(ch % OB_NS) * OB_RC * W;
+    const int jb = B.p0 + ch * OB_RC, je = min(jb + OB_RC, B.p0 + B.len);
+    if (act)
+      for (int j = jb; j < je; j++) {
+        const double *Lj = stage + (long)(j - jb) * W + bw - j;  // Lj[k] = L_jk (shared memory)
+        const int k0 = max(B.p0, j - bw), n = j - k0;
+        const double nxt = (j + 1 < B.p0 + B.len) ? Ls[j + 1] : 0.0;
+        const int st = (k0 - B.p0) % M, first = min(n, M - st);
+        double acc = chain_sub(init, rs + st, 1, Lj + k0, 1, first);
+        acc = chain_sub(acc, rs, 1, Lj + k0 + first, 1, n - first);
+        const double v = acc / Lj[j];
+        rs[(j - B.p0) % M] = v;
+        Ls[j] = v;
+        init = nxt;
+      }
+    __syncthreads();  // stage ch % NS is refilled by the issue of iteration ch + 1
+    fence_proxy_async();
   }
 }
 
-// Separator rows against the columns j of a lower separator S' (in S's subtree), part 1: the subtree terms
-// acc(s, j) = a_sj - sum_{k in [t0(S'), p0(S'))} L_sk L_jk, all (s, j) in parallel (they do not depend on
-// each other); part 2 (k_nd_off_sep_blk) continues each chain with S'-internal columns.
-// grid.x = (S, S') pair, threads over the len(S) * len(S') entries.
-__global__ void k_nd_off_sep_dot(const int2 *pairs, const NdBlk *blk, double *Loff) {
-  const NdBlk S = blk[pairs[blockIdx.x].x], Sp = blk[pairs[blockIdx.x].y];
-  const int ne = S.len * Sp.len;
-  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < ne; e += gridDim.y * blockDim.x) {
-    const int s = e / Sp.len, jj = e % Sp.len;
-    double *Ls = Loff + S.off + (long)s * S.rs - S.t0;
-    const double *Lj = Loff + Sp.off + (long)jj * Sp.rs - Sp.t0;
-    Ls[Sp.p0 + jj] = chain_sub(Ls[Sp.p0 + jj], Ls + Sp.t0, 1, Lj + Sp.t0, 1, Sp.p0 - Sp.t0);
-  }
-}
-// part 2: for j in S' ascending: acc -= sum_{k in [p0', j)} L_sk L_jk; L_sj = acc / L_jj.  Thread per (pair, s).
-__global__ void k_nd_off_sep_blk(const int2 *pairs, const NdBlk *blk, int bw, int W, const double *Lrow,
-                                 double *Loff) {
-  const NdBlk S = blk[pairs[blockIdx.x].x], Sp = blk[pairs[blockIdx.x].y];
-  for (int s = threadIdx.x; s < S.len; s += blockDim.x) {
-    double *Ls = Loff + S.off + (long)s * S.rs - S.t0;
-    for (int j = Sp.p0; j < Sp.p0 + Sp.len; j++) {
-      const double *Lj = Lrow + (long)j * W + bw - j;
-      const double acc = chain_sub(Ls[j], Ls + Sp.p0, 1, Lj + Sp.p0, 1, j - Sp.p0);
-      Ls[j] = acc / Lj[j];
+// acc(s, j) = init(s, j) - sum_{k in [k0, k1)} A_sk B_jk (k ascending, C9 chains) for a 32 x 32 tile of
+// (s, j), k in chunks of 32 staged through shared memory; each thread owns a 2 x 2 micro-tile, one chain
+// per entry.  SCHUR: A = B = the separator's rows, lower tile entries j <= s, into the band; else A = rows
+// of S, B = rows of the lower separator S', into Loff.
+template <bool SCHUR>
+__global__ void __launch_bounds__(256) k_nd_gemm(const int2 *pairs, const NdBlk *blk, int bw, int W, double *Lrow,
+                                                 double *Loff) {
+  __shared__ double As[32][33], Bs[32][33];
+  const int2 pr = pairs[blockIdx.x];
+  const NdBlk S = blk[pr.x], Sp = blk[SCHUR ? pr.x : pr.y];
+  const int ti = blockIdx.y, tj = blockIdx.z;  // tile row / column
+  const int s0 = ti * 32, j0 = tj * 32;
+  if (s0 >= S.len || j0 >= Sp.len || (SCHUR && j0 > s0)) return;
+  const int k0 = SCHUR ? S.t0 : Sp.t0, k1 = SCHUR ? S.p0 : Sp.p0;
+  const double *Arow = Loff + S.off - S.t0;    // Arow[s * rs + k] = L_{p0+s, k}
+  const double *Brow = Loff + Sp.off - Sp.t0;  // Brow[j * rs' + k]
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double acc[2][2];
+  auto out = [&](int a, int b) -> double * {  // destination of entry (s0 + 2ty + a, j0 + 2tx + b)
+    const int s = s0 + 2 * ty + a, j = j0 + 2 * tx + b;
+    if (s >= S.len || j >= Sp.len || (SCHUR && j > s)) return nullptr;
+    if (SCHUR) return Lrow + (long)(S.p0 + s) * W + bw - (s - j);
+    return Loff + S.off + (long)s * S.rs + (Sp.p0 + j - S.t0);
+  };
+#pragma unroll
+  for (int a = 0; a < 2; a++)
+#pragma unroll
+    for (int b = 0; b < 2; b++) {
+      double *o = out(a, b);
+      acc[a][b] = o ? *o : 0.0;
+    }
+  for (int kc = k0; kc < k1; kc += 32) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < 32 * 32; e += 256) {
+      const int r = e >> 5, k = e & 31;
+      const bool kin = kc + k < k1;
+      As[k][r] = (kin && s0 + r < S.len) ? Arow[(long)(s0 + r) * S.rs + kc + k] : 0.0;
+      Bs[k][r] = (kin && j0 + r < Sp.len) ? Brow[(long)(j0 + r) * Sp.rs + kc + k] : 0.0;
+    }
+    __syncthreads();
+    const int kn = min(32, k1 - kc);
+    for (int kk = 0; kk < kn; kk++) {
+      const double a0 = As[kk][2 * ty], a1 = As[kk][2 * ty + 1];
+      const double b0 = Bs[kk][2 * tx], b1 = Bs[kk][2 * tx + 1];
+      acc[0][0] = __fma_rn(-a0, b0, acc[0][0]);
+      acc[0][1] = __fma_rn(-a0, b1, acc[0][1]);
+      acc[1][0] = __fma_rn(-a1, b0, acc[1][0]);
+      acc[1][1] = __fma_rn(-a1, b1, acc[1][1]);
     }
   }
-}
-
-// Schur complement of a separator's own block: acc(s, j) = a_sj - sum_{k in [t0, p0)} L_sk L_jk, j <= s,
-// written into the band; the in-block Cholesky continues the chains (k in [p0, j)).
-__global__ void k_nd_schur(const int *ids, const NdBlk *blk, int bw, int W, double *Lrow, const double *Loff) {
-  const NdBlk S = blk[ids[blockIdx.x]];
-  const int ncol = S.p0 - S.t0;
-  const int ne = S.len * S.len;
-  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < ne; e += gridDim.y * blockDim.x) {
-    const int s = e / S.len, j = e % S.len;
-    if (j > s) continue;
-    const long ix = (long)(S.p0 + s) * W + bw - (s - j);
-    const double *Ls = Loff + S.off + (long)s * S.rs, *Lj = Loff + S.off + (long)j * S.rs;
-    Lrow[ix] = chain_sub(Lrow[ix], Ls, 1, Lj, 1, ncol);
-  }
+#pragma unroll
+  for (int a = 0; a < 2; a++)
+#pragma unroll
+    for (int b = 0; b < 2; b++) {
+      double *o = out(a, b);
+      if (o) *o = acc[a][b];
+    }
 }
 
 // Forward, separator rows: acc_s = v_s - sum_{k in [t0, p0)} L_sk w_k (ascending k), into accbuf.
@@ -403,6 +459,9 @@ void nd_symbolic(Ctx &c) {
     Lv.groups = upload(c, groups);
     Lv.count = (int)ids.size();
     Lv.ids = upload(c, ids);
+    std::vector<int> self;
+    for (int b : ids) { self.push_back(b); self.push_back(b); c.nd_maxsep = std::max(c.nd_maxsep, E.blk[b].len); }
+    Lv.selfpairs = upload(c, self);
     Lv.p0 = upload(c, p0);
     Lv.len = upload(c, len);
     Lv.sub_ptr = upload(c, sptr);
@@ -444,6 +503,21 @@ void nd_symbolic(Ctx &c) {
   c.nd_sep_blocks = upload(c, sep_blocks);
 }
 
+static void launch_off_band(Ctx &c, int np, const int *pairs, const NdBlk *blk, int bw, int W) {
+  if (!np) return;
+  const int M = bw | 1;  // ring length >= bw, odd (bank-conflict-free rows)
+  const int threads = (c.nd_maxsep + 31) / 32 * 32;
+  const size_t smem = ((((size_t)c.nd_maxsep * M + 15) & ~(size_t)15) + (size_t)OB_NS * OB_RC * W) * sizeof(double);
+  REQUIRE(threads <= 1024 && smem <= 227 * 1024, AMGF_ERR_LIMIT, "separator too wide for the off-block factor kernel");
+  static size_t attr = 0;
+  if (smem > attr) {
+    CK(cudaFuncSetAttribute(k_nd_off_band, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  k_nd_off_band<<<np, threads, smem, c.stream>>>((const int2 *)pairs, blk, bw, W, M, c.Lrow, c.Loff);
+  after_launch(c, "k_nd_off_band");
+}
+
 void nd_numeric(Ctx &c) {
   const int nc = c.nc, bw = c.bw, W = band_stride(bw);
   const NdBlk *blk = (const NdBlk *)c.nd_blk;
@@ -457,8 +531,7 @@ void nd_numeric(Ctx &c) {
   // leaves (independent), then separator-vs-leaf columns (independent given the leaves)
   band_factor_blocks(c, nc, c.nd_nleaves, c.nd_leaf_p0, c.nd_leaf_len, bw, c.Lrow, 1);
   if (c.nd_npairs) {
-    k_nd_off_leaf<<<c.nd_npairs, 128, 0, c.stream>>>((const int2 *)c.nd_pairs, blk, bw, W, c.Lrow, c.Loff);
-    after_launch(c, "k_nd_off_leaf");
+    launch_off_band(c, c.nd_npairs, c.nd_pairs, blk, bw, W);
   }
   // separators bottom-up; for a separator S at level l, its lower separators S' (depth d > l) in postorder
   // (deepest first), each in two parts (subtree terms in parallel, then the S'-internal chain)
@@ -468,15 +541,16 @@ void nd_numeric(Ctx &c) {
     for (int d = c.nd_depth - 1; d > l; d--) {
       const int np = c.nd_sspairs_n[l][d];
       if (!np) continue;
-      dim3 g1(np, 16);
-      k_nd_off_sep_dot<<<g1, 256, 0, c.stream>>>((const int2 *)c.nd_sspairs[l][d], blk, c.Loff);
-      after_launch(c, "k_nd_off_sep_dot");
-      k_nd_off_sep_blk<<<np, 256, 0, c.stream>>>((const int2 *)c.nd_sspairs[l][d], blk, bw, W, c.Lrow, c.Loff);
-      after_launch(c, "k_nd_off_sep_blk");
+      const int nt = (c.nd_maxsep + 31) / 32;
+      dim3 g1(np, nt, nt);
+      k_nd_gemm<false><<<g1, 256, 0, c.stream>>>((const int2 *)c.nd_sspairs[l][d], blk, bw, W, c.Lrow, c.Loff);
+      after_launch(c, "k_nd_gemm");
+      launch_off_band(c, np, c.nd_sspairs[l][d], blk, bw, W);
     }
-    dim3 g2(Lv.count, 16);
-    k_nd_schur<<<g2, 256, 0, c.stream>>>(Lv.ids, blk, bw, W, c.Lrow, c.Loff);
-    after_launch(c, "k_nd_schur");
+    const int nt = (c.nd_maxsep + 31) / 32;
+    dim3 g2(Lv.count, nt, nt);
+    k_nd_gemm<true><<<g2, 256, 0, c.stream>>>((const int2 *)Lv.selfpairs, blk, bw, W, c.Lrow, c.Loff);
+    after_launch(c, "k_nd_gemm");
     band_factor_blocks(c, nc, Lv.count, Lv.p0, Lv.len, bw, c.Lrow, 1);
   }
   band_finish(c, nc, bw, c.Lrow, c.Lcol, c.Lrev, c.Ldinv);
