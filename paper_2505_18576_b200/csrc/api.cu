@@ -5,7 +5,9 @@
 //   apply_M  x1 = B r; r1 = r - S x1; y = A_w^{-1} r1[Z]; x2 = x1 + P y; r2 = r1 - S[:,Z] y;
 //            z = x2 + B r2  (Def. AMGF; three stages SPEC.md:245; C11).
 //   pcg      PAPER.md:368 (relative preconditioned residual), C15.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -133,6 +135,14 @@ void apply_M(Ctx &c, const double *r, double *z) {
     int lo = 0, hi = 0;
     CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CK(cudaStreamCreateWithPriority(&c.fstream, cudaStreamNonBlocking, hi));
+    // SM partition for the overlap: the residual SpMV runs on ~65 % of the SMs (96 of 148 measured best at
+    // cfg 3: it still ends first, ~230 us, while the A_w solve gets SMs of its own; the A_w solve alone takes
+    // 279 us, 326 us next to the partitioned SpMV, 383 us next to the unpartitioned one).  An L2 persistence
+    // window for the A_w data was measured too and did not help (it costs the V-cycles L2 capacity).
+    int dev = 0, nsm = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    c.resid_sms = std::max(1, nsm * 96 / 148);
     CK(cudaEventCreateWithFlags(&c.ev_f0, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c.ev_f1, cudaEventDisableTiming));
   }
@@ -153,7 +163,15 @@ void apply_M(Ctx &c, const double *r, double *z) {
   }
   CK(cudaEventRecord(c.ev_f1, c.fstream));
   if (te[0]) CK(cudaEventRecord(te[1], c.fstream));
-  launch_sell_spmv(c, L0.As, SPMV_RESID, c.w_x1, r, nullptr, nullptr, c.w_r1, nullptr);
+  static const bool no_overlap = getenv("AMGF_NO_OVERLAP") != nullptr;  // A/B experiments
+  if (no_overlap) CK(cudaStreamWaitEvent(c.stream, c.ev_f1, 0));
+  {
+    // 180 KB of shared memory reserved per CTA: no filter CTA (>= 49 KB) fits beside it
+    static const int spmv_sms = getenv("AMGF_SPMV_SMS") ? atoi(getenv("AMGF_SPMV_SMS")) : -1;  // A/B only
+    const int n_sms = spmv_sms >= 0 ? spmv_sms : c.resid_sms;
+    if (n_sms > 0) launch_resid_partition(c, L0.As, c.w_x1, r, c.w_r1, n_sms, 180 * 1024);
+    else launch_sell_spmv(c, L0.As, SPMV_RESID, c.w_x1, r, nullptr, nullptr, c.w_r1, nullptr);
+  }
   if (te[0]) CK(cudaEventRecord(te[2], c.stream));
   CK(cudaStreamWaitEvent(c.stream, c.ev_f1, 0));
   if (te[0]) {

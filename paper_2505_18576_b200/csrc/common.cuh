@@ -102,6 +102,9 @@ struct Ctx {
   cudaStream_t fstream = nullptr;
   cudaEvent_t ev_f0 = nullptr, ev_f1 = nullptr;
   double *rz = nullptr;
+  double *nd_arena = nullptr;  // filter solve data (filter.cu) in one range
+  size_t nd_arena_bytes = 0;
+  int resid_sms = 0;           // SMs of the residual SpMV that runs beside the A_w solve
   amgf_config cfg;
   int nodes = 0, m = 0;
   long n = 0;
@@ -229,6 +232,8 @@ void nd_symbolic(Ctx &c);
 void nd_numeric(Ctx &c);
 void nd_solve(Ctx &c, const double *r1, const int *gather);  // c.fv <- A_w^{-1} r1 (pi order; r1[gather[p]])
 void nd_scatter(Ctx &c, double *x2);                          // x2[Z] += y (c.fv)
+void launch_resid_partition(Ctx &c, const Sell &A, const double *x, const double *b, double *y, int nsm,
+                            size_t reserve);
 void launch_resid_dofs(Ctx &c, const Sell &A, int n, const int *dof, const double *x, const double *b, double *out);
 void nd_remap_positions(Ctx &c, int *pos_z, long n);  // Z positions -> pi positions
 void band_factor_blocks(Ctx &c, int n, int nblocks, const int *d_p0, const int *d_len, int bw, double *Lrow, int tag);

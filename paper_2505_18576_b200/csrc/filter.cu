@@ -17,16 +17,10 @@
 
 #include "common.cuh"
 #include "devutil.cuh"
+#include "nd_kernels.cuh"
 
 namespace amgf {
 
-struct NdBlk {
-  int p0, len, kind;  // kind 0 = leaf, 1 = separator
-  int t0;             // separator: first pi position of its subtree
-  long off;           // separator: offset of its rows in Loff (row-major: s * rs + (k - t0))
-  int level;          // separator depth (root 0)
-  int rs;             // separator: row stride of its rows in Loff (p0 - t0 rounded up to even)
-};
 
 namespace {
 
@@ -279,84 +273,16 @@ __global__ void __launch_bounds__(256) k_nd_gemm(const int2 *pairs, const NdBlk 
     }
 }
 
-// Forward, separator rows: acc_s = v_s - sum_{k in [t0, p0)} L_sk w_k (ascending k), into accbuf.
-// One warp per group of 32 rows of a separator (so a separator's rows stream through several SMs); lane l
-// owns row row0 + l.  Chunks of SF_KC columns of the 32 rows (row-major; lane q copies the q-th 16-byte piece
-// of every row) and the matching w values go through an NS-deep cp.async ring (padded smem rows).
-constexpr int SF_KC = 64, SF_LD = SF_KC + 2;
-constexpr size_t sf_smem(int G, int NS) { return (size_t)NS * (G * SF_LD + SF_KC) * sizeof(double); }
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem));
-}
-
-template <int G, int NS>
-__global__ void __launch_bounds__(32) k_nd_sep_fwd(const int2 *groups, const NdBlk *blk, const double *Loff,
-                                                   const double *r1, const int *dof, const double *w,
-                                                   const double *w2, double *accbuf) {
-  extern __shared__ __align__(16) double sfm[];  // [NS][G * SF_LD] rows, then [NS][SF_KC] w
-  const NdBlk S = blk[groups[blockIdx.x].x];
-  const int row0 = groups[blockIdx.x].y;
-  const int lane = threadIdx.x;
-  const int nrow = min(G, S.len - row0);
-  const int ncol = S.p0 - S.t0;
-  const int nch = (ncol + SF_KC - 1) / SF_KC;
-  double *sW = sfm + NS * G * SF_LD;
-  const double *wsrc = (S.t0 & 1) ? w2 + S.t0 + 1 : w + S.t0;  // 16-byte aligned view of w[t0 + k]
-  const double *Lq = Loff + S.off + (long)row0 * S.rs + 2 * lane;  // this lane's piece of row 0
-  auto issue = [&](int c) {
-    if (c < nch) {
-      const int k0 = c * SF_KC, st = c % NS;
-      if (2 * lane < ncol - k0) {  // the even row stride covers an odd tail element
-        const double *src = Lq + k0;
-        double *dst = sfm + st * G * SF_LD + 2 * lane;
-        for (int r = 0; r < nrow; r++) cp_async16(dst + r * SF_LD, src + (long)r * S.rs);
-      }
-      cp_async16(sW + st * SF_KC + 2 * lane, wsrc + k0 + 2 * lane);
-    }
-    asm volatile("cp.async.commit_group;");
-  };
-#pragma unroll
-  for (int c = 0; c < NS - 1; c++) issue(c);
-  const int prow = S.p0 + row0 + lane;
-  double acc = (lane < nrow) ? r1[dof ? dof[prow] : prow] : 0.0;
-  const int me = min(lane, G - 1);
-  for (int c = 0; c < nch; c++) {
-    issue(c + NS - 1);
-    asm volatile("cp.async.wait_group %0;" ::"n"(NS - 1));
-    __syncwarp();
-    const int st = c % NS;
-    const double *buf = sfm + st * G * SF_LD + me * SF_LD;
-    const double *wb = sW + st * SF_KC;
-    const int kn = min(SF_KC, ncol - c * SF_KC);
-    if (kn == SF_KC) {
-#pragma unroll
-      for (int kk = 0; kk < SF_KC; kk += 2) {
-        const double2 a = *(const double2 *)(buf + kk), b = *(const double2 *)(wb + kk);
-        acc = __fma_rn(-a.x, b.x, acc);
-        acc = __fma_rn(-a.y, b.y, acc);
-      }
-    } else {
-      for (int kk = 0; kk < kn; kk++) acc = __fma_rn(-buf[kk], wb[kk], acc);
-    }
-    __syncwarp();  // stage st is refilled by the issue of iteration c + 1
-  }
-  asm volatile("cp.async.wait_group 0;");
-  if (lane < nrow) accbuf[S.p0 + row0 + lane] = acc;
-}
-
 typedef void (*SepFwdFn)(const int2 *, const NdBlk *, const double *, const double *, const int *, const double *,
                          const double *, double *);
 struct SepFwdVariant {
   int G, NS;
   SepFwdFn fn;
 };
-static const SepFwdVariant kSepFwd[] = {{32, 4, k_nd_sep_fwd<32, 4>},  {32, 8, k_nd_sep_fwd<32, 8>},
-                                        {32, 12, k_nd_sep_fwd<32, 12>}, {16, 8, k_nd_sep_fwd<16, 8>},
-                                        {16, 16, k_nd_sep_fwd<16, 16>}, {8, 8, k_nd_sep_fwd<8, 8>},
-                                        {8, 16, k_nd_sep_fwd<8, 16>},   {4, 16, k_nd_sep_fwd<4, 16>},
-                                        {4, 24, k_nd_sep_fwd<4, 24>},   {2, 16, k_nd_sep_fwd<2, 16>}};
-constexpr int kSepFwdDefault = 7;  // G = 4, NS = 16: measured best with 5 and 9 (tools/time_apply.py)
+// measured variants (tools/mb_sepfwd.cu); the first is used unless AMGF_SF_VARIANT selects another
+static const SepFwdVariant kSepFwd[] = {{1, 6, k_nd_sep_fwd<1, 6, SF_KC>}, {2, 6, k_nd_sep_fwd<2, 6, SF_KC>},
+                                        {4, 4, k_nd_sep_fwd<4, 4, SF_KC>}};
+constexpr int kSepFwdDefault = 0;
 
 static int sep_fwd_variant() {
   static int v = -1;
@@ -368,19 +294,38 @@ static int sep_fwd_variant() {
     }
     const SepFwdVariant &V = kSepFwd[v];
     CK(cudaFuncSetAttribute((const void *)V.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)sf_smem(V.G, V.NS)));
+                            (int)sf_smem(V.G, V.NS, SF_KC)));
   }
   return v;
 }
 
 // Backward, subtree rows of a separator: acc_k -= sum_{s descending} L_sk x_s (chain continues in w).
-__global__ void k_nd_sep_bwd(const int *ids, const NdBlk *blk, const double *Loff, const double *x, double *w) {
+// One CTA per SB_TR consecutive subtree rows: the separator's len x SB_TR tile of L (row-major, 16-byte
+// pieces) and x_S are staged with cp.async in one round trip, then thread k runs its chain from shared
+// memory (the former thread-per-row form with an 8-deep register prefetch from HBM took 17 us per level).
+constexpr int SB_TR = 64;
+__global__ void __launch_bounds__(SB_TR) k_nd_sep_bwd(const int *ids, const NdBlk *blk, const double *Loff,
+                                                      const double *x, double *w) {
+  extern __shared__ __align__(16) double sbt[];  // [len][SB_TR] tile, then x_S [len]
   const NdBlk S = blk[ids[blockIdx.y]];
-  const int k = S.t0 + blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= S.p0) return;
-  const double *Lk = Loff + S.off + (k - S.t0);  // Lk[s * rs] = L_{p0+s, k}
-  // s descending: start at the last row and step backwards
-  w[k] = chain_sub(w[k], Lk + (long)(S.len - 1) * S.rs, -(long)S.rs, x + S.p0 + S.len - 1, -1, S.len);
+  const int k0 = S.t0 + blockIdx.x * SB_TR;
+  if (k0 >= S.p0) return;
+  const int nk = min(SB_TR, S.p0 - k0), tid = threadIdx.x;
+  double *sx = sbt + (long)S.len * SB_TR;
+  const double *src = Loff + S.off + (k0 - S.t0);  // 16-byte aligned: off, rs and k0 - t0 are even
+  for (int idx = tid; idx < S.len * (SB_TR / 2); idx += SB_TR) {
+    const int sr = idx / (SB_TR / 2), p = idx % (SB_TR / 2);
+    if (2 * p < nk) cp_async16(sbt + sr * SB_TR + 2 * p, src + (long)sr * S.rs + 2 * p);
+  }
+  asm volatile("cp.async.commit_group;");
+  for (int sr = tid; sr < S.len; sr += SB_TR) sx[sr] = x[S.p0 + sr];
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  if (tid < nk) {
+    double acc = w[k0 + tid];
+    for (int sr = S.len - 1; sr >= 0; sr--) acc = __fma_rn(-sbt[sr * SB_TR + tid], sx[sr], acc);
+    w[k0 + tid] = acc;
+  }
 }
 
 __global__ void k_nd_scatter(int nc, const int *dof, const double *y, double *x2) {
@@ -486,19 +431,26 @@ void nd_symbolic(Ctx &c) {
   // storage
   const int W = band_stride(bw);
   const size_t total = (size_t)(nc + 2 * BAND_PAD_ROWS) * W;
-  double *r = c.alloc<double>(total), *cl = c.alloc<double>(total), *rv = c.alloc<double>(total);
-  CK(cudaMemsetAsync(cl, 0, total * sizeof(double), c.stream));
-  CK(cudaMemsetAsync(rv, 0, total * sizeof(double), c.stream));
+  double *r = c.alloc<double>(total);
   CK(cudaMemsetAsync(r, 0, total * sizeof(double), c.stream));
   c.Lrow = r + (size_t)BAND_PAD_ROWS * W;
-  c.Lcol = cl + (size_t)BAND_PAD_ROWS * W;
-  c.Lrev = rv + (size_t)BAND_PAD_ROWS * W;
-  c.Ldinv = c.alloc<double>(nc);
-  c.Loff = c.alloc<double>(std::max(off, 1L));
-  c.fv = c.alloc<double>(nc);
-  c.rz = c.alloc<double>(nc);
-  c.fw = c.alloc<double>(nc + SF_KC + 4);
-  c.fw2 = c.alloc<double>(nc + SF_KC + 4);
+  // Everything the solve reads (the two band copies, the separator rows, 1/L_ii and the work vectors) in
+  // one arena (one range for tools and for an L2 access-policy window; measured without benefit so far).
+  auto al = [](size_t n) { return (n + 31) & ~(size_t)31; };  // 256-byte alignment
+  const size_t n_band = al(total), n_off = al(off + 2), n_vec = al(nc), n_w = al(nc + SF_KC + 4);
+  const size_t arena = 2 * n_band + n_off + 3 * n_vec + 2 * n_w;
+  double *A = c.alloc<double>(arena);
+  c.nd_arena = A;
+  c.nd_arena_bytes = arena * sizeof(double);
+  CK(cudaMemsetAsync(A, 0, 2 * n_band * sizeof(double), c.stream));
+  c.Lcol = A + (size_t)BAND_PAD_ROWS * W;
+  c.Lrev = A + n_band + (size_t)BAND_PAD_ROWS * W;
+  c.Loff = A + 2 * n_band;  // +2: the 16-byte staging of an odd row tail may read one past the end
+  c.Ldinv = c.Loff + n_off;
+  c.fv = c.Ldinv + n_vec;
+  c.rz = c.fv + n_vec;
+  c.fw = c.rz + n_vec;
+  c.fw2 = c.fw + n_w;
   c.nd_nsep = (int)sep_blocks.size();
   c.nd_sep_blocks = upload(c, sep_blocks);
 }
@@ -572,18 +524,26 @@ void nd_solve(Ctx &c, const double *r1, const int *gather) {
     Ctx::NdLevel &Lv = c.nd_lev[l];
     if (!Lv.count) continue;
     const SepFwdVariant &V = kSepFwd[sep_fwd_variant()];
-    V.fn<<<Lv.ngroups, 32, sf_smem(V.G, V.NS), c.stream>>>((const int2 *)Lv.groups, blk, c.Loff, r1, gather, w,
+    V.fn<<<Lv.ngroups, 32, sf_smem(V.G, V.NS, SF_KC), c.stream>>>((const int2 *)Lv.groups, blk, c.Loff, r1, gather, w,
                                                            c.fw2, y);
     after_launch(c, "k_nd_sep_fwd");
     launch_band_sweep(c, Lv.count, Lv.p0, Lv.len, nc, bw, true, c.Lcol, c.Lrev, c.Ldinv, y, nullptr, w, c.fw2);
   }
   // backward: separators top-down (then their subtree rows), then leaves
+  const size_t sb_smem = (size_t)c.nd_maxsep * (SB_TR + 1) * sizeof(double);
+  {
+    static size_t attr = 0;
+    if (sb_smem > attr && sb_smem > 48 * 1024) {
+      CK(cudaFuncSetAttribute(k_nd_sep_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb_smem));
+      attr = sb_smem;
+    }
+  }
   for (int l = 0; l < c.nd_depth; l++) {
     Ctx::NdLevel &Lv = c.nd_lev[l];
     if (!Lv.count) continue;
     launch_band_sweep(c, Lv.count, Lv.p0, Lv.len, nc, bw, false, c.Lcol, c.Lrev, c.Ldinv, w, nullptr, y);
-    dim3 grid((nc + 127) / 128, Lv.count);
-    k_nd_sep_bwd<<<grid, 128, 0, c.stream>>>(Lv.ids, blk, c.Loff, y, w);
+    dim3 grid((nc + SB_TR - 1) / SB_TR, Lv.count);
+    k_nd_sep_bwd<<<grid, SB_TR, sb_smem, c.stream>>>(Lv.ids, blk, c.Loff, y, w);
     after_launch(c, "k_nd_sep_bwd");
   }
   launch_band_sweep(c, c.nd_nleaves, c.nd_leaf_p0, c.nd_leaf_len, nc, bw, false, c.Lcol, c.Lrev, c.Ldinv, w, nullptr,

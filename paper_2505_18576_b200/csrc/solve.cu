@@ -44,19 +44,17 @@ __device__ __forceinline__ double cta_tree(double v, double *s) {
 enum { MODE_Y = SPMV_Y, MODE_RESID = SPMV_RESID, MODE_SMOOTH = SPMV_SMOOTH, MODE_DOT = SPMV_DOT,
        MODE_SMOOTH_ADD = SPMV_SMOOTH_ADD, MODE_ADDTO = 5 };
 
-template <int BR, int BC, int MODE>
-__global__ void __launch_bounds__(CTA) k_sell(int nrows, const int *__restrict__ slice_ptr,
-                                              const int *__restrict__ rowlen, const int *__restrict__ col,
-                                              const double *__restrict__ val, const double *__restrict__ x,
-                                              const double *__restrict__ b, const double *__restrict__ d,
-                                              const double *__restrict__ add, double *__restrict__ y,
-                                              double *__restrict__ dot_part, const int *__restrict__ perm) {
-  const int row = blockIdx.x * CTA + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  double acc[BR];
+// The SELL row chain of one block row (C2): acc[r] = sum over slots s (ascending) and block columns e
+// (ascending) of val * x, software-pipelined (slot s+1's column, values and x gather in flight while slot s
+// is consumed).
+template <int BR, int BC>
+__device__ __forceinline__ void sell_row(int row, const int *__restrict__ slice_ptr, const int *__restrict__ rowlen,
+                                         const int *__restrict__ col, const double *__restrict__ val,
+                                         const double *__restrict__ x, double (&acc)[BR]) {
+  const int lane = row & 31;
 #pragma unroll
   for (int r = 0; r < BR; r++) acc[r] = 0.0;
-  if (row < nrows) {
+  {
     const int len = rowlen[row];
     const long base = slice_ptr[row >> 5];
     const int *cp = col + base * 32 + lane;
@@ -93,6 +91,20 @@ __global__ void __launch_bounds__(CTA) k_sell(int nrows, const int *__restrict__
       cnext = cnn;
     }
   }
+}
+
+template <int BR, int BC, int MODE>
+__global__ void __launch_bounds__(CTA) k_sell(int nrows, const int *__restrict__ slice_ptr,
+                                              const int *__restrict__ rowlen, const int *__restrict__ col,
+                                              const double *__restrict__ val, const double *__restrict__ x,
+                                              const double *__restrict__ b, const double *__restrict__ d,
+                                              const double *__restrict__ add, double *__restrict__ y,
+                                              double *__restrict__ dot_part, const int *__restrict__ perm) {
+  const int row = blockIdx.x * CTA + threadIdx.x;
+  double acc[BR];
+#pragma unroll
+  for (int r = 0; r < BR; r++) acc[r] = 0.0;
+  if (row < nrows) sell_row<BR, BC>(row, slice_ptr, rowlen, col, val, x, acc);
   if (MODE == MODE_DOT) {
     __shared__ double red[CTA];
     double s = 0.0;
@@ -245,6 +257,39 @@ void launch_prolong(Ctx &c, const Sell &P, const double *xc, double *x) {
   else if (P.br == 1) sell_dispatch<1, 6>(c, P, MODE_ADDTO, xc, nullptr, nullptr, nullptr, x, nullptr);
   else if (P.br == 6) sell_dispatch<6, 6>(c, P, MODE_ADDTO, xc, nullptr, nullptr, nullptr, x, nullptr);
   else throw Error{AMGF_ERR_ARG, "prolong: unsupported block shape"};
+}
+
+// Residual y = b - S x on a partition of the SMs: a grid-stride loop over block rows in CTAs of 1024
+// threads that each reserve most of an SM's shared memory, so the grid (one CTA per SM, fewer CTAs than
+// SMs) leaves whole SMs free for the A_w solve running concurrently on the filter stream (apply_M).  Same
+// row chain as k_sell (C2).
+template <int BR, int BC>
+__global__ void __launch_bounds__(1024) k_sell_resid_part(int nrows, const int *__restrict__ slice_ptr,
+                                                          const int *__restrict__ rowlen, const int *__restrict__ col,
+                                                          const double *__restrict__ val,
+                                                          const double *__restrict__ x,
+                                                          const double *__restrict__ b, double *__restrict__ y) {
+  for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < nrows; row += gridDim.x * blockDim.x) {
+    double acc[BR];
+    sell_row<BR, BC>(row, slice_ptr, rowlen, col, val, x, acc);
+#pragma unroll
+    for (int r = 0; r < BR; r++) {
+      const long i = (long)row * BR + r;
+      y[i] = b[i] - acc[r];
+    }
+  }
+}
+
+void launch_resid_partition(Ctx &c, const Sell &A, const double *x, const double *b, double *y, int nsm,
+                            size_t reserve) {
+  REQUIRE(A.br == 3 && A.bc == 3 && !A.perm, AMGF_ERR_ARG, "resid_partition: fine-level 3x3 SELL expected");
+  static size_t attr = 0;
+  if (reserve > attr) {
+    CK(cudaFuncSetAttribute(k_sell_resid_part<3, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reserve));
+    attr = reserve;
+  }
+  k_sell_resid_part<3, 3><<<nsm, 1024, reserve, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, y);
+  after_launch(c, "k_sell_resid_part");
 }
 
 // Residual b - S x at the dofs dof[p] only (p < n), into out[p]: the same SELL chain as k_sell<3,3> for
