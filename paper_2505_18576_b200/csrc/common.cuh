@@ -184,6 +184,25 @@ struct Ctx {
 
 inline int nblk(long n, int t = CTA) { return (int)((n + t - 1) / t); }
 
+// Launch with programmatic dependent launch (PDL) on c.stream: the kernel may start while the previous
+// kernel of the stream is finishing; it must call pdl_wait() (devutil.cuh) before reading that kernel's
+// results.  Used for the chain of small latency-bound kernels of the A_w solve.
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(cudaStream_t st, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, ((KArgs)args)...);
+  if (e != cudaSuccess) throw Error{AMGF_ERR_CUDA, std::string("cudaLaunchKernelEx (PDL): ") + cudaGetErrorString(e)};
+}
+
 // Post-launch bookkeeping: count the launch, surface launch errors; with AMGF_DEBUG_SYNC=1 in the
 // environment also synchronise and name the kernel that faulted.
 bool debug_sync();

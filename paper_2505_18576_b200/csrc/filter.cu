@@ -307,6 +307,7 @@ constexpr int SB_TR = 64;
 __global__ void __launch_bounds__(SB_TR) k_nd_sep_bwd(const int *ids, const NdBlk *blk, const double *Loff,
                                                       const double *x, double *w) {
   extern __shared__ __align__(16) double sbt[];  // [len][SB_TR] tile, then x_S [len]
+  pdl_launch_dependents();
   const NdBlk S = blk[ids[blockIdx.y]];
   const int k0 = S.t0 + blockIdx.x * SB_TR;
   if (k0 >= S.p0) return;
@@ -318,6 +319,7 @@ __global__ void __launch_bounds__(SB_TR) k_nd_sep_bwd(const int *ids, const NdBl
     if (2 * p < nk) cp_async16(sbt + sr * SB_TR + 2 * p, src + (long)sr * S.rs + 2 * p);
   }
   asm volatile("cp.async.commit_group;");
+  pdl_wait();  // the factor tile above does not depend on the previous kernel; x_S and w do
   for (int sr = tid; sr < S.len; sr += SB_TR) sx[sr] = x[S.p0 + sr];
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
@@ -524,8 +526,8 @@ void nd_solve(Ctx &c, const double *r1, const int *gather) {
     Ctx::NdLevel &Lv = c.nd_lev[l];
     if (!Lv.count) continue;
     const SepFwdVariant &V = kSepFwd[sep_fwd_variant()];
-    V.fn<<<Lv.ngroups, 32, sf_smem(V.G, V.NS, SF_KC), c.stream>>>((const int2 *)Lv.groups, blk, c.Loff, r1, gather, w,
-                                                           c.fw2, y);
+    launch_pdl(c.stream, V.fn, dim3(Lv.ngroups), dim3(32), sf_smem(V.G, V.NS, SF_KC), (const int2 *)Lv.groups, blk,
+               (const double *)c.Loff, r1, gather, (const double *)w, (const double *)c.fw2, y);
     after_launch(c, "k_nd_sep_fwd");
     launch_band_sweep(c, Lv.count, Lv.p0, Lv.len, nc, bw, true, c.Lcol, c.Lrev, c.Ldinv, y, nullptr, w, c.fw2);
   }
@@ -543,7 +545,8 @@ void nd_solve(Ctx &c, const double *r1, const int *gather) {
     if (!Lv.count) continue;
     launch_band_sweep(c, Lv.count, Lv.p0, Lv.len, nc, bw, false, c.Lcol, c.Lrev, c.Ldinv, w, nullptr, y);
     dim3 grid((nc + SB_TR - 1) / SB_TR, Lv.count);
-    k_nd_sep_bwd<<<grid, SB_TR, sb_smem, c.stream>>>(Lv.ids, blk, c.Loff, y, w);
+    launch_pdl(c.stream, k_nd_sep_bwd, grid, dim3(SB_TR), sb_smem, (const int *)Lv.ids, blk, (const double *)c.Loff,
+               (const double *)y, w);
     after_launch(c, "k_nd_sep_bwd");
   }
   launch_band_sweep(c, c.nd_nleaves, c.nd_leaf_p0, c.nd_leaf_len, nc, bw, false, c.Lcol, c.Lrev, c.Ldinv, w, nullptr,

@@ -3,6 +3,8 @@
 #pragma once
 #include <stdint.h>
 
+#include "devutil.cuh"
+
 namespace amgf {
 
 struct NdBlk {
@@ -33,6 +35,7 @@ __global__ void __launch_bounds__(32) k_nd_sep_fwd(const int2 *groups, const NdB
                                                    const double *w2, double *accbuf) {
   constexpr int LD = KC + 2;
   extern __shared__ __align__(16) double sfm[];  // [NS][G * LD] rows, then [NS][KC] w
+  pdl_launch_dependents();
   const NdBlk S = blk[groups[blockIdx.x].x];
   const int row0 = groups[blockIdx.x].y;
   const int lane = threadIdx.x;
@@ -42,21 +45,37 @@ __global__ void __launch_bounds__(32) k_nd_sep_fwd(const int2 *groups, const NdB
   double *sW = sfm + NS * G * LD;
   const double *wsrc = (S.t0 & 1) ? w2 + S.t0 + 1 : w + S.t0;  // 16-byte aligned view of w[t0 + k]
   const double *Lq = Loff + S.off + (long)row0 * S.rs;
-  auto issue = [&](int c) {
+  auto issue_L = [&](int c) {
     if (c < nch) {
       const int k0 = c * KC, st = c % NS;
-      for (int p = lane; p < KC / 2; p += 32) {
+      for (int p = lane; p < KC / 2; p += 32)
         if (2 * p < ncol - k0) {  // the even row stride covers an odd tail element
           double *dst = sfm + st * G * LD + 2 * p;
           for (int r = 0; r < nrow; r++) cp_async16(dst + r * LD, Lq + (long)r * S.rs + k0 + 2 * p);
         }
-        cp_async16(sW + st * KC + 2 * p, wsrc + k0 + 2 * p);
-      }
     }
+  };
+  auto issue_w = [&](int c) {
+    if (c < nch) {
+      const int k0 = c * KC, st = c % NS;
+      for (int p = lane; p < KC / 2; p += 32) cp_async16(sW + st * KC + 2 * p, wsrc + k0 + 2 * p);
+    }
+  };
+  auto issue = [&](int c) {
+    issue_L(c);
+    issue_w(c);
     asm volatile("cp.async.commit_group;");
   };
+  // The factor rows of the first NS-1 chunks do not depend on the previous kernel (PDL): they are issued
+  // before the wait and land in group 0 with w of chunk 0; groups 1..NS-2 hold w of chunks 1..NS-2.
 #pragma unroll
-  for (int c = 0; c < NS - 1; c++) issue(c);
+  for (int c = 0; c < NS - 1; c++) issue_L(c);
+  pdl_wait();
+#pragma unroll
+  for (int c = 0; c < NS - 1; c++) {
+    issue_w(c);
+    asm volatile("cp.async.commit_group;");
+  }
   const int prow = S.p0 + row0 + lane;
   double acc = (lane < nrow) ? r1[dof ? dof[prow] : prow] : 0.0;
   const int me = min(lane, G - 1);

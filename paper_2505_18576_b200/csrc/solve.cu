@@ -745,16 +745,16 @@ static void sweep_RN(Ctx &c, int nblocks, const int *p0, const int *len, int bw,
                               (int)smem));
       attr_f = true;
     }
-    k_band_sweep<R, NB, true, BLOCKED><<<nblocks, 32, smem, c.stream>>>(p0, len, bw, Lcol, Lrev, dinv, in, gather,
-                                                                         out, out_shift);
+    launch_pdl(c.stream, k_band_sweep<R, NB, true, BLOCKED>, dim3(nblocks), dim3(32), smem, p0, len, bw, Lcol, Lrev,
+               dinv, in, gather, out, out_shift);
   } else {
     if (!attr_b) {
       CK(cudaFuncSetAttribute(k_band_sweep<R, NB, false, BLOCKED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)smem));
       attr_b = true;
     }
-    k_band_sweep<R, NB, false, BLOCKED><<<nblocks, 32, smem, c.stream>>>(p0, len, bw, Lcol, Lrev, dinv, in, gather,
-                                                                          out, out_shift);
+    launch_pdl(c.stream, k_band_sweep<R, NB, false, BLOCKED>, dim3(nblocks), dim3(32), smem, p0, len, bw, Lcol,
+               Lrev, dinv, in, gather, out, out_shift);
   }
 }
 
