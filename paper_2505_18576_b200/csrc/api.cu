@@ -33,6 +33,9 @@ Ctx::~Ctx() {
   drop_caches(*this);
   for (auto &g : pcg_graph)
     if (g) cudaGraphExecDestroy(g);
+  for (auto &g : pcg_loop)
+    if (g) cudaGraphExecDestroy(g);
+  if (loop_host) cudaFreeHost(loop_host);
   if (gstream) cudaStreamDestroy(gstream);
   if (ev_in) cudaEventDestroy(ev_in);
   if (ev_out) cudaEventDestroy(ev_out);
@@ -193,7 +196,7 @@ void apply_M(Ctx &c, const double *r, double *z) {
 // rho' = r.z and beta, p = z + beta p, then the scalars and the error flag to pinned host memory.  The
 // p update of the final iteration is harmless (p is not used afterwards).  All pointers are the handle's
 // own buffers, so the body is captured once into a CUDA graph and replayed (values change, pointers do not).
-static void pcg_body(Ctx &c, int precond) {
+static void pcg_body(Ctx &c, int precond, bool host_copies = true) {
   const long n = c.n;
   launch_sell_spmv(c, c.lev[0].As, SPMV_DOT, c.p, nullptr, nullptr, nullptr, c.q, c.dot_part);
   launch_dot_finish(c, nblk(c.lev[0].As.nrows), DOT_PI);  // pi = p.q, alpha = rho / pi
@@ -202,8 +205,72 @@ static void pcg_body(Ctx &c, int precond) {
   else vcycle(c, 0, c.rr, c.zz, nullptr);
   launch_dot(c, n, 3, c.rr, c.zz, DOT_RHO1);             // rho' = r.z, beta = rho'/rho, rho = rho'
   launch_xpby(c, n, c.zz, c.p);
-  CK(cudaMemcpyAsync(c.sc_host, c.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, c.stream));
-  CK(cudaMemcpyAsync(c.err_host, c.err, 2 * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  if (host_copies) {
+    CK(cudaMemcpyAsync(c.sc_host, c.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaMemcpyAsync(c.err_host, c.err, 2 * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  }
+}
+
+// End of one device-side PCG iteration: it += 1, rel = sqrt(rho1 / rho0) (the host loop's formula), stop
+// on rel < rtol, on it == max_it or on a raised error flag; the WHILE node repeats the body while 1.
+__global__ void k_pcg_control(cudaGraphConditionalHandle h, const Scalars *sc, LoopState *ls, const int *err) {
+  const int it = ls->it + 1;
+  const double rel = sqrt(sc->rho1 / sc->rho0);
+  const bool stop = (rel < ls->rtol) || (it >= ls->max_it) || (err[0] != 0);
+  ls->it = it;
+  ls->rel = rel;
+  ls->stop = stop;
+  cudaGraphSetConditional(h, stop ? 0u : 1u);
+}
+
+// Capture the iteration body into the body graph of a conditional WHILE node (one graph launch per solve,
+// no host round trip per iteration).  Returns false (and leaves the host loop in charge) if the driver
+// refuses any step.
+static bool build_pcg_loop(Ctx &c, int precond) {
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ex = nullptr;
+  const int64_t l0 = c.launches;
+  bool ok = false;
+  try {
+    if (!c.loop) {
+      c.loop = c.alloc<LoopState>(1);
+      CK(cudaMallocHost(&c.loop_host, sizeof(LoopState)));
+    }
+    CK(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h;
+    CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    CK(cudaGraphAddNode(&node, g, nullptr, 0, &np));
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    c.capturing = true;
+    CK(cudaStreamBeginCaptureToGraph(c.stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    try {
+      pcg_body(c, precond, false);
+      k_pcg_control<<<1, 1, 0, c.stream>>>(h, c.sc, c.loop, c.err);
+      after_launch(c, "k_pcg_control");
+    } catch (...) {
+      cudaGraph_t tmp;
+      cudaStreamEndCapture(c.stream, &tmp);
+      throw;
+    }
+    CK(cudaStreamEndCapture(c.stream, &body));
+    c.capturing = false;
+    CK(cudaGraphInstantiate(&ex, g, 0));
+    c.pcg_loop[precond] = ex;
+    c.graph_launches[precond] = c.launches - l0;
+    ok = true;
+  } catch (const Error &) {
+    c.capturing = false;
+    cudaGetLastError();
+  }
+  c.launches = l0;
+  if (g) cudaGraphDestroy(g);
+  return ok;
 }
 
 static amgf_status pcg_impl(Ctx &c, const double *b, double *x, double rtol, int max_it, int precond,
@@ -230,6 +297,27 @@ static amgf_status pcg_impl(Ctx &c, const double *b, double *x, double rtol, int
     throw Error{AMGF_ERR_BREAKDOWN, "pcg: r.Mr <= 0"};
   } else {
     launch_copy(c, n, c.zz, c.p);
+    static const bool host_loop = getenv("AMGF_HOST_LOOP") != nullptr;  // A/B experiments
+    if (!host_loop && !c.pcg_loop_tried[precond] && max_it > 0) {
+      c.pcg_loop_tried[precond] = true;
+      build_pcg_loop(c, precond);
+    }
+    if (!host_loop && c.pcg_loop[precond] && max_it > 0) {
+      LoopState ls = {};
+      ls.max_it = max_it;
+      ls.rtol = rtol;
+      *c.loop_host = ls;
+      CK(cudaMemcpyAsync(c.loop, c.loop_host, sizeof(LoopState), cudaMemcpyHostToDevice, c.stream));
+      CK(cudaGraphLaunch(c.pcg_loop[precond], c.stream));
+      CK(cudaMemcpyAsync(c.loop_host, c.loop, sizeof(LoopState), cudaMemcpyDeviceToHost, c.stream));
+      CK(cudaMemcpyAsync(c.err_host, c.err, 2 * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+      CK(cudaStreamSynchronize(c.stream));
+      it = c.loop_host->it;
+      rel = c.loop_host->rel;
+      c.launches += c.graph_launches[precond] * it;
+      if (c.err_host[0]) check_dev_error(c, "pcg");
+      st = (rel < rtol) ? AMGF_OK : AMGF_NOT_CONVERGED;
+    } else {
     if (!c.pcg_graph[precond] && max_it > 0) {
       cudaGraph_t g;
       const int64_t l0 = c.launches;
@@ -260,6 +348,7 @@ static amgf_status pcg_impl(Ctx &c, const double *b, double *x, double rtol, int
       if (it == max_it) break;
     }
     if (it > max_it) it = max_it;
+    }
   }
   if (x != c.xx) launch_copy(c, n, c.xx, x);
   CK(cudaEventRecord(e1, c.stream));

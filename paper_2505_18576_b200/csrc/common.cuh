@@ -92,6 +92,12 @@ struct Level {
 struct Scalars {
   double rho0, rho, pi, alpha, beta, rho1, dot, pad;
 };
+// Device-side PCG loop control (api.cu, k_pcg_control): the whole iteration loop is one CUDA graph with a
+// conditional WHILE node; the convergence test runs on the device with the host's formula.
+struct LoopState {
+  int it, max_it, stop, pad;
+  double rtol, rel;
+};
 
 struct Ctx {
   cudaStream_t stream = nullptr;
@@ -165,6 +171,9 @@ struct Ctx {
   cudaStream_t gstream = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   cudaGraphExec_t pcg_graph[2] = {nullptr, nullptr};
+  cudaGraphExec_t pcg_loop[2] = {nullptr, nullptr};  // device-side loop (conditional WHILE node)
+  bool pcg_loop_tried[2] = {false, false};
+  LoopState *loop = nullptr, *loop_host = nullptr;
   int64_t graph_launches[2] = {0, 0};
   bool capturing = false;
   std::vector<void *> allocs;
