@@ -121,6 +121,13 @@ amgf_status amgf_level_info(amgf_handle h, int64_t *info);
  * {int p0, len, kind, t0; int64 off; int level, pad}.  Sizes follow amgf_level_info.  Synchronises the handle's last stream. */
 amgf_status amgf_level_get(amgf_handle h, int32_t which, int32_t level, void *dst);
 
+/* PCG coefficients of the last amgf_pcg_solve: alpha_k = rho_k / (p_k . S p_k) and beta_k = rho_{k+1} / rho_k
+ * of iterations k = 1..n (n <= iterations of that solve), into HOST arrays of n doubles.  They define the
+ * Lanczos matrix of M S whose eigenvalues (Ritz values) estimate its spectrum (paper remark
+ * upper_bound_estimate, section 4: beta = condition number of the AMG-preconditioned contact-free
+ * operator).  AMGF_ERR_ARG if n exceeds the iterations of the last solve. */
+amgf_status amgf_pcg_history(amgf_handle h, int32_t n, double *alpha, double *beta);
+
 /* Number of kernel launches issued by this handle since creation (bench accounting). */
 int64_t amgf_launch_count(amgf_handle h);
 

@@ -18,7 +18,7 @@ STATUS = {0: "AMGF_OK", 1: "AMGF_NOT_CONVERGED", -1: "AMGF_ERR_ARG", -2: "AMGF_E
 
 SYMBOLS = ["amgf_default_config", "amgf_setup", "amgf_update_D", "amgf_apply", "amgf_vcycle", "amgf_spmv",
            "amgf_pcg_solve", "amgf_pcg_solve_host", "amgf_level_info", "amgf_level_get", "amgf_launch_count",
-           "amgf_last_error", "amgf_destroy"]
+           "amgf_pcg_history", "amgf_last_error", "amgf_destroy"]
 
 
 def lib_path() -> str:
@@ -70,6 +70,8 @@ def load_library():
     L.amgf_level_info.restype = I
     L.amgf_level_get.argtypes = [P, I, I, P]
     L.amgf_level_get.restype = I
+    L.amgf_pcg_history.argtypes = [P, I, P, P]
+    L.amgf_pcg_history.restype = I
     L.amgf_launch_count.argtypes = [P]
     L.amgf_launch_count.restype = ctypes.c_int64
     L.amgf_last_error.restype = ctypes.c_char_p
@@ -207,6 +209,14 @@ class AMGF:
         _check(st, allow=(0, 1))
         return dict(iterations=rep.iterations, converged=bool(rep.converged), relres=rep.rel_pres_norm,
                     solve_ms=rep.solve_ms)
+
+    def history(self, n):
+        """alpha_k, beta_k (k = 1..n) of the last PCG solve (numpy arrays)."""
+        a = np.zeros(n)
+        bt = np.zeros(n)
+        _check(load_library().amgf_pcg_history(self.h, n, a.ctypes.data_as(ctypes.c_void_p),
+                                                bt.ctypes.data_as(ctypes.c_void_p)))
+        return a, bt
 
     @property
     def launches(self) -> int:

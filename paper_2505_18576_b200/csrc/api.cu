@@ -216,6 +216,10 @@ static void pcg_body(Ctx &c, int precond, bool host_copies = true) {
 __global__ void k_pcg_control(cudaGraphConditionalHandle h, const Scalars *sc, LoopState *ls, const int *err) {
   const int it = ls->it + 1;
   const double rel = sqrt(sc->rho1 / sc->rho0);
+  if (it <= ls->cap) {
+    ls->hist[2 * (it - 1)] = sc->alpha;
+    ls->hist[2 * (it - 1) + 1] = sc->beta;
+  }
   const bool stop = (rel < ls->rtol) || (it >= ls->max_it) || (err[0] != 0);
   ls->it = it;
   ls->rel = rel;
@@ -303,9 +307,15 @@ static amgf_status pcg_impl(Ctx &c, const double *b, double *x, double rtol, int
       build_pcg_loop(c, precond);
     }
     if (!host_loop && c.pcg_loop[precond] && max_it > 0) {
+      if (c.hist_cap < max_it) {  // history buffer (read through LoopState: the graph keeps its pointers)
+        c.hist_cap = std::min(max_it, 100000);
+        c.hist = c.alloc<double>(2 * (size_t)c.hist_cap);
+      }
       LoopState ls = {};
       ls.max_it = max_it;
       ls.rtol = rtol;
+      ls.cap = c.hist_cap;
+      ls.hist = c.hist;
       *c.loop_host = ls;
       CK(cudaMemcpyAsync(c.loop, c.loop_host, sizeof(LoopState), cudaMemcpyHostToDevice, c.stream));
       CK(cudaGraphLaunch(c.pcg_loop[precond], c.stream));
@@ -314,10 +324,12 @@ static amgf_status pcg_impl(Ctx &c, const double *b, double *x, double rtol, int
       CK(cudaStreamSynchronize(c.stream));
       it = c.loop_host->it;
       rel = c.loop_host->rel;
+      c.hist_n = std::min(it, c.hist_cap);
       c.launches += c.graph_launches[precond] * it;
       if (c.err_host[0]) check_dev_error(c, "pcg");
       st = (rel < rtol) ? AMGF_OK : AMGF_NOT_CONVERGED;
     } else {
+    c.host_hist.clear();
     if (!c.pcg_graph[precond] && max_it > 0) {
       cudaGraph_t g;
       const int64_t l0 = c.launches;
@@ -344,10 +356,13 @@ static amgf_status pcg_impl(Ctx &c, const double *b, double *x, double rtol, int
       if (c.err_host[0]) check_dev_error(c, "pcg");
       const double rho1 = c.sc_host->rho1;
       rel = std::sqrt(rho1 / rho0);
+      c.host_hist.push_back(c.sc_host->alpha);
+      c.host_hist.push_back(c.sc_host->beta);
       if (rel < rtol) { st = AMGF_OK; break; }
       if (it == max_it) break;
     }
     if (it > max_it) it = max_it;
+    c.hist_n = -(int)(c.host_hist.size() / 2);  // negative: the history is on the host
     }
   }
   if (x != c.xx) launch_copy(c, n, c.xx, x);
@@ -593,6 +608,27 @@ amgf_status amgf_level_get(amgf_handle h, int32_t which, int32_t level, void *ds
 }
 
 int64_t amgf_launch_count(amgf_handle h) { return h ? h->launches : -1; }
+
+amgf_status amgf_pcg_history(amgf_handle h, int32_t n, double *alpha, double *beta) {
+  if (!h || (n > 0 && (!alpha || !beta))) { set_error("null argument"); return AMGF_ERR_ARG; }
+  return guarded([&]() -> amgf_status {
+    const int avail = h->hist_n >= 0 ? h->hist_n : -h->hist_n;
+    REQUIRE(n >= 0 && n <= avail, AMGF_ERR_ARG, "pcg_history: n exceeds the iterations of the last solve");
+    std::vector<double> buf(2 * (size_t)n);
+    if (n > 0) {
+      if (h->hist_n >= 0) {
+        CK(cudaMemcpy(buf.data(), h->hist, buf.size() * sizeof(double), cudaMemcpyDeviceToHost));
+      } else {
+        std::copy(h->host_hist.begin(), h->host_hist.begin() + buf.size(), buf.begin());
+      }
+    }
+    for (int k = 0; k < n; k++) {
+      alpha[k] = buf[2 * k];
+      beta[k] = buf[2 * k + 1];
+    }
+    return AMGF_OK;
+  });
+}
 
 void amgf_destroy(amgf_handle h) {
   if (!h) return;

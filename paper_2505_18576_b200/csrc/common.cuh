@@ -95,8 +95,9 @@ struct Scalars {
 // Device-side PCG loop control (api.cu, k_pcg_control): the whole iteration loop is one CUDA graph with a
 // conditional WHILE node; the convergence test runs on the device with the host's formula.
 struct LoopState {
-  int it, max_it, stop, pad;
+  int it, max_it, stop, cap;
   double rtol, rel;
+  double *hist;  // [2 * cap]: alpha_k, beta_k of iteration k (PCG history, amgf_pcg_history)
 };
 
 struct Ctx {
@@ -174,6 +175,9 @@ struct Ctx {
   cudaGraphExec_t pcg_loop[2] = {nullptr, nullptr};  // device-side loop (conditional WHILE node)
   bool pcg_loop_tried[2] = {false, false};
   LoopState *loop = nullptr, *loop_host = nullptr;
+  double *hist = nullptr;  // device PCG coefficient history, capacity hist_cap iterations
+  int hist_cap = 0, hist_n = 0;
+  std::vector<double> host_hist;  // same, host-loop fallback
   int64_t graph_launches[2] = {0, 0};
   bool capturing = false;
   std::vector<void *> allocs;

@@ -317,3 +317,30 @@ def test_fused_tail_matches_level_kernels(oracle_lib, amgf_mod, torch_cuda, cfg,
     assert np.array_equal(g.apply(r).cpu().numpy(), h.apply(r).cpu().numpy())
     if cfg == 2:
         assert np.array_equal(g.vcycle(r).cpu().numpy(), oracle_lib.Oracle.from_problem(p).vcycle(r))
+
+
+def _ritz(alpha, beta):
+    k = len(alpha)
+    T = np.zeros((k, k))
+    for j in range(k):
+        T[j, j] = 1.0 / alpha[j] + (beta[j - 1] / alpha[j - 1] if j > 0 else 0.0)
+        if j + 1 < k:
+            T[j, j + 1] = T[j + 1, j] = np.sqrt(beta[j]) / alpha[j]
+    return np.linalg.eigvalsh(T)
+
+
+def test_pcg_history_ritz(amgf_mod, torch_cuda):
+    """PCG coefficient history (amgf_pcg_history): one (alpha, beta) per iteration, both positive, and the
+    Ritz values of M S inside (0, 1] (lambda_max(M S) <= 1 for the convergent l1 smoother, PAPER.md eq. for
+    the AMGF bounds; SURVEY A18 tolerance), AMG-only likewise."""
+    p = gen.config(1)
+    g = amgf_mod.AMGF.from_problem(p)
+    for precond in ("amgf", "amg"):
+        _, rep = g.pcg(p.b, rtol=p.rtol, precond=precond)
+        k = rep["iterations"]
+        a, bt = g.history(k)
+        assert np.all(a > 0) and np.all(bt > 0)
+        ev = _ritz(a, bt)
+        assert ev[0] > 0 and ev[-1] <= 1.0 + 1e-6, (precond, ev[0], ev[-1])
+        with pytest.raises(Exception):
+            g.history(k + 1)
