@@ -20,6 +20,13 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-std=c11"]
 
 
+def cheb_coefs(k: int, ratio: float):
+    """Chebyshev smoother coefficients (c0, [(a_s, b_s) for s = 1..k-1]) of the oracle (reading R18)."""
+    out = np.zeros(2 * k)
+    lib().orc_cheb_coefs(k, ratio, _p(out))
+    return out[0], [(out[2 * s - 1], out[2 * s]) for s in range(1, k)]
+
+
 def build(force: bool = False) -> str:
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         subprocess.check_call(["gcc", *CFLAGS, "-o", _LIB, _SRC, "-lm"])
@@ -30,11 +37,13 @@ class OrcConfig(ctypes.Structure):
     _fields_ = [("pre_sweeps", ctypes.c_int), ("post_sweeps", ctypes.c_int),
                 ("coarsest_size", ctypes.c_int), ("max_levels", ctypes.c_int),
                 ("power_iters", ctypes.c_int), ("factor_filter", ctypes.c_int),
-                ("agg_seed", ctypes.c_uint64), ("nd_levels", ctypes.c_int), ("pad_", ctypes.c_int)]
+                ("agg_seed", ctypes.c_uint64), ("nd_levels", ctypes.c_int), ("smoother", ctypes.c_int),
+                ("cheb_degree", ctypes.c_int), ("pad_", ctypes.c_int), ("cheb_ratio", ctypes.c_double)]
 
 
 DEFAULTS = dict(pre_sweeps=1, post_sweeps=1, coarsest_size=64, max_levels=25,
-                power_iters=10, factor_filter=1, agg_seed=0x5EED, nd_levels=3)
+                power_iters=10, factor_filter=1, agg_seed=0x5EED, nd_levels=3, smoother=0, cheb_degree=2,
+                cheb_ratio=30.0)
 
 _lib = None
 
@@ -57,6 +66,7 @@ def lib():
         L.orc_priority.restype = ctypes.c_uint64
         L.orc_priority.argtypes = [ctypes.c_int, ctypes.c_uint64]
         L.orc_vcycle.argtypes = [P, P, P]
+        L.orc_cheb_coefs.argtypes = [ctypes.c_int, ctypes.c_double, P]
         L.orc_apply.argtypes = [P, P, P]
         L.orc_spmv.argtypes = [P, ctypes.c_int, P, P]
         L.orc_filter_solve.argtypes = [P, P, P]

@@ -207,7 +207,10 @@ typedef struct {
   int pre_sweeps, post_sweeps, coarsest_size, max_levels, power_iters, factor_filter;
   uint64_t agg_seed;
   int nd_levels;  /* nested-dissection depth of A_w's elimination order (contract C9/C10, reading R16) */
+  int smoother;   /* 0 = l1-Jacobi (default), 1 = Chebyshev in D_l1^{-1} A (variant f4, reading R18) */
+  int cheb_degree;
   int pad_;
+  double cheb_ratio;
 } orc_config;
 
 typedef struct {
@@ -869,6 +872,11 @@ orc_ctx *orc_create(int nodes, const int *Kptr, const int *Kcol, const double *K
   }
   for (int k = 0; k < m; k++)
     if (!(D[k] > 0.0)) { *status = fail(ORC_ERR_DOMAIN, "D must be strictly positive"); return NULL; }
+  if (cfg->smoother < 0 || cfg->smoother > 1 ||
+      (cfg->smoother == 1 && (cfg->cheb_degree < 1 || cfg->cheb_degree > 32 || !(cfg->cheb_ratio > 1.0)))) {
+    *status = fail(ORC_ERR_ARG, "bad smoother configuration");
+    return NULL;
+  }
   orc_ctx *cx = (orc_ctx *)calloc(1, sizeof(orc_ctx));
   cx->cfg = *cfg;
   cx->nodes = nodes;
@@ -883,6 +891,62 @@ orc_ctx *orc_create(int nodes, const int *Kptr, const int *Kcol, const double *K
 }
 
 /* ---------- solve phase ---------- */
+/* Chebyshev smoother coefficients (reading R18): degree k polynomial in D_l1^{-1} A on the interval
+ * [1/ratio, 1] (lambda_max(D_l1^{-1} A) <= 1 for the l1 diagonal), three-term recurrence
+ *   theta = (1 + 1/ratio)/2, delta = (1 - 1/ratio)/2, sigma = theta/delta, rho_0 = 1/sigma,
+ *   rho_s = 1/(2 sigma - rho_{s-1}),  a_s = rho_s rho_{s-1},  b_s = 2 rho_s / delta   (s = 1..k-1),
+ *   c0 = 1/theta.  The error after one application is T_k((theta - lambda)/delta) / T_k(sigma). */
+static void cheb_coefs(int k, double ratio, double *c0, double *a, double *bb) {
+  const double theta = (1.0 + 1.0 / ratio) / 2.0, delta = (1.0 - 1.0 / ratio) / 2.0;
+  const double sigma = theta / delta;
+  double rho = 1.0 / sigma;
+  *c0 = 1.0 / theta;
+  for (int s = 1; s < k; s++) {
+    const double rn = 1.0 / (2.0 * sigma - rho);
+    a[s] = rn * rho;
+    bb[s] = 2.0 * rn / delta;
+    rho = rn;
+  }
+}
+void orc_cheb_coefs(int k, double ratio, double *out) {  /* out = {c0, a_1, b_1, ..., a_{k-1}, b_{k-1}} */
+  double a[64], bb[64];
+  cheb_coefs(k, ratio, &out[0], a, bb);
+  for (int s = 1; s < k; s++) { out[2 * s - 1] = a[s]; out[2 * s] = bb[s]; }
+}
+
+/* One Chebyshev application (contract C23): from zero: t = b/d, dir = c0 t, x = dir; else
+ * r = b - A x, t = r/d, dir = c0 t, x = x + dir; then for s = 1..k-1: r = b - A x, t = r/d,
+ * dir = fma(a_s, dir, b_s t), x = x + dir. */
+static void cheb_smooth(orc_ctx *cx, level_t *L, const double *b, double *x, int from_zero, double *r,
+                        double *dir) {
+  const long n = L->n;
+  const int k = cx->cfg.cheb_degree;
+  double c0, a[64], bb[64];
+  cheb_coefs(k, cx->cfg.cheb_ratio, &c0, a, bb);
+  if (from_zero) {
+    for (long i = 0; i < n; i++) {
+      const double t = b[i] / L->dl1[i];
+      dir[i] = c0 * t;
+      x[i] = dir[i];
+    }
+  } else {
+    bsr_spmv(&L->A, x, b, r, 1);
+    for (long i = 0; i < n; i++) {
+      const double t = r[i] / L->dl1[i];
+      dir[i] = c0 * t;
+      x[i] = x[i] + dir[i];
+    }
+  }
+  for (int s = 1; s < k; s++) {
+    bsr_spmv(&L->A, x, b, r, 1);
+    for (long i = 0; i < n; i++) {
+      const double t = r[i] / L->dl1[i];
+      dir[i] = fma(a[s], dir[i], bb[s] * t);
+      x[i] = x[i] + dir[i];
+    }
+  }
+}
+
 static void vcycle(orc_ctx *cx, int l, const double *b, double *x) {
   level_t *L = &cx->lev[l];
   long n = L->n;
@@ -894,18 +958,27 @@ static void vcycle(orc_ctx *cx, int l, const double *b, double *x) {
   double *bc = cx->work[l + 1][1];
   double *xc = cx->work[l + 1][2];
   double *xn = cx->work[l][3];
-  /* pre-smoothing, l1-Jacobi (contract C4) */
-  for (long i = 0; i < n; i++) x[i] = b[i] / L->dl1[i];
-  for (int s = 1; s < cx->cfg.pre_sweeps; s++) {
-    bsr_spmv(&L->A, x, b, r, 1);
-    for (long i = 0; i < n; i++) xn[i] = x[i] + r[i] / L->dl1[i];
-    memcpy(x, xn, (size_t)n * sizeof(double));
+  const int cheb = cx->cfg.smoother == 1;
+  if (cheb) {  /* pre-smoothing, Chebyshev (C23) */
+    for (int s = 0; s < cx->cfg.pre_sweeps; s++) cheb_smooth(cx, L, b, x, s == 0, r, xn);
+  } else {
+    /* pre-smoothing, l1-Jacobi (contract C4) */
+    for (long i = 0; i < n; i++) x[i] = b[i] / L->dl1[i];
+    for (int s = 1; s < cx->cfg.pre_sweeps; s++) {
+      bsr_spmv(&L->A, x, b, r, 1);
+      for (long i = 0; i < n; i++) xn[i] = x[i] + r[i] / L->dl1[i];
+      memcpy(x, xn, (size_t)n * sizeof(double));
+    }
   }
   bsr_spmv(&L->A, x, b, r, 1);          /* r = b - A x            */
   bsr_spmv_warp32(&L->R, r, bc);        /* b_c = R r   (C5)       */
   vcycle(cx, l + 1, bc, xc);            /* x_c = B_{l+1} b_c      */
   bsr_spmv(&L->P, xc, NULL, xn, 0);     /* x += P x_c  (C6)       */
   for (long i = 0; i < n; i++) x[i] = x[i] + xn[i];
+  if (cheb) {
+    for (int s = 0; s < cx->cfg.post_sweeps; s++) cheb_smooth(cx, L, b, x, 0, r, xn);
+    return;
+  }
   for (int s = 0; s < cx->cfg.post_sweeps; s++) {
     bsr_spmv(&L->A, x, b, r, 1);
     for (long i = 0; i < n; i++) xn[i] = x[i] + r[i] / L->dl1[i];

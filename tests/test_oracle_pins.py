@@ -574,3 +574,65 @@ def test_amgf_robust_vs_amg(oracle_lib):
     amg_hi = it(o_hi, "amg")
     assert amg_hi >= 4 * amgf_hi
     assert amgf_hi <= 2 * amgf_lo
+
+
+# ------------------------------------------------ Chebyshev smoother (variant f4, reading R18)
+@pytest.mark.parametrize("k,ratio", [(1, 30.0), (2, 30.0), (3, 30.0), (4, 10.0)])
+def test_cheb_coefficients_closed_form(oracle_lib, k, ratio):
+    """The oracle's three-term coefficients reproduce the scaled Chebyshev polynomial: running the update
+    recurrence on a scalar 'matrix' lambda gives the error factor T_k((theta - lambda)/delta) / T_k(sigma)."""
+    from numpy.polynomial import chebyshev as C
+    c0, ab = oracle_lib.cheb_coefs(k, ratio)
+    theta, delta = (1 + 1 / ratio) / 2, (1 - 1 / ratio) / 2
+    Tk = C.Chebyshev.basis(k)
+    for lam in np.linspace(0.0, 1.0, 23):
+        e = 1.0  # error of x for b = 0 (x* = 0): x = e, the update uses r = -lam * x
+        d = c0 * (-lam * e)
+        e = e + d
+        for a, b in ab:
+            d = a * d + b * (-lam * e)
+            e = e + d
+        assert abs(e - Tk((theta - lam) / delta) / Tk(theta / delta)) <= 1e-12
+
+
+def _dense_vcycle_cheb(o, k, ratio):
+    """B from the operator-product form with Chebyshev smoothers S = T_k((theta I - D^{-1}A)/delta)/T_k(sigma)
+    (matrix three-term recurrence T_{j+1} = 2 X T_j - T_{j-1})."""
+    theta, delta = (1 + 1 / ratio) / 2, (1 - 1 / ratio) / 2
+    from numpy.polynomial import chebyshev as C
+    tks = C.Chebyshev.basis(k)(theta / delta)
+    Bc = np.linalg.inv(o.get(23))
+    for l in range(o.nlev - 2, -1, -1):
+        A = o.level_matrix(l).toarray()
+        P = o.level_matrix(l, "P").toarray()
+        I = np.eye(A.shape[0])
+        X = (theta * I - np.diag(1 / o.get(9, l)) @ A) / delta
+        T0, T1 = I, X
+        for _ in range(k - 1):
+            T0, T1 = T1, 2 * X @ T1 - T0
+        S = (T1 if k >= 1 else T0) / tks
+        E = S @ (I - P @ Bc @ P.T @ A) @ S
+        Bc = (I - E) @ np.linalg.inv(A)
+    return Bc
+
+
+@pytest.mark.parametrize("N,matching,k", [(2, True, 2), (3, False, 3), (3, False, 1)])
+def test_cheb_vcycle_operator(oracle_lib, N, matching, k):
+    p = tiny(N=N, matching=matching, e_max=3.0)
+    o = oracle_lib.Oracle.from_problem(p, coarsest_size=16, smoother=1, cheb_degree=k, cheb_ratio=30.0)
+    assert o.nlev >= 2
+    B = dense_op(o.vcycle, p.n)
+    Bref = _dense_vcycle_cheb(o, k, 30.0)
+    assert np.abs(B - Bref).max() <= 1e-9 * np.abs(Bref).max()
+    assert np.abs(B - B.T).max() <= 1e-11 * np.abs(B).max()  # symmetric smoother => symmetric V-cycle
+    A = o.level_matrix(0).toarray()
+    Lc = np.linalg.cholesky(A)
+    ev = np.linalg.eigvalsh(Lc.T @ B @ Lc)
+    assert ev[-1] <= 1 + 1e-9 and ev[0] > 0  # convergent on [0, 1]: |T_k((theta-l)/delta)| <= T_k(sigma)
+
+
+def test_cheb_config_errors(oracle_lib):
+    p = tiny(N=2)
+    for bad in (dict(smoother=1, cheb_degree=0), dict(smoother=1, cheb_ratio=1.0), dict(smoother=2)):
+        with pytest.raises(Exception):
+            oracle_lib.Oracle.from_problem(p, **bad)
