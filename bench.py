@@ -88,8 +88,13 @@ class Clocks:
 
 
 def level_bytes(g):
-    """Algorithmic HBM bytes of one V-cycle: per level 2 passes of A, one of R and
-    one of P (values + int32 block columns), plus the vector traffic of the five kernels."""
+    """Algorithmic HBM bytes of one V-cycle, one pre- and one post-sweep: per level the
+    passes of A (2 for l1-Jacobi: residual + post sweep; 2k for a degree-k Chebyshev sweep: k-1 pre steps,
+    residual, k post steps), one of R and one of P (values + int32 block columns), plus the vector traffic
+    of the kernels (Jacobi start 24n, residual 24n, restriction, prolongation, l1 sweep 32n; Chebyshev start
+    32n, step 48n: x gather, b, d, dir read/write, new x)."""
+    cheb = int(getattr(g.config, "smoother", 0)) == 1
+    k = int(getattr(g.config, "cheb_degree", 1))
     tot = 0
     for l, L in enumerate(g.levels):
         b, n = L["b"], L["nodes"] * L["b"]
@@ -99,8 +104,11 @@ def level_bytes(g):
         A = L["nnzb"] * (8 * b * b + 4) + 4 * L["nodes"]
         Pb = L["nnzb_P"] * (8 * 6 * b + 4)
         nc6 = 6 * L["n_agg"]
-        vec = 24 * n + (24 * n) + (8 * n + 8 * nc6) + (8 * nc6 + 16 * n) + 32 * n
-        tot += 2 * A + 2 * Pb + vec
+        common = (24 * n) + (8 * n + 8 * nc6) + (8 * nc6 + 16 * n)  # residual, restriction, prolongation
+        if cheb:
+            tot += 2 * k * A + 2 * Pb + common + 32 * n + (2 * k - 1) * 48 * n
+        else:
+            tot += 2 * A + 2 * Pb + common + 24 * n + 32 * n
     return tot
 
 
@@ -259,7 +267,10 @@ def run_amgf(args, rank, world, local_rank):
         "config": {"workload": f"cfg{args.cfg}: two-block N={p.N}, n={p.n} dofs, m={p.m}, n_c={g.nc}, "
                                f"{nsys}-system IP-like D sequence, rtol={p.rtol}",
                    "levels": [(L["nodes"] * L["b"]) for L in g.levels], "band_width_Aw": g.bw,
-                   "l2": "inputs larger than L2 (fine operator 1.1 GB)", "parallelism": f"replicas x{world}"},
+                   "l2": "inputs larger than L2 (fine operator 1.1 GB)", "parallelism": f"replicas x{world}",
+                   "smoother": (f"chebyshev degree {g.config.cheb_degree} on [1/{g.config.cheb_ratio:g}, 1] of "
+                                f"D_l1^-1 A (DESIGN R18)" if g.config.smoother == 1 else "l1-jacobi"),
+                   "sweeps": [g.config.pre_sweeps, g.config.post_sweeps]},
         "pcg_iterations": iters,
         "systems": systems,
         "solve_ms_per_system": solve_ms,
@@ -329,7 +340,7 @@ def run_reference(args, rank, world):
     for _ in range(min(args.warmup, 1)):
         o.spmv(x)
     vals = []
-    iters_guess = 60
+    iters_guess = 47  # mean PCG iterations of the GPU path over the cfg 3 sequence (default smoother)
     for k in range(args.steps):
         t = time.perf_counter(); o.vcycle(x); t_v = time.perf_counter() - t
         t = time.perf_counter(); o.spmv(x); t_s = time.perf_counter() - t

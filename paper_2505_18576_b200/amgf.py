@@ -29,7 +29,8 @@ class Config(ctypes.Structure):
     _fields_ = [("pre_sweeps", ctypes.c_int32), ("post_sweeps", ctypes.c_int32),
                 ("coarsest_size", ctypes.c_int32), ("max_levels", ctypes.c_int32),
                 ("power_iters", ctypes.c_int32), ("nd_levels", ctypes.c_int32),
-                ("agg_seed", ctypes.c_uint64)]
+                ("smoother", ctypes.c_int32), ("cheb_degree", ctypes.c_int32),
+                ("agg_seed", ctypes.c_uint64), ("cheb_ratio", ctypes.c_double)]
 
 
 class Report(ctypes.Structure):

@@ -102,6 +102,30 @@ void vcycle(Ctx &c, int l, const double *b, double *x, const double *add) {
   }
   Level &Lc = c.lev[l + 1];
   const int pre = c.cfg.pre_sweeps, post = c.cfg.post_sweeps;
+  if (c.cfg.smoother == 1) {  // Chebyshev (C23): each SpMV step writes the other buffer of {x, x2}
+    const int k = c.cfg.cheb_degree;
+    const int nswap = (k - 1) + (pre - 1) * k + post * k;
+    double *bufs[2] = {x, L.x2};
+    int ci = nswap & 1;  // so that the last step lands in x
+    auto step = [&](bool first, int s, const double *addp) {
+      launch_sell_cheb(c, L.As, first, bufs[ci], b, L.dl1, L.dir, first ? c.cheb_c0 : c.cheb_a[s],
+                       first ? 0.0 : c.cheb_b[s], addp, bufs[1 - ci]);
+      ci = 1 - ci;
+    };
+    launch_cheb0(c, L.n, b, L.dl1, c.cheb_c0, L.dir, bufs[ci]);
+    for (int s = 1; s < k; s++) step(false, s, nullptr);
+    for (int sw = 1; sw < pre; sw++) {
+      step(true, 0, nullptr);
+      for (int s = 1; s < k; s++) step(false, s, nullptr);
+    }
+    launch_sell_spmv(c, L.As, SPMV_RESID, bufs[ci], b, nullptr, nullptr, L.r, nullptr);
+    launch_restrict(c, L.R, L.r, Lc.bv);
+    vcycle(c, l + 1, Lc.bv, Lc.x, nullptr);
+    launch_prolong(c, L.Ps, Lc.x, bufs[ci]);
+    for (int sw = 0; sw < post; sw++)
+      for (int s = 0; s < k; s++) step(s == 0, s, (add && sw == post - 1 && s == k - 1) ? add : nullptr);
+    return;
+  }
   double *bufs[2] = {x, L.x2};
   int ci = ((pre - 1) + post) & 1;  // so that the last post-sweep lands in x
   launch_jacobi0(c, L.n, b, L.dl1, bufs[ci]);
@@ -435,7 +459,10 @@ void amgf_default_config(amgf_config *cfg) {
   cfg->max_levels = 25;
   cfg->power_iters = 10;
   cfg->nd_levels = 3;
+  cfg->smoother = 1;  // Chebyshev degree 2 (DESIGN R18); 0 = l1-Jacobi
+  cfg->cheb_degree = 2;
   cfg->agg_seed = 0x5EED;
+  cfg->cheb_ratio = 30.0;
 }
 
 const char *amgf_last_error(void) { return get_error(); }
@@ -455,6 +482,22 @@ amgf_status amgf_setup(int32_t nodes, const int32_t *K_ptr, const int32_t *K_col
     if (cfg) c->cfg = *cfg; else amgf_default_config(&c->cfg);
     REQUIRE(c->cfg.pre_sweeps >= 1 && c->cfg.post_sweeps >= 1 && c->cfg.max_levels >= 1 && c->cfg.power_iters >= 1,
             AMGF_ERR_ARG, "invalid config");
+    REQUIRE(c->cfg.smoother == 0 || (c->cfg.smoother == 1 && c->cfg.cheb_degree >= 1 && c->cfg.cheb_degree <= 32 &&
+                                     c->cfg.cheb_ratio > 1.0),
+            AMGF_ERR_ARG, "invalid smoother config");
+    if (c->cfg.smoother == 1) {  // Chebyshev coefficients (C23): same formulas, in the same order, as the oracle
+      const double ratio = c->cfg.cheb_ratio;
+      const double theta = (1.0 + 1.0 / ratio) / 2.0, delta = (1.0 - 1.0 / ratio) / 2.0;
+      const double sigma = theta / delta;
+      double rho = 1.0 / sigma;
+      c->cheb_c0 = 1.0 / theta;
+      for (int k = 1; k < c->cfg.cheb_degree; k++) {
+        const double rn = 1.0 / (2.0 * sigma - rho);
+        c->cheb_a[k] = rn * rho;
+        c->cheb_b[k] = 2.0 * rn / delta;
+        rho = rn;
+      }
+    }
     c->nodes = nodes;
     c->n = 3L * nodes;
     c->m = m;

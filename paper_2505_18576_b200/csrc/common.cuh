@@ -86,6 +86,7 @@ struct Level {
   double lambda = 0, omega = 0;
   // solve workspace
   double *x = nullptr, *x2 = nullptr, *bv = nullptr, *r = nullptr;
+  double *dir = nullptr;  // Chebyshev direction (smoother 1)
 };
 
 // Device scalars of PCG (C15) and dot results.
@@ -111,7 +112,8 @@ struct Ctx {
   double *rz = nullptr;
   double *nd_arena = nullptr;  // filter solve data (filter.cu) in one range
   size_t nd_arena_bytes = 0;
-  int resid_sms = 0;           // SMs of the residual SpMV that runs beside the A_w solve
+  int resid_sms = 0;
+  double cheb_c0 = 0.0, cheb_a[33] = {}, cheb_b[33] = {};  // Chebyshev coefficients (C23)           // SMs of the residual SpMV that runs beside the A_w solve
   amgf_config cfg;
   int nodes = 0, m = 0;
   long n = 0;
@@ -225,7 +227,15 @@ void after_launch(Ctx &c, const char *name);
 void check_dev_error(Ctx &c, const char *where);
 
 // ------------------------------------------------------------------ solve kernels (solve.cu)
-enum SpmvMode { SPMV_Y = 0, SPMV_RESID = 1, SPMV_SMOOTH = 2, SPMV_DOT = 3, SPMV_SMOOTH_ADD = 4 };
+enum SpmvMode { SPMV_Y = 0, SPMV_RESID = 1, SPMV_SMOOTH = 2, SPMV_DOT = 3, SPMV_SMOOTH_ADD = 4, SPMV_CHEB1 = 6,
+                SPMV_CHEB = 7 };
+struct ChebArgs {  // Chebyshev step of the SpMV epilogue (solve.cu, contract C23)
+  double ca = 0.0, cb = 0.0;
+  double *dir = nullptr;
+};
+void launch_sell_cheb(Ctx &c, const Sell &A, bool first, const double *x, const double *b, const double *dl1,
+                      double *dir, double ca, double cb, const double *add, double *y);
+void launch_cheb0(Ctx &c, long n, const double *b, const double *d, double c0, double *dir, double *x);
 void launch_sell_spmv(Ctx &c, const Sell &A, int mode, const double *x, const double *b, const double *d,
                       const double *add, double *y, double *dot_part);
 void launch_jacobi0(Ctx &c, long n, const double *b, const double *d, double *x);

@@ -1421,6 +1421,7 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
     L.x2 = c.alloc<double>(L.n);
     L.bv = c.alloc<double>(L.n);
     L.r = c.alloc<double>(L.n);
+    if (c.cfg.smoother == 1) L.dir = c.alloc<double>(L.n);
   }
   if (c.nlev == 1) build_sell(c, L0.A, L0.As, true, false);
   c.w_x1 = c.alloc<double>(n);

@@ -42,7 +42,19 @@ __device__ __forceinline__ double cta_tree(double v, double *s) {
 }
 
 enum { MODE_Y = SPMV_Y, MODE_RESID = SPMV_RESID, MODE_SMOOTH = SPMV_SMOOTH, MODE_DOT = SPMV_DOT,
-       MODE_SMOOTH_ADD = SPMV_SMOOTH_ADD, MODE_ADDTO = 5 };
+       MODE_SMOOTH_ADD = SPMV_SMOOTH_ADD, MODE_ADDTO = 5, MODE_CHEB1 = SPMV_CHEB1, MODE_CHEB = SPMV_CHEB };
+
+// Chebyshev step epilogue (contract C23): t = (b - acc)/d; first step dir = ca t, later dir = fma(ca, dir,
+// cb t); x_new = x + dir (then add + x_new when add is given, as SMOOTH_ADD).
+__device__ __forceinline__ double cheb_epilogue(int mode, double res, double di, double xi, double *dir, long i,
+                                                double ca, double cb, const double *add) {
+  const double t = res / di;
+  const double dv = (mode == MODE_CHEB1) ? ca * t : __fma_rn(ca, dir[i], cb * t);
+  dir[i] = dv;
+  double xn = xi + dv;
+  if (add) xn = add[i] + xn;
+  return xn;
+}
 
 // The SELL row chain of one block row (C2): acc[r] = sum over slots s (ascending) and block columns e
 // (ascending) of val * x, software-pipelined (slot s+1's column, values and x gather in flight while slot s
@@ -99,7 +111,8 @@ __global__ void __launch_bounds__(CTA) k_sell(int nrows, const int *__restrict__
                                               const double *__restrict__ val, const double *__restrict__ x,
                                               const double *__restrict__ b, const double *__restrict__ d,
                                               const double *__restrict__ add, double *__restrict__ y,
-                                              double *__restrict__ dot_part, const int *__restrict__ perm) {
+                                              double *__restrict__ dot_part, const int *__restrict__ perm,
+                                              ChebArgs ch) {
   const int row = blockIdx.x * CTA + threadIdx.x;
   double acc[BR];
 #pragma unroll
@@ -136,6 +149,8 @@ __global__ void __launch_bounds__(CTA) k_sell(int nrows, const int *__restrict__
       y[i] = xn;
     } else if (MODE == MODE_ADDTO) {
       y[i] = y[i] + acc[r];
+    } else if (MODE == MODE_CHEB1 || MODE == MODE_CHEB) {
+      y[i] = cheb_epilogue(MODE, b[i] - acc[r], d[i], x[i], ch.dir, i, ch.ca, ch.cb, add);
     }
   }
 }
@@ -148,7 +163,7 @@ __global__ void __launch_bounds__(CTA) k_sell_r1(int nrows, const int *__restric
                                                  const double *__restrict__ val, const double *__restrict__ x,
                                                  const double *__restrict__ b, const double *__restrict__ d,
                                                  const double *__restrict__ add, double *__restrict__ y,
-                                                 const int *__restrict__ perm) {
+                                                 const int *__restrict__ perm, ChebArgs ch) {
   const int row = blockIdx.x * CTA + threadIdx.x;
   const int lane = threadIdx.x & 31;
   if (row >= nrows) return;
@@ -204,12 +219,14 @@ __global__ void __launch_bounds__(CTA) k_sell_r1(int nrows, const int *__restric
     y[i] = xn;
   } else if (MODE == MODE_ADDTO) {
     y[i] = y[i] + acc;
+  } else if (MODE == MODE_CHEB1 || MODE == MODE_CHEB) {
+    y[i] = cheb_epilogue(MODE, b[i] - acc, d[i], x[i], ch.dir, i, ch.ca, ch.cb, add);
   }
 }
 
 template <int BR, int BC>
 static void sell_dispatch(Ctx &c, const Sell &A, int mode, const double *x, const double *b, const double *d,
-                          const double *add, double *y, double *dp) {
+                          const double *add, double *y, double *dp, ChebArgs ch = ChebArgs{}) {
   dim3 g(nblk(A.nrows)), t(CTA);
   if (A.nrows == 0) return;
   {
@@ -224,22 +241,26 @@ static void sell_dispatch(Ctx &c, const Sell &A, int mode, const double *x, cons
   }
   if (BR == 1 && mode != MODE_DOT) {
     switch (mode) {
-      case MODE_Y: k_sell_r1<BC, MODE_Y, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm); break;
-      case MODE_RESID: k_sell_r1<BC, MODE_RESID, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm); break;
-      case MODE_SMOOTH: k_sell_r1<BC, MODE_SMOOTH, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm); break;
-      case MODE_SMOOTH_ADD: k_sell_r1<BC, MODE_SMOOTH_ADD, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm); break;
-      case MODE_ADDTO: k_sell_r1<BC, MODE_ADDTO, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm); break;
+      case MODE_Y: k_sell_r1<BC, MODE_Y, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm, ch); break;
+      case MODE_RESID: k_sell_r1<BC, MODE_RESID, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm, ch); break;
+      case MODE_SMOOTH: k_sell_r1<BC, MODE_SMOOTH, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm, ch); break;
+      case MODE_SMOOTH_ADD: k_sell_r1<BC, MODE_SMOOTH_ADD, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm, ch); break;
+      case MODE_ADDTO: k_sell_r1<BC, MODE_ADDTO, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm, ch); break;
+      case MODE_CHEB1: k_sell_r1<BC, MODE_CHEB1, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm, ch); break;
+      case MODE_CHEB: k_sell_r1<BC, MODE_CHEB, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm, ch); break;
     }
     after_launch(c, "k_sell_r1");
     return;
   }
   switch (mode) {
-    case MODE_Y: k_sell<BR, BC, MODE_Y><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm); break;
-    case MODE_RESID: k_sell<BR, BC, MODE_RESID><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm); break;
-    case MODE_SMOOTH: k_sell<BR, BC, MODE_SMOOTH><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm); break;
-    case MODE_DOT: k_sell<BR, BC, MODE_DOT><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm); break;
-    case MODE_SMOOTH_ADD: k_sell<BR, BC, MODE_SMOOTH_ADD><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm); break;
-    case MODE_ADDTO: k_sell<BR, BC, MODE_ADDTO><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm); break;
+    case MODE_Y: k_sell<BR, BC, MODE_Y><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
+    case MODE_RESID: k_sell<BR, BC, MODE_RESID><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
+    case MODE_SMOOTH: k_sell<BR, BC, MODE_SMOOTH><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
+    case MODE_DOT: k_sell<BR, BC, MODE_DOT><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
+    case MODE_SMOOTH_ADD: k_sell<BR, BC, MODE_SMOOTH_ADD><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
+    case MODE_ADDTO: k_sell<BR, BC, MODE_ADDTO><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
+    case MODE_CHEB1: k_sell<BR, BC, MODE_CHEB1><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
+    case MODE_CHEB: k_sell<BR, BC, MODE_CHEB><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
   }
   after_launch(c, __func__);
 }
@@ -250,6 +271,30 @@ void launch_sell_spmv(Ctx &c, const Sell &A, int mode, const double *x, const do
   else if (A.br == 1 && A.bc == 6) sell_dispatch<1, 6>(c, A, mode, x, b, d, add, y, dp);
   else if (A.br == 6 && A.bc == 6) sell_dispatch<6, 6>(c, A, mode, x, b, d, add, y, dp);
   else throw Error{AMGF_ERR_ARG, "sell spmv: unsupported block shape"};
+}
+
+void launch_sell_cheb(Ctx &c, const Sell &A, bool first, const double *x, const double *b, const double *dl1,
+                      double *dir, double ca, double cb, const double *add, double *y) {
+  const ChebArgs ch{ca, cb, dir};
+  const int mode = first ? MODE_CHEB1 : MODE_CHEB;
+  if (A.br == 3 && A.bc == 3) sell_dispatch<3, 3>(c, A, mode, x, b, dl1, add, y, nullptr, ch);
+  else if (A.br == 1 && A.bc == 6) sell_dispatch<1, 6>(c, A, mode, x, b, dl1, add, y, nullptr, ch);
+  else throw Error{AMGF_ERR_ARG, "sell cheb: unsupported block shape"};
+}
+
+// Chebyshev application from x = 0 (C23): t = b/d, dir = c0 t, x = dir.
+__global__ void k_cheb0(long n, const double *__restrict__ b, const double *__restrict__ d, double c0,
+                        double *__restrict__ dir, double *__restrict__ x) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    const double t = b[i] / d[i];
+    const double v = c0 * t;
+    dir[i] = v;
+    x[i] = v;
+  }
+}
+void launch_cheb0(Ctx &c, long n, const double *b, const double *d, double c0, double *dir, double *x) {
+  k_cheb0<<<nblk(n), CTA, 0, c.stream>>>(n, b, d, c0, dir, x);
+  after_launch(c, "k_cheb0");
 }
 
 void launch_prolong(Ctx &c, const Sell &P, const double *xc, double *x) {

@@ -46,6 +46,9 @@ struct TailArgs {
   double *x, *x2, *r, *bc, *xc;                       // level t solution / second buffer / residual, coarse b, x
   int xs, maxv, maxc, maxpv, maxpc;                   // shared-memory layout (doubles / ints per array)
   unsigned long long *tm;                             // optional per-phase timestamps [ncta][16]
+  int cheb, kdeg;                                     // smoother: 0 = l1-Jacobi, 1 = Chebyshev of degree kdeg
+  double *dir;                                        // Chebyshev direction of level t
+  double c0, ca[33], cb[33];                          // Chebyshev coefficients (C23)
 };
 
 __device__ __forceinline__ void tail_mark(const TailArgs &a, int ph) {
@@ -90,15 +93,20 @@ __device__ __forceinline__ double tail_row(const double *sv, const int *sc, cons
 // out[i] (rows of this CTA) from the SELL chain over A_t with x staged in shared memory (C2)
 template <int MODE>
 __device__ __forceinline__ void tail_spmv(const TailArgs &a, int row0, int row1, int q0, const double *sx,
-                                          const double *sv, const int *sc, double *out) {
+                                          const double *sv, const int *sc, double *out, int step = 0) {
   for (int i = row0 + threadIdx.x; i < row1; i += blockDim.x) {
     const double acc = tail_row(sv, sc, sx, a.a_sp[i >> 5] - q0, a.a_len[i], i & 31);
     if (MODE == SPMV_RESID) {
       __stcg(out + i, a.b[i] - acc);
-    } else {  // SPMV_SMOOTH
+    } else if (MODE == SPMV_SMOOTH) {
       const double res = a.b[i] - acc;
       const double t = res / a.d[i];
       __stcg(out + i, sx[i] + t);
+    } else {  // SPMV_CHEB1 / SPMV_CHEB (C23), step s in a.ca / a.cb
+      const double t = (a.b[i] - acc) / a.d[i];
+      const double dv = (MODE == SPMV_CHEB1) ? a.c0 * t : __fma_rn(a.ca[step], __ldcg(a.dir + i), a.cb[step] * t);
+      __stcg(a.dir + i, dv);
+      __stcg(out + i, sx[i] + dv);
     }
   }
 }
@@ -156,8 +164,16 @@ __global__ void __launch_bounds__(TAIL_THREADS) k_vcycle_tail(TailArgs a) {
       sL[idx] = (i >= j) ? a.Lc[(long)j * a.Wc + (i - j)] : 0.0;
     }
   double *xb[2] = {a.x, a.x2};
-  int ci = ((a.pre - 1) + a.post) & 1;
-  for (int i = row0 + tid; i < row1; i += blockDim.x) __stcg(xb[ci] + i, a.b[i] / a.d[i]);  // jacobi0
+  int ci = a.cheb ? (((a.kdeg - 1) + (a.pre - 1) * a.kdeg + a.post * a.kdeg) & 1) : (((a.pre - 1) + a.post) & 1);
+  if (a.cheb) {  // Chebyshev from zero (C23): t = b/d, dir = c0 t, x = dir
+    for (int i = row0 + tid; i < row1; i += blockDim.x) {
+      const double v = a.c0 * (a.b[i] / a.d[i]);
+      __stcg(a.dir + i, v);
+      __stcg(xb[ci] + i, v);
+    }
+  } else {
+    for (int i = row0 + tid; i < row1; i += blockDim.x) __stcg(xb[ci] + i, a.b[i] / a.d[i]);  // jacobi0
+  }
   if (staged) mbar_wait(&bar, 0);
   tail_mark(a, 0);
   tail_sync(cl);
@@ -166,11 +182,30 @@ __global__ void __launch_bounds__(TAIL_THREADS) k_vcycle_tail(TailArgs a) {
     for (int i = tid; i < a.n; i += blockDim.x) sx[i] = __ldcg(xin + i);
     __syncthreads();
   };
-  for (int s = 1; s < a.pre; s++) {
+  // one smoothing step = stage x, SpMV epilogue into the other buffer, barrier
+  auto cheb_step = [&](bool first, int st) {
     stage_x(xb[ci]);
-    tail_spmv<SPMV_SMOOTH>(a, row0, row1, q0, sx, sv, sc, xb[1 - ci]);
+    if (first) tail_spmv<SPMV_CHEB1>(a, row0, row1, q0, sx, sv, sc, xb[1 - ci]);
+    else tail_spmv<SPMV_CHEB>(a, row0, row1, q0, sx, sv, sc, xb[1 - ci], st);
     ci = 1 - ci;
-    tail_sync(cl);
+  };
+  if (a.cheb) {
+    for (int st = 1; st < a.kdeg; st++) {
+      cheb_step(false, st);
+      tail_sync(cl);
+    }
+    for (int sw = 1; sw < a.pre; sw++)
+      for (int st = 0; st < a.kdeg; st++) {
+        cheb_step(st == 0, st);
+        tail_sync(cl);
+      }
+  } else {
+    for (int s = 1; s < a.pre; s++) {
+      stage_x(xb[ci]);
+      tail_spmv<SPMV_SMOOTH>(a, row0, row1, q0, sx, sv, sc, xb[1 - ci]);
+      ci = 1 - ci;
+      tail_sync(cl);
+    }
   }
   stage_x(xb[ci]);
   tail_mark(a, 2);
@@ -253,11 +288,19 @@ __global__ void __launch_bounds__(TAIL_THREADS) k_vcycle_tail(TailArgs a) {
   tail_mark(a, 9);
   tail_sync(cl);
   tail_mark(a, 10);
-  for (int s = 0; s < a.post; s++) {
-    stage_x(xb[ci]);
-    tail_spmv<SPMV_SMOOTH>(a, row0, row1, q0, sx, sv, sc, xb[1 - ci]);
-    ci = 1 - ci;
-    if (s + 1 < a.post) tail_sync(cl);
+  if (a.cheb) {
+    const int nsteps = a.post * a.kdeg;
+    for (int q = 0; q < nsteps; q++) {
+      cheb_step(q % a.kdeg == 0, q % a.kdeg);
+      if (q + 1 < nsteps) tail_sync(cl);
+    }
+  } else {
+    for (int s = 0; s < a.post; s++) {
+      stage_x(xb[ci]);
+      tail_spmv<SPMV_SMOOTH>(a, row0, row1, q0, sx, sv, sc, xb[1 - ci]);
+      ci = 1 - ci;
+      if (s + 1 < a.post) tail_sync(cl);
+    }
   }
   tail_mark(a, 11);
 }
@@ -371,6 +414,11 @@ void tail_vcycle(Ctx &c, const double *b, double *x) {
   a.b = b;
   a.x = x; a.x2 = L.x2; a.r = L.r; a.bc = Lc.bv; a.xc = Lc.x;
   a.xs = c.tail_xs; a.maxv = c.tail_maxv; a.maxc = c.tail_maxc; a.maxpv = c.tail_maxpv; a.maxpc = c.tail_maxpc;
+  a.cheb = c.cfg.smoother == 1;
+  a.kdeg = c.cfg.cheb_degree;
+  a.dir = L.dir;
+  a.c0 = c.cheb_c0;
+  for (int k = 0; k < 33; k++) { a.ca[k] = c.cheb_a[k]; a.cb[k] = c.cheb_b[k]; }
   static const bool timing = getenv("AMGF_TAIL_TIMING") != nullptr;  // phase timestamps (tools only)
   a.tm = nullptr;
   if (timing && !c.capturing) a.tm = c.alloc<unsigned long long>(c.tail_ncta * 16);

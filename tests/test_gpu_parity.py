@@ -344,3 +344,23 @@ def test_pcg_history_ritz(amgf_mod, torch_cuda):
         assert ev[0] > 0 and ev[-1] <= 1.0 + 1e-6, (precond, ev[0], ev[-1])
         with pytest.raises(Exception):
             g.history(k + 1)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_chebyshev_smoother_parity(oracle_lib, amgf_mod, torch_cuda, k):
+    """Chebyshev smoother variant (DESIGN R18, contract C23): V-cycle, AMGF apply, PCG iterations and
+    solution bitwise equal to the oracle (tiny non-matching case and cfg 1)."""
+    cfg = dict(smoother=1, cheb_degree=k, cheb_ratio=30.0)
+    p = tiny(N=3, matching=False, e_max=8.0)
+    o, g = build_pair(oracle_lib, amgf_mod, p, coarsest_size=16, **cfg)
+    assert g.nlev >= 2
+    r = np.random.default_rng(30 + k).standard_normal(p.n)
+    assert np.array_equal(g.vcycle(r).cpu().numpy(), o.vcycle(r))
+    assert np.array_equal(g.apply(r).cpu().numpy(), o.apply(r))
+    p = gen.config(1)
+    o, g = build_pair(oracle_lib, amgf_mod, p, **cfg)
+    r = np.random.default_rng(40).standard_normal(p.n)
+    assert np.array_equal(g.vcycle(r).cpu().numpy(), o.vcycle(r))
+    xo, ro = o.pcg(p.b, rtol=p.rtol)
+    xg, rg = g.pcg(p.b, rtol=p.rtol)
+    assert rg["iterations"] == ro["iterations"] and np.array_equal(xg.cpu().numpy(), xo)

@@ -430,8 +430,9 @@ def _dense_vcycle(o):
 
 @pytest.mark.parametrize("N,matching,e_max", [(2, True, 4.0), (3, False, 3.0)])
 def test_vcycle_operator(oracle_lib, N, matching, e_max):
+    """l1-Jacobi smoother (smoother=0, contract C4)."""
     p = tiny(N=N, matching=matching, e_max=e_max)
-    o = oracle_lib.Oracle.from_problem(p, coarsest_size=16)
+    o = oracle_lib.Oracle.from_problem(p, coarsest_size=16, smoother=0)
     assert o.nlev >= 2
     B = dense_op(o.vcycle, p.n)
     Bref = _dense_vcycle(o)
