@@ -170,11 +170,12 @@ __global__ void __launch_bounds__(1024) k_nd_off_band(const int2 *pairs, const N
   extern __shared__ __align__(128) double ring[];  // [S.len][M] rings, then [OB_NS][OB_RC][W] band rows
   __shared__ __align__(8) uint64_t bar[OB_NS];
   const NdBlk S = blk[pairs[blockIdx.x].x], B = blk[pairs[blockIdx.x].y];
-  const int s = threadIdx.x;
+  const int s = blockIdx.y * blockDim.x + threadIdx.x;  // wide separators: rows split over grid.y
+  if ((int)(blockIdx.y * blockDim.x) >= S.len) return;
   const bool act = s < S.len;
-  double *Lbuf = ring + (((long)S.len * M + 15) & ~15L);
+  double *Lbuf = ring + (((long)blockDim.x * M + 15) & ~15L);
   const int nch = (B.len + OB_RC - 1) / OB_RC;
-  if (s == 0) {
+  if (threadIdx.x == 0) {
     for (int q = 0; q < OB_NS; q++) mbar_init(&bar[q], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -186,13 +187,13 @@ __global__ void __launch_bounds__(1024) k_nd_off_band(const int2 *pairs, const N
     mbar_arrive_expect(&bar[ch % OB_NS], bytes);
     bulk_g2s(Lbuf + (long)(ch % OB_NS) * OB_RC * W, Lrow + (long)r0 * W, bytes, &bar[ch % OB_NS]);
   };
-  if (s == 0)
+  if (threadIdx.x == 0)
     for (int ch = 0; ch < OB_NS - 1; ch++) issue(ch);
-  double *rs = ring + (long)min(s, S.len - 1) * M;
+  double *rs = ring + (long)threadIdx.x * M;
   double *Ls = Loff + S.off + (long)min(s, S.len - 1) * S.rs - S.t0;  // Ls[k] = L_sk
   double init = act ? Ls[B.p0] : 0.0;
   for (int ch = 0; ch < nch; ch++) {
-    if (s == 0) issue(ch + OB_NS - 1);
+    if (threadIdx.x == 0) issue(ch + OB_NS - 1);
     mbar_wait(&bar[ch % OB_NS], (ch / OB_NS) & 1);
     const double *stage = Lbuf + (long)(ch % OB_NS) * OB_RC * W;
     const int jb = B.p0 + ch * OB_RC, je = min(jb + OB_RC, B.p0 + B.len);
@@ -460,15 +461,21 @@ void nd_symbolic(Ctx &c) {
 static void launch_off_band(Ctx &c, int np, const int *pairs, const NdBlk *blk, int bw, int W) {
   if (!np) return;
   const int M = bw | 1;  // ring length >= bw, odd (bank-conflict-free rows)
-  const int threads = (c.nd_maxsep + 31) / 32 * 32;
-  const size_t smem = ((((size_t)c.nd_maxsep * M + 15) & ~(size_t)15) + (size_t)OB_NS * OB_RC * W) * sizeof(double);
-  REQUIRE(threads <= 1024 && smem <= 227 * 1024, AMGF_ERR_LIMIT, "separator too wide for the off-block factor kernel");
+  auto smem_of = [&](int t) {
+    return ((((size_t)t * M + 15) & ~(size_t)15) + (size_t)OB_NS * OB_RC * W) * sizeof(double);
+  };
+  // as many separator rows per CTA as the rings fit in shared memory; the rest go to grid.y
+  int threads = std::min(1024, (c.nd_maxsep + 31) / 32 * 32);
+  while (threads > 32 && smem_of(threads) > 227 * 1024) threads -= 32;
+  const size_t smem = smem_of(threads);
+  REQUIRE(smem <= 227 * 1024, AMGF_ERR_LIMIT, "band too wide for the off-block factor kernel");
+  const dim3 grid(np, (c.nd_maxsep + threads - 1) / threads);
   static size_t attr = 0;
   if (smem > attr) {
     CK(cudaFuncSetAttribute(k_nd_off_band, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
-  k_nd_off_band<<<np, threads, smem, c.stream>>>((const int2 *)pairs, blk, bw, W, M, c.Lrow, c.Loff);
+  k_nd_off_band<<<grid, threads, smem, c.stream>>>((const int2 *)pairs, blk, bw, W, M, c.Lrow, c.Loff);
   after_launch(c, "k_nd_off_band");
 }
 
