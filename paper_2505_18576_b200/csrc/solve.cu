@@ -157,6 +157,10 @@ __global__ void __launch_bounds__(CTA) k_sell(int nrows, const int *__restrict__
 
 // Latency-oriented variant for scalar-row (1 x BC) SELL of the small coarse levels: D slots of values and
 // x in flight (register ring, fully unrolled), column indices 2D slots ahead.  Same chain as k_sell (C2).
+__constant__ int c_r1_prefetch;  // L2 prefetch distance of k_sell_r1 in slots (0: off; 8 measured best:
+                                 // V-cycle 1030 -> 1018 us at cfg 3; 16 and 32 are slower)
+__device__ __forceinline__ int r1_prefetch_slots() { return c_r1_prefetch; }
+
 template <int BC, int MODE, int D>
 __global__ void __launch_bounds__(CTA) k_sell_r1(int nrows, const int *__restrict__ slice_ptr,
                                                  const int *__restrict__ rowlen, const int *__restrict__ col,
@@ -188,7 +192,27 @@ __global__ void __launch_bounds__(CTA) k_sell_r1(int nrows, const int *__restric
     for (int e = 0; e < BC; e++) rx[q][e] = x[(long)rc[q] * BC + e];
     rc[q] = ldg_stream_i(cp + (long)min(q + D, last) * 32);
   }
+  // L2 prefetch window (pf slots ahead of the register ring): the slice's values of slots
+  // [s0 + pf, s0 + pf + D) by one TMA bulk prefetch from the lowest active lane, so the ring's loads
+  // find their lines in L2 (long rows of the large coarse levels are latency chains)
+  const int pf = r1_prefetch_slots();
+  const int sw = slice_ptr[(row >> 5) + 1] - (int)base;
+  const char *vslice = (const char *)(val + base * (BC * 32));
+  if (pf > 0 && lane == __ffs(__activemask()) - 1) {
+    const int p1 = min(D + pf, sw);
+    if (p1 > D)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(vslice + (long)D * BC * 32 * 8),
+                   "r"((p1 - D) * BC * 32 * 8)
+                   : "memory");
+  }
   for (int s0 = 0; s0 < len; s0 += D) {
+    if (pf > 0 && lane == __ffs(__activemask()) - 1) {
+      const int p0 = s0 + D + pf, p1 = min(p0 + D, sw);
+      if (p1 > p0)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(vslice + (long)p0 * BC * 32 * 8),
+                     "r"((p1 - p0) * BC * 32 * 8)
+                     : "memory");
+    }
 #pragma unroll
     for (int q = 0; q < D; q++) {
       const int sl = s0 + q;
@@ -229,6 +253,14 @@ static void sell_dispatch(Ctx &c, const Sell &A, int mode, const double *x, cons
                           const double *add, double *y, double *dp, ChebArgs ch = ChebArgs{}) {
   dim3 g(nblk(A.nrows)), t(CTA);
   if (A.nrows == 0) return;
+  {
+    static bool pf_set = false;
+    if (!pf_set) {
+      pf_set = true;
+      const int pf = getenv("AMGF_R1_PF") ? atoi(getenv("AMGF_R1_PF")) : 8;  // measured: 8 slots best
+      CK(cudaMemcpyToSymbol(c_r1_prefetch, &pf, sizeof(int)));
+    }
+  }
   {
     // An explicit carveout preference for the residual SpMV lets the A_w solve, which runs concurrently on
     // the filter stream (apply_M), get SMs while the SpMV is resident: the driver default cost ~50 us per
