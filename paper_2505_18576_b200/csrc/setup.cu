@@ -1438,29 +1438,67 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
 }
 
 // =================================================================== numeric re-setup (new D)
+// Optional phase timing of the numeric re-setup (AMGF_SETUP_TIMING=1, tools only): CUDA events on the main
+// stream after each phase, printed to stderr.
+struct PhaseTimer {
+  bool on = false;
+  cudaStream_t st = nullptr;
+  std::vector<std::pair<const char *, cudaEvent_t>> ev;
+  void mark(const char *name) {
+    if (!on) return;
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    CK(cudaEventRecord(e, st));
+    ev.emplace_back(name, e);
+  }
+  void report() {
+    if (!on || ev.empty()) return;
+    CK(cudaEventSynchronize(ev.back().second));
+    fprintf(stderr, "update_D phases (ms):");
+    for (size_t i = 1; i < ev.size(); i++) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second));
+      fprintf(stderr, " %s %.2f", ev[i].first, ms);
+    }
+    fprintf(stderr, "\n");
+    for (auto &p : ev) cudaEventDestroy(p.second);
+  }
+};
+
 void setup_numeric(Ctx &c, const double *D) {
   Caches &C = caches(c);
+  static const bool timing = getenv("AMGF_SETUP_TIMING") != nullptr;
+  PhaseTimer pt;
+  pt.on = timing;
+  pt.st = c.stream;
+  pt.mark("start");
   d2d(c, c.D, D, c.m);
   LAUNCH(k_check_finite, c.m, c.m, c.D, c.err, DERR_NONFINITE);
   LAUNCH(k_check_pos, c.m, c.m, c.D, c.err);
   check_dev_error(c, "D check");
   S_numeric(c, C.s.S_rowof);
+  pt.mark("S");
   Level &L0 = c.lev[0];
   if (c.nc > 0) {
     fork_filter(c);
     thin_numeric(c, C.thin_nnz);
   }
   LAUNCH(k_diag, L0.n, L0.nodes, 3, L0.A.ptr, L0.A.col, L0.A.val, L0.dl1, L0.dpt);
+  static const char *lvname[] = {"level0", "level1", "level2", "level3", "level4", "level5"};
   for (int l = 0; l + 1 < c.nlev; l++) {
     build_sell(c, c.lev[l].A, c.lev[l].As, false, l > 0);
     level_numeric(c, l, C.lc[l]);
     check_dev_error(c, "Galerkin product");
     build_sell(c, c.lev[l].P, c.lev[l].Ps, false, l > 0);
+    pt.mark(l < 6 ? lvname[l] : "level");
   }
   if (c.nlev == 1) build_sell(c, L0.A, L0.As, false, false);
   coarsest_numeric(c);
+  pt.mark("coarsest");
   join_filter(c);
+  pt.mark("join(A_w)");
   check_dev_error(c, "numeric setup (A_w / coarsest Cholesky)");
+  pt.report();
 }
 
 }  // namespace amgf

@@ -12,8 +12,11 @@ from paper_2505_18576_b200 import AMGF  # noqa: E402
 p = amgf_gen.config(int(sys.argv[1]) if len(sys.argv) > 1 else 3)
 b = torch.from_numpy(p.b).cuda()
 systems = [0, 5, 9] if p.D_seq.shape[0] >= 10 else [0]
-for name, cfg in (("l1-jacobi", {}), ("cheb2", dict(smoother=1, cheb_degree=2)),
-                  ("cheb3", dict(smoother=1, cheb_degree=3))):
+variants = (("l1-jacobi", dict(smoother=0)), ("cheb2", dict(smoother=1, cheb_degree=2)),
+            ("cheb3", dict(smoother=1, cheb_degree=3)))
+if len(sys.argv) > 2:  # extra: JSON list of [name, config] pairs
+    variants = json.loads(sys.argv[2])
+for name, cfg in variants:
     g = AMGF.from_problem(p, D=p.D_seq[systems[0]], config=cfg)
     for s in systems:
         g.update_D(torch.from_numpy(p.D_seq[s]).cuda())
