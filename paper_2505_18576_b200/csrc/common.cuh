@@ -164,6 +164,7 @@ struct Ctx {
   double *p = nullptr, *q = nullptr, *rr = nullptr, *zz = nullptr, *xx = nullptr, *bb = nullptr;
   double *dot_part = nullptr;
   double *pw_v = nullptr, *pw_w = nullptr;  // power-iteration work vectors (allocated once)
+  double *pw_s = nullptr;                    // power-iteration scalars {w.w, v.v, lambda}
   Scalars *sc = nullptr;      // device
   Scalars *sc_host = nullptr; // pinned
   int *err = nullptr;         // device [2]

@@ -612,6 +612,15 @@ __global__ void k_scale_div(long n, const double *w, double s, double *v) {
   long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
   if (i < n) v[i] = w[i] / s;
 }
+// power step on the device (C18): pw[0] = w.w, pw[1] = v.v (copied from the dot result); ||w|| = sqrt(pw[0]),
+// lambda = ||w|| / sqrt(pw[1]) into pw[2]; v = w / ||w|| -- the host's formulas, no host round trip
+__global__ void k_pow_keep(const Scalars *sc, double *pw, int slot) { pw[slot] = sc->dot; }
+__global__ void k_pow_scale(long n, const double *w, double *pw, double *v) {
+  const double nw = sqrt(pw[0]);
+  long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (i == 0) pw[2] = nw / sqrt(pw[1]);
+  if (i < n) v[i] = w[i] / nw;
+}
 
 constexpr int PCAP = 128;
 __global__ void k_P_count(int nodes, const int *ptr, const int *col, const int *agg, int *cnt, int *err) {
@@ -1007,20 +1016,21 @@ static void power_iteration(Ctx &c, Level &L) {
     c.pw_w = c.alloc<double>(c.n);
   }
   double *v = c.pw_v, *w = c.pw_w;
+  if (!c.pw_s) c.pw_s = c.alloc<double>(4);
   LAUNCH(k_pow_init, L.n, L.n, v);
-  double lam = 0.0;
   for (int it = 0; it < c.cfg.power_iters; it++) {
     if (L.As.val) launch_sell_spmv(c, L.As, SPMV_Y, v, nullptr, nullptr, nullptr, w, nullptr);
     else launch_bsr_spmv(c, L.A, v, w);
     LAUNCH(k_div, L.n, L.n, w, L.dpt);
     launch_dot(c, L.n, L.b, w, w, DOT_PLAIN);
-    double ww = d2h1(c, &c.sc->dot);
+    k_pow_keep<<<1, 1, 0, c.stream>>>(c.sc, c.pw_s, 0);
+    after_launch(c, "k_pow_keep");
     launch_dot(c, L.n, L.b, v, v, DOT_PLAIN);
-    double vv = d2h1(c, &c.sc->dot);
-    double nw = sqrt(ww), nv = sqrt(vv);
-    lam = nw / nv;
-    LAUNCH(k_scale_div, L.n, L.n, w, nw, v);
+    k_pow_keep<<<1, 1, 0, c.stream>>>(c.sc, c.pw_s, 1);
+    after_launch(c, "k_pow_keep");
+    LAUNCH(k_pow_scale, L.n, L.n, w, c.pw_s, v);
   }
+  const double lam = d2h1(c, c.pw_s + 2);  // one host read per level (omega is a kernel argument)
   L.lambda = lam;
   L.omega = 4.0 / (3.0 * lam);
 }
