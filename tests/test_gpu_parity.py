@@ -299,14 +299,14 @@ def test_full_size_cfg3(oracle_lib, amgf_mod, torch_cuda):
     assert np.linalg.norm(S @ xs - p.b) <= 1e-5 * np.linalg.norm(p.b)
 
 
-@pytest.mark.parametrize("cfg", [1, 2, 3])
-def test_fused_tail_matches_level_kernels(oracle_lib, amgf_mod, torch_cuda, cfg, monkeypatch):
+@pytest.mark.parametrize("cfg,smoother", [(1, 1), (2, 1), (3, 1), (3, 0)])
+def test_fused_tail_matches_level_kernels(oracle_lib, amgf_mod, torch_cuda, cfg, smoother, monkeypatch):
     """The fused coarse-tail kernel (tail.cu: one cluster launch for the two coarsest levels) gives the
-    same bits as the separate level kernels (AMGF_NO_TAIL=1), and at cfg 2 as the oracle."""
+    same bits as the separate level kernels (AMGF_NO_TAIL=1), for both smoothers, and at cfg 2 as the oracle."""
     p = gen.config(cfg)
-    g = amgf_mod.AMGF.from_problem(p)
+    g = amgf_mod.AMGF.from_problem(p, config=dict(smoother=smoother))
     monkeypatch.setenv("AMGF_NO_TAIL", "1")
-    h = amgf_mod.AMGF.from_problem(p)
+    h = amgf_mod.AMGF.from_problem(p, config=dict(smoother=smoother))
     monkeypatch.delenv("AMGF_NO_TAIL")
     assert h.tail_level == -1
     if cfg == 3:
@@ -361,6 +361,19 @@ def test_chebyshev_smoother_parity(oracle_lib, amgf_mod, torch_cuda, k):
     o, g = build_pair(oracle_lib, amgf_mod, p, **cfg)
     r = np.random.default_rng(40).standard_normal(p.n)
     assert np.array_equal(g.vcycle(r).cpu().numpy(), o.vcycle(r))
+    xo, ro = o.pcg(p.b, rtol=p.rtol)
+    xg, rg = g.pcg(p.b, rtol=p.rtol)
+    assert rg["iterations"] == ro["iterations"] and np.array_equal(xg.cpu().numpy(), xo)
+
+
+def test_l1_jacobi_smoother_parity(oracle_lib, amgf_mod, torch_cuda):
+    """l1-Jacobi smoother (smoother=0, contract C4; the default before R18): V-cycle, apply, PCG iterations and
+    solution bitwise vs the oracle at cfg 1."""
+    p = gen.config(1)
+    o, g = build_pair(oracle_lib, amgf_mod, p, smoother=0)
+    r = np.random.default_rng(50).standard_normal(p.n)
+    assert np.array_equal(g.vcycle(r).cpu().numpy(), o.vcycle(r))
+    assert np.array_equal(g.apply(r).cpu().numpy(), o.apply(r))
     xo, ro = o.pcg(p.b, rtol=p.rtol)
     xg, rg = g.pcg(p.b, rtol=p.rtol)
     assert rg["iterations"] == ro["iterations"] and np.array_equal(xg.cpu().numpy(), xo)
