@@ -162,14 +162,14 @@ void apply_M(Ctx &c, const double *r, double *z) {
     int lo = 0, hi = 0;
     CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CK(cudaStreamCreateWithPriority(&c.fstream, cudaStreamNonBlocking, hi));
-    // SM partition for the overlap: the residual SpMV runs on ~65 % of the SMs (96 of 148 measured best at
-    // cfg 3: it still ends first, ~230 us, while the A_w solve gets SMs of its own; the A_w solve alone takes
-    // 279 us, 326 us next to the partitioned SpMV, 383 us next to the unpartitioned one).  An L2 persistence
-    // window for the A_w data was measured too and did not help (it costs the V-cycles L2 capacity).
+    // SM partition for the overlap: the residual SpMV runs on 80 of the 148 SMs (measured at cfg 3 with PDL:
+    // 80 SMs -> A_w solve done at 250 us, SpMV at 257 us; 84-96 SMs -> A_w solve 278-284 us, SpMV 235-255 us;
+    // the A_w solve alone takes 234 us, and 383 us next to the unpartitioned SpMV).  An L2 persistence window
+    // for the A_w data was measured too and did not help (it costs the V-cycles L2 capacity).
     int dev = 0, nsm = 0;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    c.resid_sms = std::max(1, nsm * 96 / 148);
+    c.resid_sms = std::max(1, nsm * 80 / 148);
     CK(cudaEventCreateWithFlags(&c.ev_f0, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c.ev_f1, cudaEventDisableTiming));
   }
