@@ -88,7 +88,7 @@ void check_dev_error(Ctx &c, const char *where) {
 }
 
 // ------------------------------------------------------------------ V-cycle
-void vcycle(Ctx &c, int l, const double *b, double *x, const double *add) {
+void vcycle(Ctx &c, int l, const double *b, double *x, const double *add, VcOpts o) {
   Level &L = c.lev[l];
   if (l == c.nlev - 1) {
     double *dst = add ? L.x2 : x;
@@ -112,7 +112,7 @@ void vcycle(Ctx &c, int l, const double *b, double *x, const double *add) {
                        first ? 0.0 : c.cheb_b[s], addp, bufs[1 - ci]);
       ci = 1 - ci;
     };
-    launch_cheb0(c, L.n, b, L.dl1, c.cheb_c0, L.dir, bufs[ci]);
+    if (!o.prestarted) launch_cheb0(c, L.n, b, L.dl1, c.cheb_c0, L.dir, bufs[ci]);
     for (int s = 1; s < k; s++) step(false, s, nullptr);
     for (int sw = 1; sw < pre; sw++) {
       step(true, 0, nullptr);
@@ -123,7 +123,16 @@ void vcycle(Ctx &c, int l, const double *b, double *x, const double *add) {
     vcycle(c, l + 1, Lc.bv, Lc.x, nullptr);
     launch_prolong(c, L.Ps, Lc.x, bufs[ci]);
     for (int sw = 0; sw < post; sw++)
-      for (int s = 0; s < k; s++) step(s == 0, s, (add && sw == post - 1 && s == k - 1) ? add : nullptr);
+      for (int s = 0; s < k; s++) {
+        const bool last = (sw == post - 1 && s == k - 1);
+        if (last && o.dot_r && s > 0) {  // final step fused with the PCG dot's level-1 partials (C14)
+          launch_sell_cheb(c, L.As, false, bufs[ci], b, L.dl1, L.dir, c.cheb_a[s], c.cheb_b[s], add,
+                           bufs[1 - ci], o.dot_r);
+          ci = 1 - ci;
+        } else {
+          step(s == 0, s, (add && last) ? add : nullptr);
+        }
+      }
     return;
   }
   double *bufs[2] = {x, L.x2};
@@ -146,13 +155,15 @@ void vcycle(Ctx &c, int l, const double *b, double *x, const double *add) {
 }
 
 // ------------------------------------------------------------------ AMGF apply (C11)
-void apply_M(Ctx &c, const double *r, double *z) {
+void apply_M(Ctx &c, const double *r, double *z, VcOpts first, const double *dot_r) {
   Level &L0 = c.lev[0];
-  vcycle(c, 0, r, c.w_x1, nullptr);
+  vcycle(c, 0, r, c.w_x1, nullptr, first);
   if (c.nc == 0) {
     // I_c empty: filter stage is the identity
     launch_sell_spmv(c, L0.As, SPMV_RESID, c.w_x1, r, nullptr, nullptr, c.w_r1, nullptr);
-    vcycle(c, 0, c.w_r1, z, c.w_x1);
+    VcOpts second;
+    second.dot_r = dot_r;
+    vcycle(c, 0, c.w_r1, z, c.w_x1, second);
     return;
   }
   // r1 at the Z rows first (pi order), then the A_w solve on the high-priority filter stream while the
@@ -212,7 +223,9 @@ void apply_M(Ctx &c, const double *r, double *z) {
   }
   nd_scatter(c, c.w_x1);  // x2 = x1 + P y
   launch_thin_resid(c, c.nthin, c.thin_row, c.thin_ptr, c.thin_pos, c.thin_val, c.fv, c.w_r1);
-  vcycle(c, 0, c.w_r1, z, c.w_x1);
+  VcOpts second;
+  second.dot_r = dot_r;
+  vcycle(c, 0, c.w_r1, z, c.w_x1, second);
 }
 
 // ------------------------------------------------------------------ PCG (C15)
@@ -224,10 +237,29 @@ static void pcg_body(Ctx &c, int precond, bool host_copies = true) {
   const long n = c.n;
   launch_sell_spmv(c, c.lev[0].As, SPMV_DOT, c.p, nullptr, nullptr, nullptr, c.q, c.dot_part);
   launch_dot_finish(c, nblk(c.lev[0].As.nrows), DOT_PI);  // pi = p.q, alpha = rho / pi
-  launch_axpy2(c, n, c.p, c.q, c.xx, c.rr);
-  if (precond == 0) apply_M(c, c.rr, c.zz);
-  else vcycle(c, 0, c.rr, c.zz, nullptr);
-  launch_dot(c, n, 3, c.rr, c.zz, DOT_RHO1);             // rho' = r.z, beta = rho'/rho, rho = rho'
+  // Chebyshev: the x, r update also writes the from-zero start of V-cycle #1 at level 0, and the last level-0
+  // step of the last V-cycle forms the partials of r.z (both bitwise the same as the separate kernels)
+  Level &L0 = c.lev[0];
+  const bool pre0 = (c.cfg.smoother == 1 && c.nlev >= 2);
+  const bool fdot = pre0 && c.cfg.cheb_degree >= 2;
+  if (pre0) {
+    const int k = c.cfg.cheb_degree, pre = c.cfg.pre_sweeps, post = c.cfg.post_sweeps;
+    const int ci = ((k - 1) + (pre - 1) * k + post * k) & 1;  // vcycle's start-buffer parity
+    double *xs = ci ? L0.x2 : (precond == 0 ? c.w_x1 : c.zz);
+    launch_axpy2_cheb0(c, n, c.p, c.q, c.xx, c.rr, L0.dl1, c.cheb_c0, L0.dir, xs);
+  } else {
+    launch_axpy2(c, n, c.p, c.q, c.xx, c.rr);
+  }
+  VcOpts first;
+  first.prestarted = pre0;
+  if (precond == 0) {
+    apply_M(c, c.rr, c.zz, first, fdot ? c.rr : nullptr);
+  } else {
+    first.dot_r = fdot ? c.rr : nullptr;
+    vcycle(c, 0, c.rr, c.zz, nullptr, first);
+  }
+  if (fdot) launch_dot_finish(c, nblk(L0.As.nrows), DOT_RHO1);  // rho' = r.z, beta = rho'/rho, rho = rho'
+  else launch_dot(c, n, 3, c.rr, c.zz, DOT_RHO1);
   launch_xpby(c, n, c.zz, c.p);
   if (host_copies) {
     CK(cudaMemcpyAsync(c.sc_host, c.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, c.stream));

@@ -233,9 +233,13 @@ enum SpmvMode { SPMV_Y = 0, SPMV_RESID = 1, SPMV_SMOOTH = 2, SPMV_DOT = 3, SPMV_
 struct ChebArgs {  // Chebyshev step of the SpMV epilogue (solve.cu, contract C23)
   double ca = 0.0, cb = 0.0;
   double *dir = nullptr;
+  const double *dot_r = nullptr;  // fused dot(dot_r, y) partials (C14 level 1) into dot_part, or null
+  double *dot_part = nullptr;
 };
 void launch_sell_cheb(Ctx &c, const Sell &A, bool first, const double *x, const double *b, const double *dl1,
-                      double *dir, double ca, double cb, const double *add, double *y);
+                      double *dir, double ca, double cb, const double *add, double *y, const double *dot_r = nullptr);
+void launch_axpy2_cheb0(Ctx &c, long n, const double *p, const double *q, double *x, double *r, const double *d,
+                        double c0, double *dir, double *xs);
 void launch_cheb0(Ctx &c, long n, const double *b, const double *d, double c0, double *dir, double *x);
 void launch_sell_spmv(Ctx &c, const Sell &A, int mode, const double *x, const double *b, const double *d,
                       const double *add, double *y, double *dot_part);
@@ -288,9 +292,16 @@ void drop_caches(Ctx &c);
 void build_sell(Ctx &c, const Bsr &A, Sell &S, bool alloc, bool split, bool sort_rows = false);
 
 // ------------------------------------------------------------------ solve orchestration (api.cu)
-void vcycle(Ctx &c, int l, const double *b, double *x, const double *add);
+// Fusion hooks of the PCG iteration into the V-cycles (Chebyshev smoother only; bitwise unchanged):
+//   prestarted  level 0's from-zero start (dir, start buffer) was written by k_axpy2_cheb0
+//   dot_r       the last level-0 step also forms the C14 partials of dot(dot_r, x) into c.dot_part
+struct VcOpts {
+  bool prestarted = false;
+  const double *dot_r = nullptr;
+};
+void vcycle(Ctx &c, int l, const double *b, double *x, const double *add, VcOpts o = VcOpts{});
 void tail_plan(Ctx &c);                                   // after setup_all: enable the fused coarse tail
 void tail_vcycle(Ctx &c, const double *b, double *x);    // V-cycle from level c.tail_level down, one launch
-void apply_M(Ctx &c, const double *r, double *z);
+void apply_M(Ctx &c, const double *r, double *z, VcOpts first = VcOpts{}, const double *dot_r = nullptr);
 
 }  // namespace amgf

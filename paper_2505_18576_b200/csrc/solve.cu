@@ -42,14 +42,15 @@ __device__ __forceinline__ double cta_tree(double v, double *s) {
 }
 
 enum { MODE_Y = SPMV_Y, MODE_RESID = SPMV_RESID, MODE_SMOOTH = SPMV_SMOOTH, MODE_DOT = SPMV_DOT,
-       MODE_SMOOTH_ADD = SPMV_SMOOTH_ADD, MODE_ADDTO = 5, MODE_CHEB1 = SPMV_CHEB1, MODE_CHEB = SPMV_CHEB };
+       MODE_SMOOTH_ADD = SPMV_SMOOTH_ADD, MODE_ADDTO = 5, MODE_CHEB1 = SPMV_CHEB1, MODE_CHEB = SPMV_CHEB,
+       MODE_CHEB_DOT = 8 };
 
 // Chebyshev step epilogue (contract C23): t = (b - acc)/d; first step dir = ca t, later dir = fma(ca, dir,
 // cb t); x_new = x + dir (then add + x_new when add is given, as SMOOTH_ADD).
 __device__ __forceinline__ double cheb_epilogue(int mode, double res, double di, double xi, double *dir, long i,
                                                 double ca, double cb, const double *add) {
   const double t = res / di;
-  const double dv = (mode == MODE_CHEB1) ? ca * t : __fma_rn(ca, dir[i], cb * t);
+  const double dv = (mode == MODE_CHEB1) ? ca * t : __fma_rn(ca, dir[i], cb * t);  // MODE_CHEB(_DOT)
   dir[i] = dv;
   double xn = xi + dv;
   if (add) xn = add[i] + xn;
@@ -130,6 +131,22 @@ __global__ void __launch_bounds__(CTA) k_sell(int nrows, const int *__restrict__
     }
     double tot = cta_tree(s, red);
     if (threadIdx.x == 0) dot_part[blockIdx.x] = tot;
+    return;
+  }
+  if (MODE == MODE_CHEB_DOT) {  // last Chebyshev step (+ add) fused with the C14 partials of dot(r, y)
+    __shared__ double red2[CTA];
+    double s = 0.0;
+    if (row < nrows) {
+#pragma unroll
+      for (int r = 0; r < BR; r++) {
+        const long i = (long)row * BR + r;
+        const double yi = cheb_epilogue(MODE_CHEB, b[i] - acc[r], d[i], x[i], ch.dir, i, ch.ca, ch.cb, add);
+        y[i] = yi;
+        s = __fma_rn(ch.dot_r[i], yi, s);
+      }
+    }
+    double tot = cta_tree(s, red2);
+    if (threadIdx.x == 0) ch.dot_part[blockIdx.x] = tot;
     return;
   }
   if (row >= nrows) return;
@@ -293,6 +310,7 @@ static void sell_dispatch(Ctx &c, const Sell &A, int mode, const double *x, cons
     case MODE_ADDTO: k_sell<BR, BC, MODE_ADDTO><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
     case MODE_CHEB1: k_sell<BR, BC, MODE_CHEB1><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
     case MODE_CHEB: k_sell<BR, BC, MODE_CHEB><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
+    case MODE_CHEB_DOT: k_sell<BR, BC, MODE_CHEB_DOT><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
   }
   after_launch(c, __func__);
 }
@@ -306,12 +324,35 @@ void launch_sell_spmv(Ctx &c, const Sell &A, int mode, const double *x, const do
 }
 
 void launch_sell_cheb(Ctx &c, const Sell &A, bool first, const double *x, const double *b, const double *dl1,
-                      double *dir, double ca, double cb, const double *add, double *y) {
-  const ChebArgs ch{ca, cb, dir};
-  const int mode = first ? MODE_CHEB1 : MODE_CHEB;
+                      double *dir, double ca, double cb, const double *add, double *y, const double *dot_r) {
+  const ChebArgs ch{ca, cb, dir, dot_r, c.dot_part};
+  REQUIRE(!dot_r || (!first && A.br == 3 && A.bc == 3 && !A.perm), AMGF_ERR_ARG, "fused dot: fine level, later step");
+  const int mode = dot_r ? MODE_CHEB_DOT : (first ? MODE_CHEB1 : MODE_CHEB);
   if (A.br == 3 && A.bc == 3) sell_dispatch<3, 3>(c, A, mode, x, b, dl1, add, y, nullptr, ch);
   else if (A.br == 1 && A.bc == 6) sell_dispatch<1, 6>(c, A, mode, x, b, dl1, add, y, nullptr, ch);
   else throw Error{AMGF_ERR_ARG, "sell cheb: unsupported block shape"};
+}
+
+// PCG update (C15) fused with the from-zero Chebyshev start of the next V-cycle #1 at level 0 (C23):
+// x = fma(alpha, p, x); r = fma(-alpha, q, r); t = r/d; dir = c0 t; xs = dir.
+__global__ void k_axpy2_cheb0(long n, const Scalars *__restrict__ sc, const double *__restrict__ p,
+                              const double *__restrict__ q, double *__restrict__ x, double *__restrict__ r,
+                              const double *__restrict__ d, double c0, double *__restrict__ dir,
+                              double *__restrict__ xs) {
+  const double a = sc->alpha;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    x[i] = __fma_rn(a, p[i], x[i]);
+    const double rn = __fma_rn(-a, q[i], r[i]);
+    r[i] = rn;
+    const double v = c0 * (rn / d[i]);
+    dir[i] = v;
+    xs[i] = v;
+  }
+}
+void launch_axpy2_cheb0(Ctx &c, long n, const double *p, const double *q, double *x, double *r, const double *d,
+                        double c0, double *dir, double *xs) {
+  k_axpy2_cheb0<<<nblk(n), CTA, 0, c.stream>>>(n, c.sc, p, q, x, r, d, c0, dir, xs);
+  after_launch(c, "k_axpy2_cheb0");
 }
 
 // Chebyshev application from x = 0 (C23): t = b/d, dir = c0 t, x = dir.
