@@ -149,7 +149,8 @@ def run_amgf(args, rank, world, local_rank):
 
     t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
-    g = AMGF.from_problem(p, D=p.D_seq[rank % nsys], stream=stream)
+    cfg_over = json.loads(os.environ["AMGF_BENCH_CONFIG"]) if os.environ.get("AMGF_BENCH_CONFIG") else None
+    g = AMGF.from_problem(p, D=p.D_seq[rank % nsys], stream=stream, config=cfg_over)
     t1.record(stream); t1.synchronize()
     full_setup_ms = t0.elapsed_time(t1)
 
