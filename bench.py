@@ -166,6 +166,7 @@ def run_amgf(args, rank, world, local_rank):
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream); g.update_D(D_dev[0]); e1.record(stream); e1.synchronize()
     upd_ms = e0.elapsed_time(e1)
+    upd_breakdown = g.setup_times()
 
     launches0 = g.launches
     clocks = Clocks(local_rank)
@@ -276,6 +277,7 @@ def run_amgf(args, rank, world, local_rank):
         "systems": systems,
         "solve_ms_per_system": solve_ms,
         "numeric_setup_ms": upd_ms,
+        "numeric_setup_breakdown_ms": upd_breakdown,
         "full_setup_ms": full_setup_ms,
         "vcycle_ms": vcycle_ms,
         "vcycle_gbs": vb / (vcycle_ms * 1e-3) / 1e9,

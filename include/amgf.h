@@ -133,6 +133,11 @@ amgf_status amgf_level_get(amgf_handle h, int32_t which, int32_t level, void *ds
  * operator).  AMGF_ERR_ARG if n exceeds the iterations of the last solve. */
 amgf_status amgf_pcg_history(amgf_handle h, int32_t n, double *alpha, double *beta);
 
+/* Device times (CUDA events, ms) of the last amgf_update_D into HOST ms[5]: {total, S = K + J^T D J,
+ * hierarchy (power iterations, prolongators, Galerkin products, SELL refresh), coarsest Cholesky, A_w
+ * factorization (side stream, concurrent with the hierarchy)}.  Zeros before the first update. */
+amgf_status amgf_setup_times(amgf_handle h, double *ms);
+
 /* Number of kernel launches issued by this handle since creation (bench accounting). */
 int64_t amgf_launch_count(amgf_handle h);
 

@@ -18,7 +18,7 @@ STATUS = {0: "AMGF_OK", 1: "AMGF_NOT_CONVERGED", -1: "AMGF_ERR_ARG", -2: "AMGF_E
 
 SYMBOLS = ["amgf_default_config", "amgf_setup", "amgf_update_D", "amgf_apply", "amgf_vcycle", "amgf_spmv",
            "amgf_pcg_solve", "amgf_pcg_solve_host", "amgf_level_info", "amgf_level_get", "amgf_launch_count",
-           "amgf_pcg_history", "amgf_last_error", "amgf_destroy"]
+           "amgf_pcg_history", "amgf_setup_times", "amgf_last_error", "amgf_destroy"]
 
 
 def lib_path() -> str:
@@ -71,6 +71,8 @@ def load_library():
     L.amgf_level_info.restype = I
     L.amgf_level_get.argtypes = [P, I, I, P]
     L.amgf_level_get.restype = I
+    L.amgf_setup_times.argtypes = [P, P]
+    L.amgf_setup_times.restype = I
     L.amgf_pcg_history.argtypes = [P, I, P, P]
     L.amgf_pcg_history.restype = I
     L.amgf_launch_count.argtypes = [P]
@@ -210,6 +212,12 @@ class AMGF:
         _check(st, allow=(0, 1))
         return dict(iterations=rep.iterations, converged=bool(rep.converged), relres=rep.rel_pres_norm,
                     solve_ms=rep.solve_ms)
+
+    def setup_times(self):
+        """Phase times (ms) of the last update_D: total, S, hierarchy, coarsest, A_w factor (side stream)."""
+        ms = np.zeros(5)
+        _check(load_library().amgf_setup_times(self.h, ms.ctypes.data_as(ctypes.c_void_p)))
+        return dict(zip(("total", "S", "hierarchy", "coarsest", "A_w_factor_side"), ms.tolist()))
 
     def history(self, n):
         """alpha_k, beta_k (k = 1..n) of the last PCG solve (numpy arrays)."""

@@ -41,6 +41,8 @@ Ctx::~Ctx() {
   if (ev_out) cudaEventDestroy(ev_out);
   if (side) cudaStreamDestroy(side);
   if (ev_fork) cudaEventDestroy(ev_fork);
+  for (auto &e : ph_ev)
+    if (e) cudaEventDestroy(e);
   if (fstream) cudaStreamDestroy(fstream);
   if (ev_f0) cudaEventDestroy(ev_f0);
   if (ev_f1) cudaEventDestroy(ev_f1);
@@ -683,6 +685,12 @@ amgf_status amgf_level_get(amgf_handle h, int32_t which, int32_t level, void *ds
 }
 
 int64_t amgf_launch_count(amgf_handle h) { return h ? h->launches : -1; }
+
+amgf_status amgf_setup_times(amgf_handle h, double *ms) {
+  if (!h || !ms) { set_error("null argument"); return AMGF_ERR_ARG; }
+  for (int i = 0; i < 5; i++) ms[i] = h->setup_ms[i];
+  return AMGF_OK;
+}
 
 amgf_status amgf_pcg_history(amgf_handle h, int32_t n, double *alpha, double *beta) {
   if (!h || (n > 0 && (!alpha || !beta))) { set_error("null argument"); return AMGF_ERR_ARG; }

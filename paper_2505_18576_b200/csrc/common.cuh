@@ -113,6 +113,8 @@ struct Ctx {
   double *nd_arena = nullptr;  // filter solve data (filter.cu) in one range
   size_t nd_arena_bytes = 0;
   int resid_sms = 0;
+  cudaEvent_t ph_ev[8] = {};  // numeric re-setup phase events (setup.cu)
+  double setup_ms[5] = {};    // last numeric re-setup: total, S, hierarchy, coarsest, A_w factor (side)
   double cheb_c0 = 0.0, cheb_a[33] = {}, cheb_b[33] = {};  // Chebyshev coefficients (C23)           // SMs of the residual SpMV that runs beside the A_w solve
   amgf_config cfg;
   int nodes = 0, m = 0;

@@ -1037,6 +1037,13 @@ static void filter_numeric(Ctx &c) {
 
 // Run the A_w band fill + Cholesky (single-SM kernel) on the side stream, concurrently with the
 // hierarchy's numeric setup on the main stream; join_filter() makes the main stream wait for it.
+// Phase events of the numeric re-setup (amgf_setup_times): main stream start / S formed / hierarchy done /
+// coarsest done / joined, side stream A_w factorization start / end.
+static void setup_mark(Ctx &c, int i, cudaStream_t st) {
+  if (!c.ph_ev[i]) CK(cudaEventCreate(&c.ph_ev[i]));
+  CK(cudaEventRecord(c.ph_ev[i], st));
+}
+
 static void fork_filter(Ctx &c) {
   if (c.nc == 0) return;
   if (!c.side) {
@@ -1048,6 +1055,7 @@ static void fork_filter(Ctx &c) {
   CK(cudaEventRecord(c.ev_fork, main));
   CK(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
   c.stream = c.side;
+  setup_mark(c, 5, c.side);
   try {
     filter_numeric(c);
   } catch (...) {
@@ -1055,6 +1063,7 @@ static void fork_filter(Ctx &c) {
     throw;
   }
   c.stream = main;
+  setup_mark(c, 6, c.side);
   CK(cudaEventRecord(c.ev_join, c.side));
 }
 static void join_filter(Ctx &c) {
@@ -1536,67 +1545,48 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
 }
 
 // =================================================================== numeric re-setup (new D)
-// Optional phase timing of the numeric re-setup (AMGF_SETUP_TIMING=1, tools only): CUDA events on the main
-// stream after each phase, printed to stderr.
-struct PhaseTimer {
-  bool on = false;
-  cudaStream_t st = nullptr;
-  std::vector<std::pair<const char *, cudaEvent_t>> ev;
-  void mark(const char *name) {
-    if (!on) return;
-    cudaEvent_t e;
-    CK(cudaEventCreate(&e));
-    CK(cudaEventRecord(e, st));
-    ev.emplace_back(name, e);
-  }
-  void report() {
-    if (!on || ev.empty()) return;
-    CK(cudaEventSynchronize(ev.back().second));
-    fprintf(stderr, "update_D phases (ms):");
-    for (size_t i = 1; i < ev.size(); i++) {
-      float ms = 0;
-      CK(cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second));
-      fprintf(stderr, " %s %.2f", ev[i].first, ms);
-    }
-    fprintf(stderr, "\n");
-    for (auto &p : ev) cudaEventDestroy(p.second);
-  }
-};
-
 void setup_numeric(Ctx &c, const double *D) {
   Caches &C = caches(c);
-  static const bool timing = getenv("AMGF_SETUP_TIMING") != nullptr;
-  PhaseTimer pt;
-  pt.on = timing;
-  pt.st = c.stream;
-  pt.mark("start");
+  setup_mark(c, 0, c.stream);
   d2d(c, c.D, D, c.m);
   LAUNCH(k_check_finite, c.m, c.m, c.D, c.err, DERR_NONFINITE);
   LAUNCH(k_check_pos, c.m, c.m, c.D, c.err);
   check_dev_error(c, "D check");
   S_numeric(c, C.s.S_rowof);
-  pt.mark("S");
+  setup_mark(c, 1, c.stream);
   Level &L0 = c.lev[0];
   if (c.nc > 0) {
     fork_filter(c);
     thin_numeric(c, C.thin_nnz);
   }
   LAUNCH(k_diag, L0.n, L0.nodes, 3, L0.A.ptr, L0.A.col, L0.A.val, L0.dl1, L0.dpt);
-  static const char *lvname[] = {"level0", "level1", "level2", "level3", "level4", "level5"};
   for (int l = 0; l + 1 < c.nlev; l++) {
     build_sell(c, c.lev[l].A, c.lev[l].As, false, l > 0);
     level_numeric(c, l, C.lc[l]);
     check_dev_error(c, "Galerkin product");
     build_sell(c, c.lev[l].P, c.lev[l].Ps, false, l > 0);
-    pt.mark(l < 6 ? lvname[l] : "level");
   }
   if (c.nlev == 1) build_sell(c, L0.A, L0.As, false, false);
+  setup_mark(c, 2, c.stream);
   coarsest_numeric(c);
-  pt.mark("coarsest");
+  setup_mark(c, 3, c.stream);
   join_filter(c);
-  pt.mark("join(A_w)");
+  setup_mark(c, 4, c.stream);
   check_dev_error(c, "numeric setup (A_w / coarsest Cholesky)");
-  pt.report();
+  auto ms = [&](int a, int b) {
+    float v = 0;
+    CK(cudaEventElapsedTime(&v, c.ph_ev[a], c.ph_ev[b]));
+    return (double)v;
+  };
+  CK(cudaEventSynchronize(c.ph_ev[4]));
+  c.setup_ms[0] = ms(0, 4);                           // total
+  c.setup_ms[1] = ms(0, 1);                           // S = K + J^T D J (+ D checks)
+  c.setup_ms[2] = ms(1, 2);                           // hierarchy: power iteration, P, Galerkin, SELL refresh
+  c.setup_ms[3] = ms(2, 3);                           // coarsest Cholesky
+  c.setup_ms[4] = c.nc > 0 ? ms(5, 6) : 0.0;          // A_w factorization (side stream, concurrent)
+  if (getenv("AMGF_SETUP_TIMING"))
+    fprintf(stderr, "update_D ms: total %.2f S %.2f hierarchy %.2f coarsest %.2f A_w(side) %.2f\n", c.setup_ms[0],
+            c.setup_ms[1], c.setup_ms[2], c.setup_ms[3], c.setup_ms[4]);
 }
 
 }  // namespace amgf
