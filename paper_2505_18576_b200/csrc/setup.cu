@@ -1047,7 +1047,12 @@ static void setup_mark(Ctx &c, int i, cudaStream_t st) {
 static void fork_filter(Ctx &c) {
   if (c.nc == 0) return;
   if (!c.side) {
-    CK(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
+    // high priority: the A_w factorization is a chain of small latency-bound grids; its CTAs take the
+    // first free SM slots while the hierarchy's large grids run on the main stream
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    static const bool low = getenv("AMGF_SIDE_LOWPRIO") != nullptr;  // A/B experiments only
+    CK(cudaStreamCreateWithPriority(&c.side, cudaStreamNonBlocking, low ? lo : hi));
     CK(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming));
   }
