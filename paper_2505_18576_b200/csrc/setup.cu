@@ -1152,6 +1152,23 @@ static void build_pairs(Ctx &c, long nnzc, const int *rowof, const int *ccol, co
 static void level_numeric(Ctx &c, int l, LevelCache &lc) {
   Level &L = c.lev[l];
   Level &Lc = c.lev[l + 1];
+  {
+    // explicit carveout on the large hierarchy grids, as for the solve's residual SpMV: lets the side
+    // stream's shared-memory-heavy A_w factorization CTAs find room (A/B: AMGF_HIER_CARVEOUT=-1 disables)
+    static bool once = false;
+    if (!once) {
+      once = true;
+      const int cv = getenv("AMGF_HIER_CARVEOUT") ? atoi(getenv("AMGF_HIER_CARVEOUT")) : 50;
+      if (cv >= 0) {
+        CK(cudaFuncSetAttribute(k_spgemm_dense<3, 3, 6>, cudaFuncAttributePreferredSharedMemoryCarveout, cv));
+        CK(cudaFuncSetAttribute(k_spgemm_dense<6, 3, 6>, cudaFuncAttributePreferredSharedMemoryCarveout, cv));
+        CK(cudaFuncSetAttribute(k_P_values<3>, cudaFuncAttributePreferredSharedMemoryCarveout, cv));
+        CK(cudaFuncSetAttribute(k_transpose_vals, cudaFuncAttributePreferredSharedMemoryCarveout, cv));
+        CK(cudaFuncSetAttribute(k_spgemm_vals_warp<6, 6, 6>, cudaFuncAttributePreferredSharedMemoryCarveout, cv));
+        CK(cudaFuncSetAttribute(k_sell_vals, cudaFuncAttributePreferredSharedMemoryCarveout, cv));
+      }
+    }
+  }
   power_iteration(c, L);
   if (L.b == 3)
     LAUNCH(k_P_values<3>, L.P.nnzb, L.P.nnzb, lc.P_rowof, L.P.col, L.A.ptr, L.A.col, L.A.val, L.agg, L.Pt.ptr,

@@ -286,6 +286,8 @@ static void sell_dispatch(Ctx &c, const Sell &A, int mode, const double *x, cons
     if (!once) {
       once = true;
       CK(cudaFuncSetAttribute(k_sell<BR, BC, MODE_RESID>, cudaFuncAttributePreferredSharedMemoryCarveout, 50));
+      // the setup's power iteration (MODE_Y) runs beside the A_w factorization: same reason
+      CK(cudaFuncSetAttribute(k_sell<BR, BC, MODE_Y>, cudaFuncAttributePreferredSharedMemoryCarveout, 50));
     }
   }
   if (BR == 1 && mode != MODE_DOT) {
