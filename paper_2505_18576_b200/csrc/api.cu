@@ -198,7 +198,12 @@ void apply_M(Ctx &c, const double *r, double *z, VcOpts first, const double *dot
   {
     cudaStream_t main = c.stream;
     c.stream = c.fstream;
-    nd_solve(c, c.rz, nullptr);  // y = A_w^{-1} r1[Z] (pi order, c.fv)
+    try {
+      nd_solve(c, c.rz, nullptr);  // y = A_w^{-1} r1[Z] (pi order, c.fv)
+    } catch (...) {
+      c.stream = main;
+      throw;
+    }
     c.stream = main;
   }
   CK(cudaEventRecord(c.ev_f1, c.fstream));
