@@ -95,16 +95,20 @@ template <int MODE>
 __device__ __forceinline__ void tail_spmv(const TailArgs &a, int row0, int row1, int q0, const double *sx,
                                           const double *sv, const int *sc, double *out, int step = 0) {
   for (int i = row0 + threadIdx.x; i < row1; i += blockDim.x) {
+    // the epilogue's vector operands are loaded before the row chain (their latency hides behind it)
+    const double bi = a.b[i];
+    const double di = (MODE == SPMV_RESID) ? 0.0 : a.d[i];
+    const double diri = (MODE == SPMV_CHEB) ? __ldcg(a.dir + i) : 0.0;
     const double acc = tail_row(sv, sc, sx, a.a_sp[i >> 5] - q0, a.a_len[i], i & 31);
     if (MODE == SPMV_RESID) {
-      __stcg(out + i, a.b[i] - acc);
+      __stcg(out + i, bi - acc);
     } else if (MODE == SPMV_SMOOTH) {
-      const double res = a.b[i] - acc;
-      const double t = res / a.d[i];
+      const double res = bi - acc;
+      const double t = res / di;
       __stcg(out + i, sx[i] + t);
     } else {  // SPMV_CHEB1 / SPMV_CHEB (C23), step s in a.ca / a.cb
-      const double t = (a.b[i] - acc) / a.d[i];
-      const double dv = (MODE == SPMV_CHEB1) ? a.c0 * t : __fma_rn(a.ca[step], __ldcg(a.dir + i), a.cb[step] * t);
+      const double t = (bi - acc) / di;
+      const double dv = (MODE == SPMV_CHEB1) ? a.c0 * t : __fma_rn(a.ca[step], diri, a.cb[step] * t);
       __stcg(a.dir + i, dv);
       __stcg(out + i, sx[i] + dv);
     }
