@@ -377,3 +377,23 @@ def test_l1_jacobi_smoother_parity(oracle_lib, amgf_mod, torch_cuda):
     xo, ro = o.pcg(p.b, rtol=p.rtol)
     xg, rg = g.pcg(p.b, rtol=p.rtol)
     assert rg["iterations"] == ro["iterations"] and np.array_equal(xg.cpu().numpy(), xo)
+
+
+def test_device_loop_reuse(oracle_lib, amgf_mod, torch_cuda):
+    """The captured PCG loop (conditional WHILE node) is reused across solves with different max_it / rtol,
+    across update_D, and for both preconditioners: every solve still equals the oracle's bitwise."""
+    p = gen.config(1)
+    g = amgf_mod.AMGF.from_problem(p)
+    o = oracle_lib.Oracle.from_problem(p)
+    for rtol, max_it in ((p.rtol, 3), (1e-4, 5000), (p.rtol, 5000)):
+        xo, ro = o.pcg(p.b, rtol=rtol, maxit=max_it)
+        xg, rg = g.pcg(p.b, rtol=rtol, max_it=max_it)
+        assert rg["iterations"] == ro["iterations"] and rg["converged"] == ro["converged"], (rtol, max_it)
+        assert np.array_equal(xg.cpu().numpy(), xo)
+    D2 = 10.0 ** (6.0 * np.random.default_rng(19).random(p.m))
+    g.update_D(D2)
+    o2 = oracle_lib.Oracle.from_problem(p, D=D2)
+    for precond in ("amgf", "amg"):
+        xo, ro = o2.pcg(p.b, rtol=p.rtol, precond=precond)
+        xg, rg = g.pcg(p.b, rtol=p.rtol, precond=precond)
+        assert rg["iterations"] == ro["iterations"] and np.array_equal(xg.cpu().numpy(), xo), precond
