@@ -343,7 +343,7 @@ def run_reference(args, rank, world):
     for _ in range(min(args.warmup, 1)):
         o.spmv(x)
     vals = []
-    iters_guess = 47  # mean PCG iterations of the GPU path over the cfg 3 sequence (default smoother)
+    iters_guess = 46  # mean PCG iterations of the GPU path over the cfg 3 sequence (default smoother)
     for k in range(args.steps):
         t = time.perf_counter(); o.vcycle(x); t_v = time.perf_counter() - t
         t = time.perf_counter(); o.spmv(x); t_s = time.perf_counter() - t

@@ -57,7 +57,7 @@ typedef struct {
                               0 = l1-Jacobi (contract C4)                                     */
   int32_t cheb_degree;     /* 1..32 (default 2)                                               */
   uint64_t agg_seed;       /* aggregation priority seed (default 0x5EED)                     */
-  double cheb_ratio;       /* > 1 (default 30)                                                */
+  double cheb_ratio;       /* > 1 (default 20)                                                */
 } amgf_config;
 
 typedef struct {

@@ -501,7 +501,7 @@ void amgf_default_config(amgf_config *cfg) {
   cfg->smoother = 1;  // Chebyshev degree 2 (DESIGN R18); 0 = l1-Jacobi
   cfg->cheb_degree = 2;
   cfg->agg_seed = 0x5EED;
-  cfg->cheb_ratio = 30.0;
+  cfg->cheb_ratio = 20.0;
 }
 
 const char *amgf_last_error(void) { return get_error(); }
