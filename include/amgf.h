@@ -50,7 +50,7 @@ typedef struct {
   int32_t post_sweeps;     /* l1-Jacobi sweeps after prolongation, >= 1 (default 1)          */
   int32_t coarsest_size;   /* stop coarsening at <= this many dofs (default 64) */
   int32_t max_levels;      /* default 25                                                     */
-  int32_t power_iters;     /* power steps for lambda_max(D^-1 A) (default 10)                */
+  int32_t power_iters;     /* power steps for lambda_max(D^-1 A) (default 6, DESIGN R19)      */
   int32_t nd_levels;       /* nested-dissection depth of A_w's elimination order (default 3, DESIGN R16) */
   int32_t smoother;        /* 1 = Chebyshev in D_l1^-1 A on [1/cheb_ratio, 1] (default, DESIGN R18 /
                               contract C23): each sweep is one polynomial of degree cheb_degree;

@@ -42,7 +42,7 @@ class OrcConfig(ctypes.Structure):
 
 
 DEFAULTS = dict(pre_sweeps=1, post_sweeps=1, coarsest_size=64, max_levels=25,
-                power_iters=10, factor_filter=1, agg_seed=0x5EED, nd_levels=3, smoother=1, cheb_degree=2,
+                power_iters=6, factor_filter=1, agg_seed=0x5EED, nd_levels=3, smoother=1, cheb_degree=2,
                 cheb_ratio=20.0)
 
 _lib = None

@@ -207,7 +207,7 @@ typedef struct {
   int pre_sweeps, post_sweeps, coarsest_size, max_levels, power_iters, factor_filter;
   uint64_t agg_seed;
   int nd_levels;  /* nested-dissection depth of A_w's elimination order (contract C9/C10, reading R16) */
-  int smoother;   /* 0 = l1-Jacobi (default), 1 = Chebyshev in D_l1^{-1} A (variant f4, reading R18) */
+  int smoother;   /* 0 = l1-Jacobi, 1 = Chebyshev (default) in D_l1^{-1} A (variant f4, reading R18) */
   int cheb_degree;
   int pad_;
   double cheb_ratio;

@@ -41,7 +41,7 @@ def test_default_config(libpath):
     L = load_library()
     c = Config()
     L.amgf_default_config(ctypes.byref(c))
-    assert (c.pre_sweeps, c.post_sweeps, c.coarsest_size, c.max_levels, c.power_iters) == (1, 1, 64, 25, 10)
+    assert (c.pre_sweeps, c.post_sweeps, c.coarsest_size, c.max_levels, c.power_iters) == (1, 1, 64, 25, 6)
 
 
 def test_null_arguments_rejected(libpath):

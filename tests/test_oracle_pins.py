@@ -479,7 +479,9 @@ def test_amgf_operator_identity_and_splitting(oracle_lib, N, matching, e_max):
     Pi = I - P @ np.linalg.solve(Aw, P.T @ A)
     lhs = I - M @ A
     rhs = (I - B @ A) @ Pi @ (I - B @ A)
-    assert np.abs(lhs - rhs).max() <= 1e-7
+    # rounding of the inner solves grows with cond(A) ~ 1e6 at D <= 1e4 (reading R13): measured 5e-8 (10 power
+    # steps) and 1.5e-7 (6, R19) against max|I - MA| = 0.7 / 1.7; a dropped term or wrong sign is O(1)
+    assert np.abs(lhs - rhs).max() <= 1e-6 * max(1.0, np.abs(lhs).max())
     # splitting form
     Binv = np.linalg.inv(B)
     nc = P.shape[1]
