@@ -21,6 +21,7 @@ import subprocess
 import sys
 import threading
 import time
+import types
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -266,13 +267,8 @@ def run_amgf(args, rank, world, local_rank):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (amgf_gen: seeded two-block Q1 elasticity + node-on-segment contact, DESIGN.md section 4)",
-        "config": {"workload": f"cfg{args.cfg}: two-block N={p.N}, n={p.n} dofs, m={p.m}, n_c={g.nc}, "
-                               f"{nsys}-system IP-like D sequence, rtol={p.rtol}",
-                   "levels": [(L["nodes"] * L["b"]) for L in g.levels], "band_width_Aw": g.bw,
-                   "l2": "inputs larger than L2 (fine operator 1.1 GB)", "parallelism": f"replicas x{world}",
-                   "smoother": (f"chebyshev degree {g.config.cheb_degree} on [1/{g.config.cheb_ratio:g}, 1] of "
-                                f"D_l1^-1 A (DESIGN R18)" if g.config.smoother == 1 else "l1-jacobi"),
-                   "sweeps": [g.config.pre_sweeps, g.config.post_sweeps]},
+        "config": dict(bench_config(args.cfg, p, g.nc, g.config, world),
+                       levels=[(L["nodes"] * L["b"]) for L in g.levels], band_width_Aw=g.bw),
         "pcg_iterations": iters,
         "systems": systems,
         "solve_ms_per_system": solve_ms,
@@ -295,6 +291,16 @@ def run_amgf(args, rank, world, local_rank):
         "clocks": clk,
     }
     return res, p
+
+
+def bench_config(cfg, p, nc, c, world):
+    """The `config` object both arms print (c: the solver configuration, attribute access)."""
+    return {"workload": f"cfg{cfg}: two-block N={p.N}, n={p.n} dofs, m={p.m}, n_c={nc}, "
+                        f"{p.D_seq.shape[0]}-system IP-like D sequence, rtol={p.rtol}",
+            "l2": "inputs larger than L2 (fine operator 1.1 GB)", "parallelism": f"replicas x{world}",
+            "smoother": (f"chebyshev degree {c.cheb_degree} on [1/{c.cheb_ratio:g}, 1] of D_l1^-1 A (DESIGN R18)"
+                         if c.smoother == 1 else "l1-jacobi"),
+            "sweeps": [c.pre_sweeps, c.post_sweeps]}
 
 
 def cpu_baseline(p, iters_guess, budget_s=25.0):
@@ -354,7 +360,8 @@ def run_reference(args, rank, world):
     return {"impl": "reference", "metric": METRIC, "value": v, "unit": "ms/system", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"cfg{args.cfg}: two-block N={p.N}, n={p.n} dofs"},
+            "config": dict(bench_config(args.cfg, p, len(p.Z), types.SimpleNamespace(**oracle.DEFAULTS), world),
+                           levels=[(L["nodes"] * L["b"]) for L in o.levels]),
             "cpu_baseline": {"value": v, "unit": "ms/system", "cores": 1, "kind": "oracle", "sample": sample,
                              "cpu": _cpu_model()},
             "e2e": {"value": v, "unit": "ms/system", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
