@@ -250,7 +250,10 @@ def run_amgf(args, rank, world, local_rank):
     tpath = os.path.join(ROOT, "profiles", "spmv_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+            tr = json.load(open(tpath))
+            # the capture is of one workload: only report it for that workload (same algorithmic bytes)
+            if tr.get("algorithmic_bytes_per_launch") == sb:
+                traffic = tr.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     spmv_gbs = sb / (spmv_ms * 1e-3) / 1e9
