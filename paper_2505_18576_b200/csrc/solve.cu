@@ -57,6 +57,24 @@ __device__ __forceinline__ double cheb_epilogue(int mode, double res, double di,
   return xn;
 }
 
+// x block of column c (BC consecutive doubles): 16-byte vector loads when BC is even (x is 16-byte aligned,
+// checked by the dispatcher), i.e. half the load instructions and L1 requests of the scalar gathers.
+template <int BC>
+__device__ __forceinline__ void gather_x(const double *__restrict__ x, int c, double (&v)[BC]) {
+  if constexpr (BC % 2 == 0) {
+    const double2 *p = reinterpret_cast<const double2 *>(x + (long)c * BC);
+#pragma unroll
+    for (int h = 0; h < BC / 2; h++) {
+      const double2 t = p[h];
+      v[2 * h] = t.x;
+      v[2 * h + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < BC; e++) v[e] = x[(long)c * BC + e];
+  }
+}
+
 // The SELL row chain of one block row (C2): acc[r] = sum over slots s (ascending) and block columns e
 // (ascending) of val * x, software-pipelined (slot s+1's column, values and x gather in flight while slot s
 // is consumed).
@@ -77,8 +95,7 @@ __device__ __forceinline__ void sell_row(int row, const int *__restrict__ slice_
     int cnext = 0;
     if (len > 0) {
       const int c0 = ldg_stream_i(cp);
-#pragma unroll
-      for (int e = 0; e < BC; e++) xcur[e] = x[(long)c0 * BC + e];
+      gather_x<BC>(x, c0, xcur);
 #pragma unroll
       for (int q = 0; q < BR * BC; q++) vcur[q] = ldg_stream(vp + q * 32);
       cnext = ldg_stream_i(cp + (len > 1 ? 32 : 0));
@@ -90,8 +107,7 @@ __device__ __forceinline__ void sell_row(int row, const int *__restrict__ slice_
       double vnx[BR * BC], xnx[BC];
 #pragma unroll
       for (int q = 0; q < BR * BC; q++) vnx[q] = ldg_stream(v + q * 32);
-#pragma unroll
-      for (int e = 0; e < BC; e++) xnx[e] = x[(long)cnext * BC + e];
+      gather_x<BC>(x, cnext, xnx);
       const int cnn = ldg_stream_i(cp + (long)s2 * 32);
 #pragma unroll
       for (int r = 0; r < BR; r++)
@@ -206,7 +222,7 @@ __global__ void __launch_bounds__(CTA) k_sell_r1(int nrows, const int *__restric
 #pragma unroll
     for (int e = 0; e < BC; e++) rv[q][e] = ldg_stream(vp + ((long)sq * BC + e) * 32);
 #pragma unroll
-    for (int e = 0; e < BC; e++) rx[q][e] = x[(long)rc[q] * BC + e];
+    gather_x<BC>(x, rc[q], rx[q]);
     rc[q] = ldg_stream_i(cp + (long)min(q + D, last) * 32);
   }
   // L2 prefetch window (pf slots ahead of the register ring): the slice's values of slots
@@ -242,7 +258,7 @@ __global__ void __launch_bounds__(CTA) k_sell_r1(int nrows, const int *__restric
 #pragma unroll
       for (int e = 0; e < BC; e++) rv[q][e] = ldg_stream(vp + ((long)sn * BC + e) * 32);
 #pragma unroll
-      for (int e = 0; e < BC; e++) rx[q][e] = x[(long)rc[q] * BC + e];
+      gather_x<BC>(x, rc[q], rx[q]);
       rc[q] = ldg_stream_i(cp + (long)sc * 32);
     }
   }
@@ -270,6 +286,8 @@ static void sell_dispatch(Ctx &c, const Sell &A, int mode, const double *x, cons
                           const double *add, double *y, double *dp, ChebArgs ch = ChebArgs{}) {
   dim3 g(nblk(A.nrows)), t(CTA);
   if (A.nrows == 0) return;
+  // the x gathers of even block widths are 16-byte vector loads (gather_x)
+  if (BC % 2 == 0) REQUIRE(((uintptr_t)x & 15) == 0, AMGF_ERR_ARG, "SELL SpMV: x must be 16-byte aligned");
   {
     static bool pf_set = false;
     if (!pf_set) {
