@@ -53,6 +53,11 @@ struct Bsr {
   long nnzb = 0;
   int *ptr = nullptr, *col = nullptr;
   double *val = nullptr;
+  // level-0 restriction only: val regrouped per row into groups of 32 consecutive blocks (the blocks one
+  // warp step of k_restrict reads), component-major inside a group: block gb + l, component q at
+  // ival[gb * bs + q * gs + l] with gs = min(32, row end - gb), bs = br * bc; every load instruction of the
+  // warp is then one contiguous segment (C5's order is unchanged)
+  double *ival = nullptr;
 };
 
 // SELL-32 block matrix: slices of 32 consecutive block rows; slot s of a slice holds the s-th block

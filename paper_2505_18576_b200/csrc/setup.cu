@@ -682,6 +682,21 @@ __global__ void k_P_values(long nnzb, const int *P_rowof, const int *P_col, cons
 }
 
 // ------------------------------------------------------------------ s7: transpose, SpGEMMs, symmetrisation
+// Bsr::ival from val: one warp per block row, lane l of step t moves block gb + l (gb = beg + 32 t); writes
+// coalesced per component (140 us at cfg 3; coalescing the reads instead was 3x slower).
+__global__ void k_interleave_rows(int nbr, const int *__restrict__ ptr, int bs, const double *__restrict__ val,
+                                  double *__restrict__ ival) {
+  const int w = (blockIdx.x * CTA + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= nbr) return;
+  const int beg = ptr[w], end = ptr[w + 1];
+  for (int gb = beg; gb < end; gb += 32) {
+    const int gs = min(32, end - gb);
+    if (lane < gs)
+      for (int q = 0; q < bs; q++) ival[(long)gb * bs + (long)q * gs + lane] = val[(long)(gb + lane) * bs + q];
+  }
+}
+
 __global__ void k_transpose_vals(long nnzb, int br, int bc, const int *perm, const double *src, double *dst) {
   long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
   if (t >= nnzb) return;
@@ -1177,6 +1192,10 @@ static void level_numeric(Ctx &c, int l, LevelCache &lc) {
     LAUNCH(k_P_values<6>, L.P.nnzb, L.P.nnzb, lc.P_rowof, L.P.col, L.A.ptr, L.A.col, L.A.val, L.agg, L.Pt.ptr,
            L.Pt.val, L.dpt, L.omega, L.P.val);
   LAUNCH(k_transpose_vals, L.R.nnzb, L.R.nnzb, L.b, 6, lc.R_perm, L.P.val, L.R.val);
+  if (L.b == 3) {  // level-0 restriction reads R's values group-interleaved (Bsr::ival)
+    if (!L.R.ival) L.R.ival = c.alloc<double>((size_t)L.R.nnzb * 18);
+    LAUNCH(k_interleave_rows, (long)L.R.nbr * 32, L.R.nbr, L.R.ptr, 18, L.R.val, L.R.ival);
+  }
   // AP = A * P, G = R * AP over the precomputed block-product lists
   {
     // dense-over-row products at the fine level (measured update_D 17.0 -> 15.3 ms at cfg 3); on the 6x6

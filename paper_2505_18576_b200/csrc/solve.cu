@@ -495,7 +495,13 @@ __global__ void __launch_bounds__(CTA, 2) k_restrict(int nrows, const int *__res
     double2 v[3 * B];
     double rv[B];
 #pragma unroll
-    for (int h = 0; h < 3 * B; h++) v[h] = __ldg(reinterpret_cast<const double2 *>(val + (long)k * 6 * B) + h);
+    for (int h = 0; h < 3 * B; h++) {
+      // group-interleaved layout (Bsr::ival): block k = gb + lane of the group starting at gb = k - lane
+      const int gb = k - lane, gs = min(32, end - gb);
+      const double *q = val + (long)gb * 6 * B + lane;
+      v[h].x = __ldg(q + (2 * h) * gs);
+      v[h].y = __ldg(q + (2 * h + 1) * gs);
+    }
 #pragma unroll
     for (int e = 0; e < B; e++) rv[e] = r[(long)c * B + e];
 #pragma unroll
@@ -580,7 +586,11 @@ void launch_restrict(Ctx &c, const Bsr &R, const double *r, double *bc) {
   long threads = (long)R.nbr * 32;
   // level 0 (3 x 3 -> 6 x 3 blocks): one warp per coarse block row moves full blocks (measured 69 us at cfg 3
   // vs 112 us split by scalar row); coarse levels are latency-bound: one warp per scalar row (23 vs 31 us)
-  if (R.bc == 3) k_restrict<3><<<nblk(threads), CTA, 0, c.stream>>>(R.nbr, R.ptr, R.col, R.val, r, bc);
+  // (level 0 reads the group-interleaved copy of R's values: 68 -> 59 us at cfg 3)
+  if (R.bc == 3) {
+    REQUIRE(R.ival, AMGF_ERR_ARG, "restriction: interleaved R values missing");
+    k_restrict<3><<<nblk(threads), CTA, 0, c.stream>>>(R.nbr, R.ptr, R.col, R.ival, r, bc);
+  }
   else k_restrict_row<6><<<nblk(threads * 6), CTA, 0, c.stream>>>(R.nbr * 6, R.ptr, R.col, R.val, r, bc);
   after_launch(c, __func__);
 }
