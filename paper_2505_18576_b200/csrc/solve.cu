@@ -524,23 +524,27 @@ __global__ void __launch_bounds__(CTA, 2) k_restrict(int nrows, const int *__res
   }
 }
 
+// CTA size of k_restrict_row: two warps, so that the ~1k warps of level 1 spread over all 148 SMs
+constexpr int RCTA = 64;
+
 // One warp per SCALAR row of R (6 per coarse block row): the same lane-strided chain and butterfly per
 // scalar row as k_restrict (C5), with 6x more warps for the latency-bound coarse levels.
 template <int B>
-__global__ void __launch_bounds__(CTA) k_restrict_row(int nrows6, const int *__restrict__ ptr,
+__global__ void __launch_bounds__(RCTA) k_restrict_row(int nrows6, const int *__restrict__ ptr,
                                                       const int *__restrict__ col, const double *__restrict__ val,
                                                       const double *__restrict__ r, double *__restrict__ out) {
-  const int w = (blockIdx.x * CTA + threadIdx.x) >> 5;
+  const int w = (blockIdx.x * RCTA + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= nrows6) return;  // warp-uniform
   const int a = w / 6, rr = w % 6;
   const int beg = ptr[a], end = ptr[a + 1];
   double acc = 0.0;
-  // software pipeline over batches of U lane-strided blocks (k, k+32, ...): the next batch's values and
+  // software pipeline over batches of U lane-strided blocks (k, k+32, ...; U = 4: 18 -> 15 us at cfg 3, with
+  // 64-thread CTAs 13 us): the next batch's values and
   // r entries are in flight while this batch's FMAs run, its columns one batch further ahead; the chain
   // still runs over the lane's blocks in ascending order (C5).  Indices are clamped so that every load
   // is unconditional.
-  constexpr int U = 2;
+  constexpr int U = 4;
   if (beg + lane < end) {
     const int last = end - 1;
     double v[U][B], rv[U][B];
@@ -591,7 +595,7 @@ void launch_restrict(Ctx &c, const Bsr &R, const double *r, double *bc) {
     REQUIRE(R.ival, AMGF_ERR_ARG, "restriction: interleaved R values missing");
     k_restrict<3><<<nblk(threads), CTA, 0, c.stream>>>(R.nbr, R.ptr, R.col, R.ival, r, bc);
   }
-  else k_restrict_row<6><<<nblk(threads * 6), CTA, 0, c.stream>>>(R.nbr * 6, R.ptr, R.col, R.val, r, bc);
+  else k_restrict_row<6><<<nblk(threads * 6, RCTA), RCTA, 0, c.stream>>>(R.nbr * 6, R.ptr, R.col, R.val, r, bc);
   after_launch(c, __func__);
 }
 
