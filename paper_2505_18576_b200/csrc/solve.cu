@@ -1042,15 +1042,29 @@ __global__ void k_thin(int nthin, const int *__restrict__ rows, const int *__res
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nthin) return;
   double acc = 0.0;
-  for (int e = ptr[t]; e < ptr[t + 1]; e++) acc = __fma_rn(val[e], y[pos[e]], acc);
+  const int e0 = ptr[t], e1 = ptr[t + 1];
   const int p = rows[t];
-  r[p] = r[p] - acc;
+  const double rp = r[p];
+  // batches of 4 entries: positions, values and y gathers of a batch in flight together; chain order kept
+  int e = e0;
+  for (; e + 4 <= e1; e += 4) {
+    int q[4];
+    double v[4], yv[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) { q[u] = pos[e + u]; v[u] = val[e + u]; }
+#pragma unroll
+    for (int u = 0; u < 4; u++) yv[u] = y[q[u]];
+#pragma unroll
+    for (int u = 0; u < 4; u++) acc = __fma_rn(v[u], yv[u], acc);
+  }
+  for (; e < e1; e++) acc = __fma_rn(val[e], y[pos[e]], acc);
+  r[p] = rp - acc;
 }
 
 void launch_thin_resid(Ctx &c, int nthin, const int *rows, const int *ptr, const int *pos, const double *val,
                        const double *y, double *r) {
   if (nthin == 0) return;
-  k_thin<<<nblk(nthin), CTA, 0, c.stream>>>(nthin, rows, ptr, pos, val, y, r);
+  k_thin<<<nblk(nthin, 64), 64, 0, c.stream>>>(nthin, rows, ptr, pos, val, y, r);  // 64: spread over all SMs
   after_launch(c, __func__);
 }
 
