@@ -385,8 +385,25 @@ __global__ void k_cheb0(long n, const double *__restrict__ b, const double *__re
     x[i] = v;
   }
 }
+// the same per-element arithmetic on pairs (16-byte loads and stores)
+__global__ void k_cheb0_v2(long n2, const double2 *__restrict__ b, const double2 *__restrict__ d, double c0,
+                           double2 *__restrict__ dir, double2 *__restrict__ x) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n2; i += (long)gridDim.x * blockDim.x) {
+    const double2 bb = b[i], dd = d[i];
+    double2 v;
+    v.x = c0 * (bb.x / dd.x);
+    v.y = c0 * (bb.y / dd.y);
+    dir[i] = v;
+    x[i] = v;
+  }
+}
 void launch_cheb0(Ctx &c, long n, const double *b, const double *d, double c0, double *dir, double *x) {
-  k_cheb0<<<nblk(n), CTA, 0, c.stream>>>(n, b, d, c0, dir, x);
+  const bool v2 = (n % 2 == 0) && !(((uintptr_t)b | (uintptr_t)d | (uintptr_t)dir | (uintptr_t)x) & 15);
+  if (v2)
+    k_cheb0_v2<<<nblk(n / 2), CTA, 0, c.stream>>>(n / 2, (const double2 *)b, (const double2 *)d, c0, (double2 *)dir,
+                                                  (double2 *)x);
+  else
+    k_cheb0<<<nblk(n), CTA, 0, c.stream>>>(n, b, d, c0, dir, x);
   after_launch(c, "k_cheb0");
 }
 
