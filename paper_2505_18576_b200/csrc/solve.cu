@@ -369,9 +369,41 @@ __global__ void k_axpy2_cheb0(long n, const Scalars *__restrict__ sc, const doub
     xs[i] = v;
   }
 }
+// the same per-element arithmetic on pairs (16-byte loads and stores)
+__global__ void k_axpy2_cheb0_v2(long n2, const Scalars *__restrict__ sc, const double2 *__restrict__ p,
+                                 const double2 *__restrict__ q, double2 *__restrict__ x, double2 *__restrict__ r,
+                                 const double2 *__restrict__ d, double c0, double2 *__restrict__ dir,
+                                 double2 *__restrict__ xs) {
+  const double a = sc->alpha;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n2; i += (long)gridDim.x * blockDim.x) {
+    const double2 pp = p[i], qq = q[i], dd = d[i];
+    double2 xx = x[i], rr = r[i], v;
+    xx.x = __fma_rn(a, pp.x, xx.x);
+    xx.y = __fma_rn(a, pp.y, xx.y);
+    x[i] = xx;
+    rr.x = __fma_rn(-a, qq.x, rr.x);
+    rr.y = __fma_rn(-a, qq.y, rr.y);
+    r[i] = rr;
+    v.x = c0 * (rr.x / dd.x);
+    v.y = c0 * (rr.y / dd.y);
+    dir[i] = v;
+    xs[i] = v;
+  }
+}
+static bool pairs_ok(long n, std::initializer_list<const void *> ps) {
+  if (n % 2) return false;
+  for (const void *p : ps)
+    if ((uintptr_t)p & 15) return false;
+  return true;
+}
 void launch_axpy2_cheb0(Ctx &c, long n, const double *p, const double *q, double *x, double *r, const double *d,
                         double c0, double *dir, double *xs) {
-  k_axpy2_cheb0<<<nblk(n), CTA, 0, c.stream>>>(n, c.sc, p, q, x, r, d, c0, dir, xs);
+  if (pairs_ok(n, {p, q, x, r, d, dir, xs}))
+    k_axpy2_cheb0_v2<<<nblk(n / 2), CTA, 0, c.stream>>>(n / 2, c.sc, (const double2 *)p, (const double2 *)q,
+                                                        (double2 *)x, (double2 *)r, (const double2 *)d, c0,
+                                                        (double2 *)dir, (double2 *)xs);
+  else
+    k_axpy2_cheb0<<<nblk(n), CTA, 0, c.stream>>>(n, c.sc, p, q, x, r, d, c0, dir, xs);
   after_launch(c, "k_axpy2_cheb0");
 }
 
@@ -644,6 +676,17 @@ __global__ void k_xpby(long n, const Scalars *__restrict__ sc, const double *__r
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
     p[i] = __fma_rn(be, p[i], z[i]);
 }
+__global__ void k_xpby_v2(long n2, const Scalars *__restrict__ sc, const double2 *__restrict__ z,
+                          double2 *__restrict__ p) {
+  const double be = sc->beta;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n2; i += (long)gridDim.x * blockDim.x) {
+    const double2 zz = z[i];
+    double2 pp = p[i];
+    pp.x = __fma_rn(be, pp.x, zz.x);
+    pp.y = __fma_rn(be, pp.y, zz.y);
+    p[i] = pp;
+  }
+}
 
 static int vgrid(long n) {
   long g = (n + CTA - 1) / CTA;
@@ -666,7 +709,11 @@ void launch_axpy2(Ctx &c, long n, const double *p, const double *q, double *x, d
   k_axpy2<<<vgrid(n), CTA, 0, c.stream>>>(n, c.sc, p, q, x, r); after_launch(c, __func__);
 }
 void launch_xpby(Ctx &c, long n, const double *z, double *p) {
-  k_xpby<<<vgrid(n), CTA, 0, c.stream>>>(n, c.sc, z, p); after_launch(c, __func__);
+  if (pairs_ok(n, {z, p}))
+    k_xpby_v2<<<vgrid(n / 2), CTA, 0, c.stream>>>(n / 2, c.sc, (const double2 *)z, (double2 *)p);
+  else
+    k_xpby<<<vgrid(n), CTA, 0, c.stream>>>(n, c.sc, z, p);
+  after_launch(c, __func__);
 }
 
 // ------------------------------------------------------------------ dots (C14, C15)
