@@ -192,7 +192,7 @@ void apply_M(Ctx &c, const double *r, double *z, VcOpts first, const double *dot
     for (auto &e : te) CK(cudaEventCreate(&e));
     CK(cudaEventRecord(te[0], c.stream));
   }
-  launch_resid_dofs(c, L0.As, c.nc, c.dof, c.w_x1, r, c.rz);
+  launch_resid_dofs(c, c.nc, c.dof, c.w_x1, r, c.rz);
   CK(cudaEventRecord(c.ev_f0, c.stream));
   CK(cudaStreamWaitEvent(c.fstream, c.ev_f0, 0));
   {

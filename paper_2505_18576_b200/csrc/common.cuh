@@ -157,6 +157,11 @@ struct Ctx {
   int nthin = 0;
   int *thin_row = nullptr, *thin_ptr = nullptr, *thin_pos = nullptr, *thin_src = nullptr;
   double *thin_val = nullptr;
+  // the fine rows S[dof[p], :] of the n_c filter dofs (elimination order) in a compact copy for the Z-row
+  // residual (k_resid_dofs): block columns and the row's 3 values per block, in the row's block order
+  int *zr_ptr = nullptr, *zr_col = nullptr, *zr_src = nullptr;
+  double *zr_val = nullptr;
+  long zr_nnz = 0;
   // hierarchy
   int nlev = 0;
   Level lev[MAXLEV];
@@ -288,7 +293,7 @@ void nd_solve(Ctx &c, const double *r1, const int *gather);  // c.fv <- A_w^{-1}
 void nd_scatter(Ctx &c, double *x2);                          // x2[Z] += y (c.fv)
 void launch_resid_partition(Ctx &c, const Sell &A, const double *x, const double *b, double *y, int nsm,
                             size_t reserve);
-void launch_resid_dofs(Ctx &c, const Sell &A, int n, const int *dof, const double *x, const double *b, double *out);
+void launch_resid_dofs(Ctx &c, int n, const int *dof, const double *x, const double *b, double *out);
 void nd_remap_positions(Ctx &c, int *pos_z, long n);  // Z positions -> pi positions
 void band_factor_blocks(Ctx &c, int n, int nblocks, const int *d_p0, const int *d_len, int bw, double *Lrow, int tag);
 void band_finish(Ctx &c, int n, int bw, const double *Lrow, double *Lcol, double *Lrev, double *dinv);

@@ -412,6 +412,28 @@ __global__ void k_flag_nonzero(long n, const int *cnt, int *flag) {
   long p = blockIdx.x * (long)blockDim.x + threadIdx.x;
   if (p < n) flag[p] = cnt[p] > 0;
 }
+// Ctx::zr_* (compact fine rows of the filter dofs, k_resid_dofs): counts, structure, values.
+__global__ void k_zr_count(int nc, const int *dof, const int *ptr, int *cnt) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < nc) cnt[p] = ptr[dof[p] / 3 + 1] - ptr[dof[p] / 3];
+}
+__global__ void k_zr_fill(int nc, const int *dof, const int *ptr, const int *col, const int *zr_ptr, int *zr_col,
+                          int *zr_src) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= nc) return;
+  const int i = dof[p] / 3, r = dof[p] % 3, o = zr_ptr[p];
+  for (int k = ptr[i]; k < ptr[i + 1]; k++) {
+    zr_col[o + k - ptr[i]] = col[k];
+    zr_src[o + k - ptr[i]] = k * 9 + r * 3;  // block k, row r of the 3 x 3 block
+  }
+}
+__global__ void k_zr_vals(long nnz, const int *zr_src, const double *val, double *zr_val) {
+  const long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (k >= nnz) return;
+#pragma unroll
+  for (int e = 0; e < 3; e++) zr_val[k * 3 + e] = val[(long)zr_src[k] + e];
+}
+
 __global__ void k_gather_vals(long n, const int *src, const double *from, double *to) {
   long e = blockIdx.x * (long)blockDim.x + threadIdx.x;
   if (e < n) to[e] = src[e] >= 0 ? from[src[e]] : 0.0;
@@ -1093,6 +1115,7 @@ static void join_filter(Ctx &c) {
 
 static void thin_numeric(Ctx &c, long nthin_nnz) {
   LAUNCH(k_gather_vals, nthin_nnz, nthin_nnz, c.thin_src, c.lev[0].A.val, c.thin_val);
+  LAUNCH(k_zr_vals, c.zr_nnz, c.zr_nnz, c.zr_src, c.lev[0].A.val, c.zr_val);
 }
 
 static void power_iteration(Ctx &c, Level &L) {
@@ -1381,6 +1404,19 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
     int tn = (int)tnnz;
     CK(cudaMemcpyAsync(c.thin_ptr + c.nthin, &tn, sizeof(int), cudaMemcpyHostToDevice, c.stream));
     C.thin_nnz = tnnz;
+    // compact fine rows of the filter dofs (elimination order) for the Z-row residual
+    {
+      int *zc = c.alloc<int>(c.nc + 1);
+      CK(cudaMemsetAsync(zc, 0, (c.nc + 1) * sizeof(int), c.stream));
+      LAUNCH(k_zr_count, c.nc, c.nc, c.dof, L0.A.ptr, zc);
+      c.zr_ptr = c.alloc<int>(c.nc + 1);
+      c.zr_nnz = scan_ex(c, zc, c.zr_ptr, c.nc);
+      c.release(zc);
+      c.zr_col = c.alloc<int>(c.zr_nnz);
+      c.zr_src = c.alloc<int>(c.zr_nnz);
+      c.zr_val = c.alloc<double>(c.zr_nnz * 3);
+      LAUNCH(k_zr_fill, c.nc, c.nc, c.dof, L0.A.ptr, L0.A.col, c.zr_ptr, c.zr_col, c.zr_src);
+    }
     thin_numeric(c, tnnz);
     c.release(cnt); c.release(off); c.release(flag); c.release(foff);
   }

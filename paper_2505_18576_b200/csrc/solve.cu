@@ -479,32 +479,31 @@ void launch_resid_partition(Ctx &c, const Sell &A, const double *x, const double
   after_launch(c, "k_sell_resid_part");
 }
 
-// Residual b - S x at the dofs dof[p] only (p < n), into out[p]: the same SELL chain as k_sell<3,3> for
-// that scalar row (C2), so the values equal the full residual's at those rows bitwise.  One warp per dof:
-// lane s loads slot s (column, the row's 3 values, the 3 x entries), all in flight at once, then every
-// lane runs the row's chain over shuffled operands (slots ascending, components ascending) and lane 0
-// writes.  Used to start the A_w solve before the full residual SpMV (apply_M).
-__global__ void __launch_bounds__(CTA) k_resid_dofs(int n, const int *__restrict__ dof,
-                                                    const int *__restrict__ slice_ptr, const int *__restrict__ rowlen,
-                                                    const int *__restrict__ col, const double *__restrict__ val,
+// Residual b - S x at the dofs dof[p] only (p < n), into out[p]: the same chain as k_sell<3,3> for that
+// scalar row (C2: the row's blocks in order, components ascending), so the values equal the full residual's
+// at those rows bitwise.  The rows come from the compact copy Ctx::zr_* (contiguous per row, refreshed by
+// every numeric re-setup) instead of the SELL slices, where each of them is a strided 8-byte-per-sector
+// gather.  One warp per dof: lane s loads block s (column, 3 values, 3 x entries), all in flight at once,
+// then every lane runs the row's chain over shuffled operands and lane 0 writes.  Used to start the A_w
+// solve before the full residual SpMV (apply_M).
+__global__ void __launch_bounds__(CTA) k_resid_dofs(int n, const int *__restrict__ dof, const int *__restrict__ zr_ptr,
+                                                    const int *__restrict__ zr_col, const double *__restrict__ zr_val,
                                                     const double *__restrict__ x, const double *__restrict__ b,
                                                     double *__restrict__ out) {
   const int p = (blockIdx.x * CTA + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (p >= n) return;  // warp-uniform
-  const int d = dof[p], i = d / 3, r = d % 3, il = i & 31;
-  const long base = slice_ptr[i >> 5];
-  const int len = rowlen[i];
+  const int beg = zr_ptr[p], len = zr_ptr[p + 1] - beg;
   double acc = 0.0;
   for (int s0 = 0; s0 < len; s0 += 32) {
     const int s = s0 + lane;
     double v[3] = {0.0, 0.0, 0.0}, xv[3] = {0.0, 0.0, 0.0};
     if (s < len) {
-      const long slot = base + s;
-      const int c = col[slot * 32 + il];
+      const long k = beg + s;
+      const int c = zr_col[k];
 #pragma unroll
       for (int e = 0; e < 3; e++) {
-        v[e] = val[(slot * 9 + r * 3 + e) * 32 + il];
+        v[e] = zr_val[k * 3 + e];
         xv[e] = x[(long)c * 3 + e];
       }
     }
@@ -514,13 +513,13 @@ __global__ void __launch_bounds__(CTA) k_resid_dofs(int n, const int *__restrict
       for (int e = 0; e < 3; e++)
         acc = __fma_rn(__shfl_sync(0xffffffffu, v[e], q), __shfl_sync(0xffffffffu, xv[e], q), acc);
   }
-  if (lane == 0) out[p] = b[d] - acc;
+  if (lane == 0) out[p] = b[dof[p]] - acc;
 }
 
-void launch_resid_dofs(Ctx &c, const Sell &A, int n, const int *dof, const double *x, const double *b, double *out) {
+void launch_resid_dofs(Ctx &c, int n, const int *dof, const double *x, const double *b, double *out) {
   if (n == 0) return;
-  REQUIRE(A.br == 3 && A.bc == 3 && !A.perm, AMGF_ERR_ARG, "resid_dofs: fine-level 3x3 SELL expected");
-  k_resid_dofs<<<nblk((long)n * 32), CTA, 0, c.stream>>>(n, dof, A.slice_ptr, A.rowlen, A.col, A.val, x, b, out);
+  REQUIRE(c.zr_ptr && c.zr_val, AMGF_ERR_ARG, "resid_dofs: compact Z rows missing");
+  k_resid_dofs<<<nblk((long)n * 32), CTA, 0, c.stream>>>(n, dof, c.zr_ptr, c.zr_col, c.zr_val, x, b, out);
   after_launch(c, "k_resid_dofs");
 }
 
