@@ -730,7 +730,16 @@ __global__ void __launch_bounds__(CTA) k_dot1(long nb, int b, const double *__re
 __global__ void __launch_bounds__(CTA) k_dot2(long C, const double *__restrict__ part, Scalars *sc, int kind, int *err) {
   __shared__ double red[CTA];
   double acc = 0.0;
-  for (long c = threadIdx.x; c < C; c += CTA) acc = acc + part[c];
+  // the same sequential sum per thread (c = tid, tid + CTA, ...), its loads issued 8 at a time
+  long c = threadIdx.x;
+  for (; c + 7 * CTA < C; c += 8 * CTA) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) v[u] = part[c + u * CTA];
+#pragma unroll
+    for (int u = 0; u < 8; u++) acc = acc + v[u];
+  }
+  for (; c < C; c += CTA) acc = acc + part[c];
   double s = cta_tree(acc, red);
   if (threadIdx.x == 0) {
     switch (kind) {
