@@ -228,8 +228,8 @@ void apply_M(Ctx &c, const double *r, double *z, VcOpts first, const double *dot
     fprintf(stderr, "filter overlap: filter done at %.1f us, residual SpMV done at %.1f us\n", a * 1e3, b * 1e3);
     for (auto &e : te) cudaEventDestroy(e);
   }
-  nd_scatter(c, c.w_x1);  // x2 = x1 + P y
-  launch_thin_resid(c, c.nthin, c.thin_row, c.thin_ptr, c.thin_pos, c.thin_val, c.fv, c.w_r1);
+  // x2 = x1 + P y (scatter) and the thin residual r2 = r1 - S[:,Z] y in one launch
+  launch_thin_resid(c, c.nthin, c.thin_row, c.thin_ptr, c.thin_pos, c.thin_val, c.fv, c.w_r1, c.nc, c.dof, c.w_x1);
   VcOpts second;
   second.dot_r = dot_r;
   vcycle(c, 0, c.w_r1, z, c.w_x1, second);

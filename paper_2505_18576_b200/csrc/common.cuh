@@ -273,7 +273,7 @@ __host__ __device__ inline int band_R(int bw) { return (bw + 31) / 32 + 1; }
 __host__ __device__ inline int band_stride(int bw) { return band_R(bw) <= 8 ? 32 * band_R(bw) : ((bw + 2) & ~1); }
 constexpr int BAND_PAD_ROWS = 64;
 void launch_thin_resid(Ctx &c, int nthin, const int *rows, const int *ptr, const int *pos, const double *val,
-                       const double *y, double *r);
+                       const double *y, double *r, int nsc = 0, const int *sdof = nullptr, double *x2 = nullptr);
 void launch_bsr_spmv(Ctx &c, const Bsr &A, const double *x, double *y);  // setup-side, thread per block row
 void launch_copy(Ctx &c, long n, const double *src, double *dst);
 void launch_zero(Ctx &c, long n, double *dst);
@@ -290,7 +290,6 @@ void setup_numeric(Ctx &c, const double *D);  // update_D
 void nd_symbolic(Ctx &c);
 void nd_numeric(Ctx &c);
 void nd_solve(Ctx &c, const double *r1, const int *gather);  // c.fv <- A_w^{-1} r1 (pi order; r1[gather[p]])
-void nd_scatter(Ctx &c, double *x2);                          // x2[Z] += y (c.fv)
 void launch_resid_partition(Ctx &c, const Sell &A, const double *x, const double *b, double *y, int nsm,
                             size_t reserve);
 void launch_resid_dofs(Ctx &c, int n, const int *dof, const double *x, const double *b, double *out);

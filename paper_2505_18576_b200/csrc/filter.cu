@@ -331,11 +331,6 @@ __global__ void __launch_bounds__(SB_TR) k_nd_sep_bwd(const int *ids, const NdBl
   }
 }
 
-__global__ void k_nd_scatter(int nc, const int *dof, const double *y, double *x2) {
-  int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p < nc) x2[dof[p]] = x2[dof[p]] + y[p];
-}
-
 // ------------------------------------------------------------------ host
 void nd_remap_positions(Ctx &c, int *pos_z, long n) {
   if (n <= 0) return;
@@ -517,10 +512,6 @@ void nd_numeric(Ctx &c) {
   band_finish(c, nc, bw, c.Lrow, c.Lcol, c.Lrev, c.Ldinv);
 }
 
-void nd_scatter(Ctx &c, double *x2) {
-  k_nd_scatter<<<nblk(c.nc), CTA, 0, c.stream>>>(c.nc, c.dof, c.fv, x2);
-  after_launch(c, "k_nd_scatter");
-}
 
 void nd_solve(Ctx &c, const double *r1, const int *gather) {
   const int nc = c.nc, bw = c.bw;

@@ -1108,11 +1108,16 @@ void launch_band_trsv(Ctx &c, int n, int bw, const double *Lcol, const double *L
 }
 
 // ------------------------------------------------------------------ thin second residual (C11)
+// threads [nthin, nthin + nsc) also do the filter scatter x2[sdof[p]] += y[p] (one launch for both)
 __global__ void k_thin(int nthin, const int *__restrict__ rows, const int *__restrict__ ptr,
                        const int *__restrict__ pos, const double *__restrict__ val, const double *__restrict__ y,
-                       double *__restrict__ r) {
+                       double *__restrict__ r, int nsc, const int *__restrict__ sdof, double *__restrict__ x2) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nthin) return;
+  if (t >= nthin) {
+    const int q = t - nthin;
+    if (q < nsc) x2[sdof[q]] = x2[sdof[q]] + y[q];
+    return;
+  }
   double acc = 0.0;
   const int e0 = ptr[t], e1 = ptr[t + 1];
   const int p = rows[t];
@@ -1134,9 +1139,10 @@ __global__ void k_thin(int nthin, const int *__restrict__ rows, const int *__res
 }
 
 void launch_thin_resid(Ctx &c, int nthin, const int *rows, const int *ptr, const int *pos, const double *val,
-                       const double *y, double *r) {
-  if (nthin == 0) return;
-  k_thin<<<nblk(nthin, 64), 64, 0, c.stream>>>(nthin, rows, ptr, pos, val, y, r);  // 64: spread over all SMs
+                       const double *y, double *r, int nsc, const int *sdof, double *x2) {
+  if (nthin + nsc == 0) return;
+  k_thin<<<nblk(nthin + nsc, 64), 64, 0, c.stream>>>(nthin, rows, ptr, pos, val, y, r, nsc, sdof,
+                                                      x2);  // 64: spread over all SMs
   after_launch(c, __func__);
 }
 
