@@ -42,12 +42,14 @@ typedef enum {
   AMGF_ERR_BREAKDOWN = -6,     /* PCG: p.Sp <= 0 or r.Mr < 0                      */
   AMGF_ERR_CUDA = -7,          /* CUDA runtime error                                            */
   AMGF_ERR_OOM = -8,           /* device allocation failed                                      */
-  AMGF_ERR_LIMIT = -9          /* an internal capacity limit was exceeded (message says which)  */
+  AMGF_ERR_LIMIT = -9,         /* an internal capacity limit was exceeded (message says which)  */
+  AMGF_ERR_FORMAT = -10        /* amgf_import: missing / truncated / inconsistent hierarchy file  */
 } amgf_status;
 
 typedef struct {
-  int32_t pre_sweeps;      /* l1-Jacobi sweeps before restriction, >= 1 (default 1)          */
-  int32_t post_sweeps;     /* l1-Jacobi sweeps after prolongation, >= 1 (default 1)          */
+  int32_t pre_sweeps;      /* smoother sweeps before restriction, >= 1 (default 1); a sweep is one
+                              Chebyshev polynomial or one l1-Jacobi step (see `smoother`)     */
+  int32_t post_sweeps;     /* smoother sweeps after prolongation, >= 1 (default 1)           */
   int32_t coarsest_size;   /* stop coarsening at <= this many dofs (default 64) */
   int32_t max_levels;      /* default 25                                                     */
   int32_t power_iters;     /* power steps for lambda_max(D^-1 A) (default 6, DESIGN R19)      */
@@ -60,11 +62,20 @@ typedef struct {
   double cheb_ratio;       /* > 1 (default 20)                                                */
 } amgf_config;
 
+#define AMGF_MAX_LEVELS 32
+
 typedef struct {
   int32_t iterations;      /* number of S*p products                                         */
   int32_t converged;       /* 1 if sqrt(r.Mr / r0.Mr0) < rtol                                */
   double rel_pres_norm;    /* final sqrt(r.Mr / r0.Mr0)                                      */
   double solve_ms;         /* device time of the solve (CUDA events)                         */
+  double setup_ms;         /* the handle's last setup: amgf_setup / amgf_import wall time, or the device
+                              time of the last amgf_update_D (numeric re-setup)                */
+  int32_t n_levels;        /* levels of the AMG hierarchy (1 = the coarsest solve only)       */
+  int32_t pad_;
+  int64_t level_dofs[AMGF_MAX_LEVELS];  /* scalar unknowns per level (0 beyond n_levels)       */
+  int64_t level_nnzb[AMGF_MAX_LEVELS];  /* stored blocks of each level operator (3x3 at level 0,
+                                           6x6 below)                                        */
 } amgf_report;
 
 typedef struct amgf_ctx *amgf_handle;
@@ -111,6 +122,32 @@ amgf_status amgf_pcg_solve(amgf_handle h, const double *b, double *x, double rto
 amgf_status amgf_pcg_solve_host(amgf_handle h, const double *b_host, double *x_host, double rtol,
                                 int32_t max_it, int32_t precond, amgf_report *rep, void *stream);
 
+/* Write the handle's preconditioner to the existing directory `dir` (the exchange format
+ * with the oracle, oracle/__init__.py Oracle.export): raw little-endian binary files plus a text manifest.
+ *   amgf_hierarchy.txt   "amgf_hierarchy 1", then "key value" lines: nodes nlev nc bw nco and the solver
+ *                        configuration (pre_sweeps post_sweeps smoother cheb_degree cheb_ratio nd_levels
+ *                        coarsest_size max_levels power_iters agg_seed), then per level
+ *                        "level l nodes b nnzb nnzb_P n_agg"
+ *   L<l>_A_{ptr,col}.i32, L<l>_A_val.f64   level operator A_l (BSR, b x b row-major blocks; A_0 = S)
+ *   L<l>_l1.f64                            l1 row sums d_l1 of A_l (smoother diagonal)
+ *   L<l>_{P,R}_{ptr,col}.i32, _val.f64     prolongator P_l (b x 6 blocks) and R_l = P_l^T (6 x b), l < nlev-1
+ *   Z.i32 [nc]                             contact dofs in P's column order
+ *   pi.i32 [nc]                            elimination order of A_w as Z positions (DESIGN R16)
+ *   Lw.f64 [nc*nc]                         dense lower Cholesky factor of A_w[pi,pi], row-major
+ *   Lc.f64 [nco*nco]                       dense lower Cholesky factor of the coarsest operator
+ * Dense factors are written in full (n_c^2 doubles: 571 MB at cfg 3).  Synchronises the handle's stream. */
+amgf_status amgf_export(amgf_handle h, const char *dir);
+
+/* Build a handle from a directory in the amgf_export format (written by amgf_export or by the oracle) so
+ * that amgf_apply / amgf_vcycle / amgf_spmv / amgf_pcg_solve run on exactly that hierarchy (north star:
+ * "single preconditioner applies on an identical exported hierarchy").  Nothing is recomputed: operators,
+ * l1 diagonals, transfer operators and both factors are taken as stored; the solver configuration comes
+ * from the manifest.  The A_w factor must vanish outside the structure of the nested-dissection order the
+ * manifest's (nc, bw, nd_levels) define, pi must be that order and bw must be the structural band width
+ * of S[Z, Z] (AMGF_ERR_FORMAT otherwise).  The handle has no K, J or D: amgf_update_D returns
+ * AMGF_ERR_ARG.  Synchronises `stream`; *out = NULL on error. */
+amgf_status amgf_import(const char *dir, void *stream, amgf_handle *out);
+
 /* Hierarchy introspection (tests, bench).  info[0] = levels, info[1] = nc, info[2] = coarsest dofs,
  * info[3] = band width of A_w's factor, then per level l: info[4+6l .. 9+6l] =
  * {nodes, block size, nnzb(A), nnzb(P), n_agg, SELL slots of A}; info[196] = size of the separator
@@ -122,7 +159,8 @@ amgf_status amgf_level_info(amgf_handle h, int64_t *info);
  * 5 P.val 6 R.ptr 7 R.col 8 R.val 9 l1 diagonal 10 aggregate ids 11 near-null space 12 {lambda,
  * omega} 14 root flags 15 component labels 20 Z 22 in-block band of the factor of A_w[pi,pi] (nc x W
  * row-major over pi positions, W = band stride, L_ik at column bw-(i-k), diagonal at column bw)
- * 23 separator-vs-subtree factor entries 25 pi (elimination order as Z positions) 27 block table
+ * 23 separator-vs-subtree factor entries 24 coarsest factor band (nco x Wc row-major, Wc =
+ * band_stride(nco-1), L_ik at column nco-1-(i-k)) 25 pi (elimination order as Z positions) 27 block table
  * {int p0, len, kind, t0; int64 off; int level, pad}.  Sizes follow amgf_level_info.  Synchronises the handle's last stream. */
 amgf_status amgf_level_get(amgf_handle h, int32_t which, int32_t level, void *dst);
 

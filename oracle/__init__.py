@@ -20,6 +20,21 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-std=c11"]
 
 
+def _host_has_fma() -> bool:
+    try:
+        return any(ln.startswith("flags") and " fma " in ln + " " for ln in open("/proc/cpuinfo"))
+    except OSError:
+        return False
+
+
+# -mfma lets gcc emit fma() as one vfmadd instruction instead of a libm call.  fma() is one correctly
+# rounded operation either way (IEEE 754 fusedMultiplyAdd), so the results are bit-identical (pinned by
+# tests/test_oracle_pins.py::test_fma_build_bit_identical); -ffp-contract=off still forbids any FMA that
+# is not written.  The oracle's dense Cholesky (a dependent FMA chain) runs about 1.6x faster.
+if _host_has_fma():
+    CFLAGS = CFLAGS + ["-mfma"]
+
+
 def cheb_coefs(k: int, ratio: float):
     """Chebyshev smoother coefficients (c0, [(a_s, b_s) for s = 1..k-1]) of the oracle (reading R18)."""
     out = np.zeros(2 * k)
@@ -27,10 +42,15 @@ def cheb_coefs(k: int, ratio: float):
     return out[0], [(out[2 * s - 1], out[2 * s]) for s in range(1, k)]
 
 
-def build(force: bool = False) -> str:
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", *CFLAGS, "-o", _LIB, _SRC, "-lm"])
-    return _LIB
+def build(force: bool = False, out: str = _LIB, flags=None) -> str:
+    flags = CFLAGS if flags is None else flags
+    stamp = out + ".flags"
+    same = os.path.exists(stamp) and open(stamp).read() == " ".join(flags)
+    if force or not same or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", *flags, "-o", out, _SRC, "-lm"])
+        with open(stamp, "w") as f:
+            f.write(" ".join(flags))
+    return out
 
 
 class OrcConfig(ctypes.Structure):
@@ -51,7 +71,11 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        L = ctypes.CDLL(build())
+        if os.environ.get("AMGF_ORACLE_NOFMA") == "1":   # libm fma() calls (pin of the -mfma build)
+            path = build(out=os.path.join(_HERE, "liboracle_nofma.so"), flags=[f for f in CFLAGS if f != "-mfma"])
+        else:
+            path = build()
+        L = ctypes.CDLL(path)
         P = ctypes.c_void_p
         L.orc_create.restype = P
         L.orc_create.argtypes = [ctypes.c_int, P, P, P, ctypes.c_int, P, P, P, P, P, ctypes.c_int, P,
@@ -75,6 +99,7 @@ def lib():
         L.orc_info.argtypes = [P, P]
         L.orc_bsr_spmv.argtypes = [ctypes.c_int] * 4 + [P] * 5
         L.orc_get.argtypes = [P, ctypes.c_int, ctypes.c_int, P]
+        L.orc_times.argtypes = [P, P]
         _lib = L
     return _lib
 
@@ -206,6 +231,49 @@ class Oracle:
             return sp.bsr_matrix((val, col, ptr), shape=(L["nodes"] * b, nc * 6))
         ptr, col, val = self.get(6, level), self.get(7, level), self.get(8, level).reshape(-1, 6, b)
         return sp.bsr_matrix((val, col, ptr), shape=(nc * 6, L["nodes"] * b))
+
+    def times(self):
+        """Wall seconds of the setup phases (instrumentation): S, A_w assembly, A_w Cholesky, hierarchy."""
+        t = np.zeros(4)
+        lib().orc_times(self.h, _p(t))
+        return dict(zip(("S", "A_w_assembly", "A_w_cholesky", "hierarchy"), t.tolist()))
+
+    def export(self, path):
+        """Write this oracle hierarchy in the amgf_export exchange format (include/amgf.h: manifest + raw
+        little-endian arrays), so the CUDA path can apply exactly this preconditioner (amgf_import).  The
+        writer is independent of the CUDA path's reader: it only lays out the oracle's own arrays."""
+        os.makedirs(path, exist_ok=True)
+        c = self.cfg
+        lines = ["amgf_hierarchy 1", f"nodes {self.levels[0]['nodes']}", f"nlev {self.nlev}", f"nc {self.nc}",
+                 f"bw {int(self.get(26)[0])}", f"nco {self.nco}"]
+        for k in ("pre_sweeps", "post_sweeps", "smoother", "cheb_degree", "nd_levels", "coarsest_size",
+                  "max_levels", "power_iters"):
+            lines.append(f"{k} {int(c[k])}")
+        lines.append(f"cheb_ratio {float(c['cheb_ratio'])!r}")
+        lines.append(f"agg_seed {int(c['agg_seed'])}")
+        for l, L in enumerate(self.levels):
+            co = l == self.nlev - 1
+            lines.append(f"level {l} {L['nodes']} {L['b']} {L['nnzb']} {0 if co else L['nnzb_P']} "
+                         f"{0 if co else L['n_agg']}")
+        with open(os.path.join(path, "amgf_hierarchy.txt"), "w") as f:
+            f.write("\n".join(lines) + "\n")
+
+        def w(name, a, dt):
+            np.ascontiguousarray(a, dtype=dt).astype(np.dtype(dt).newbyteorder("<")).tofile(os.path.join(path, name))
+
+        for l in range(self.nlev):
+            for which, stem, dt in ((0, "A_ptr.i32", np.int32), (1, "A_col.i32", np.int32), (2, "A_val.f64", np.float64),
+                                    (9, "l1.f64", np.float64)):
+                w(f"L{l}_{stem}", self.get(which, l), dt)
+            if l < self.nlev - 1:
+                for which, stem, dt in ((3, "P_ptr.i32", np.int32), (4, "P_col.i32", np.int32),
+                                        (5, "P_val.f64", np.float64), (6, "R_ptr.i32", np.int32),
+                                        (7, "R_col.i32", np.int32), (8, "R_val.f64", np.float64)):
+                    w(f"L{l}_{stem}", self.get(which, l), dt)
+        w("Z.i32", self.get(20), np.int32)
+        w("pi.i32", self.get(25), np.int32)
+        w("Lw.f64", self.get(22) if self.nc else np.zeros(0), np.float64)
+        w("Lc.f64", self.get(24), np.float64)
 
     # --- operators ---
     def spmv(self, x, level=0):

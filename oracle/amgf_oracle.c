@@ -27,11 +27,13 @@
  * paper's lemmas, golden fixtures).  Functions without such a pin are listed
  * as "parity unpinned" in DESIGN.md; at present: none.
  */
+#define _POSIX_C_SOURCE 199309L
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
 #include <stdio.h>
+#include <time.h>
 
 #define ORC_OK 0
 #define ORC_NOT_CONVERGED 1
@@ -248,7 +250,15 @@ typedef struct {
   double *Ac, *Lc; /* coarsest dense operator and factor */
   int nco;
   double *work[MAXLEV][4];
+  double t_phase[4]; /* wall seconds of orc_create's phases: S, A_w assembly, A_w Cholesky, hierarchy */
 } orc_ctx;
+
+/* Wall clock for the phase times (instrumentation only; no effect on any result). */
+static double now_s(void) {
+  struct timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+}
 
 static int cmp_int(const void *a, const void *b) {
   int x = *(const int *)a, y = *(const int *)b;
@@ -423,7 +433,9 @@ static int setup_filter(orc_ctx *cx, int m, const int *Jptr, const int *Jcol, co
   }
   for (int i = 0; i < nc; i++)
     for (int j = 0; j < nc; j++) Ap[(size_t)i * nc + j] = cx->Aw[(size_t)cx->pi[i] * nc + cx->pi[j]];
+  double t0 = now_s();
   int st = orc_cholesky_dense(nc, Ap, cx->Lw);
+  cx->t_phase[2] = now_s() - t0;
   free(Ap);
   if (st) {
     char buf[512];
@@ -882,9 +894,15 @@ orc_ctx *orc_create(int nodes, const int *Kptr, const int *Kcol, const double *K
   cx->nodes = nodes;
   cx->n = 3L * nodes;
   cx->m = m;
+  double t0 = now_s();
   int st = form_S(cx, Kptr, Kcol, Kval, m, Jptr, Jcol, Jval, D);
+  double t1 = now_s();
+  cx->t_phase[0] = t1 - t0;
   if (!st) st = setup_filter(cx, m, Jptr, Jcol, Z, nc);
+  double t2 = now_s();
+  cx->t_phase[1] = (t2 - t1) - cx->t_phase[2];
   if (!st) st = build_hierarchy(cx, Bnns, Kptr, Kcol);
+  cx->t_phase[3] = now_s() - t2;
   *status = st;
   if (st) { cx->lev[0].A.ptr = NULL; cx->lev[0].A.col = NULL; cx->lev[0].A.val = NULL; orc_free(cx); return NULL; }
   return cx;
@@ -1104,6 +1122,9 @@ void orc_info(orc_ctx *cx, long *out) {
     out[3 + 5 * l + 4] = (l < cx->nlev - 1) ? L->n_agg : 0;
   }
 }
+
+/* Phase wall times (s) of orc_create: {S, A_w assembly, A_w dense Cholesky, AMG hierarchy}. */
+void orc_times(orc_ctx *cx, double *out) { memcpy(out, cx->t_phase, sizeof cx->t_phase); }
 
 /* which: 0 A.ptr 1 A.col 2 A.val 3 P.ptr 4 P.col 5 P.val 6 R.ptr 7 R.col 8 R.val
  *        9 dl1 10 agg 11 Bnn 12 [lambda, omega] 13 Pt.val 14 root 15 comp

@@ -14,11 +14,13 @@ _lib = None
 
 STATUS = {0: "AMGF_OK", 1: "AMGF_NOT_CONVERGED", -1: "AMGF_ERR_ARG", -2: "AMGF_ERR_NONFINITE",
           -3: "AMGF_ERR_DOMAIN", -4: "AMGF_ERR_NOT_SPD", -5: "AMGF_ERR_RANK", -6: "AMGF_ERR_BREAKDOWN",
-          -7: "AMGF_ERR_CUDA", -8: "AMGF_ERR_OOM", -9: "AMGF_ERR_LIMIT"}
+          -7: "AMGF_ERR_CUDA", -8: "AMGF_ERR_OOM", -9: "AMGF_ERR_LIMIT", -10: "AMGF_ERR_FORMAT"}
 
 SYMBOLS = ["amgf_default_config", "amgf_setup", "amgf_update_D", "amgf_apply", "amgf_vcycle", "amgf_spmv",
            "amgf_pcg_solve", "amgf_pcg_solve_host", "amgf_level_info", "amgf_level_get", "amgf_launch_count",
-           "amgf_pcg_history", "amgf_setup_times", "amgf_last_error", "amgf_destroy"]
+           "amgf_pcg_history", "amgf_setup_times", "amgf_export", "amgf_import", "amgf_last_error",
+           "amgf_destroy"]
+MAX_LEVELS = 32
 
 
 def lib_path() -> str:
@@ -35,7 +37,15 @@ class Config(ctypes.Structure):
 
 class Report(ctypes.Structure):
     _fields_ = [("iterations", ctypes.c_int32), ("converged", ctypes.c_int32),
-                ("rel_pres_norm", ctypes.c_double), ("solve_ms", ctypes.c_double)]
+                ("rel_pres_norm", ctypes.c_double), ("solve_ms", ctypes.c_double), ("setup_ms", ctypes.c_double),
+                ("n_levels", ctypes.c_int32), ("pad_", ctypes.c_int32),
+                ("level_dofs", ctypes.c_int64 * MAX_LEVELS), ("level_nnzb", ctypes.c_int64 * MAX_LEVELS)]
+
+    def as_dict(self):
+        nl = self.n_levels
+        return dict(iterations=self.iterations, converged=bool(self.converged), relres=self.rel_pres_norm,
+                    solve_ms=self.solve_ms, setup_ms=self.setup_ms, n_levels=nl,
+                    level_dofs=list(self.level_dofs[:nl]), level_nnzb=list(self.level_nnzb[:nl]))
 
 
 class AmgfError(RuntimeError):
@@ -75,6 +85,10 @@ def load_library():
     L.amgf_setup_times.restype = I
     L.amgf_pcg_history.argtypes = [P, I, P, P]
     L.amgf_pcg_history.restype = I
+    L.amgf_export.argtypes = [P, ctypes.c_char_p]
+    L.amgf_export.restype = I
+    L.amgf_import.argtypes = [ctypes.c_char_p, P, ctypes.POINTER(P)]
+    L.amgf_import.restype = I
     L.amgf_launch_count.argtypes = [P]
     L.amgf_launch_count.restype = ctypes.c_int64
     L.amgf_last_error.restype = ctypes.c_char_p
@@ -130,6 +144,10 @@ class AMGF:
                           ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(h))
         _check(st)
         self.h = h
+        self._load_info()
+
+    def _load_info(self):
+        L = load_library()
         info = np.zeros(4 + 6 * 32 + 4, dtype=np.int64)
         _check(L.amgf_level_info(self.h, info.ctypes.data_as(ctypes.c_void_p)))
         self.nlev, self.nc, self.nco, self.bw = (int(v) for v in info[:4])
@@ -138,6 +156,32 @@ class AMGF:
                        for l in range(self.nlev)]
         self.loff_size, self.nd_nblocks = int(info[4 + 6 * 32]), int(info[5 + 6 * 32])
         self.tail_level, self.tail_ncta = int(info[6 + 6 * 32]), int(info[7 + 6 * 32])
+
+    @classmethod
+    def import_dir(cls, path, stream=None):
+        """Handle on a hierarchy written in the amgf_export format (by amgf_export or by the oracle)."""
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("AMGF needs a CUDA device (no CPU fallback)")
+        L = load_library()
+        self = cls.__new__(cls)
+        self.torch = torch
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        self._in = {}
+        h = ctypes.c_void_p()
+        _check(L.amgf_import(os.fsencode(path), ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(h)))
+        self.h = h
+        self.config = None
+        self._load_info()
+        self.nodes = self.levels[0]["nodes"]
+        self.n = 3 * self.nodes
+        self.m = 0
+        self.imported = True
+        return self
+
+    def export(self, path):
+        """Write this handle's hierarchy and factors to the existing directory `path` (amgf_export)."""
+        _check(load_library().amgf_export(self.h, os.fsencode(path)))
 
     @classmethod
     def from_problem(cls, p, D=None, Z="lattice", config=None, stream=None):
@@ -169,7 +213,7 @@ class AMGF:
         return x if (x.is_cuda and x.dtype == T.float64 and x.is_contiguous()) else x.to("cuda", T.float64).contiguous()
 
     def update_D(self, D):
-        D = self._vec(D, self.m)
+        D = self._vec(D, None if getattr(self, "imported", False) else self.m)  # imported: the library rejects
         self._in["D_upd"] = D
         _check(load_library().amgf_update_D(self.h, _ptr(D), self._s))
 
@@ -198,8 +242,7 @@ class AMGF:
         st = load_library().amgf_pcg_solve(self.h, _ptr(b), _ptr(x), rtol, max_it, 0 if precond == "amgf" else 1,
                                            ctypes.byref(rep), self._s)
         _check(st, allow=(0, 1))
-        return x, dict(iterations=rep.iterations, converged=bool(rep.converged), relres=rep.rel_pres_norm,
-                       solve_ms=rep.solve_ms)
+        return x, rep.as_dict()
 
     def pcg_host(self, b_host, x_host, rtol=1e-8, max_it=5000, precond="amgf"):
         """b_host, x_host: CPU float64 tensors (pinned for async copies)."""
@@ -210,8 +253,7 @@ class AMGF:
                                                 ctypes.c_void_p(x_host.data_ptr()), rtol, max_it,
                                                 0 if precond == "amgf" else 1, ctypes.byref(rep), self._s)
         _check(st, allow=(0, 1))
-        return dict(iterations=rep.iterations, converged=bool(rep.converged), relres=rep.rel_pres_norm,
-                    solve_ms=rep.solve_ms)
+        return rep.as_dict()
 
     def setup_times(self):
         """Phase times (ms) of the last update_D: total, S, hierarchy, coarsest, A_w factor (side stream)."""
@@ -231,6 +273,11 @@ class AMGF:
     def launches(self) -> int:
         return int(load_library().amgf_launch_count(self.h))
 
+    @staticmethod
+    def _band_stride(bw):
+        R = (bw + 31) // 32 + 1
+        return 32 * R if R <= 8 else (bw + 2) & ~1
+
     def get(self, which, level=0):
         Lv = self.levels[level]
         b, nodes = Lv["b"], Lv["nodes"]
@@ -242,7 +289,8 @@ class AMGF:
                   8: ((Lv["nnzb_P"], 6 * b), np.float64), 9: (nodes * b, np.float64), 10: (nodes, np.int32),
                   11: ((nodes * b, 6), np.float64), 12: (2, np.float64), 14: (nodes, np.int32),
                   15: (nodes, np.int32), 20: (self.nc, np.int32), 22: ((self.nc, W), np.float64),
-                  23: (self.loff_size, np.float64), 25: (self.nc, np.int32)}
+                  23: (self.loff_size, np.float64), 25: (self.nc, np.int32),
+                  24: ((self.nco, self._band_stride(self.nco - 1)), np.float64)}
         if which == 27:
             dt = np.dtype([("p0", np.int32), ("len", np.int32), ("kind", np.int32), ("t0", np.int32),
                            ("off", np.int64), ("level", np.int32), ("rs", np.int32)])

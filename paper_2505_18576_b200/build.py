@@ -4,7 +4,7 @@ import subprocess
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SRC = [os.path.join(HERE, "csrc", f) for f in ("solve.cu", "setup.cu", "filter.cu", "tail.cu", "api.cu")]
+SRC = [os.path.join(HERE, "csrc", f) for f in ("solve.cu", "setup.cu", "filter.cu", "tail.cu", "io.cu", "api.cu")]
 LIB = os.path.join(HERE, "libamgf.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "--fmad=false", "-std=c++17",
@@ -12,7 +12,8 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "--fm
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    deps = SRC + [os.path.join(HERE, "csrc", "common.cuh"), os.path.join(HERE, "csrc", "devutil.cuh"), os.path.join(HERE, "..", "include", "amgf.h")]
+    csrc = os.path.join(HERE, "csrc")
+    deps = [os.path.join(csrc, f) for f in os.listdir(csrc)] + [os.path.join(HERE, "..", "include", "amgf.h")]
     if not force and os.path.exists(LIB) and all(os.path.getmtime(LIB) >= os.path.getmtime(d) for d in deps):
         return LIB
     cmd = [NVCC, *FLAGS, "-o", LIB, *SRC]

@@ -12,6 +12,10 @@
 
 #include "common.cuh"
 
+#include <chrono>
+#include <map>
+#include <mutex>
+
 namespace amgf {
 
 static thread_local std::string g_last_error;
@@ -50,6 +54,15 @@ Ctx::~Ctx() {
   for (void *p : allocs) cudaFree(p);
   if (sc_host) cudaFreeHost(sc_host);
   if (err_host) cudaFreeHost(err_host);
+}
+
+size_t &device_slot(const void *key) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void *>, size_t> slots;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  return slots[{dev, key}];  // std::map references stay valid across insertions
 }
 
 bool debug_sync() {
@@ -360,6 +373,7 @@ static amgf_status pcg_impl(Ctx &c, const double *b, double *x, double rtol, int
   amgf_status st = AMGF_NOT_CONVERGED;
   if (rho0 == 0.0) {
     st = AMGF_OK;
+    c.hist_n = 0;  // no iterations: no history (not the previous solve's)
   } else if (!(rho0 > 0.0)) {
     throw Error{AMGF_ERR_BREAKDOWN, "pcg: r.Mr <= 0"};
   } else {
@@ -370,8 +384,10 @@ static amgf_status pcg_impl(Ctx &c, const double *b, double *x, double rtol, int
       build_pcg_loop(c, precond);
     }
     if (!host_loop && c.pcg_loop[precond] && max_it > 0) {
-      if (c.hist_cap < max_it) {  // history buffer (read through LoopState: the graph keeps its pointers)
-        c.hist_cap = std::min(max_it, 100000);
+      const int want = std::min(max_it, 100000);  // history capacity (iterations beyond it are not recorded)
+      if (c.hist_cap < want) {  // history buffer (read through LoopState: the graph keeps its pointers)
+        if (c.hist) c.release(c.hist);
+        c.hist_cap = want;
         c.hist = c.alloc<double>(2 * (size_t)c.hist_cap);
       }
       LoopState ls = {};
@@ -440,6 +456,12 @@ static amgf_status pcg_impl(Ctx &c, const double *b, double *x, double rtol, int
     rep->converged = st == AMGF_OK;
     rep->rel_pres_norm = rel;
     rep->solve_ms = ms;
+    rep->setup_ms = c.last_setup_ms;
+    rep->n_levels = c.nlev;
+    for (int l = 0; l < MAXLEV; l++) {
+      rep->level_dofs[l] = l < c.nlev ? c.lev[l].n : 0;
+      rep->level_nnzb[l] = l < c.nlev ? c.lev[l].A.nnzb : 0;
+    }
   }
   return st;
 }
@@ -469,25 +491,39 @@ static amgf_status pcg(Ctx &c, const double *b, double *x, double rtol, int max_
   return st;
 }
 
+void ctx_init(Ctx &c, void *stream) {
+  c.stream = (cudaStream_t)stream;
+  REQUIRE(c.cfg.pre_sweeps >= 1 && c.cfg.post_sweeps >= 1 && c.cfg.max_levels >= 1 && c.cfg.power_iters >= 1,
+          AMGF_ERR_ARG, "invalid config");
+  REQUIRE(c.cfg.smoother == 0 || (c.cfg.smoother == 1 && c.cfg.cheb_degree >= 1 && c.cfg.cheb_degree <= 32 &&
+                                  c.cfg.cheb_ratio > 1.0),
+          AMGF_ERR_ARG, "invalid smoother config");
+  if (c.cfg.smoother == 1) {  // Chebyshev coefficients (C23): same formulas, in the same order, as the oracle
+    const double ratio = c.cfg.cheb_ratio;
+    const double theta = (1.0 + 1.0 / ratio) / 2.0, delta = (1.0 - 1.0 / ratio) / 2.0;
+    const double sigma = theta / delta;
+    double rho = 1.0 / sigma;
+    c.cheb_c0 = 1.0 / theta;
+    for (int k = 1; k < c.cfg.cheb_degree; k++) {
+      const double rn = 1.0 / (2.0 * sigma - rho);
+      c.cheb_a[k] = rn * rho;
+      c.cheb_b[k] = 2.0 * rn / delta;
+      rho = rn;
+    }
+  }
+  c.sc = c.alloc<Scalars>(1);
+  c.err = c.alloc<int>(2);
+  CK(cudaMemsetAsync(c.err, 0, 2 * sizeof(int), c.stream));
+  CK(cudaMemsetAsync(c.sc, 0, sizeof(Scalars), c.stream));
+  CK(cudaMallocHost(&c.sc_host, sizeof(Scalars)));
+  CK(cudaMallocHost(&c.err_host, 2 * sizeof(int)));
+}
+
 }  // namespace amgf
 
 // =================================================================== C ABI
 using namespace amgf;
 
-struct amgf_ctx : public Ctx {};
-
-template <class F>
-static amgf_status guarded(F &&f) {
-  try {
-    return f();
-  } catch (const Error &e) {
-    set_error(e.msg);
-    return e.code;
-  } catch (const std::exception &e) {
-    set_error(e.what());
-    return AMGF_ERR_ARG;
-  }
-}
 
 extern "C" {
 
@@ -517,37 +553,15 @@ amgf_status amgf_setup(int32_t nodes, const int32_t *K_ptr, const int32_t *K_col
     REQUIRE(nodes > 0 && K_ptr && K_col && K_val && B_nns, AMGF_ERR_ARG, "null K / near-null space or nodes <= 0");
     REQUIRE(m >= 0 && (m == 0 || (J_ptr && J_col && J_val && D)), AMGF_ERR_ARG, "null J or D");
     REQUIRE(!Z || nc >= 0, AMGF_ERR_ARG, "negative nc");
-    c->stream = (cudaStream_t)stream;
     if (cfg) c->cfg = *cfg; else amgf_default_config(&c->cfg);
-    REQUIRE(c->cfg.pre_sweeps >= 1 && c->cfg.post_sweeps >= 1 && c->cfg.max_levels >= 1 && c->cfg.power_iters >= 1,
-            AMGF_ERR_ARG, "invalid config");
-    REQUIRE(c->cfg.smoother == 0 || (c->cfg.smoother == 1 && c->cfg.cheb_degree >= 1 && c->cfg.cheb_degree <= 32 &&
-                                     c->cfg.cheb_ratio > 1.0),
-            AMGF_ERR_ARG, "invalid smoother config");
-    if (c->cfg.smoother == 1) {  // Chebyshev coefficients (C23): same formulas, in the same order, as the oracle
-      const double ratio = c->cfg.cheb_ratio;
-      const double theta = (1.0 + 1.0 / ratio) / 2.0, delta = (1.0 - 1.0 / ratio) / 2.0;
-      const double sigma = theta / delta;
-      double rho = 1.0 / sigma;
-      c->cheb_c0 = 1.0 / theta;
-      for (int k = 1; k < c->cfg.cheb_degree; k++) {
-        const double rn = 1.0 / (2.0 * sigma - rho);
-        c->cheb_a[k] = rn * rho;
-        c->cheb_b[k] = 2.0 * rn / delta;
-        rho = rn;
-      }
-    }
+    ctx_init(*c, stream);
     c->nodes = nodes;
     c->n = 3L * nodes;
     c->m = m;
-    c->sc = c->alloc<Scalars>(1);
-    c->err = c->alloc<int>(2);
-    CK(cudaMemsetAsync(c->err, 0, 2 * sizeof(int), c->stream));
-    CK(cudaMemsetAsync(c->sc, 0, sizeof(Scalars), c->stream));
-    CK(cudaMallocHost(&c->sc_host, sizeof(Scalars)));
-    CK(cudaMallocHost(&c->err_host, 2 * sizeof(int)));
     c->dot_part = c->alloc<double>(nblk(c->n) + 1);
+    const auto t0 = std::chrono::steady_clock::now();
     setup_all(*c, K_ptr, K_col, K_val, J_ptr, J_col, J_val, D, Z, nc, B_nns);
+    c->last_setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     return AMGF_OK;
   });
   if (st != AMGF_OK) {
@@ -562,9 +576,11 @@ amgf_status amgf_setup(int32_t nodes, const int32_t *K_ptr, const int32_t *K_col
 amgf_status amgf_update_D(amgf_handle h, const double *D, void *stream) {
   if (!h) { set_error("null handle"); return AMGF_ERR_ARG; }
   return guarded([&]() -> amgf_status {
+    REQUIRE(!h->imported, AMGF_ERR_ARG, "update_D: an imported hierarchy has no K, J (set it up with amgf_setup)");
     REQUIRE(h->m == 0 || D, AMGF_ERR_ARG, "null D");
     h->stream = (cudaStream_t)stream;
     setup_numeric(*h, D);
+    h->last_setup_ms = h->setup_ms[0];
     CK(cudaStreamSynchronize(h->stream));
     return AMGF_OK;
   });
@@ -680,6 +696,7 @@ amgf_status amgf_level_get(amgf_handle h, int32_t which, int32_t level, void *ds
       case 20: cp(h->Z, h->nc * 4); break;
       case 22: cp(h->Lrow, (size_t)h->nc * band_stride(h->bw) * 8); break;
       case 23: cp(h->Loff, (size_t)h->loff_size * 8); break;
+      case 24: cp(h->Lc_row, (size_t)h->nco * band_stride(h->nco - 1) * 8); break;
       case 25: cp(h->pi_z, (size_t)h->nc * 4); break;
       case 27: cp(h->nd_blk, (size_t)h->nd_nblocks * 32); break;
       default: throw Error{AMGF_ERR_ARG, "unknown array id"};

@@ -195,6 +195,8 @@ struct Ctx {
   std::vector<double> host_hist;  // same, host-loop fallback
   int64_t graph_launches[2] = {0, 0};
   bool capturing = false;
+  bool imported = false;      // built by amgf_import: no K, J, D (amgf_update_D unavailable)
+  double last_setup_ms = 0;   // amgf_setup / amgf_import wall time or the last amgf_update_D device time
   std::vector<void *> allocs;
 
   template <class T>
@@ -230,6 +232,11 @@ inline void launch_pdl(cudaStream_t st, void (*kernel)(KArgs...), dim3 grid, dim
   cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, ((KArgs)args)...);
   if (e != cudaSuccess) throw Error{AMGF_ERR_CUDA, std::string("cudaLaunchKernelEx (PDL): ") + cudaGetErrorString(e)};
 }
+
+// One-time per-DEVICE state of a kernel (function attributes, __constant__ setup): cudaFuncSetAttribute and
+// cudaMemcpyToSymbol act on the current device only, so a process-wide static guard would skip them for a
+// second device.  Returns the slot of (current device, key), 0 before its first use; thread-safe.
+size_t &device_slot(const void *key);
 
 // Post-launch bookkeeping: count the launch, surface launch errors; with AMGF_DEBUG_SYNC=1 in the
 // environment also synchronise and name the kernel that faulted.
@@ -302,6 +309,15 @@ void launch_band_sweep(Ctx &c, int nblocks, const int *d_p0, const int *d_len, i
 void drop_caches(Ctx &c);
 void build_sell(Ctx &c, const Bsr &A, Sell &S, bool alloc, bool split, bool sort_rows = false);
 
+// pieces of setup_all reused by amgf_import (io.cu)
+void build_thin(Ctx &c);
+void alloc_workspaces(Ctx &c);
+void r_interleave(Ctx &c, Bsr &R);
+void coarsest_alloc(Ctx &c);
+int band_width(Ctx &c);
+// api.cu: handle basics shared by amgf_setup and amgf_import
+void ctx_init(Ctx &c, void *stream);  // validates c.cfg, Chebyshev coefficients, scalars and error flags
+
 // ------------------------------------------------------------------ solve orchestration (api.cu)
 // Fusion hooks of the PCG iteration into the V-cycles (Chebyshev smoother only; bitwise unchanged):
 //   prestarted  level 0's from-zero start (dir, start buffer) was written by k_axpy2_cheb0
@@ -315,4 +331,26 @@ void tail_plan(Ctx &c);                                   // after setup_all: en
 void tail_vcycle(Ctx &c, const double *b, double *x);    // V-cycle from level c.tail_level down, one launch
 void apply_M(Ctx &c, const double *r, double *z, VcOpts first = VcOpts{}, const double *dot_r = nullptr);
 
+}  // namespace amgf
+
+// The opaque handle of the C ABI (include/amgf.h).
+struct amgf_ctx : public amgf::Ctx {};
+
+namespace amgf {
+// Run f, mapping exceptions to an amgf_status (no exception crosses the ABI).
+template <class F>
+amgf_status guarded(F &&f) {
+  try {
+    return f();
+  } catch (const Error &e) {
+    set_error(e.msg);
+    return e.code;
+  } catch (const std::bad_alloc &) {
+    set_error("host allocation failed");
+    return AMGF_ERR_OOM;
+  } catch (const std::exception &e) {
+    set_error(e.what());
+    return AMGF_ERR_ARG;
+  }
+}
 }  // namespace amgf

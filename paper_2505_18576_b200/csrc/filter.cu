@@ -465,7 +465,7 @@ static void launch_off_band(Ctx &c, int np, const int *pairs, const NdBlk *blk, 
   const size_t smem = smem_of(threads);
   REQUIRE(smem <= 227 * 1024, AMGF_ERR_LIMIT, "band too wide for the off-block factor kernel");
   const dim3 grid(np, (c.nd_maxsep + threads - 1) / threads);
-  static size_t attr = 0;
+  size_t &attr = device_slot((const void *)k_nd_off_band);
   if (smem > attr) {
     CK(cudaFuncSetAttribute(k_nd_off_band, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
@@ -532,7 +532,7 @@ void nd_solve(Ctx &c, const double *r1, const int *gather) {
   // backward: separators top-down (then their subtree rows), then leaves
   const size_t sb_smem = (size_t)c.nd_maxsep * (SB_TR + 1) * sizeof(double);
   {
-    static size_t attr = 0;
+    size_t &attr = device_slot((const void *)k_nd_sep_bwd);
     if (sb_smem > attr && sb_smem > 48 * 1024) {
       CK(cudaFuncSetAttribute(k_nd_sep_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb_smem));
       attr = sb_smem;

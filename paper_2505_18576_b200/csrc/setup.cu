@@ -1193,9 +1193,9 @@ static void level_numeric(Ctx &c, int l, LevelCache &lc) {
   {
     // explicit carveout on the large hierarchy grids, as for the solve's residual SpMV: lets the side
     // stream's shared-memory-heavy A_w factorization CTAs find room (A/B: AMGF_HIER_CARVEOUT=-1 disables)
-    static bool once = false;
+    size_t &once = device_slot((const void *)k_spgemm_dense<3, 3, 6>);
     if (!once) {
-      once = true;
+      once = 1;
       const int cv = getenv("AMGF_HIER_CARVEOUT") ? atoi(getenv("AMGF_HIER_CARVEOUT")) : 50;
       if (cv >= 0) {
         CK(cudaFuncSetAttribute(k_spgemm_dense<3, 3, 6>, cudaFuncAttributePreferredSharedMemoryCarveout, cv));
@@ -1216,8 +1216,7 @@ static void level_numeric(Ctx &c, int l, LevelCache &lc) {
            L.Pt.val, L.dpt, L.omega, L.P.val);
   LAUNCH(k_transpose_vals, L.R.nnzb, L.R.nnzb, L.b, 6, lc.R_perm, L.P.val, L.R.val);
   if (L.b == 3) {  // level-0 restriction reads R's values group-interleaved (Bsr::ival)
-    if (!L.R.ival) L.R.ival = c.alloc<double>((size_t)L.R.nnzb * 18);
-    LAUNCH(k_interleave_rows, (long)L.R.nbr * 32, L.R.nbr, L.R.ptr, 18, L.R.val, L.R.ival);
+    r_interleave(c, L.R);
   }
   // AP = A * P, G = R * AP over the precomputed block-product lists
   {
@@ -1269,6 +1268,91 @@ void drop_caches(Ctx &c) {
   delete static_cast<Caches *>(c.setup_cache);
   c.setup_cache = nullptr;
 }
+
+// Thin second-residual structure S[:, Z] (reading R11) and the compact Z rows of S (k_resid_dofs); needs the
+// level-0 operator, pos (Z positions) and the elimination-order maps of nd_symbolic.
+void build_thin(Ctx &c) {
+  Caches &C = caches(c);
+  Level &L0 = c.lev[0];
+  const long n = c.n;
+  // thin structure
+  int *cnt = c.alloc<int>(n + 1), *off = c.alloc<int>(n + 1), *flag = c.alloc<int>(n + 1), *foff = c.alloc<int>(n + 1);
+  CK(cudaMemsetAsync(cnt, 0, (n + 1) * sizeof(int), c.stream));
+  CK(cudaMemsetAsync(flag, 0, (n + 1) * sizeof(int), c.stream));
+  LAUNCH(k_thin_count, n, n, L0.A.ptr, L0.A.col, c.pos, cnt);
+  long tnnz = scan_ex(c, cnt, off, n);
+  LAUNCH(k_flag_nonzero, n, n, cnt, flag);
+  c.nthin = (int)scan_ex(c, flag, foff, n);
+  c.thin_row = c.alloc<int>(c.nthin);
+  c.thin_ptr = c.alloc<int>(c.nthin + 1);
+  c.thin_pos = c.alloc<int>(tnnz);
+  c.thin_src = c.alloc<int>(tnnz);
+  c.thin_val = c.alloc<double>(tnnz);
+  LAUNCH(k_thin_fill, n, n, L0.A.ptr, L0.A.col, c.pos, off, foff, c.thin_row, c.thin_ptr, c.thin_pos, c.thin_src);
+  nd_remap_positions(c, c.thin_pos, tnnz);  // thin entries address y in elimination (pi) order
+  int tn = (int)tnnz;
+  CK(cudaMemcpyAsync(c.thin_ptr + c.nthin, &tn, sizeof(int), cudaMemcpyHostToDevice, c.stream));
+  C.thin_nnz = tnnz;
+  // compact fine rows of the filter dofs (elimination order) for the Z-row residual
+  {
+    int *zc = c.alloc<int>(c.nc + 1);
+    CK(cudaMemsetAsync(zc, 0, (c.nc + 1) * sizeof(int), c.stream));
+    LAUNCH(k_zr_count, c.nc, c.nc, c.dof, L0.A.ptr, zc);
+    c.zr_ptr = c.alloc<int>(c.nc + 1);
+    c.zr_nnz = scan_ex(c, zc, c.zr_ptr, c.nc);
+    c.release(zc);
+    c.zr_col = c.alloc<int>(c.zr_nnz);
+    c.zr_src = c.alloc<int>(c.zr_nnz);
+    c.zr_val = c.alloc<double>(c.zr_nnz * 3);
+    LAUNCH(k_zr_fill, c.nc, c.nc, c.dof, L0.A.ptr, L0.A.col, c.zr_ptr, c.zr_col, c.zr_src);
+  }
+  thin_numeric(c, tnnz);
+  c.release(cnt); c.release(off); c.release(flag); c.release(foff);
+}
+
+// Solve workspaces of every level and of the PCG (and the level-0 SELL of a one-level hierarchy).
+void alloc_workspaces(Ctx &c) {
+  Level &L0 = c.lev[0];
+  const long n = c.n;
+  for (int q = 0; q < c.nlev; q++) {
+    Level &L = c.lev[q];
+    L.x = c.alloc<double>(L.n);
+    L.x2 = c.alloc<double>(L.n);
+    L.bv = c.alloc<double>(L.n);
+    L.r = c.alloc<double>(L.n);
+    if (c.cfg.smoother == 1) L.dir = c.alloc<double>(L.n);
+  }
+  if (c.nlev == 1) build_sell(c, L0.A, L0.As, true, false);
+  c.w_x1 = c.alloc<double>(n);
+  c.w_r1 = c.alloc<double>(n);
+  c.w_xv = c.alloc<double>(n);
+  c.p = c.alloc<double>(n);
+  c.q = c.alloc<double>(n);
+  c.rr = c.alloc<double>(n);
+  c.zz = c.alloc<double>(n);
+  c.xx = c.alloc<double>(n);
+  c.bb = c.alloc<double>(n);
+}
+
+// Level-0 restriction values regrouped for k_restrict (Bsr::ival).
+void r_interleave(Ctx &c, Bsr &R) {
+  if (!R.ival) R.ival = c.alloc<double>((size_t)R.nnzb * R.br * R.bc);
+  LAUNCH(k_interleave_rows, (long)R.nbr * 32, R.nbr, R.ptr, R.br * R.bc, R.val, R.ival);
+}
+
+// Structural lower band width of A_w in Z order: max_a (a - min{b <= a : S[Z_a, Z_b] stored}).
+int band_width(Ctx &c) {
+  Level &L0 = c.lev[0];
+  int *bwd = c.alloc<int>(1);
+  CK(cudaMemsetAsync(bwd, 0, sizeof(int), c.stream));
+  LAUNCH(k_band_start, c.nc, c.nc, c.Z, c.pos, L0.A.ptr, L0.A.col, bwd);
+  const int bw = d2h1(c, bwd);
+  c.release(bwd);
+  return bw;
+}
+
+// Coarsest dense factor storage (band of width nco - 1).
+void coarsest_alloc(Ctx &c) { band_alloc(c, c.nco, c.nco - 1, c.Lc_row, c.Lc_col, c.Lc_rev, c.Lc_dinv); }
 
 // =================================================================== setup_all
 void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, const int *J_ptr, const int *J_col,
@@ -1378,47 +1462,11 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
 
   // ---- s3: A_w band, factor, thin residual
   if (c.nc > 0) {
-    int *bwd = c.alloc<int>(1);
-    CK(cudaMemsetAsync(bwd, 0, sizeof(int), c.stream));
-    LAUNCH(k_band_start, c.nc, c.nc, c.Z, c.pos, L0.A.ptr, L0.A.col, bwd);
-    c.bw = d2h1(c, bwd);
-    c.release(bwd);
+    c.bw = band_width(c);
     nd_symbolic(c);
     filter_numeric(c);
     check_dev_error(c, "A_w Cholesky");
-    // thin structure
-    int *cnt = c.alloc<int>(n + 1), *off = c.alloc<int>(n + 1), *flag = c.alloc<int>(n + 1), *foff = c.alloc<int>(n + 1);
-    CK(cudaMemsetAsync(cnt, 0, (n + 1) * sizeof(int), c.stream));
-    CK(cudaMemsetAsync(flag, 0, (n + 1) * sizeof(int), c.stream));
-    LAUNCH(k_thin_count, n, n, L0.A.ptr, L0.A.col, c.pos, cnt);
-    long tnnz = scan_ex(c, cnt, off, n);
-    LAUNCH(k_flag_nonzero, n, n, cnt, flag);
-    c.nthin = (int)scan_ex(c, flag, foff, n);
-    c.thin_row = c.alloc<int>(c.nthin);
-    c.thin_ptr = c.alloc<int>(c.nthin + 1);
-    c.thin_pos = c.alloc<int>(tnnz);
-    c.thin_src = c.alloc<int>(tnnz);
-    c.thin_val = c.alloc<double>(tnnz);
-    LAUNCH(k_thin_fill, n, n, L0.A.ptr, L0.A.col, c.pos, off, foff, c.thin_row, c.thin_ptr, c.thin_pos, c.thin_src);
-    nd_remap_positions(c, c.thin_pos, tnnz);  // thin entries address y in elimination (pi) order
-    int tn = (int)tnnz;
-    CK(cudaMemcpyAsync(c.thin_ptr + c.nthin, &tn, sizeof(int), cudaMemcpyHostToDevice, c.stream));
-    C.thin_nnz = tnnz;
-    // compact fine rows of the filter dofs (elimination order) for the Z-row residual
-    {
-      int *zc = c.alloc<int>(c.nc + 1);
-      CK(cudaMemsetAsync(zc, 0, (c.nc + 1) * sizeof(int), c.stream));
-      LAUNCH(k_zr_count, c.nc, c.nc, c.dof, L0.A.ptr, zc);
-      c.zr_ptr = c.alloc<int>(c.nc + 1);
-      c.zr_nnz = scan_ex(c, zc, c.zr_ptr, c.nc);
-      c.release(zc);
-      c.zr_col = c.alloc<int>(c.zr_nnz);
-      c.zr_src = c.alloc<int>(c.zr_nnz);
-      c.zr_val = c.alloc<double>(c.zr_nnz * 3);
-      LAUNCH(k_zr_fill, c.nc, c.nc, c.dof, L0.A.ptr, L0.A.col, c.zr_ptr, c.zr_col, c.zr_src);
-    }
-    thin_numeric(c, tnnz);
-    c.release(cnt); c.release(off); c.release(flag); c.release(foff);
+    build_thin(c);
   }
 
   // ---- hierarchy
@@ -1594,29 +1642,11 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
     Level &L = c.lev[c.nlev - 1];
     REQUIRE(L.n <= 16384, AMGF_ERR_LIMIT, "coarsest level too large for a dense factor (" + std::to_string(L.n) + ")");
     c.nco = (int)L.n;
-    band_alloc(c, c.nco, c.nco - 1, c.Lc_row, c.Lc_col, c.Lc_rev, c.Lc_dinv);
+    coarsest_alloc(c);
     coarsest_numeric(c);
     check_dev_error(c, "coarsest Cholesky");
   }
-  // ---- workspaces
-  for (int q = 0; q < c.nlev; q++) {
-    Level &L = c.lev[q];
-    L.x = c.alloc<double>(L.n);
-    L.x2 = c.alloc<double>(L.n);
-    L.bv = c.alloc<double>(L.n);
-    L.r = c.alloc<double>(L.n);
-    if (c.cfg.smoother == 1) L.dir = c.alloc<double>(L.n);
-  }
-  if (c.nlev == 1) build_sell(c, L0.A, L0.As, true, false);
-  c.w_x1 = c.alloc<double>(n);
-  c.w_r1 = c.alloc<double>(n);
-  c.w_xv = c.alloc<double>(n);
-  c.p = c.alloc<double>(n);
-  c.q = c.alloc<double>(n);
-  c.rr = c.alloc<double>(n);
-  c.zz = c.alloc<double>(n);
-  c.xx = c.alloc<double>(n);
-  c.bb = c.alloc<double>(n);
+  alloc_workspaces(c);
   CK(cudaStreamSynchronize(c.stream));
   tail_plan(c);
 }

@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(CTA) k_sell(int nrows, const int *__restrict__
 
 // Latency-oriented variant for scalar-row (1 x BC) SELL of the small coarse levels: D slots of values and
 // x in flight (register ring, fully unrolled), column indices 2D slots ahead.  Same chain as k_sell (C2).
-__constant__ int c_r1_prefetch;  // L2 prefetch distance of k_sell_r1 in slots (0: off; 8 measured best:
+__constant__ int c_r1_prefetch = 8;  // L2 prefetch distance of k_sell_r1 in slots (0: off; 8 measured best:
                                  // V-cycle 1030 -> 1018 us at cfg 3; 16 and 32 are slower)
 __device__ __forceinline__ int r1_prefetch_slots() { return c_r1_prefetch; }
 
@@ -289,9 +289,9 @@ static void sell_dispatch(Ctx &c, const Sell &A, int mode, const double *x, cons
   // the x gathers of even block widths are 16-byte vector loads (gather_x)
   if (BC % 2 == 0) REQUIRE(((uintptr_t)x & 15) == 0, AMGF_ERR_ARG, "SELL SpMV: x must be 16-byte aligned");
   {
-    static bool pf_set = false;
+    size_t &pf_set = device_slot((const void *)&c_r1_prefetch);
     if (!pf_set) {
-      pf_set = true;
+      pf_set = 1;
       const int pf = getenv("AMGF_R1_PF") ? atoi(getenv("AMGF_R1_PF")) : 8;  // measured: 8 slots best
       CK(cudaMemcpyToSymbol(c_r1_prefetch, &pf, sizeof(int)));
     }
@@ -300,9 +300,9 @@ static void sell_dispatch(Ctx &c, const Sell &A, int mode, const double *x, cons
     // An explicit carveout preference for the residual SpMV lets the A_w solve, which runs concurrently on
     // the filter stream (apply_M), get SMs while the SpMV is resident: the driver default cost ~50 us per
     // AMGF apply at cfg 3; any value in 0..60 % gave the same time, above that the SpMV loses L1.
-    static bool once = false;
+    size_t &once = device_slot((const void *)k_sell<BR, BC, MODE_RESID>);
     if (!once) {
-      once = true;
+      once = 1;
       CK(cudaFuncSetAttribute(k_sell<BR, BC, MODE_RESID>, cudaFuncAttributePreferredSharedMemoryCarveout, 50));
       // the setup's power iteration (MODE_Y) runs beside the A_w factorization: same reason
       CK(cudaFuncSetAttribute(k_sell<BR, BC, MODE_Y>, cudaFuncAttributePreferredSharedMemoryCarveout, 50));
@@ -470,7 +470,7 @@ __global__ void __launch_bounds__(1024) k_sell_resid_part(int nrows, const int *
 void launch_resid_partition(Ctx &c, const Sell &A, const double *x, const double *b, double *y, int nsm,
                             size_t reserve) {
   REQUIRE(A.br == 3 && A.bc == 3 && !A.perm, AMGF_ERR_ARG, "resid_partition: fine-level 3x3 SELL expected");
-  static size_t attr = 0;
+  size_t &attr = device_slot((const void *)k_sell_resid_part<3, 3>);
   if (reserve > attr) {
     CK(cudaFuncSetAttribute(k_sell_resid_part<3, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reserve));
     attr = reserve;
@@ -962,12 +962,13 @@ static void sweep_RN(Ctx &c, int nblocks, const int *p0, const int *len, int bw,
                      const double *Lrev, const double *dinv, const double *in, const int *gather, double *out,
                      double *out_shift) {
   const size_t smem = (size_t)NB * 32 * (32 * R) * sizeof(double);
-  static bool attr_f = false, attr_b = false;
+  size_t &attr_f = device_slot((const void *)k_band_sweep<R, NB, true, BLOCKED>);
+  size_t &attr_b = device_slot((const void *)k_band_sweep<R, NB, false, BLOCKED>);
   if (fwd) {
     if (!attr_f) {
       CK(cudaFuncSetAttribute(k_band_sweep<R, NB, true, BLOCKED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)smem));
-      attr_f = true;
+      attr_f = 1;
     }
     launch_pdl(c.stream, k_band_sweep<R, NB, true, BLOCKED>, dim3(nblocks), dim3(32), smem, p0, len, bw, Lcol, Lrev,
                dinv, in, gather, out, out_shift);
@@ -975,7 +976,7 @@ static void sweep_RN(Ctx &c, int nblocks, const int *p0, const int *len, int bw,
     if (!attr_b) {
       CK(cudaFuncSetAttribute(k_band_sweep<R, NB, false, BLOCKED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)smem));
-      attr_b = true;
+      attr_b = 1;
     }
     launch_pdl(c.stream, k_band_sweep<R, NB, false, BLOCKED>, dim3(nblocks), dim3(32), smem, p0, len, bw, Lcol,
                Lrev, dinv, in, gather, out, out_shift);
@@ -1080,10 +1081,10 @@ static void trsv_R(Ctx &c, int n, int bw, const double *Lcol, const double *Lrev
   // as many rounds in flight as 220 KB of shared memory allow (TMA latency > one round of 32 pivots)
   constexpr int NB = (220 * 1024) / (32 * 32 * R * 8) >= 4 ? 4 : 3;
   const size_t smem = (size_t)NB * 32 * (32 * R) * sizeof(double);
-  static bool attr_set = false;
+  size_t &attr_set = device_slot((const void *)k_band_trsv<R, NB>);
   if (!attr_set) {
     CK(cudaFuncSetAttribute(k_band_trsv<R, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_set = true;
+    attr_set = 1;
   }
   k_band_trsv<R, NB><<<1, 32, smem, c.stream>>>(n, bw, Lcol, Lrev, dinv, v, gather, y, scatter, xout, w);
 }

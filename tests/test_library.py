@@ -65,10 +65,23 @@ def test_no_cpu_fallback():
         AMGF.from_problem(amgf_gen.generate(2))
 
 
-def test_product_path_does_not_import_oracle():
-    for f in os.listdir(os.path.join(ROOT, "paper_2505_18576_b200")):
+def test_product_path_does_not_import_oracle(libpath):
+    """The product path never imports, includes, links or loads anything under oracle/ (comments may cite it)."""
+    pkg = os.path.join(ROOT, "paper_2505_18576_b200")
+    for f in os.listdir(pkg):
         if f.endswith(".py"):
-            src = open(os.path.join(ROOT, "paper_2505_18576_b200", f)).read()
-            assert "import oracle" not in src and "from oracle" not in src
-    for f in os.listdir(os.path.join(ROOT, "paper_2505_18576_b200", "csrc")):
-        assert "oracle" not in open(os.path.join(ROOT, "paper_2505_18576_b200", "csrc", f)).read().lower() or f
+            src = open(os.path.join(pkg, f)).read()
+            assert not re.search(r"^\s*(import|from)\s+oracle\b", src, re.M), f
+            assert "liboracle" not in src and "amgf_oracle" not in src, f
+    for f in os.listdir(os.path.join(pkg, "csrc")):
+        src = open(os.path.join(pkg, "csrc", f)).read()
+        code = re.sub(r"//[^\n]*|/\*.*?\*/", "", src, flags=re.S)   # strip comments
+        assert not re.search(r"#\s*include\s*[<\"][^>\"]*oracle", code), f
+        assert "orc_" not in code and "liboracle" not in code and "dlopen" not in code, f
+    # the built library neither needs nor references the oracle's library or symbols
+    dyn = subprocess.run(["readelf", "-d", libpath], capture_output=True, text=True).stdout
+    assert "oracle" not in dyn
+    syms = subprocess.run(["nm", "-D", libpath], capture_output=True, text=True).stdout
+    assert not re.search(r"\borc_", syms)
+    from paper_2505_18576_b200 import build
+    assert not any("oracle" in x for x in build.SRC + build.FLAGS)
