@@ -23,6 +23,8 @@ import threading
 import time
 import types
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -300,29 +302,111 @@ def bench_config(cfg, p, nc, c, world):
     """The `config` object both arms print (c: the solver configuration, attribute access)."""
     return {"workload": f"cfg{cfg}: two-block N={p.N}, n={p.n} dofs, m={p.m}, n_c={nc}, "
                         f"{p.D_seq.shape[0]}-system IP-like D sequence, rtol={p.rtol}",
-            "l2": "inputs larger than L2 (fine operator 1.1 GB)", "parallelism": f"replicas x{world}",
+            "l2": (f"inputs larger than L2 (fine operator {p.K_col.size * 76 / 1e9:.2f} GB + hierarchy)"
+                   if p.K_col.size * 76 > 126e6 else "L2-resident workload (parity case, not a bench line)"),
+            "parallelism": f"replicas x{world}",
             "smoother": (f"chebyshev degree {c.cheb_degree} on [1/{c.cheb_ratio:g}, 1] of D_l1^-1 A (DESIGN R18)"
                          if c.smoother == 1 else "l1-jacobi"),
             "sweeps": [c.pre_sweeps, c.post_sweeps]}
 
 
-def cpu_baseline(p, iters_guess, budget_s=25.0):
-    """Oracle as it stands, on a bounded sample of cfg 3: hierarchy setup without the dense A_w factor,
-    then V-cycles and S SpMVs; per-system time = setup + iters * (2 V-cycles + 2 S SpMVs)."""
-    import numpy as np
-    import oracle
-    oracle.build()
-    t = time.perf_counter()
-    o = oracle.Oracle.from_problem(p, factor_filter=0)
-    t_setup = time.perf_counter() - t
-    x = np.random.default_rng(0).standard_normal(p.n)
-    t = time.perf_counter(); o.vcycle(x); t_v = time.perf_counter() - t
-    t = time.perf_counter(); o.spmv(x); t_s = time.perf_counter() - t
-    per_sys = t_setup + iters_guess * (2 * t_v + 2 * t_s)
-    return {"value": per_sys * 1e3, "unit": "ms/system", "cores": 1, "kind": "oracle",
-            "sample": f"cfg3: oracle setup without the dense A_w factor ({t_setup:.1f} s) + 1 V-cycle "
-                      f"({t_v:.2f} s) + 1 S SpMV ({t_s:.3f} s); value = setup + {iters_guess} PCG iterations "
-                      f"x (2 V-cycles + 2 SpMVs), filter cost excluded (underestimates the oracle)",
+def oracle_iterations(cfg, systems):
+    """The oracle's OWN PCG iteration counts for these systems, from its cached full-size runs
+    (tests/golden/oracle/, written by tools/oracle_golden.py with the plain oracle only)."""
+    out = []
+    for s in systems:
+        path = os.path.join(ROOT, "tests", "golden", "oracle", f"cfg{cfg}_s{s}.json")
+        if not os.path.exists(path):
+            return None
+        out.append(json.load(open(path))["pcg"]["iterations"])
+    return out
+
+
+def _chol_fma(n):
+    """Fused multiply-adds of the oracle's dense left-looking Cholesky (orc_cholesky_dense) of order n:
+    column j costs j for the pivot and j for each of its n-1-j sub-diagonal entries."""
+    j = np.arange(n, dtype=np.float64)
+    return float(np.sum(j * (n - j)))
+
+
+class OracleSample:
+    """Bounded timing of the oracle as it stands (one host core) on the full-size workload p.
+
+    Measured here: the setup without the dense A_w factor (S = K + J^T D J and the AMG hierarchy, full size),
+    the dense Cholesky on an n0 x n0 SPD sample (its cost is data-independent: no pivoting, no zero
+    skipping), one V-cycle, one S SpMV and one dense TRSV pair of the full order n_c.  A system then costs
+    setup + Cholesky(n_c) [scaled by the exact FMA count] + iterations x (2 V-cycles + 3 S-sized passes
+    (S x1, the thin residual's loop over S, S p) + TRSV pair), with the oracle's own iteration count from its
+    cached full-size runs -- no number from the GPU path."""
+
+    def __init__(self, p, n0=2000):
+        import oracle
+        oracle.build()
+        self.p = p
+        t = time.perf_counter()
+        self.o = oracle.Oracle.from_problem(p, factor_filter=0)
+        self.t_setup = time.perf_counter() - t
+        self.nc = self.o.nc
+        self.bw = int(self.o.get(26)[0])
+        rng = np.random.default_rng(0)
+        n0 = min(n0, max(self.nc, 1))
+        A = rng.standard_normal((n0, n0))
+        A = A @ A.T + n0 * np.eye(n0)
+        t = time.perf_counter(); oracle.cholesky(A); t_c = time.perf_counter() - t
+        self.n0 = n0
+        self.t_chol = t_c * _chol_fma(self.nc) / _chol_fma(n0) if self.nc else 0.0
+        Lt = np.tril(rng.random((self.nc, self.nc))) + self.nc * np.eye(self.nc)
+        v = rng.standard_normal(self.nc)
+        t = time.perf_counter(); oracle.chol_solve(Lt, v); self.t_trsv = time.perf_counter() - t
+        del Lt
+        self.x = rng.standard_normal(p.n)
+        self.sample_iteration()
+
+    def sample_iteration(self):
+        t = time.perf_counter(); self.o.vcycle(self.x); self.t_v = time.perf_counter() - t
+        t = time.perf_counter(); self.o.spmv(self.x); self.t_s = time.perf_counter() - t
+        return self.per_iteration()
+
+    def per_iteration(self):
+        return 2 * self.t_v + 3 * self.t_s + self.t_trsv
+
+    def per_system_s(self, iters):
+        return self.t_setup + self.t_chol + iters * self.per_iteration()
+
+    def sample_text(self, iters_src):
+        return (f"oracle (plain C, 1 core) on the full {self.p.name} system: measured setup without "
+                f"the dense A_w factor {self.t_setup:.1f} s, Cholesky of a {self.n0}^2 SPD sample scaled by the exact "
+                f"FMA count to n_c={self.nc} -> {self.t_chol:.0f} s, V-cycle {self.t_v:.2f} s, S SpMV {self.t_s:.3f} s, "
+                f"TRSV pair {self.t_trsv:.2f} s; per system = setup + Cholesky + iterations x (2 V + 3 S passes + TRSV "
+                f"pair) with {iters_src}.  Full-system oracle runs (tests/golden/oracle/*.json times_s) took "
+                f"{_golden_full_time(self.p)}")
+
+
+def _golden_full_time(p):
+    cfg = p.name[3:] if p.name.startswith("cfg") else "?"
+    ts = []
+    cpu = "?"
+    for s in range(p.D_seq.shape[0]):
+        path = os.path.join(ROOT, "tests", "golden", "oracle", f"cfg{cfg}_s{s}.json")
+        if os.path.exists(path):
+            r = json.load(open(path))
+            ts.append(r["times_s"]["setup_total"] + r["times_s"]["pcg"])
+            cpu = r["host"]["cpu"]
+    if not ts:
+        return "n/a"
+    return f"{statistics.mean(ts):.0f} s per system on average ({len(ts)} systems, {cpu}, shared with other runs)"
+
+
+def cpu_baseline(p, cfg, systems):
+    """GPU arm's cpu_baseline: the oracle, bounded sample (OracleSample), on the systems the timed region solved."""
+    iters = oracle_iterations(cfg, systems)
+    if iters is None:
+        return {"value": None, "unit": "ms/system", "cores": 1, "kind": "oracle",
+                "sample": "oracle iteration counts for these systems are not cached (tools/oracle_golden.py)"}
+    smp = OracleSample(p)
+    v = statistics.mean(smp.per_system_s(i) for i in iters) * 1e3
+    return {"value": v, "unit": "ms/system", "cores": 1, "kind": "oracle",
+            "sample": smp.sample_text(f"the oracle's own iteration counts (mean {statistics.mean(iters):.1f})"),
             "cpu": _cpu_model()}
 
 
@@ -337,34 +421,36 @@ def _cpu_model():
 
 
 def run_reference(args, rank, world):
-    """Reference arm: the CPU oracle (this tier has no reference implementation), same metric/config."""
+    """Reference arm: the CPU oracle (this tier has no reference implementation), same metric/config.
+    Each step is a bounded sample (one V-cycle and one S SpMV re-timed) of one system of the sequence, in the
+    same replica schedule as the GPU arm; setup and the Cholesky sample are timed once."""
     if rank != 0:
         return None
-    import numpy as np
     import amgf_gen
     import oracle
-    oracle.build()
     p = amgf_gen.config(args.cfg)
-    t = time.perf_counter()
-    o = oracle.Oracle.from_problem(p, factor_filter=0)
-    t_setup = time.perf_counter() - t
-    x = np.random.default_rng(0).standard_normal(p.n)
+    nsys = p.D_seq.shape[0]
+    smp = OracleSample(p)
     for _ in range(min(args.warmup, 1)):
-        o.spmv(x)
-    vals = []
-    iters_guess = 46  # mean PCG iterations of the GPU path over the cfg 3 sequence (default smoother)
+        smp.sample_iteration()
+    vals, its = [], []
     for k in range(args.steps):
-        t = time.perf_counter(); o.vcycle(x); t_v = time.perf_counter() - t
-        t = time.perf_counter(); o.spmv(x); t_s = time.perf_counter() - t
-        vals.append((t_setup + iters_guess * (2 * t_v + 2 * t_s)) * 1e3)
+        s = system_of(0, 1, args.warmup + k, nsys)
+        it = oracle_iterations(args.cfg, [s])
+        if it is None:
+            raise RuntimeError(f"no cached oracle run for cfg{args.cfg} system {s} (tools/oracle_golden.py)")
+        smp.sample_iteration()
+        vals.append(smp.per_system_s(it[0]) * 1e3)
+        its.append(it[0])
     v = statistics.mean(vals)
-    sample = (f"cfg3 oracle: per step 1 V-cycle + 1 S SpMV timed, value = setup without the dense A_w factor "
-              f"({t_setup:.1f} s, once) + {iters_guess} iterations x (2 V + 2 SpMV); filter excluded")
+    sample = smp.sample_text(f"the oracle's own iteration counts per system {its}")
+    cfgns = types.SimpleNamespace(**oracle.DEFAULTS)
     return {"impl": "reference", "metric": METRIC, "value": v, "unit": "ms/system", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": dict(bench_config(args.cfg, p, len(p.Z), types.SimpleNamespace(**oracle.DEFAULTS), world),
-                           levels=[(L["nodes"] * L["b"]) for L in o.levels]),
+            "config": dict(bench_config(args.cfg, p, smp.nc, cfgns, world),
+                           levels=[(L["nodes"] * L["b"]) for L in smp.o.levels], band_width_Aw=smp.bw),
+            "pcg_iterations": its,
             "cpu_baseline": {"value": v, "unit": "ms/system", "cores": 1, "kind": "oracle", "sample": sample,
                              "cpu": _cpu_model()},
             "e2e": {"value": v, "unit": "ms/system", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -396,7 +482,7 @@ def main():
     res, p = run_amgf(args, rank, world, local_rank)
     if rank == 0:
         if not args.no_cpu_baseline and world == 1:
-            res["cpu_baseline"] = cpu_baseline(p, int(statistics.mean(res["pcg_iterations"])))
+            res["cpu_baseline"] = cpu_baseline(p, args.cfg, res["systems"])
         print(json.dumps(res))
     if world > 1:
         import torch
