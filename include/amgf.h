@@ -176,6 +176,12 @@ amgf_status amgf_pcg_history(amgf_handle h, int32_t n, double *alpha, double *be
  * factorization (side stream, concurrent with the hierarchy)}.  Zeros before the first update. */
 amgf_status amgf_setup_times(amgf_handle h, double *ms);
 
+/* Debug bounds check (no compute-sanitizer on the target pool): with AMGF_GUARD=1 in the environment every
+ * internal allocation of a handle is followed by a 4 KB guard zone of a fixed byte pattern; this returns the
+ * number of guard zones that were overwritten (out-of-bounds writes) since creation, -2 when AMGF_GUARD is not
+ * set, -1 on a null handle or CUDA error.  Synchronises the device. */
+int64_t amgf_debug_guard_check(amgf_handle h);
+
 /* Number of kernel launches issued by this handle since creation (bench accounting). */
 int64_t amgf_launch_count(amgf_handle h);
 

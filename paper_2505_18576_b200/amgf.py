@@ -18,7 +18,8 @@ STATUS = {0: "AMGF_OK", 1: "AMGF_NOT_CONVERGED", -1: "AMGF_ERR_ARG", -2: "AMGF_E
 
 SYMBOLS = ["amgf_default_config", "amgf_setup", "amgf_update_D", "amgf_apply", "amgf_vcycle", "amgf_spmv",
            "amgf_pcg_solve", "amgf_pcg_solve_host", "amgf_level_info", "amgf_level_get", "amgf_launch_count",
-           "amgf_pcg_history", "amgf_setup_times", "amgf_export", "amgf_import", "amgf_last_error",
+           "amgf_pcg_history", "amgf_setup_times", "amgf_export", "amgf_import", "amgf_debug_guard_check",
+           "amgf_last_error",
            "amgf_destroy"]
 MAX_LEVELS = 32
 
@@ -89,6 +90,8 @@ def load_library():
     L.amgf_export.restype = I
     L.amgf_import.argtypes = [ctypes.c_char_p, P, ctypes.POINTER(P)]
     L.amgf_import.restype = I
+    L.amgf_debug_guard_check.argtypes = [P]
+    L.amgf_debug_guard_check.restype = ctypes.c_int64
     L.amgf_launch_count.argtypes = [P]
     L.amgf_launch_count.restype = ctypes.c_int64
     L.amgf_last_error.restype = ctypes.c_char_p
@@ -268,6 +271,10 @@ class AMGF:
         _check(load_library().amgf_pcg_history(self.h, n, a.ctypes.data_as(ctypes.c_void_p),
                                                 bt.ctypes.data_as(ctypes.c_void_p)))
         return a, bt
+
+    def guard_violations(self) -> int:
+        """Overwritten guard zones of this handle (AMGF_GUARD=1 debug allocations; -2 if not enabled)."""
+        return int(load_library().amgf_debug_guard_check(self.h))
 
     @property
     def launches(self) -> int:

@@ -22,8 +22,37 @@ static thread_local std::string g_last_error;
 void set_error(const std::string &m) { g_last_error = m; }
 const char *get_error() { return g_last_error.c_str(); }
 
+bool Ctx::guard_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("AMGF_GUARD");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+long Ctx::guard_violations() {
+  cudaDeviceSynchronize();
+  long bad = 0;
+  std::vector<unsigned char> buf(kGuardBytes);
+  for (auto &g : guards) {
+    if (cudaMemcpy(buf.data(), (char *)g.first + g.second, kGuardBytes, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    for (unsigned char b : buf)
+      if (b != kGuardByte) {
+        bad++;
+        break;
+      }
+  }
+  return bad;
+}
+
 void Ctx::release(void *p) {
   if (!p) return;
+  for (size_t i = 0; i < guards.size(); i++)
+    if (guards[i].first == p) {
+      guards[i] = guards.back();
+      guards.pop_back();
+      break;
+    }
   for (size_t i = 0; i < allocs.size(); i++)
     if (allocs[i] == p) {
       cudaFree(p);
@@ -707,6 +736,12 @@ amgf_status amgf_level_get(amgf_handle h, int32_t which, int32_t level, void *ds
 }
 
 int64_t amgf_launch_count(amgf_handle h) { return h ? h->launches : -1; }
+
+int64_t amgf_debug_guard_check(amgf_handle h) {
+  if (!h) return -1;
+  if (!Ctx::guard_enabled()) return -2;
+  return h->guard_violations();
+}
 
 amgf_status amgf_setup_times(amgf_handle h, double *ms) {
   if (!h || !ms) { set_error("null argument"); return AMGF_ERR_ARG; }

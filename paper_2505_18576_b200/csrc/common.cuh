@@ -199,15 +199,30 @@ struct Ctx {
   double last_setup_ms = 0;   // amgf_setup / amgf_import wall time or the last amgf_update_D device time
   std::vector<void *> allocs;
 
+  // Debug guard zones (environment AMGF_GUARD=1): every allocation is followed by kGuardBytes of a fixed byte
+  // pattern; guard_violations() counts the zones a kernel wrote into (out-of-bounds writes), see
+  // amgf_debug_guard_check.  compute-sanitizer is not available on this pool, so this is the library's own
+  // bounds check, used by tests/test_gpu_parity.py::test_guard_zones on every code path of a small solve.
+  static constexpr size_t kGuardBytes = 4096;
+  static constexpr unsigned char kGuardByte = 0xA5;
+  std::vector<std::pair<void *, size_t>> guards;  // (allocation, payload bytes)
+  static bool guard_enabled();
+
   template <class T>
   T *alloc(size_t count) {
     void *p = nullptr;
     if (count == 0) count = 1;
-    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
-    if (e != cudaSuccess) throw Error{AMGF_ERR_OOM, "cudaMalloc " + std::to_string(count * sizeof(T)) + " bytes"};
+    const size_t bytes = count * sizeof(T), extra = guard_enabled() ? kGuardBytes : 0;
+    cudaError_t e = cudaMalloc(&p, bytes + extra);
+    if (e != cudaSuccess) throw Error{AMGF_ERR_OOM, "cudaMalloc " + std::to_string(bytes) + " bytes"};
     allocs.push_back(p);
+    if (extra) {
+      cudaMemset((char *)p + bytes, kGuardByte, extra);
+      guards.emplace_back(p, bytes);
+    }
     return (T *)p;
   }
+  long guard_violations();
   void release(void *p);
   ~Ctx();
 };

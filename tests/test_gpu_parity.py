@@ -5,6 +5,8 @@ floating-point output and exact equality for every integer output (patterns, agg
 Comparisons use np.array_equal, which treats +0 and -0 as equal (the only freedom the contract
 leaves: the sign of an exact zero produced by skipped zero terms of the banded factor, R3).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -435,3 +437,66 @@ def test_device_loop_reuse(oracle_lib, amgf_mod, torch_cuda):
         xo, ro = o2.pcg(p.b, rtol=p.rtol, precond=precond)
         xg, rg = g.pcg(p.b, rtol=p.rtol, precond=precond)
         assert rg["iterations"] == ro["iterations"] and np.array_equal(xg.cpu().numpy(), xo), precond
+
+
+def _shift_node(p, node, shift):
+    Kv = p.K_val.copy()
+    for k in range(p.K_ptr[node], p.K_ptr[node + 1]):
+        if p.K_col[k] == node:
+            Kv[k] = Kv[k] - shift * np.eye(3).ravel()
+    return Kv
+
+
+def test_error_codes_match_oracle(oracle_lib, amgf_mod):
+    """NOT_SPD (A_w indefinite), RANK (degenerate near-null space) and BREAKDOWN (S indefinite: p.Sp <= 0
+    inside PCG) are raised by the GPU path exactly where the oracle raises them."""
+    p = tiny(N=3, matching=False, e_max=6.0)
+    cfg = dict(coarsest_size=16)
+
+    def both(Kv=None, B=None):
+        Kv = p.K_val if Kv is None else Kv
+        B = p.B_nns if B is None else B
+        args = (p.nodes, p.K_ptr, p.K_col, Kv, p.J_ptr, p.J_col, p.J_val, p.D, p.Z, B)
+        codes = []
+        for mk, err in ((lambda: oracle_lib.Oracle(*args, **cfg), oracle_lib.OracleError),
+                        (lambda: amgf_mod.AMGF(*args, config=cfg), amgf_mod.AmgfError)):
+            try:
+                h = mk()
+            except err as e:
+                codes.append(("setup", e.code))
+                continue
+            try:
+                if isinstance(h, oracle_lib.Oracle):
+                    _, info = h.pcg(p.b, rtol=1e-10, maxit=500)
+                else:
+                    _, info = h.pcg(p.b, rtol=1e-10, max_it=500)
+                codes.append(("pcg", info["iterations"]))
+            except err as e:
+                codes.append(("pcg", e.code))
+        return codes
+
+    # A_w indefinite: an interface node's diagonal block shifted by -1e8
+    assert both(Kv=_shift_node(p, int(p.Z[0]) // 3, 1e8)) == [("setup", -4)] * 2
+    # near-null space with two equal columns: rank-deficient tentative prolongator
+    B = p.B_nns.copy()
+    B[:, 5] = B[:, 4]
+    assert both(B=B) == [("setup", -5)] * 2
+    # S indefinite away from the interface: setup succeeds, PCG breaks down (p.Sp <= 0)
+    interior = [v for v in range(p.nodes) if not p.dirichlet[v]]
+    assert both(Kv=_shift_node(p, interior[len(interior) // 4], 2.0)) == [("pcg", -6)] * 2
+
+
+def test_guard_zones(amgf_mod):
+    """Library-level bounds check (AMGF_GUARD=1 guard zones after every device allocation; the pool has no
+    compute-sanitizer): no kernel of setup / update_D / apply / V-cycle / SpMV / PCG / import writes past an
+    allocation, on cfg 0-2 and the tiny edge cases (tools/sanitize_run.py)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for extra in ({}, {"AMGF_HOST_LOOP": "1"}):
+        out = subprocess.run([sys.executable, os.path.join(root, "tools", "sanitize_run.py")], capture_output=True,
+                             text=True, env=dict(os.environ, AMGF_GUARD="1", **extra), timeout=1200)
+        assert out.returncode == 0, out.stderr[-3000:]
+        res = json.loads(out.stdout.strip().splitlines()[-1])
+        assert res and all(v == 0 for v in res.values()), res
