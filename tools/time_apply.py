@@ -12,7 +12,8 @@ from paper_2505_18576_b200 import AMGF  # noqa: E402
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 p = amgf_gen.config(cfg)
-g = AMGF.from_problem(p, D=p.D_seq[-1])
+cfg_over = json.loads(os.environ["AMGF_TIME_CONFIG"]) if os.environ.get("AMGF_TIME_CONFIG") else None
+g = AMGF.from_problem(p, D=p.D_seq[-1], config=cfg_over)
 torch.manual_seed(0)
 x = torch.randn(p.n, dtype=torch.float64, device="cuda")
 y = torch.empty_like(x)
@@ -32,4 +33,5 @@ for name, fn in (("apply", g.apply), ("vcycle", g.vcycle)):
     if name == "apply":
         res["apply_checksum"] = float(y.double().abs().sum())
 res["levels"] = g.levels
+res["config"] = cfg_over
 print(json.dumps(res))
