@@ -281,3 +281,19 @@ def with_D(p: Problem, D: np.ndarray) -> Problem:
     q = dataclasses.replace(p)
     q.D = np.ascontiguousarray(D, dtype=np.float64)
     return q
+
+
+def box_diagonals(p: Problem, e_max: float = 6.0, seed: int = 1000):
+    """Bound-constraint diagonals (D_lo, D_up) for the bound-constrained system of Remark boundconstr
+    (PAPER.md:271-295): log-barrier Hessians of the box u - u* in [delta_lo, delta_up] on every free dof,
+    D = 10^(e_max * xi), xi ~ U[0,1) from SplitMix64(seed), lower diagonal first, dof order; 0 on Dirichlet
+    dofs (no bound there).  Inputs only: no method arithmetic."""
+    rng = SplitMix64(seed)
+    free = np.repeat(~p.dirichlet, 3)
+    out = []
+    for _ in range(2):
+        xi = np.array([rng.uniform() for _ in range(p.n)])
+        d = 10.0 ** (e_max * xi)
+        d[~free] = 0.0
+        out.append(d.astype(np.float64))
+    return out[0], out[1]

@@ -104,6 +104,15 @@ amgf_status amgf_setup(int32_t nodes, const int32_t *K_ptr, const int32_t *K_col
  * values; aggregation and all sparsity patterns are reused (they do not depend on D, reading R5). */
 amgf_status amgf_update_D(amgf_handle h, const double *D, void *stream);
 
+/* Numeric re-setup for the bound-constrained system (Remark boundconstr):
+ *   A~ = K + J~^T D~ J~,  J~ = [J; I; -I],  D~ = diag(D, D_lo, D_up),
+ * i.e. S = K + J^T D J + diag(D_lo) + diag(D_up); in the entry chain of contract C1 the rows of I and -I
+ * follow J's rows, so a diagonal entry continues with fma(1*D_lo[p], 1, acc) then fma(-1*D_up[p], -1, acc).
+ *   D_lo[n], D_up[n]   device arrays, finite and >= 0 (0: no bound on that dof); either may be NULL (zeros);
+ *                      both NULL is amgf_update_D.  The bounds do not change I_c (Z stays J's contact dofs).
+ * Errors as amgf_update_D (AMGF_ERR_DOMAIN for a negative bound diagonal). */
+amgf_status amgf_update_D_box(amgf_handle h, const double *D, const double *D_lo, const double *D_up, void *stream);
+
 /* z = M r, one AMGF application (Def. AMGF, three stages SPEC.md:245).  r, z: n doubles. */
 amgf_status amgf_apply(amgf_handle h, const double *r, double *z, void *stream);
 

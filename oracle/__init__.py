@@ -80,6 +80,9 @@ def lib():
         L.orc_create.restype = P
         L.orc_create.argtypes = [ctypes.c_int, P, P, P, ctypes.c_int, P, P, P, P, P, ctypes.c_int, P,
                                  ctypes.POINTER(OrcConfig), ctypes.POINTER(ctypes.c_int)]
+        L.orc_create_box.restype = P
+        L.orc_create_box.argtypes = [ctypes.c_int, P, P, P, ctypes.c_int, P, P, P, P, P, P, P, ctypes.c_int, P,
+                                     ctypes.POINTER(OrcConfig), ctypes.POINTER(ctypes.c_int)]
         L.orc_free.argtypes = [P]
         L.orc_last_error.restype = ctypes.c_char_p
         L.orc_dot.restype = ctypes.c_double
@@ -160,7 +163,8 @@ def priority(v: int, seed: int) -> int:
 class Oracle:
     """Oracle AMGF hierarchy for one system S = K + J^T D J."""
 
-    def __init__(self, nodes, K_ptr, K_col, K_val, J_ptr, J_col, J_val, D, Z, B_nns, **cfg):
+    def __init__(self, nodes, K_ptr, K_col, K_val, J_ptr, J_col, J_val, D, Z, B_nns, D_lo=None, D_up=None, **cfg):
+        """D_lo / D_up (n, >= 0, optional): bound-constraint diagonals of A~ = K + J~^T D~ J~."""
         c = dict(DEFAULTS); c.update(cfg)
         self.cfg = c
         self._keep = [_c(K_ptr, np.int32), _c(K_col, np.int32), _c(K_val, np.float64),
@@ -171,9 +175,11 @@ class Oracle:
         m = len(k[3]) - 1
         conf = OrcConfig(**c)
         st = ctypes.c_int(0)
-        self.h = lib().orc_create(nodes, _p(k[0]), _p(k[1]), _p(k[2]), m, _p(k[3]), _p(k[4]), _p(k[5]),
-                                  _p(k[6]), _p(k[7]), 0 if Z is None else len(k[7]), _p(k[8]),
-                                  ctypes.byref(conf), ctypes.byref(st))
+        box = [None if v is None else _c(v, np.float64) for v in (D_lo, D_up)]
+        self._keep += box
+        self.h = lib().orc_create_box(nodes, _p(k[0]), _p(k[1]), _p(k[2]), m, _p(k[3]), _p(k[4]), _p(k[5]),
+                                      _p(k[6]), _p(box[0]), _p(box[1]), _p(k[7]), 0 if Z is None else len(k[7]),
+                                      _p(k[8]), ctypes.byref(conf), ctypes.byref(st))
         if not self.h:
             raise OracleError(st.value, lib().orc_last_error().decode())
         self.n = 3 * nodes
@@ -185,10 +191,10 @@ class Oracle:
                             nnzb_P=int(info[6 + 5 * l]), n_agg=int(info[7 + 5 * l])) for l in range(self.nlev)]
 
     @classmethod
-    def from_problem(cls, p, D=None, Z="lattice", **cfg):
+    def from_problem(cls, p, D=None, Z="lattice", D_lo=None, D_up=None, **cfg):
         Zv = p.Z if isinstance(Z, str) and Z == "lattice" else Z
         return cls(p.nodes, p.K_ptr, p.K_col, p.K_val, p.J_ptr, p.J_col, p.J_val,
-                   p.D if D is None else D, Zv, p.B_nns, **cfg)
+                   p.D if D is None else D, Zv, p.B_nns, D_lo=D_lo, D_up=D_up, **cfg)
 
     def __del__(self):
         if getattr(self, "h", None):

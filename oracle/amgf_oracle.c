@@ -267,7 +267,8 @@ static int cmp_int(const void *a, const void *b) {
 
 /* ---------- S = K + J^T D J (eq:linsystem1), contract C1 ---------- */
 static int form_S(orc_ctx *cx, const int *Kptr, const int *Kcol, const double *Kval,
-                  int m, const int *Jptr, const int *Jcol, const double *Jval, const double *D) {
+                  int m, const int *Jptr, const int *Jcol, const double *Jval, const double *D,
+                  const double *Dlo, const double *Dup) {
   int nodes = cx->nodes;
   long n = cx->n;
   /* J^T as lists per dof (constraint rows ascending) */
@@ -337,6 +338,14 @@ static int form_S(orc_ctx *cx, const int *Kptr, const int *Kcol, const double *K
               acc = fma(t, tv[bb], acc);
               a++; bb++;
             }
+          }
+          if (p == qd) {
+            /* bound-constrained A~ = K + J~^T D~ J~, J~ = [J; I; -I], D~ = diag(D, D_lo, D_up) (Remark
+             * boundconstr): the rows of I and -I come after J's, so the diagonal entry
+             * continues the same chain with t = 1 * D_lo[p], fma(t, 1, acc), then t = -1 * D_up[p],
+             * fma(t, -1, acc) (contract C1); off-diagonal entries have no bound rows. */
+            if (Dlo) { double t = 1.0 * Dlo[p]; acc = fma(t, 1.0, acc); }
+            if (Dup) { double t = -1.0 * Dup[p]; acc = fma(t, -1.0, acc); }
           }
           blk[3 * r + c] = acc;
         }
@@ -870,9 +879,10 @@ static int all_finite(const double *x, long n) {
   return 1;
 }
 
-orc_ctx *orc_create(int nodes, const int *Kptr, const int *Kcol, const double *Kval,
-                    int m, const int *Jptr, const int *Jcol, const double *Jval, const double *D,
-                    const int *Z, int nc, const double *Bnns, const orc_config *cfg, int *status) {
+orc_ctx *orc_create_box(int nodes, const int *Kptr, const int *Kcol, const double *Kval,
+                        int m, const int *Jptr, const int *Jcol, const double *Jval, const double *D,
+                        const double *Dlo, const double *Dup,
+                        const int *Z, int nc, const double *Bnns, const orc_config *cfg, int *status) {
   g_err[0] = 0;
   if (nodes <= 0 || m < 0 || !Kptr || !Kcol || !Kval || !Bnns || !cfg) {
     *status = fail(ORC_ERR_ARG, "bad arguments");
@@ -884,6 +894,13 @@ orc_ctx *orc_create(int nodes, const int *Kptr, const int *Kcol, const double *K
   }
   for (int k = 0; k < m; k++)
     if (!(D[k] > 0.0)) { *status = fail(ORC_ERR_DOMAIN, "D must be strictly positive"); return NULL; }
+  for (int w = 0; w < 2; w++) {
+    const double *Db = w ? Dup : Dlo;
+    if (!Db) continue;
+    if (!all_finite(Db, 3L * nodes)) { *status = fail(ORC_ERR_NONFINITE, "non-finite bound diagonal"); return NULL; }
+    for (long p = 0; p < 3L * nodes; p++)
+      if (!(Db[p] >= 0.0)) { *status = fail(ORC_ERR_DOMAIN, "bound diagonals must be >= 0"); return NULL; }
+  }
   if (cfg->smoother < 0 || cfg->smoother > 1 ||
       (cfg->smoother == 1 && (cfg->cheb_degree < 1 || cfg->cheb_degree > 32 || !(cfg->cheb_ratio > 1.0)))) {
     *status = fail(ORC_ERR_ARG, "bad smoother configuration");
@@ -895,7 +912,7 @@ orc_ctx *orc_create(int nodes, const int *Kptr, const int *Kcol, const double *K
   cx->n = 3L * nodes;
   cx->m = m;
   double t0 = now_s();
-  int st = form_S(cx, Kptr, Kcol, Kval, m, Jptr, Jcol, Jval, D);
+  int st = form_S(cx, Kptr, Kcol, Kval, m, Jptr, Jcol, Jval, D, Dlo, Dup);
   double t1 = now_s();
   cx->t_phase[0] = t1 - t0;
   if (!st) st = setup_filter(cx, m, Jptr, Jcol, Z, nc);
@@ -906,6 +923,12 @@ orc_ctx *orc_create(int nodes, const int *Kptr, const int *Kcol, const double *K
   *status = st;
   if (st) { cx->lev[0].A.ptr = NULL; cx->lev[0].A.col = NULL; cx->lev[0].A.val = NULL; orc_free(cx); return NULL; }
   return cx;
+}
+
+orc_ctx *orc_create(int nodes, const int *Kptr, const int *Kcol, const double *Kval,
+                    int m, const int *Jptr, const int *Jcol, const double *Jval, const double *D,
+                    const int *Z, int nc, const double *Bnns, const orc_config *cfg, int *status) {
+  return orc_create_box(nodes, Kptr, Kcol, Kval, m, Jptr, Jcol, Jval, D, NULL, NULL, Z, nc, Bnns, cfg, status);
 }
 
 /* ---------- solve phase ---------- */

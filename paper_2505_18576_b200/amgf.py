@@ -16,7 +16,7 @@ STATUS = {0: "AMGF_OK", 1: "AMGF_NOT_CONVERGED", -1: "AMGF_ERR_ARG", -2: "AMGF_E
           -3: "AMGF_ERR_DOMAIN", -4: "AMGF_ERR_NOT_SPD", -5: "AMGF_ERR_RANK", -6: "AMGF_ERR_BREAKDOWN",
           -7: "AMGF_ERR_CUDA", -8: "AMGF_ERR_OOM", -9: "AMGF_ERR_LIMIT", -10: "AMGF_ERR_FORMAT"}
 
-SYMBOLS = ["amgf_default_config", "amgf_setup", "amgf_update_D", "amgf_apply", "amgf_vcycle", "amgf_spmv",
+SYMBOLS = ["amgf_default_config", "amgf_setup", "amgf_update_D", "amgf_update_D_box", "amgf_apply", "amgf_vcycle", "amgf_spmv",
            "amgf_pcg_solve", "amgf_pcg_solve_host", "amgf_level_info", "amgf_level_get", "amgf_launch_count",
            "amgf_pcg_history", "amgf_setup_times", "amgf_export", "amgf_import", "amgf_debug_guard_check",
            "amgf_last_error",
@@ -69,6 +69,8 @@ def load_library():
     L.amgf_setup.restype = I
     L.amgf_update_D.argtypes = [P, P, P]
     L.amgf_update_D.restype = I
+    L.amgf_update_D_box.argtypes = [P, P, P, P, P]
+    L.amgf_update_D_box.restype = I
     for f in ("amgf_apply", "amgf_vcycle"):
         getattr(L, f).argtypes = [P, P, P, P]
         getattr(L, f).restype = I
@@ -219,6 +221,14 @@ class AMGF:
         D = self._vec(D, None if getattr(self, "imported", False) else self.m)  # imported: the library rejects
         self._in["D_upd"] = D
         _check(load_library().amgf_update_D(self.h, _ptr(D), self._s))
+
+    def update_D_box(self, D, D_lo=None, D_up=None):
+        """Numeric re-setup of A~ = K + J^T D J + diag(D_lo) + diag(D_up) (bound constraints)."""
+        D = self._vec(D, self.m)
+        lo = None if D_lo is None else self._vec(D_lo, self.n)
+        up = None if D_up is None else self._vec(D_up, self.n)
+        self._in["D_upd"], self._in["D_lo"], self._in["D_up"] = D, lo, up
+        _check(load_library().amgf_update_D_box(self.h, _ptr(D), _ptr(lo), _ptr(up), self._s))
 
     def apply(self, r, out=None):
         r = self._vec(r, self.n)

@@ -120,7 +120,7 @@ void check_dev_error(Ctx &c, const char *where) {
   std::string w = std::string(where) + ": ";
   switch (code) {
     case DERR_NONFINITE: throw Error{AMGF_ERR_NONFINITE, w + "non-finite value at index " + std::to_string(info)};
-    case DERR_DOMAIN: throw Error{AMGF_ERR_DOMAIN, w + "D must be strictly positive (index " + std::to_string(info) + ")"};
+    case DERR_DOMAIN: throw Error{AMGF_ERR_DOMAIN, w + "D must be > 0 and bound diagonals >= 0 (index " + std::to_string(info) + ")"};
     case DERR_NOT_SPD:
       throw Error{AMGF_ERR_NOT_SPD, w + "non-positive pivot " + std::to_string(info % 1000000) +
                                         (info / 1000000 == 1 ? " of A_w" : " of the coarsest operator")};
@@ -609,6 +609,19 @@ amgf_status amgf_update_D(amgf_handle h, const double *D, void *stream) {
     REQUIRE(h->m == 0 || D, AMGF_ERR_ARG, "null D");
     h->stream = (cudaStream_t)stream;
     setup_numeric(*h, D);
+    h->last_setup_ms = h->setup_ms[0];
+    CK(cudaStreamSynchronize(h->stream));
+    return AMGF_OK;
+  });
+}
+
+amgf_status amgf_update_D_box(amgf_handle h, const double *D, const double *D_lo, const double *D_up, void *stream) {
+  if (!h) { set_error("null handle"); return AMGF_ERR_ARG; }
+  return guarded([&]() -> amgf_status {
+    REQUIRE(!h->imported, AMGF_ERR_ARG, "update_D_box: an imported hierarchy has no K, J (set it up with amgf_setup)");
+    REQUIRE(h->m == 0 || D, AMGF_ERR_ARG, "null D");
+    h->stream = (cudaStream_t)stream;
+    setup_numeric(*h, D, D_lo, D_up);
     h->last_setup_ms = h->setup_ms[0];
     CK(cudaStreamSynchronize(h->stream));
     return AMGF_OK;

@@ -132,6 +132,8 @@ struct Ctx {
   int *Jt_ptr = nullptr, *Jt_row = nullptr;  // J^T (per dof: constraint rows ascending)
   double *Jt_val = nullptr;
   double *D = nullptr;
+  double *D_lo = nullptr, *D_up = nullptr;  // bound-constraint diagonals of A~ (n each; has_box: in use)
+  bool has_box = false;
   int *S_kblk = nullptr;  // per S block: index of the K block (-1 if none)
   // filter (A_w factor in nested-dissection order, filter.cu)
   struct NdLevel { int count = 0, ngroups = 0; int *ids = nullptr, *p0 = nullptr, *len = nullptr, *sub_ptr = nullptr, *sub_list = nullptr, *groups = nullptr, *selfpairs = nullptr; };
@@ -307,7 +309,8 @@ enum DotFinish { DOT_PLAIN = 0, DOT_PI = 1, DOT_RHO0 = 2, DOT_RHO1 = 3 };
 void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, const int *J_ptr,
                const int *J_col, const double *J_val, const double *D, const int *Z, int nc,
                const double *B_nns);
-void setup_numeric(Ctx &c, const double *D);  // update_D
+void setup_numeric(Ctx &c, const double *D, const double *D_lo = nullptr,
+                   const double *D_up = nullptr);  // update_D (+ bound-constraint diagonals)
 // filter.cu
 void nd_symbolic(Ctx &c);
 void nd_numeric(Ctx &c);

@@ -130,6 +130,11 @@ __global__ void k_check_pos(long n, const double *v, int *err) {
   if (i < n && !(v[i] > 0.0)) raise_err(err, DERR_DOMAIN, (int)i);
 }
 
+__global__ void k_check_nonneg(long n, const double *v, int *err) {
+  long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (i < n && !(v[i] >= 0.0)) raise_err(err, DERR_DOMAIN, (int)i);
+}
+
 // ------------------------------------------------------------------ s1: S = K + J^T D J
 constexpr int SCAP = 96;
 
@@ -179,8 +184,12 @@ __global__ void k_S_fill(int nodes, const int *K_ptr, const int *K_col, const in
 }
 
 // one thread per S block: C1
+// S = K + J^T D J (C1); with the bound-constraint diagonals (Remark boundconstr, PAPER.md:271-295:
+// A~ = K + J~^T D~ J~, J~ = [J; I; -I]) the diagonal entries continue the chain with the rows of I and -I:
+// t = 1 * D_lo[p], fma(t, 1, acc); t = -1 * D_up[p], fma(t, -1, acc).
 __global__ void k_S_values(long nnzb, const int *S_rowof, const int *S_col, const int *S_kblk, const double *K_val,
-                           const int *Jt_ptr, const int *Jt_row, const double *Jt_val, const double *D, double *S_val) {
+                           const int *Jt_ptr, const int *Jt_row, const double *Jt_val, const double *D,
+                           const double *D_lo, const double *D_up, double *S_val) {
   long e = blockIdx.x * (long)blockDim.x + threadIdx.x;
   if (e >= nnzb) return;
   const int I = S_rowof[e], Jn = S_col[e], kb = S_kblk[e];
@@ -198,6 +207,10 @@ __global__ void k_S_values(long nnzb, const int *S_rowof, const int *S_col, cons
           acc = __fma_rn(t, Jt_val[b], acc);
           a++; b++;
         }
+      }
+      if (p == q) {
+        if (D_lo) { const double t = 1.0 * D_lo[p]; acc = __fma_rn(t, 1.0, acc); }
+        if (D_up) { const double t = -1.0 * D_up[p]; acc = __fma_rn(t, -1.0, acc); }
       }
       S_val[e * 9 + 3 * r + cc] = acc;
     }
@@ -1108,7 +1121,7 @@ struct SetupCache {  // per-context arrays needed for numeric re-setup
 static void S_numeric(Ctx &c, const int *S_rowof) {
   Level &L0 = c.lev[0];
   LAUNCH(k_S_values, L0.A.nnzb, L0.A.nnzb, S_rowof, L0.A.col, c.S_kblk, c.K.val, c.Jt_ptr, c.Jt_row, c.Jt_val, c.D,
-         L0.A.val);
+         c.has_box ? c.D_lo : nullptr, c.has_box ? c.D_up : nullptr, L0.A.val);
 }
 
 static void filter_numeric(Ctx &c) {
@@ -1696,13 +1709,25 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
 }
 
 // =================================================================== numeric re-setup (new D)
-void setup_numeric(Ctx &c, const double *D) {
+void setup_numeric(Ctx &c, const double *D, const double *D_lo, const double *D_up) {
   Caches &C = caches(c);
   setup_mark(c, 0, c.stream);
   d2d(c, c.D, D, c.m);
   LAUNCH(k_check_finite, c.m, c.m, c.D, c.err, DERR_NONFINITE);
   LAUNCH(k_check_pos, c.m, c.m, c.D, c.err);
   check_dev_error(c, "D check");
+  // bound-constraint diagonals (both or neither; amgf_update_D_box): zero-filled when only one is given
+  c.has_box = D_lo || D_up;
+  if (c.has_box) {
+    if (!c.D_lo) { c.D_lo = c.alloc<double>(c.n); c.D_up = c.alloc<double>(c.n); }
+    if (D_lo) d2d(c, c.D_lo, D_lo, c.n); else CK(cudaMemsetAsync(c.D_lo, 0, c.n * sizeof(double), c.stream));
+    if (D_up) d2d(c, c.D_up, D_up, c.n); else CK(cudaMemsetAsync(c.D_up, 0, c.n * sizeof(double), c.stream));
+    LAUNCH(k_check_finite, c.n, c.n, c.D_lo, c.err, DERR_NONFINITE);
+    LAUNCH(k_check_finite, c.n, c.n, c.D_up, c.err, DERR_NONFINITE);
+    LAUNCH(k_check_nonneg, c.n, c.n, c.D_lo, c.err);
+    LAUNCH(k_check_nonneg, c.n, c.n, c.D_up, c.err);
+    check_dev_error(c, "bound diagonal check");
+  }
   S_numeric(c, C.s.S_rowof);
   setup_mark(c, 1, c.stream);
   Level &L0 = c.lev[0];

@@ -500,3 +500,32 @@ def test_guard_zones(amgf_mod):
         assert out.returncode == 0, out.stderr[-3000:]
         res = json.loads(out.stdout.strip().splitlines()[-1])
         assert res and all(v == 0 for v in res.values()), res
+
+
+@pytest.mark.parametrize("cfg", [None, 0, 1])
+def test_bound_constrained_parity(oracle_lib, amgf_mod, cfg):
+    """Bound-constrained A~ = K + J~^T D~ J~ (Remark boundconstr) through amgf_update_D_box:
+    hierarchy, apply and PCG bitwise equal to the oracle built on the same D, D_lo, D_up; a later plain
+    amgf_update_D drops the bounds again; a negative bound diagonal is AMGF_ERR_DOMAIN."""
+    p = tiny(N=3, matching=False, e_max=8.0) if cfg is None else gen.config(cfg)
+    kw = dict(coarsest_size=16) if cfg is None else {}
+    lo, up = gen.box_diagonals(p, e_max=6.0, seed=21)
+    g = amgf_mod.AMGF.from_problem(p, config=kw)
+    g.update_D_box(p.D, lo, up)
+    o = oracle_lib.Oracle.from_problem(p, D_lo=lo, D_up=up, **kw)
+    assert_hierarchy_equal(o, g)
+    assert_filter_factor_equal(o, g)
+    r = np.random.default_rng(31).standard_normal(p.n)
+    assert np.array_equal(g.apply(r).cpu().numpy(), o.apply(r))
+    xo, ro = o.pcg(p.b, rtol=p.rtol)
+    xg, rg = g.pcg(p.b, rtol=p.rtol)
+    assert rg["iterations"] == ro["iterations"] and np.array_equal(xg.cpu().numpy(), xo)
+    # only the lower bounds (upper NULL = zeros)
+    g.update_D_box(p.D, lo, None)
+    o1 = oracle_lib.Oracle.from_problem(p, D_lo=lo, **kw)
+    assert np.array_equal(g.get(2), o1.get(2))
+    g.update_D(p.D)
+    assert np.array_equal(g.apply(r).cpu().numpy(), oracle_lib.Oracle.from_problem(p, **kw).apply(r))
+    with pytest.raises(amgf_mod.AmgfError) as e:
+        g.update_D_box(p.D, -lo, up)
+    assert e.value.code == -3

@@ -197,6 +197,37 @@ def test_S_equals_dense_K_plus_JtDJ(oracle_lib, matching):
     assert all(r in Zs and c in Zs for r, c in zip(diff.row[nz], diff.col[nz]))
 
 
+@pytest.mark.parametrize("matching", [True, False])
+def test_bound_constrained_S(oracle_lib, matching):
+    """Remark boundconstr: A~ = K + J~^T D~ J~ with J~ = [J; I; -I], D~ = diag(D, D_lo, D_up),
+    built here densely from the explicit stacked J~ (not the oracle's diagonal shortcut).  Off-diagonal
+    entries equal the box-free S bit for bit; the diagonal differs by D_lo + D_up; zero bounds give S."""
+    p = tiny(N=3, matching=matching, e_max=8.0)
+    lo, up = gen.box_diagonals(p, e_max=6.0, seed=11)
+    o0 = oracle_lib.Oracle.from_problem(p)
+    o = oracle_lib.Oracle.from_problem(p, D_lo=lo, D_up=up)
+    S0, S = o0.level_matrix(0).toarray(), o.level_matrix(0).toarray()
+    I = sp.identity(p.n, format="csr")
+    Jt = sp.vstack([J_csr(p), I, -I]).tocsr()
+    Dt = sp.diags(np.concatenate([p.D, lo, up]))
+    ref = (K_csr(p) + Jt.T @ Dt @ Jt).toarray()
+    assert np.abs(S - ref).max() <= 4 * EPS * np.abs(ref).max()
+    off = ~np.eye(p.n, dtype=bool)
+    assert np.array_equal(S[off], S0[off])
+    d = np.diag(S) - np.diag(S0)
+    assert np.allclose(d, lo + up, rtol=1e-15, atol=4 * EPS * np.abs(np.diag(S)).max())
+    assert np.array_equal(oracle_lib.Oracle.from_problem(p, D_lo=np.zeros(p.n), D_up=np.zeros(p.n)).get(2), o0.get(2))
+    # SPD and the AMGF-PCG solve is the dense solve of A~
+    x, info = o.pcg(p.b, rtol=1e-12)
+    assert info["converged"]
+    xd = np.linalg.solve(ref, p.b)
+    assert np.linalg.norm(x - xd) <= 1e-8 * np.linalg.norm(xd)
+    # a negative bound diagonal is a domain error (SPEC.md:35)
+    with pytest.raises(oracle_lib.OracleError) as e:
+        oracle_lib.Oracle.from_problem(p, D_lo=-lo)
+    assert e.value.code == -3
+
+
 def test_matching_S_block_count(oracle_lib):
     # node-to-node matching: S adds exactly 2 cross blocks per constraint
     p = gen.config(0)
