@@ -297,3 +297,22 @@ def box_diagonals(p: Problem, e_max: float = 6.0, seed: int = 1000):
         d[~free] = 0.0
         out.append(d.astype(np.float64))
     return out[0], out[1]
+
+
+def ip_data(p: Problem):
+    """Interior-point data of the two-block contact problem (section 3; inputs only):
+    g0 (m)  gap of each constraint at u = 0: 0, the bodies touch at rest (the top face is pushed down);
+    Ms (m)  diagonal lumped boundary mass of the slack space ("diagonal lumped mass-matrix M_s
+            associated to s"): the non-mortar face nodes' tributary areas h^2 x (1/2 per boundary axis);
+    Mu (n)  lumped volume mass of the displacement space (the M_u^{-1} norm of r_u in e_opt):
+            nodal tributary volumes h^3 x (1/2 per boundary axis), per dof."""
+    N = p.N
+    n1 = N + 1
+    h = 1.0 / N
+    edge = lambda a: np.where((a == 0) | (a == N), 0.5, 1.0)  # noqa: E731
+    fj, fi = np.meshgrid(np.arange(n1), np.arange(n1), indexing="ij")
+    Ms = (h * h * edge(fj) * edge(fi)).ravel().astype(np.float64)
+    k, j, i = np.meshgrid(np.arange(n1), np.arange(n1), np.arange(n1), indexing="ij")
+    vol = (h ** 3 * edge(k) * edge(j) * edge(i)).ravel()
+    Mu = np.repeat(np.concatenate([vol, vol]), 3).astype(np.float64)
+    return np.zeros(p.m), Ms, Mu
