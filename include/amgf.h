@@ -122,6 +122,12 @@ amgf_status amgf_vcycle(amgf_handle h, const double *b, double *x, void *stream)
 /* y = A_level x (level 0: S).  Sizes: 3*nodes at level 0, 6*n_agg below. */
 amgf_status amgf_spmv(amgf_handle h, int32_t level, const double *x, double *y, void *stream);
 
+/* y = K x with the stiffness matrix the handle was set up with (contract C2 chains: per scalar row an fma chain
+ * from +0 over K's blocks in ascending column, components ascending).  For the interior-point driver's residual
+ * r_u = K u - f + J^T lambda (PAPER.md eq:optConditionsPrimalDual).  x, y: n doubles.  AMGF_ERR_ARG on an
+ * imported handle. */
+amgf_status amgf_spmv_K(amgf_handle h, const double *x, double *y, void *stream);
+
 /* PCG on S x = b with AMGF (precond = 0) or AMG-only (precond = 1), x0 = 0, stops when
  * sqrt(r.Mr / r0.Mr0) < rtol or after max_it iterations.  Synchronises `stream`. */
 amgf_status amgf_pcg_solve(amgf_handle h, const double *b, double *x, double rtol, int32_t max_it,

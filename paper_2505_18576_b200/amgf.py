@@ -17,7 +17,7 @@ STATUS = {0: "AMGF_OK", 1: "AMGF_NOT_CONVERGED", -1: "AMGF_ERR_ARG", -2: "AMGF_E
           -7: "AMGF_ERR_CUDA", -8: "AMGF_ERR_OOM", -9: "AMGF_ERR_LIMIT", -10: "AMGF_ERR_FORMAT"}
 
 SYMBOLS = ["amgf_default_config", "amgf_setup", "amgf_update_D", "amgf_update_D_box", "amgf_apply", "amgf_vcycle", "amgf_spmv",
-           "amgf_pcg_solve", "amgf_pcg_solve_host", "amgf_level_info", "amgf_level_get", "amgf_launch_count",
+           "amgf_spmv_K", "amgf_pcg_solve", "amgf_pcg_solve_host", "amgf_level_info", "amgf_level_get", "amgf_launch_count",
            "amgf_pcg_history", "amgf_setup_times", "amgf_export", "amgf_import", "amgf_debug_guard_check",
            "amgf_last_error",
            "amgf_destroy"]
@@ -76,6 +76,8 @@ def load_library():
         getattr(L, f).restype = I
     L.amgf_spmv.argtypes = [P, I, P, P, P]
     L.amgf_spmv.restype = I
+    L.amgf_spmv_K.argtypes = [P, P, P, P]
+    L.amgf_spmv_K.restype = I
     L.amgf_pcg_solve.argtypes = [P, P, P, D, I, I, ctypes.POINTER(Report), P]
     L.amgf_pcg_solve.restype = I
     L.amgf_pcg_solve_host.argtypes = [P, P, P, D, I, I, ctypes.POINTER(Report), P]
@@ -246,6 +248,13 @@ class AMGF:
         x = self._vec(x, self.levels[level]["nodes"] * self.levels[level]["b"])
         y = out if out is not None else self._vec(n=x.numel())
         _check(load_library().amgf_spmv(self.h, level, _ptr(x), _ptr(y), self._s))
+        return y
+
+    def spmv_K(self, x, out=None):
+        """y = K x (the stiffness matrix of the setup; interior-point residuals)."""
+        x = self._vec(x, self.n)
+        y = out if out is not None else self._vec(n=self.n)
+        _check(load_library().amgf_spmv_K(self.h, _ptr(x), _ptr(y), self._s))
         return y
 
     def pcg(self, b, rtol=1e-8, max_it=5000, precond="amgf", out=None):

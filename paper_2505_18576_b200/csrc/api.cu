@@ -658,6 +658,16 @@ amgf_status amgf_spmv(amgf_handle h, int32_t level, const double *x, double *y, 
   });
 }
 
+amgf_status amgf_spmv_K(amgf_handle h, const double *x, double *y, void *stream) {
+  if (!h || !x || !y) { set_error("null argument"); return AMGF_ERR_ARG; }
+  return guarded([&]() -> amgf_status {
+    REQUIRE(!h->imported && h->K.val, AMGF_ERR_ARG, "spmv_K: the handle holds no K (imported hierarchy)");
+    h->stream = (cudaStream_t)stream;
+    launch_bsr_spmv(*h, h->K, x, y);
+    return AMGF_OK;
+  });
+}
+
 amgf_status amgf_pcg_solve(amgf_handle h, const double *b, double *x, double rtol, int32_t max_it, int32_t precond,
                            amgf_report *rep, void *stream) {
   if (!h || !b || !x) { set_error("null argument"); return AMGF_ERR_ARG; }

@@ -63,29 +63,31 @@ class IPError(RuntimeError):
     pass
 
 
-def _bsr_matvec(ptr, col, val, x):
-    """y = K x for the 3x3 BSR K (host, one product per IP iteration for the residual r_u)."""
-    import scipy.sparse as sp
-    nb = len(ptr) - 1
-    K = sp.bsr_matrix((np.asarray(val).reshape(-1, 3, 3), col, ptr), shape=(3 * nb, 3 * nb))
-    return K @ x
-
-
 class IPProblem:
-    """min 1/2 u^T K u - f^T u  s.t.  g0 + J u >= 0  (K: 3x3 BSR; J: CSR m x n)."""
+    """min 1/2 u^T K u - f^T u  s.t.  g0 + J u >= 0  (K: 3x3 BSR arrays; J: CSR m x n)."""
 
     def __init__(self, K_ptr, K_col, K_val, f, J_ptr, J_col, J_val, g0, Ms, Mu):
         import scipy.sparse as sp
+        self.K_ptr, self.K_col = np.asarray(K_ptr), np.asarray(K_col)
+        self.K_val = np.asarray(K_val, dtype=np.float64)
         self.n = 3 * (len(K_ptr) - 1)
         self.m = len(J_ptr) - 1
-        self.K = sp.bsr_matrix((np.asarray(K_val, dtype=np.float64).reshape(-1, 3, 3), np.asarray(K_col),
-                                np.asarray(K_ptr)), shape=(self.n, self.n)).tocsr()
         self.J = sp.csr_matrix((np.asarray(J_val, dtype=np.float64), np.asarray(J_col), np.asarray(J_ptr)),
                                shape=(self.m, self.n))
         self.f = np.asarray(f, dtype=np.float64)
         self.g0 = np.asarray(g0, dtype=np.float64)
         self.Ms = np.asarray(Ms, dtype=np.float64)
         self.Mu = np.asarray(Mu, dtype=np.float64)
+        self._K = None
+
+    @property
+    def K(self):
+        """K as a scipy CSR matrix (host reference products; the driver uses the solver's K x when it has one)."""
+        if self._K is None:
+            import scipy.sparse as sp
+            self._K = sp.bsr_matrix((self.K_val.reshape(-1, 3, 3), self.K_col, self.K_ptr),
+                                    shape=(self.n, self.n)).tocsr()
+        return self._K
 
     @classmethod
     def from_generated(cls, p):
@@ -93,16 +95,13 @@ class IPProblem:
         g0, Ms, Mu = amgf_gen.ip_data(p)
         return cls(p.K_ptr, p.K_col, p.K_val, p.b, p.J_ptr, p.J_col, p.J_val, g0, Ms, Mu)
 
-    def energy(self, u):
-        return 0.5 * float(u @ (self.K @ u)) - float(self.f @ u)
-
     def gap(self, u):
         return self.g0 + self.J @ u
 
 
-def residuals(P: IPProblem, u, s, lam, z, mu):
-    """eq:optConditionsPrimalDual (PAPER.md:153-160)."""
-    r_u = P.K @ u - P.f + P.J.T @ lam
+def residuals(P: IPProblem, u, s, lam, z, mu, Ku=None):
+    """eq:optConditionsPrimalDual; Ku = K u if already computed."""
+    r_u = (P.K @ u if Ku is None else Ku) - P.f + P.J.T @ lam
     r_s = -lam - P.Ms * z
     r_l = P.gap(u) - s
     r_z = z * s - mu
@@ -128,14 +127,15 @@ def fraction_to_boundary(v, dv, tau):
     return float(min(1.0, np.min(-tau * v[neg] / dv[neg])))
 
 
-def barrier_objective(P: IPProblem, u, s, mu):
-    return P.energy(u) - mu * float(P.Ms @ np.log(s))
+def barrier_log(P: IPProblem, s, mu):
+    return -mu * float(P.Ms @ np.log(s))
 
 
 def solve(P: IPProblem, solver, opts: IPOptions | None = None, u0=None, log=None):
     """Algorithm 1.  Returns (u, s, lambda, z, records, status)."""
     o = opts or IPOptions()
     n, m = P.n, P.m
+    Kmul = getattr(solver, "matvec_K", None) or (lambda x: P.K @ x)   # K x (the solver's, C2 chains)
     u = np.zeros(n) if u0 is None else np.array(u0, dtype=np.float64)
     mu = o.mu0
     s = np.maximum(P.gap(u), o.s_floor)
@@ -145,18 +145,19 @@ def solve(P: IPProblem, solver, opts: IPOptions | None = None, u0=None, log=None
     recs: list[IPRecord] = []
     theta_min = 1e-4 * max(1.0, float(np.abs(P.gap(u) - s).sum()))
     status = "max_iter"
+    Ku = Kmul(u)
     for it in range(1, o.max_iter + 1):
-        res = residuals(P, u, s, lam, z, 0.0)
+        res = residuals(P, u, s, lam, z, 0.0, Ku)
         e_opt = optimality_error(P, res, lam, z, o.s_max)
         if e_opt < o.tol_ip:
             status = "converged"
             break
-        res_mu = residuals(P, u, s, lam, z, mu)
+        res_mu = residuals(P, u, s, lam, z, mu, Ku)
         e_mu = optimality_error(P, res_mu, lam, z, o.s_max)
         while e_mu < o.kappa_eps * mu and mu > o.tol_ip / 11.0:   # inner loop done: decrease mu, reset filter
             mu = max(o.tol_ip / 11.0, min(o.kappa_mu * mu, mu ** o.theta_mu))
             filt = []
-            res_mu = residuals(P, u, s, lam, z, mu)
+            res_mu = residuals(P, u, s, lam, z, mu, Ku)
             e_mu = optimality_error(P, res_mu, lam, z, o.s_max)
         r_u, r_s, r_l, r_z = res_mu
         # ---- reduced Newton system
@@ -175,13 +176,17 @@ def solve(P: IPProblem, solver, opts: IPOptions | None = None, u0=None, log=None
         a_max = fraction_to_boundary(s, ds, tau)
         a_d = fraction_to_boundary(z, dz, tau)
         theta = float(np.abs(r_l).sum())
-        phi = barrier_objective(P, u, s, mu)
-        grad_phi_d = float((P.K @ u - P.f) @ du) - mu * float((P.Ms / s) @ ds)
+        # E along the step is a quadratic: E(u + a du) = E(u) + a (Ku - f).du + a^2/2 du.K du (one K du product)
+        Kdu = Kmul(du)
+        gE = float((Ku - P.f) @ du)
+        cE = 0.5 * float(du @ Kdu)
+        phi = barrier_log(P, s, mu)                       # phi relative to E(u)
+        grad_phi_d = gE - mu * float((P.Ms / s) @ ds)
         alpha = a_max
         while True:
-            ut, st = u + alpha * du, s + alpha * ds
-            theta_t = float(np.abs(P.gap(ut) - st).sum())
-            phi_t = barrier_objective(P, ut, st, mu)
+            st = s + alpha * ds
+            theta_t = float(np.abs(P.gap(u + alpha * du) - st).sum())
+            phi_t = alpha * gE + alpha * alpha * cE + barrier_log(P, st, mu)
             ok_filter = all(theta_t < tf or phi_t < pf for tf, pf in filt)
             f_type = theta <= theta_min and grad_phi_d < 0   # switching condition: an Armijo (f-type) step
             if f_type:
@@ -195,6 +200,10 @@ def solve(P: IPProblem, solver, opts: IPOptions | None = None, u0=None, log=None
             alpha *= 0.5
             if alpha < o.alpha_min:
                 raise IPError(f"line search failed at IP iteration {it}")
+        # filter entries are relative to E at the accepted point: shift them by the change in E
+        dE = alpha * gE + alpha * alpha * cE
+        filt = [(tf, pf - dE) for tf, pf in filt]
+        Ku = Kmul(u + alpha * du)
         u, s, lam = u + alpha * du, s + alpha * ds, lam + alpha * dl
         z = z + a_d * dz
         recs.append(IPRecord(it, mu, e_opt, e_mu, int(info.get("iterations", 0)), alpha, a_d,
@@ -206,7 +215,7 @@ def solve(P: IPProblem, solver, opts: IPOptions | None = None, u0=None, log=None
 
 class AmgfSolver:
     """The GPU path as the IP driver's linear solver: one handle, amgf_update_D per Newton step (numeric
-    re-setup of S = K + J^T D J), amgf_pcg_solve with the AMGF preconditioner."""
+    re-setup of S = K + J^T D J), amgf_pcg_solve with the AMGF preconditioner, and amgf_spmv_K for K x."""
 
     def __init__(self, p, config=None, precond="amgf"):
         from .amgf import AMGF
@@ -220,3 +229,6 @@ class AmgfSolver:
     def solve(self, b, rtol):
         x, info = self.h.pcg(np.ascontiguousarray(b), rtol=rtol, max_it=5000, precond=self.precond)
         return x.cpu().numpy(), info
+
+    def matvec_K(self, x):
+        return self.h.spmv_K(np.ascontiguousarray(x)).cpu().numpy()

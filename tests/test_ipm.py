@@ -37,6 +37,10 @@ class OracleSolver:
     def solve(self, b, rtol):
         return self.o.pcg(b, rtol=rtol)
 
+    def matvec_K(self, x):
+        """K x in the contract's row-chain order (C2), as the GPU's amgf_spmv_K."""
+        return self.lib.bsr_spmv(self.p.K_ptr, self.p.K_col, self.p.K_val, x, 3, 3)
+
 
 def one_dof(g0):
     # min 1/2 u^2 - 2u  s.t.  g0 - u >= 0   (embedded as dof 0 of one 3-dof node; dofs 1, 2 decoupled)
