@@ -60,6 +60,10 @@ typedef struct {
   int32_t cheb_degree;     /* 1..32 (default 2)                                               */
   uint64_t agg_seed;       /* aggregation priority seed (default 0x5EED)                     */
   double cheb_ratio;       /* > 1 (default 20)                                                */
+  int32_t filter_basis;    /* 0 (default): P = the identity columns at I_c (the natural embedding,
+                              PAPER.md:391), A_w = S[Z, Z];  1: P = J^T (the generality remark, PAPER.md:583-585:
+                              any full-column-rank P), A_w = J S J^T (m x m) -- DESIGN.md R21 */
+  int32_t pad_;
 } amgf_config;
 
 #define AMGF_MAX_LEVELS 32
@@ -167,7 +171,8 @@ amgf_status amgf_import(const char *dir, void *stream, amgf_handle *out);
  * info[3] = band width of A_w's factor, then per level l: info[4+6l .. 9+6l] =
  * {nodes, block size, nnzb(A), nnzb(P), n_agg, SELL slots of A}; info[196] = size of the separator
  * off-block factor, info[197] = number of nested-dissection blocks, info[198] = first level of the fused
- * coarse-tail kernel (-1: none), info[199] = its cluster size in CTAs.  info needs 4 + 6*32 + 4 entries. */
+ * coarse-tail kernel (-1: none), info[199] = its cluster size in CTAs, info[200] = the filter-space dimension nf
+ * (n_c, or m with filter_basis 1; the size of arrays 22 and 25 below).  info needs 4 + 6*32 + 5 entries. */
 amgf_status amgf_level_info(amgf_handle h, int64_t *info);
 
 /* Copy one hierarchy array to the HOST buffer dst.  which: 0 A.ptr 1 A.col 2 A.val 3 P.ptr 4 P.col

@@ -58,12 +58,12 @@ class OrcConfig(ctypes.Structure):
                 ("coarsest_size", ctypes.c_int), ("max_levels", ctypes.c_int),
                 ("power_iters", ctypes.c_int), ("factor_filter", ctypes.c_int),
                 ("agg_seed", ctypes.c_uint64), ("nd_levels", ctypes.c_int), ("smoother", ctypes.c_int),
-                ("cheb_degree", ctypes.c_int), ("pad_", ctypes.c_int), ("cheb_ratio", ctypes.c_double)]
+                ("cheb_degree", ctypes.c_int), ("filter_basis", ctypes.c_int), ("cheb_ratio", ctypes.c_double)]
 
 
 DEFAULTS = dict(pre_sweeps=1, post_sweeps=1, coarsest_size=64, max_levels=25,
                 power_iters=6, factor_filter=1, agg_seed=0x5EED, nd_levels=3, smoother=1, cheb_degree=2,
-                cheb_ratio=20.0)
+                cheb_ratio=20.0, filter_basis=0)
 
 _lib = None
 
@@ -103,6 +103,7 @@ def lib():
         L.orc_bsr_spmv.argtypes = [ctypes.c_int] * 4 + [P] * 5
         L.orc_get.argtypes = [P, ctypes.c_int, ctypes.c_int, P]
         L.orc_times.argtypes = [P, P]
+        L.orc_nf.argtypes = [P]
         _lib = L
     return _lib
 
@@ -187,6 +188,7 @@ class Oracle:
         info = np.zeros(3 + 5 * 32, dtype=np.int64)
         lib().orc_info(self.h, _p(info))
         self.nlev, self.nc, self.nco = int(info[0]), int(info[1]), int(info[2])
+        self.nf = int(lib().orc_nf(self.h))   # filter-space dimension (n_c, or m for filter_basis = 1)
         self.levels = [dict(nodes=int(info[3 + 5 * l]), b=int(info[4 + 5 * l]), nnzb=int(info[5 + 5 * l]),
                             nnzb_P=int(info[6 + 5 * l]), n_agg=int(info[7 + 5 * l])) for l in range(self.nlev)]
 
@@ -210,9 +212,9 @@ class Oracle:
                   6: (L["n_agg"] + 1, np.int32), 7: (L["nnzb_P"], np.int32), 8: ((L["nnzb_P"], 6 * b), np.float64),
                   9: (nodes * b, np.float64), 10: (nodes, np.int32), 11: ((nodes * b, 6), np.float64),
                   12: (2, np.float64), 13: ((nodes, b * 6), np.float64), 14: (nodes, np.int32), 15: (nodes, np.int32),
-                  20: (self.nc, np.int32), 21: ((self.nc, self.nc), np.float64), 22: ((self.nc, self.nc), np.float64),
+                  20: (self.nc, np.int32), 21: ((self.nf, self.nf), np.float64), 22: ((self.nf, self.nf), np.float64),
                   23: ((self.nco, self.nco), np.float64), 24: ((self.nco, self.nco), np.float64),
-                  25: (self.nc, np.int32), 26: (1, np.int32)}
+                  25: (self.nf, np.int32), 26: (1, np.int32)}
         shape, dt = shapes[which]
         out = np.zeros(shape, dtype=dt)
         if which == 13:

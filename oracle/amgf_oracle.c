@@ -211,7 +211,8 @@ typedef struct {
   int nd_levels;  /* nested-dissection depth of A_w's elimination order (contract C9/C10, reading R16) */
   int smoother;   /* 0 = l1-Jacobi, 1 = Chebyshev (default) in D_l1^{-1} A (variant f4, reading R18) */
   int cheb_degree;
-  int pad_;
+  int filter_basis; /* 0: P = identity columns at I_c (Def. Discrete Operators); 1: P = J^T, the
+                       generality remark's full-column-rank P (variant f4, reading R21) */
   double cheb_ratio;
 } orc_config;
 
@@ -243,7 +244,11 @@ typedef struct {
   int *pos;      /* dof -> position in Z or -1 */
   int bw;        /* structural lower band width of A_w in Z order */
   int *pi;       /* elimination order: pi[i] = position in Z of the i-th eliminated dof */
-  double *Aw;    /* dense n_c x n_c, Z order */
+  int nf;        /* filter-space dimension: n_c (basis 0) or m (basis 1) */
+  int mJ;        /* basis 1: J (CSR, columns ascending) and J^T as per-dof constraint lists (rows ascending) */
+  int *Jp, *Jc, *Jtp, *Jtr;
+  double *Jv, *Jtv;
+  double *Aw;    /* dense nf x nf: S[Z,Z] (basis 0, Z order) or J S J^T (basis 1, constraint order) */
   double *Lw;    /* Cholesky factor of Aw[pi, pi] */
   int nlev;
   level_t lev[MAXLEV];
@@ -378,7 +383,105 @@ void orc_nd_order(int nc, int bw, int levels, int *out) {
 }
 
 /* ---------- I_c and A_w = P^T S P ---------- */
-static int setup_filter(orc_ctx *cx, int m, const int *Jptr, const int *Jcol, const int *Z, int nc) {
+/* S_pq if stored (block row p/3, block column q/3), else *found = 0. */
+static double S_entry(const orc_ctx *cx, long p, long q, int *found) {
+  const int I = (int)(p / 3), Jn = (int)(q / 3);
+  int lo = cx->S.ptr[I], hi = cx->S.ptr[I + 1] - 1;
+  while (lo <= hi) {
+    int mid = (lo + hi) / 2;
+    if (cx->S.col[mid] == Jn) { *found = 1; return cx->S.val[9L * mid + 3 * (p % 3) + (q % 3)]; }
+    if (cx->S.col[mid] < Jn) lo = mid + 1; else hi = mid - 1;
+  }
+  *found = 0;
+  return 0.0;
+}
+
+/* Filter basis P = J^T (variant f4; the generality remark: any full-column-rank P): the
+ * filter space is the constraint space, A_w = P^T S P = J S J^T (m x m) in constraint order.  Entry (a, b)
+ * follows the definition sum_p J_ap (sum_q S_pq J_bq) as one chain (reading R21): acc = +0; for p in J's row a
+ * ascending: t = +0; t = fma(S_pq, J_bq, t) over q in J's row b ascending with S_pq stored; acc = fma(J_ap, t,
+ * acc) -- pairs (a, b) whose rows touch no stored S entry are structural zeros.  Elimination order: the
+ * nested dissection of R16 over the structural band width of J S J^T in constraint order. */
+static int setup_filter_J(orc_ctx *cx, int m, const int *Jptr, const int *Jcol, const double *Jval) {
+  const long n = cx->n;
+  cx->mJ = m;
+  cx->nf = m;
+  cx->Jp = (int *)malloc((size_t)(m + 1) * sizeof(int));
+  memcpy(cx->Jp, Jptr, (size_t)(m + 1) * sizeof(int));
+  const int nnz = Jptr[m];
+  cx->Jc = (int *)malloc((size_t)(nnz > 0 ? nnz : 1) * sizeof(int));
+  cx->Jv = (double *)malloc((size_t)(nnz > 0 ? nnz : 1) * sizeof(double));
+  memcpy(cx->Jc, Jcol, (size_t)nnz * sizeof(int));
+  memcpy(cx->Jv, Jval, (size_t)nnz * sizeof(double));
+  cx->Jtp = (int *)calloc((size_t)n + 1, sizeof(int));
+  for (int e = 0; e < nnz; e++) cx->Jtp[Jcol[e] + 1]++;
+  for (long p = 0; p < n; p++) cx->Jtp[p + 1] += cx->Jtp[p];
+  cx->Jtr = (int *)malloc((size_t)(nnz > 0 ? nnz : 1) * sizeof(int));
+  cx->Jtv = (double *)malloc((size_t)(nnz > 0 ? nnz : 1) * sizeof(double));
+  int *fill = (int *)calloc((size_t)n, sizeof(int));
+  for (int a = 0; a < m; a++)
+    for (int e = Jptr[a]; e < Jptr[a + 1]; e++) {
+      const int p = Jcol[e];
+      cx->Jtr[cx->Jtp[p] + fill[p]] = a;
+      cx->Jtv[cx->Jtp[p] + fill[p]] = Jval[e];
+      fill[p]++;
+    }
+  free(fill);
+  /* structural band width of J S J^T in constraint order */
+  char *cand = (char *)calloc((size_t)(m > 0 ? m : 1), 1);
+  int bw = 0;
+  for (int a = 0; a < m; a++) {
+    int mn = a;
+    for (int e = Jptr[a]; e < Jptr[a + 1]; e++) {
+      const int I = Jcol[e] / 3;
+      for (int k = cx->S.ptr[I]; k < cx->S.ptr[I + 1]; k++)
+        for (int c = 0; c < 3; c++) {
+          const long q = 3L * cx->S.col[k] + c;
+          for (int t = cx->Jtp[q]; t < cx->Jtp[q + 1]; t++)
+            if (cx->Jtr[t] < mn) mn = cx->Jtr[t];
+        }
+    }
+    if (a - mn > bw) bw = a - mn;
+  }
+  free(cand);
+  cx->bw = bw;
+  cx->pi = (int *)malloc((size_t)(m > 0 ? m : 1) * sizeof(int));
+  orc_nd_order(m, bw, cx->cfg.nd_levels, cx->pi);
+  if (!cx->cfg.factor_filter || m == 0) return ORC_OK;
+  cx->Aw = (double *)calloc((size_t)m * m, sizeof(double));
+  cx->Lw = (double *)malloc((size_t)m * m * sizeof(double));
+  double *Ap = (double *)malloc((size_t)m * m * sizeof(double));
+  if (!cx->Aw || !cx->Lw || !Ap) return fail(ORC_ERR_OOM, "oom A_w (J S J^T)");
+  for (int a = 0; a < m; a++)
+    for (int b = (a - bw > 0 ? a - bw : 0); b < m && b <= a + bw; b++) {
+      double acc = 0.0;
+      for (int e = Jptr[a]; e < Jptr[a + 1]; e++) {
+        double t = 0.0;
+        for (int f = Jptr[b]; f < Jptr[b + 1]; f++) {
+          int found;
+          const double spq = S_entry(cx, Jcol[e], Jcol[f], &found);
+          if (found) t = fma(spq, Jval[f], t);
+        }
+        acc = fma(Jval[e], t, acc);
+      }
+      cx->Aw[(size_t)a * m + b] = acc;
+    }
+  for (int i = 0; i < m; i++)
+    for (int j = 0; j < m; j++) Ap[(size_t)i * m + j] = cx->Aw[(size_t)cx->pi[i] * m + cx->pi[j]];
+  double t0 = now_s();
+  int st = orc_cholesky_dense(m, Ap, cx->Lw);
+  cx->t_phase[2] = now_s() - t0;
+  free(Ap);
+  if (st) {
+    char buf[512];
+    snprintf(buf, sizeof buf, "A_w (J S J^T): %.470s", g_err);
+    return fail(st, buf);
+  }
+  return ORC_OK;
+}
+
+static int setup_filter(orc_ctx *cx, int m, const int *Jptr, const int *Jcol, const double *Jval, const int *Z,
+                        int nc) {
   long n = cx->n;
   char *mark = (char *)calloc((size_t)n, 1);
   for (int k = 0; k < m; k++)
@@ -425,6 +528,8 @@ static int setup_filter(orc_ctx *cx, int m, const int *Jptr, const int *Jcol, co
     if (a - mn > bw) bw = a - mn;
   }
   cx->bw = bw;
+  cx->nf = nc;
+  if (cx->cfg.filter_basis == 1) return setup_filter_J(cx, m, Jptr, Jcol, Jval);
   cx->pi = (int *)malloc((size_t)(nc > 0 ? nc : 1) * sizeof(int));
   orc_nd_order(nc, bw, cx->cfg.nd_levels, cx->pi);
   if (!cx->cfg.factor_filter || nc == 0) return ORC_OK;
@@ -870,6 +975,7 @@ void orc_free(orc_ctx *cx) {
   }
   bsr_free(&cx->S);
   free(cx->Z); free(cx->pos); free(cx->pi); free(cx->Aw); free(cx->Lw); free(cx->Ac); free(cx->Lc);
+  free(cx->Jp); free(cx->Jc); free(cx->Jv); free(cx->Jtp); free(cx->Jtr); free(cx->Jtv);
   free(cx);
 }
 
@@ -915,7 +1021,7 @@ orc_ctx *orc_create_box(int nodes, const int *Kptr, const int *Kcol, const doubl
   int st = form_S(cx, Kptr, Kcol, Kval, m, Jptr, Jcol, Jval, D, Dlo, Dup);
   double t1 = now_s();
   cx->t_phase[0] = t1 - t0;
-  if (!st) st = setup_filter(cx, m, Jptr, Jcol, Z, nc);
+  if (!st) st = setup_filter(cx, m, Jptr, Jcol, Jval, Z, nc);
   double t2 = now_s();
   cx->t_phase[1] = (t2 - t1) - cx->t_phase[2];
   if (!st) st = build_hierarchy(cx, Bnns, Kptr, Kcol);
@@ -1035,7 +1141,7 @@ void orc_spmv(orc_ctx *cx, int level, const double *x, double *y) {
 
 /* y = A_w^{-1} v (filter solve, contract C10): A_w[pi,pi] = L L^T, so y[pi] = L^{-T} L^{-1} v[pi]. */
 static void filter_solve(orc_ctx *cx, const double *v, double *y) {
-  int nc = cx->nc;
+  int nc = cx->nf;
   double *vp = (double *)malloc((size_t)(nc > 0 ? nc : 1) * sizeof(double));
   double *yp = (double *)malloc((size_t)(nc > 0 ? nc : 1) * sizeof(double));
   for (int i = 0; i < nc; i++) vp[i] = v[cx->pi[i]];
@@ -1059,8 +1165,29 @@ void orc_apply(orc_ctx *cx, const double *r, double *z) {
   double *y = (double *)malloc((size_t)(nc > 0 ? nc : 1) * sizeof(double));
   vcycle(cx, 0, r, x1);
   bsr_spmv(&cx->S, x1, r, r1, 1);
-  for (int a = 0; a < nc; a++) v[a] = r1[cx->Z[a]];
-  if (nc > 0) filter_solve(cx, v, y);
+  if (cx->cfg.filter_basis == 1) {
+    /* P = J^T (reading R21): v = J r1 (row chains); y = (J S J^T)^{-1} v; w = J^T y per dof (chains over the
+     * dof's constraints ascending), held at the Z positions for the x2 update and the thin residual */
+    const int m = cx->mJ;
+    double *vJ = (double *)malloc((size_t)(m > 0 ? m : 1) * sizeof(double));
+    double *yJ = (double *)malloc((size_t)(m > 0 ? m : 1) * sizeof(double));
+    for (int a = 0; a < m; a++) {
+      double acc = 0.0;
+      for (int e = cx->Jp[a]; e < cx->Jp[a + 1]; e++) acc = fma(cx->Jv[e], r1[cx->Jc[e]], acc);
+      vJ[a] = acc;
+    }
+    if (m > 0) filter_solve(cx, vJ, yJ);
+    for (int a = 0; a < nc; a++) {
+      const int p = cx->Z[a];
+      double acc = 0.0;
+      for (int t = cx->Jtp[p]; t < cx->Jtp[p + 1]; t++) acc = fma(cx->Jtv[t], yJ[cx->Jtr[t]], acc);
+      y[a] = acc;
+    }
+    free(vJ); free(yJ);
+  } else {
+    for (int a = 0; a < nc; a++) v[a] = r1[cx->Z[a]];
+    if (nc > 0) filter_solve(cx, v, y);
+  }
   /* x2 (stored in x1) and thin r2 (stored in r1) */
   const bsr_t *S = &cx->S;
   for (int I = 0; I < cx->nodes; I++)
@@ -1146,6 +1273,8 @@ void orc_info(orc_ctx *cx, long *out) {
   }
 }
 
+int orc_nf(orc_ctx *cx) { return cx->nf; }
+
 /* Phase wall times (s) of orc_create: {S, A_w assembly, A_w dense Cholesky, AMG hierarchy}. */
 void orc_times(orc_ctx *cx, double *out) { memcpy(out, cx->t_phase, sizeof cx->t_phase); }
 
@@ -1173,11 +1302,11 @@ int orc_get(orc_ctx *cx, int which, int level, void *dst) {
     case 14: if (!L->root) return -1; memcpy(dst, L->root, (size_t)L->nodes * sizeof(int)); return 0;
     case 15: memcpy(dst, L->comp, (size_t)L->nodes * sizeof(int)); return 0;
     case 20: memcpy(dst, cx->Z, (size_t)cx->nc * sizeof(int)); return 0;
-    case 21: if (!cx->Aw) return -1; memcpy(dst, cx->Aw, (size_t)cx->nc * cx->nc * sizeof(double)); return 0;
-    case 22: if (!cx->Lw) return -1; memcpy(dst, cx->Lw, (size_t)cx->nc * cx->nc * sizeof(double)); return 0;
+    case 21: if (!cx->Aw) return -1; memcpy(dst, cx->Aw, (size_t)cx->nf * cx->nf * sizeof(double)); return 0;
+    case 22: if (!cx->Lw) return -1; memcpy(dst, cx->Lw, (size_t)cx->nf * cx->nf * sizeof(double)); return 0;
     case 23: memcpy(dst, cx->Ac, (size_t)cx->nco * cx->nco * sizeof(double)); return 0;
     case 24: memcpy(dst, cx->Lc, (size_t)cx->nco * cx->nco * sizeof(double)); return 0;
-    case 25: memcpy(dst, cx->pi, (size_t)cx->nc * sizeof(int)); return 0;
+    case 25: memcpy(dst, cx->pi, (size_t)cx->nf * sizeof(int)); return 0;
     case 26: ((int *)dst)[0] = cx->bw; return 0;
   }
   return -1;

@@ -33,7 +33,8 @@ class Config(ctypes.Structure):
                 ("coarsest_size", ctypes.c_int32), ("max_levels", ctypes.c_int32),
                 ("power_iters", ctypes.c_int32), ("nd_levels", ctypes.c_int32),
                 ("smoother", ctypes.c_int32), ("cheb_degree", ctypes.c_int32),
-                ("agg_seed", ctypes.c_uint64), ("cheb_ratio", ctypes.c_double)]
+                ("agg_seed", ctypes.c_uint64), ("cheb_ratio", ctypes.c_double),
+                ("filter_basis", ctypes.c_int32), ("pad_", ctypes.c_int32)]
 
 
 class Report(ctypes.Structure):
@@ -155,7 +156,7 @@ class AMGF:
 
     def _load_info(self):
         L = load_library()
-        info = np.zeros(4 + 6 * 32 + 4, dtype=np.int64)
+        info = np.zeros(4 + 6 * 32 + 5, dtype=np.int64)
         _check(L.amgf_level_info(self.h, info.ctypes.data_as(ctypes.c_void_p)))
         self.nlev, self.nc, self.nco, self.bw = (int(v) for v in info[:4])
         self.levels = [dict(nodes=int(info[4 + 6 * l]), b=int(info[5 + 6 * l]), nnzb=int(info[6 + 6 * l]),
@@ -163,6 +164,7 @@ class AMGF:
                        for l in range(self.nlev)]
         self.loff_size, self.nd_nblocks = int(info[4 + 6 * 32]), int(info[5 + 6 * 32])
         self.tail_level, self.tail_ncta = int(info[6 + 6 * 32]), int(info[7 + 6 * 32])
+        self.nf = int(info[8 + 6 * 32])
 
     @classmethod
     def import_dir(cls, path, stream=None):
@@ -314,8 +316,8 @@ class AMGF:
                   6: (Lv["n_agg"] + 1, np.int32), 7: (Lv["nnzb_P"], np.int32),
                   8: ((Lv["nnzb_P"], 6 * b), np.float64), 9: (nodes * b, np.float64), 10: (nodes, np.int32),
                   11: ((nodes * b, 6), np.float64), 12: (2, np.float64), 14: (nodes, np.int32),
-                  15: (nodes, np.int32), 20: (self.nc, np.int32), 22: ((self.nc, W), np.float64),
-                  23: (self.loff_size, np.float64), 25: (self.nc, np.int32),
+                  15: (nodes, np.int32), 20: (self.nc, np.int32), 22: ((self.nf, W), np.float64),
+                  23: (self.loff_size, np.float64), 25: (self.nf, np.int32),
                   24: ((self.nco, self._band_stride(self.nco - 1)), np.float64)}
         if which == 27:
             dt = np.dtype([("p0", np.int32), ("len", np.int32), ("kind", np.int32), ("t0", np.int32),

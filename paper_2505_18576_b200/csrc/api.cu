@@ -237,11 +237,18 @@ void apply_M(Ctx &c, const double *r, double *z, VcOpts first, const double *dot
   launch_resid_dofs(c, c.nc, c.dof, c.w_x1, r, c.rz);
   CK(cudaEventRecord(c.ev_f0, c.stream));
   CK(cudaStreamWaitEvent(c.fstream, c.ev_f0, 0));
+  const bool basisJ = c.cfg.filter_basis == 1;
   {
     cudaStream_t main = c.stream;
     c.stream = c.fstream;
     try {
-      nd_solve(c, c.rz, nullptr);  // y = A_w^{-1} r1[Z] (pi order, c.fv)
+      if (basisJ) {  // P = J^T: v = J r1 (rz in Z order), y = (J S J^T)^{-1} v, w = J^T y (Z order)
+        filter_J_apply(c, c.rz, c.fJv, nullptr, nullptr);
+        nd_solve(c, c.fJv, nullptr);
+        filter_J_apply(c, nullptr, nullptr, c.fv, c.fJw);
+      } else {
+        nd_solve(c, c.rz, nullptr);  // y = A_w^{-1} r1[Z] (pi order, c.fv)
+      }
     } catch (...) {
       c.stream = main;
       throw;
@@ -271,7 +278,8 @@ void apply_M(Ctx &c, const double *r, double *z, VcOpts first, const double *dot
     for (auto &e : te) cudaEventDestroy(e);
   }
   // x2 = x1 + P y (scatter) and the thin residual r2 = r1 - S[:,Z] y in one launch
-  launch_thin_resid(c, c.nthin, c.thin_row, c.thin_ptr, c.thin_pos, c.thin_val, c.fv, c.w_r1, c.nc, c.dof, c.w_x1);
+  launch_thin_resid(c, c.nthin, c.thin_row, c.thin_ptr, c.thin_pos, c.thin_val, basisJ ? c.fJw : c.fv, c.w_r1, c.nc,
+                    c.dof, c.w_x1);
   VcOpts second;
   second.dot_r = dot_r;
   vcycle(c, 0, c.w_r1, z, c.w_x1, second);
@@ -527,6 +535,7 @@ void ctx_init(Ctx &c, void *stream) {
   REQUIRE(c.cfg.smoother == 0 || (c.cfg.smoother == 1 && c.cfg.cheb_degree >= 1 && c.cfg.cheb_degree <= 32 &&
                                   c.cfg.cheb_ratio > 1.0),
           AMGF_ERR_ARG, "invalid smoother config");
+  REQUIRE(c.cfg.filter_basis == 0 || c.cfg.filter_basis == 1, AMGF_ERR_ARG, "invalid filter_basis");
   if (c.cfg.smoother == 1) {  // Chebyshev coefficients (C23): same formulas, in the same order, as the oracle
     const double ratio = c.cfg.cheb_ratio;
     const double theta = (1.0 + 1.0 / ratio) / 2.0, delta = (1.0 - 1.0 / ratio) / 2.0;
@@ -567,6 +576,8 @@ void amgf_default_config(amgf_config *cfg) {
   cfg->cheb_degree = 2;
   cfg->agg_seed = 0x5EED;
   cfg->cheb_ratio = 20.0;
+  cfg->filter_basis = 0;
+  cfg->pad_ = 0;
 }
 
 const char *amgf_last_error(void) { return get_error(); }
@@ -711,6 +722,7 @@ amgf_status amgf_level_info(amgf_handle h, int64_t *info) {
   info[4 + 6 * MAXLEV + 1] = h->nd_nblocks;
   info[4 + 6 * MAXLEV + 2] = h->tail_level;
   info[4 + 6 * MAXLEV + 3] = h->tail_ncta;
+  info[4 + 6 * MAXLEV + 4] = h->nf;
   return AMGF_OK;
 }
 
@@ -746,10 +758,10 @@ amgf_status amgf_level_get(amgf_handle h, int32_t which, int32_t level, void *ds
       case 14: REQUIRE(L.root, AMGF_ERR_ARG, "no roots"); cp(L.root, L.nodes * 4); break;
       case 15: cp(L.comp, L.nodes * 4); break;
       case 20: cp(h->Z, h->nc * 4); break;
-      case 22: cp(h->Lrow, (size_t)h->nc * band_stride(h->bw) * 8); break;
+      case 22: cp(h->Lrow, (size_t)h->nf * band_stride(h->bw) * 8); break;
       case 23: cp(h->Loff, (size_t)h->loff_size * 8); break;
       case 24: cp(h->Lc_row, (size_t)h->nco * band_stride(h->nco - 1) * 8); break;
-      case 25: cp(h->pi_z, (size_t)h->nc * 4); break;
+      case 25: cp(h->pi_z, (size_t)h->nf * 4); break;
       case 27: cp(h->nd_blk, (size_t)h->nd_nblocks * 32); break;
       default: throw Error{AMGF_ERR_ARG, "unknown array id"};
     }

@@ -150,6 +150,9 @@ struct Ctx {
   long loff_size = 0;
   double *fw = nullptr;                   // filter workspace (pi order)
   int nc = 0, bw = 0;
+  int nf = 0;                // filter-space dimension: nc (filter_basis 0) or m (filter_basis 1, P = J^T)
+  double *fJv = nullptr;     // filter_basis 1: v = J r1 (elimination order, nf) and w = J^T y (Z order, nc)
+  double *fJw = nullptr;
   int *Z = nullptr, *pos = nullptr;
   double *Lrow = nullptr;   // band, row-major: Lrow[i*W + bw - (i-k)] = L_ik, W = band_stride(bw)
   double *Lcol = nullptr;   // band, column-major: Lcol[k*W + (i-k)] = L_ik
@@ -319,6 +322,9 @@ void launch_resid_partition(Ctx &c, const Sell &A, const double *x, const double
                             size_t reserve);
 void launch_resid_dofs(Ctx &c, int n, const int *dof, const double *x, const double *b, double *out);
 void nd_remap_positions(Ctx &c, int *pos_z, long n);  // Z positions -> pi positions
+int band_width_J(Ctx &c);                              // filter_basis 1: band width of J S J^T
+// filter_basis 1: v_pi = J r1 (rz: r1 at the Z positions) if v_pi, else w_z = J^T y_pi
+void filter_J_apply(Ctx &c, const double *rz, double *v_pi, const double *y_pi, double *w_z);
 void band_factor_blocks(Ctx &c, int n, int nblocks, const int *d_p0, const int *d_len, int bw, double *Lrow, int tag);
 void band_finish(Ctx &c, int n, int bw, const double *Lrow, double *Lcol, double *Lrev, double *dinv);
 void launch_band_sweep(Ctx &c, int nblocks, const int *d_p0, const int *d_len, int max_len, int bw, bool forward,

@@ -159,6 +159,85 @@ __global__ void k_nd_fill(int nc, int bw, int W, const NdBlk *blk, const int *bl
     }
 }
 
+// Filter basis P = J^T (variant f4, reading R21): A_w = J S J^T in constraint order, entry (a, b) as the oracle's
+// chain: acc = +0; for e in J's row a: t = +0; t = fma(S_pq, J_bq, t) over f in J's row b with S_pq stored;
+// acc = fma(J_ap, t, acc).  One thread per constraint a writes its lower entries of the nested-dissection layout
+// (in-block band / separator rows), as k_nd_fill does for S[Z, Z].
+__device__ __forceinline__ bool S_lookup(const int *S_ptr, const int *S_col, const double *S_val, int p, int q,
+                                         double &v) {
+  int lo = S_ptr[p / 3], hi = S_ptr[p / 3 + 1] - 1;
+  const int cq = q / 3;
+  while (lo <= hi) {
+    const int mid = (lo + hi) >> 1;
+    const int cm = S_col[mid];
+    if (cm == cq) { v = S_val[(long)mid * 9 + 3 * (p % 3) + (q % 3)]; return true; }
+    if (cm < cq) lo = mid + 1; else hi = mid - 1;
+  }
+  return false;
+}
+__global__ void k_nd_fill_J(int nf, int bw, int W, const NdBlk *blk, const int *block_of, const int *zpi,
+                            const int *J_ptr, const int *J_col, const double *J_val, const int *S_ptr, const int *S_col,
+                            const double *S_val, double *Lrow, double *Loff) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= nf) return;
+  const int p = zpi[a];
+  const NdBlk B = blk[block_of[p]];
+  const int b0 = max(0, a - bw), b1 = min(nf - 1, a + bw);
+  for (int b = b0; b <= b1; b++) {
+    const int q = zpi[b];
+    const bool in_band = q >= B.p0 && q <= p;
+    const bool in_off = B.kind == 1 && q >= B.t0 && q < B.p0;
+    if (!in_band && !in_off) continue;
+    double acc = 0.0;
+    for (int e = J_ptr[a]; e < J_ptr[a + 1]; e++) {
+      double t = 0.0;
+      for (int g = J_ptr[b]; g < J_ptr[b + 1]; g++) {
+        double spq;
+        if (S_lookup(S_ptr, S_col, S_val, J_col[e], J_col[g], spq)) t = __fma_rn(spq, J_val[g], t);
+      }
+      acc = __fma_rn(J_val[e], t, acc);
+    }
+    if (in_band) Lrow[(long)p * W + bw - (p - q)] = acc;
+    else Loff[B.off + (long)(p - B.p0) * B.rs + (q - B.t0)] = acc;
+  }
+}
+// structural band width of J S J^T in constraint order (max over a of a - min{b : (J S J^T)_ab stored})
+__global__ void k_bw_J(int m, const int *J_ptr, const int *J_col, const int *Jt_ptr, const int *Jt_row,
+                       const int *S_ptr, const int *S_col, int *bw) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= m) return;
+  int mn = a;
+  for (int e = J_ptr[a]; e < J_ptr[a + 1]; e++) {
+    const int I = J_col[e] / 3;
+    for (int k = S_ptr[I]; k < S_ptr[I + 1]; k++)
+      for (int cc = 0; cc < 3; cc++) {
+        const int q = 3 * S_col[k] + cc;
+        for (int t = Jt_ptr[q]; t < Jt_ptr[q + 1]; t++) mn = min(mn, Jt_row[t]);
+      }
+  }
+  atomicMax(bw, a - mn);
+}
+// v = J r1 (P^T r1 for P = J^T): per constraint a the chain acc = fma(J_ap, r1_p, acc) over J's row, into the
+// filter space's elimination order; r1 is given at the Z positions (rz, Z order)
+__global__ void k_J_rz(int m, const int *J_ptr, const int *J_col, const double *J_val, const int *pos,
+                       const double *rz, const int *zpi, double *v) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= m) return;
+  double acc = 0.0;
+  for (int e = J_ptr[a]; e < J_ptr[a + 1]; e++) acc = __fma_rn(J_val[e], rz[pos[J_col[e]]], acc);
+  v[zpi[a]] = acc;
+}
+// w = J^T y (P y) at the Z positions: per dof the chain over its constraints ascending, y in elimination order
+__global__ void k_Jt_y(int nc, const int *Z, const int *Jt_ptr, const int *Jt_row, const double *Jt_val,
+                       const int *zpi, const double *y, double *w) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= nc) return;
+  const int p = Z[a];
+  double acc = 0.0;
+  for (int t = Jt_ptr[p]; t < Jt_ptr[p + 1]; t++) acc = __fma_rn(Jt_val[t], y[zpi[Jt_row[t]]], acc);
+  w[a] = acc;
+}
+
 // Separator rows against the columns of a diagonal block B (a leaf, or a lower separator S' after its
 // subtree terms): for j in B ascending, L_sj = (acc_sj - sum_k L_sk L_jk) / L_jj with k ascending over
 // [max(p0(B), j - bw), j) (C9; the only nonzero terms of the band row j).  One thread per separator row s;
@@ -332,6 +411,29 @@ __global__ void __launch_bounds__(SB_TR) k_nd_sep_bwd(const int *ids, const NdBl
 }
 
 // ------------------------------------------------------------------ host
+int band_width_J(Ctx &c) {
+  Level &L0 = c.lev[0];
+  int *d = c.alloc<int>(1);
+  CK(cudaMemsetAsync(d, 0, sizeof(int), c.stream));
+  k_bw_J<<<nblk(c.m), CTA, 0, c.stream>>>(c.m, c.J_ptr, c.J_col, c.Jt_ptr, c.Jt_row, L0.A.ptr, L0.A.col, d);
+  after_launch(c, "k_bw_J");
+  int bw = 0;
+  CK(cudaMemcpyAsync(&bw, d, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  c.release(d);
+  return bw;
+}
+
+void filter_J_apply(Ctx &c, const double *rz, double *v_pi, const double *y_pi, double *w_z) {
+  if (v_pi) {
+    k_J_rz<<<nblk(c.m), CTA, 0, c.stream>>>(c.m, c.J_ptr, c.J_col, c.J_val, c.pos, rz, c.zpi, v_pi);
+    after_launch(c, "k_J_rz");
+  } else {
+    k_Jt_y<<<nblk(c.nc), CTA, 0, c.stream>>>(c.nc, c.Z, c.Jt_ptr, c.Jt_row, c.Jt_val, c.zpi, y_pi, w_z);
+    after_launch(c, "k_Jt_y");
+  }
+}
+
 void nd_remap_positions(Ctx &c, int *pos_z, long n) {
   if (n <= 0) return;
   k_remap<<<nblk(n), CTA, 0, c.stream>>>(n, c.zpi, pos_z);
@@ -339,7 +441,7 @@ void nd_remap_positions(Ctx &c, int *pos_z, long n) {
 }
 
 void nd_symbolic(Ctx &c) {
-  const int nc = c.nc, bw = c.bw;
+  const int nc = c.nf, bw = c.bw;  // the filter space: n_c Z positions (basis 0) or m constraints (basis 1)
   std::vector<Node> nodes;
   build(nodes, 0, nc, std::max(0, c.cfg.nd_levels), bw, 0);
   Emit E;
@@ -367,10 +469,22 @@ void nd_symbolic(Ctx &c) {
   c.nd_blk = upload(c, E.blk);
   c.pi_z = upload(c, E.pi);
   c.zpi = c.alloc<int>(nc);
-  c.dof = c.alloc<int>(nc);
   c.block_of = c.alloc<int>(nc);
-  k_nd_maps<<<nblk(nc), CTA, 0, c.stream>>>(nc, c.pi_z, c.Z, c.zpi, c.dof);
-  after_launch(c, "k_nd_maps");
+  if (c.cfg.filter_basis == 1) {
+    // P = J^T: the filter space is the constraint space; the fine rows the filter reads (r1 at I_c, the compact
+    // Z rows, the x2 scatter) stay in Z order
+    c.dof = c.alloc<int>(c.nc);
+    CK(cudaMemcpyAsync(c.dof, c.Z, (size_t)c.nc * sizeof(int), cudaMemcpyDeviceToDevice, c.stream));
+    int *scratch = c.alloc<int>(nc);
+    k_nd_maps<<<nblk(nc), CTA, 0, c.stream>>>(nc, c.pi_z, c.pi_z, c.zpi, scratch);
+    after_launch(c, "k_nd_maps");
+    CK(cudaStreamSynchronize(c.stream));
+    c.release(scratch);
+  } else {
+    c.dof = c.alloc<int>(nc);
+    k_nd_maps<<<nblk(nc), CTA, 0, c.stream>>>(nc, c.pi_z, c.Z, c.zpi, c.dof);
+    after_launch(c, "k_nd_maps");
+  }
   k_nd_block_of<<<c.nd_nblocks, CTA, 0, c.stream>>>(c.nd_nblocks, (const NdBlk *)c.nd_blk, c.block_of);
   after_launch(c, "k_nd_block_of");
   // leaves
@@ -435,7 +549,8 @@ void nd_symbolic(Ctx &c) {
   // Everything the solve reads (the two band copies, the separator rows, 1/L_ii and the work vectors) in
   // one arena (one range for tools and for an L2 access-policy window; measured without benefit so far).
   auto al = [](size_t n) { return (n + 31) & ~(size_t)31; };  // 256-byte alignment
-  const size_t n_band = al(total), n_off = al(off + 2), n_vec = al(nc), n_w = al(nc + SF_KC + 4);
+  const int nv = std::max(nc, c.nc);  // vectors of the filter space and of the Z rows
+  const size_t n_band = al(total), n_off = al(off + 2), n_vec = al(nv), n_w = al(nv + SF_KC + 4);
   const size_t arena = 2 * n_band + n_off + 3 * n_vec + 2 * n_w;
   double *A = c.alloc<double>(arena);
   c.nd_arena = A;
@@ -475,15 +590,21 @@ static void launch_off_band(Ctx &c, int np, const int *pairs, const NdBlk *blk, 
 }
 
 void nd_numeric(Ctx &c) {
-  const int nc = c.nc, bw = c.bw, W = band_stride(bw);
+  const int nc = c.nf, bw = c.bw, W = band_stride(bw);
   const NdBlk *blk = (const NdBlk *)c.nd_blk;
   Level &L0 = c.lev[0];
   CK(cudaMemsetAsync(c.Lrow - (size_t)BAND_PAD_ROWS * W, 0, (size_t)(nc + 2 * BAND_PAD_ROWS) * W * sizeof(double),
                      c.stream));
   if (c.loff_size) CK(cudaMemsetAsync(c.Loff, 0, c.loff_size * sizeof(double), c.stream));
-  k_nd_fill<<<nblk(nc), CTA, 0, c.stream>>>(nc, bw, W, blk, c.block_of, c.dof, c.pos, c.zpi, L0.A.ptr, L0.A.col,
-                                            L0.A.val, c.Lrow, c.Loff);
-  after_launch(c, "k_nd_fill");
+  if (c.cfg.filter_basis == 1) {
+    k_nd_fill_J<<<nblk(nc), CTA, 0, c.stream>>>(nc, bw, W, blk, c.block_of, c.zpi, c.J_ptr, c.J_col, c.J_val,
+                                                L0.A.ptr, L0.A.col, L0.A.val, c.Lrow, c.Loff);
+    after_launch(c, "k_nd_fill_J");
+  } else {
+    k_nd_fill<<<nblk(nc), CTA, 0, c.stream>>>(nc, bw, W, blk, c.block_of, c.dof, c.pos, c.zpi, L0.A.ptr, L0.A.col,
+                                              L0.A.val, c.Lrow, c.Loff);
+    after_launch(c, "k_nd_fill");
+  }
   // leaves (independent), then separator-vs-leaf columns (independent given the leaves)
   band_factor_blocks(c, nc, c.nd_nleaves, c.nd_leaf_p0, c.nd_leaf_len, bw, c.Lrow, 1);
   if (c.nd_npairs) {
@@ -514,7 +635,7 @@ void nd_numeric(Ctx &c) {
 
 
 void nd_solve(Ctx &c, const double *r1, const int *gather) {
-  const int nc = c.nc, bw = c.bw;
+  const int nc = c.nf, bw = c.bw;
   const NdBlk *blk = (const NdBlk *)c.nd_blk;
   double *w = c.fw, *y = c.fv;
   // forward: leaves (gathered r1), then separators bottom-up

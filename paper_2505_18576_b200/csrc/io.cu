@@ -146,6 +146,7 @@ void save_bsr(Ctx &c, const Bsr &A, const std::string &dir, const std::string &s
 
 // --------------------------------------------------------------------------- export
 static void export_impl(Ctx &c, const std::string &dir) {
+  REQUIRE(c.cfg.filter_basis == 0, AMGF_ERR_ARG, "export: the exchange format holds the identity filter basis only");
   CK(cudaStreamSynchronize(c.stream));
   {
     std::ofstream f(path_of(dir, kManifest));
@@ -264,6 +265,7 @@ static void import_impl(Ctx &c, const std::string &dir, void *stream) {
   // ---- A_w factor into the nested-dissection layout (filter.cu)
   if (c.nc > 0) {
     const int nc = c.nc;
+    c.nf = nc;
     c.bw = band_width(c);
     REQUIRE(c.bw == M.get("bw"), AMGF_ERR_FORMAT,
             "import: bw " + std::to_string(M.get("bw")) + " is not the band width of S[Z,Z] (" + std::to_string(c.bw) + ")");

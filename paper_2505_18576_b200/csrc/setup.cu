@@ -1346,7 +1346,8 @@ void build_thin(Ctx &c) {
   c.thin_src = c.alloc<int>(tnnz);
   c.thin_val = c.alloc<double>(tnnz);
   LAUNCH(k_thin_fill, n, n, L0.A.ptr, L0.A.col, c.pos, off, foff, c.thin_row, c.thin_ptr, c.thin_pos, c.thin_src);
-  nd_remap_positions(c, c.thin_pos, tnnz);  // thin entries address y in elimination (pi) order
+  // thin entries address y in elimination (pi) order; with P = J^T they address w = J^T y in Z order
+  if (c.cfg.filter_basis != 1) nd_remap_positions(c, c.thin_pos, tnnz);
   int tn = (int)tnnz;
   CK(cudaMemcpyAsync(c.thin_ptr + c.nthin, &tn, sizeof(int), cudaMemcpyHostToDevice, c.stream));
   C.thin_nnz = tnnz;
@@ -1519,7 +1520,16 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
 
   // ---- s3: A_w band, factor, thin residual
   if (c.nc > 0) {
-    c.bw = band_width(c);
+    if (c.cfg.filter_basis == 1) {  // P = J^T (reading R21): the filter space is the m constraints
+      REQUIRE(c.m > 0, AMGF_ERR_ARG, "filter_basis 1 needs constraints");
+      c.nf = c.m;
+      c.bw = band_width_J(c);
+      c.fJv = c.alloc<double>(c.m);
+      c.fJw = c.alloc<double>(c.nc);
+    } else {
+      c.nf = c.nc;
+      c.bw = band_width(c);
+    }
     nd_symbolic(c);
     filter_numeric(c);
     check_dev_error(c, "A_w Cholesky");

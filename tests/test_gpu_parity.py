@@ -63,7 +63,7 @@ def assert_hierarchy_equal(o, g):
 
 def gpu_dense_factor(g):
     """Dense factor of A_w[pi,pi] rebuilt from the GPU's storage: in-block band + separator off-block rows."""
-    nc, bw = g.nc, g.bw
+    nc, bw = g.nf, g.bw
     band = g.get(22)
     L = np.zeros((nc, nc))
     for t in range(bw + 1):
@@ -83,6 +83,7 @@ def gpu_dense_factor(g):
 def assert_filter_factor_equal(o, g):
     if o.nc == 0:
         return
+    assert g.nf == o.nf
     assert np.array_equal(g.get(25), o.get(25)), "elimination order pi"
     assert g.bw == int(o.get(26)[0])
     Ld = o.get(22)
@@ -529,3 +530,24 @@ def test_bound_constrained_parity(oracle_lib, amgf_mod, cfg):
     with pytest.raises(amgf_mod.AmgfError) as e:
         g.update_D_box(p.D, -lo, up)
     assert e.value.code == -3
+
+
+@pytest.mark.parametrize("cfg", [None, 0, 1])
+def test_Jt_filter_basis_parity(oracle_lib, amgf_mod, cfg):
+    """Variant f4, P = J^T (filter_basis 1; generality remark PAPER.md:583-585, reading R21): A_w = J S J^T (m x m)
+    factored in its nested-dissection order, v = J r1, w = J^T y; the factor, the apply and PCG (iterations and
+    solution) bitwise equal to the oracle's."""
+    p = tiny(N=3, matching=False, e_max=6.0) if cfg is None else gen.config(cfg)
+    kw = dict(filter_basis=1, **(dict(coarsest_size=16) if cfg is None else {}))
+    o, g = build_pair(oracle_lib, amgf_mod, p, **kw)
+    assert g.nf == p.m == o.nf
+    assert_hierarchy_equal(o, g)
+    assert_filter_factor_equal(o, g)
+    r = np.random.default_rng(41).standard_normal(p.n)
+    assert np.array_equal(g.apply(r).cpu().numpy(), o.apply(r))
+    xo, ro = o.pcg(p.b, rtol=p.rtol, maxit=2000)
+    xg, rg = g.pcg(p.b, rtol=p.rtol, max_it=2000)
+    assert rg["iterations"] == ro["iterations"] and np.array_equal(xg.cpu().numpy(), xo)
+    g.update_D(p.D * 10.0)
+    o2 = oracle_lib.Oracle.from_problem(p, D=p.D * 10.0, **kw)
+    assert np.array_equal(g.apply(r).cpu().numpy(), o2.apply(r))

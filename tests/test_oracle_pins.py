@@ -529,6 +529,43 @@ def test_amgf_operator_identity_and_splitting(oracle_lib, N, matching, e_max):
     assert np.abs(Pi @ Pi - Pi).max() <= 1e-8
 
 
+@pytest.mark.parametrize("N,matching", [(2, True), (3, False)])
+def test_amgf_Jt_basis(oracle_lib, N, matching):
+    """Variant f4, P = J^T (the generality remark; reading R21): A_w = J S J^T entry by entry
+    (dense product), the apply equals I - M A = (I - B A)(I - P A_w^{-1} P^T A)(I - B A) with P = J^T densely,
+    errors in range(J^T) are corrected exactly by the filter projector, and the Lemma main bound holds."""
+    p = tiny(N=N, matching=matching, e_max=4.0)
+    o = oracle_lib.Oracle.from_problem(p, coarsest_size=16, filter_basis=1)
+    n = p.n
+    assert o.nf == p.m
+    A = o.level_matrix(0).toarray()
+    P = J_csr(p).T.toarray()
+    Aw_ref = P.T @ A @ P
+    Aw = o.get(21)
+    assert np.abs(Aw - Aw_ref).max() <= 8 * EPS * np.abs(Aw_ref).max()
+    # the factor is of A_w[pi, pi]
+    pi = o.get(25)
+    Lw = o.get(22)
+    assert np.abs(Lw @ Lw.T - Aw[np.ix_(pi, pi)]).max() <= 1e-12 * np.abs(Aw).max()
+    M = dense_op(o.apply, n)
+    B = dense_op(o.vcycle, n)
+    I = np.eye(n)
+    Pi = I - P @ np.linalg.solve(Aw_ref, P.T @ A)
+    lhs = I - M @ A
+    rhs = (I - B @ A) @ Pi @ (I - B @ A)
+    assert np.abs(lhs - rhs).max() <= 1e-6 * max(1.0, np.abs(lhs).max())
+    assert np.abs(Pi @ P).max() <= 1e-9 * max(1.0, np.abs(P).max())
+    # the identity embedding's filter space contains range(J^T): a different (smaller) correction
+    assert np.abs(M - dense_op(oracle_lib.Oracle.from_problem(p, coarsest_size=16).apply, n)).max() > 1e-6
+    Lc = np.linalg.cholesky(A)
+    evM = np.sort(np.linalg.eigvals(Lc.T @ M @ Lc).real)
+    om = np.linalg.eigvals(Lc.T @ B @ Lc).real.max()
+    V = sla.null_space(P.T @ A)
+    beta = sla.eigh(V.T @ np.linalg.inv(0.5 * (B + B.T)) @ V, V.T @ A @ V, eigvals_only=True)[-1]
+    assert evM[0] > 0 and evM[-1] <= 1 + 1e-8
+    assert evM[-1] / evM[0] <= 2 * (beta + 2 + om) / (2 - om) * (1 + 1e-6)
+
+
 @pytest.mark.parametrize("e_max", [0.0, 4.0, 8.0, 12.0])
 def test_amgf_spectral_bounds(oracle_lib, e_max):
     # Lemma "Lower bound" (PAPER.md:462-470) => lambda_max(MA) <= 1 (reading R12),
