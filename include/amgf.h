@@ -56,7 +56,9 @@ typedef struct {
   int32_t nd_levels;       /* nested-dissection depth of A_w's elimination order (default 3, DESIGN R16) */
   int32_t smoother;        /* 1 = Chebyshev in D_l1^-1 A on [1/cheb_ratio, 1] (default, DESIGN R18 /
                               contract C23): each sweep is one polynomial of degree cheb_degree;
-                              0 = l1-Jacobi (contract C4)                                     */
+                              0 = l1-Jacobi (contract C4);
+                              2 = nodal-block l1-Jacobi: x += B^-1 (b - A x), B = blockdiag(A_ii + diag of the
+                              off-block l1 row sums) (variant f4, DESIGN R22, contracts C24/C25)            */
   int32_t cheb_degree;     /* 1..32 (default 2)                                               */
   uint64_t agg_seed;       /* aggregation priority seed (default 0x5EED)                     */
   double cheb_ratio;       /* > 1 (default 20)                                                */

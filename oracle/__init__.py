@@ -212,6 +212,7 @@ class Oracle:
                   6: (L["n_agg"] + 1, np.int32), 7: (L["nnzb_P"], np.int32), 8: ((L["nnzb_P"], 6 * b), np.float64),
                   9: (nodes * b, np.float64), 10: (nodes, np.int32), 11: ((nodes * b, 6), np.float64),
                   12: (2, np.float64), 13: ((nodes, b * 6), np.float64), 14: (nodes, np.int32), 15: (nodes, np.int32),
+                  16: ((nodes, b * (b + 1) // 2 + b), np.float64),
                   20: (self.nc, np.int32), 21: ((self.nf, self.nf), np.float64), 22: ((self.nf, self.nf), np.float64),
                   23: ((self.nco, self.nco), np.float64), 24: ((self.nco, self.nco), np.float64),
                   25: (self.nf, np.int32), 26: (1, np.int32)}

@@ -230,6 +230,8 @@ typedef struct {
   bsr_t P;          /* smoothed prolongator (b x 6) */
   bsr_t R;          /* restriction P^T (6 x b) */
   double *Bnn;      /* near-null space, n x 6 row-major */
+  double *bfac;     /* smoother 2 (nodal-block l1): per node the lower Cholesky factor of B_i, row-major
+                       b(b+1)/2 entries, then the b reciprocals 1/L_rr (contract C24) */
   double lambda, omega;
 } level_t;
 
@@ -850,6 +852,71 @@ static int smooth_P(level_t *L) {
   return ORC_OK;
 }
 
+/* Nodal-block l1 smoother data (variant f4, reading R22; the block form of the l1 smoothers of PAPER.md:589 /
+ * Baker et al.): B_i = A_ii + diag(d_i), d_i,r = sum of |a_(i,r),(j,c)| over the off-diagonal blocks j != i of the
+ * row (chain d = d + |a| from +0, blocks ascending, columns ascending); B_i = L L^T by the chains of C9 (acc = b_rc;
+ * fma(-L_rk, L_ck, acc) for k ascending; L_cc = sqrt(acc); L_rc = acc / L_cc); reciprocals 1/L_rr for the solves
+ * (C10).  B - A is block diagonally dominant, so lambda_max(B^{-1} A) <= 1: convergent with weight 1. */
+static int block_l1_data(level_t *L) {
+  const int b = L->b, nb = b * (b + 1) / 2 + b;
+  L->bfac = (double *)malloc((size_t)L->nodes * nb * sizeof(double));
+  for (int i = 0; i < L->nodes; i++) {
+    double B[36], Lf[36];
+    const double *Aii = NULL;
+    for (int r = 0; r < b; r++) {
+      double d = 0.0;
+      for (int k = L->A.ptr[i]; k < L->A.ptr[i + 1]; k++) {
+        if (L->A.col[k] == i) { Aii = L->A.val + (size_t)k * b * b; continue; }
+        for (int c = 0; c < b; c++) d = d + fabs(L->A.val[(size_t)k * b * b + r * b + c]);
+      }
+      B[r * b + r] = d;  /* the diagonal sum is completed below, once A_ii is known */
+    }
+    if (!Aii) return fail(ORC_ERR_NOT_SPD, "block smoother: node without a diagonal block");
+    for (int r = 0; r < b; r++)
+      for (int c = 0; c < b; c++) B[r * b + c] = (r == c) ? Aii[r * b + r] + B[r * b + r] : Aii[r * b + c];
+    for (int c = 0; c < b; c++) {
+      double acc = B[c * b + c];
+      for (int k = 0; k < c; k++) acc = fma(-Lf[c * b + k], Lf[c * b + k], acc);
+      if (!(acc > 0.0)) return fail(ORC_ERR_NOT_SPD, "block smoother: non-positive pivot");
+      const double lcc = sqrt(acc);
+      Lf[c * b + c] = lcc;
+      for (int r = c + 1; r < b; r++) {
+        double a = B[r * b + c];
+        for (int k = 0; k < c; k++) a = fma(-Lf[r * b + k], Lf[c * b + k], a);
+        Lf[r * b + c] = a / lcc;
+      }
+    }
+    double *o = L->bfac + (size_t)i * nb;
+    int w = 0;
+    for (int r = 0; r < b; r++)
+      for (int c = 0; c <= r; c++) o[w++] = Lf[r * b + c];
+    for (int r = 0; r < b; r++) o[w++] = 1.0 / Lf[r * b + r];
+  }
+  return ORC_OK;
+}
+
+/* t = B_i^{-1} v_i per node (C10 chains on the node's factor): forward acc = v_r; fma(-L_rk, y_k, acc) k ascending;
+ * y_r = acc * (1/L_rr); backward acc = y_r; fma(-L_kr, t_k, acc) k descending; t_r = acc * (1/L_rr). */
+static void block_solve(const level_t *L, const double *v, double *t) {
+  const int b = L->b, nb = b * (b + 1) / 2 + b;
+  for (int i = 0; i < L->nodes; i++) {
+    const double *f = L->bfac + (size_t)i * nb, *rinv = f + b * (b + 1) / 2;
+    const double *vi = v + (size_t)i * b;
+    double y[6], x[6];
+    for (int r = 0; r < b; r++) {
+      double acc = vi[r];
+      for (int k = 0; k < r; k++) acc = fma(-f[r * (r + 1) / 2 + k], y[k], acc);
+      y[r] = acc * rinv[r];
+    }
+    for (int r = b - 1; r >= 0; r--) {
+      double acc = y[r];
+      for (int k = b - 1; k > r; k--) acc = fma(-f[k * (k + 1) / 2 + r], x[k], acc);
+      x[r] = acc * rinv[r];
+    }
+    for (int r = 0; r < b; r++) t[(size_t)i * b + r] = x[r];
+  }
+}
+
 static void level_diag(level_t *L) {
   int b = L->b;
   L->dl1 = (double *)malloc((size_t)L->n * sizeof(double));
@@ -903,6 +970,10 @@ static int build_hierarchy(orc_ctx *cx, const double *Bnns, const int *Kptr, con
   for (;;) {
     level_t *L = &cx->lev[l];
     level_diag(L);
+    if (cx->cfg.smoother == 2) {
+      int st2 = block_l1_data(L);
+      if (st2) return st2;
+    }
     if (L->n <= cx->cfg.coarsest_size || l + 1 >= cx->cfg.max_levels || l + 1 >= MAXLEV) break;
     int st = aggregate(L, cx->cfg.agg_seed);
     if (st) return st;
@@ -970,7 +1041,7 @@ void orc_free(orc_ctx *cx) {
     level_t *L = &cx->lev[l];
     if (l > 0) bsr_free(&L->A);
     bsr_free(&L->Pt); bsr_free(&L->P); bsr_free(&L->R);
-    free(L->dl1); free(L->dpt); free(L->agg); free(L->comp); free(L->root); free(L->Bnn);
+    free(L->dl1); free(L->dpt); free(L->agg); free(L->comp); free(L->root); free(L->Bnn); free(L->bfac);
     for (int t = 0; t < 4; t++) free(cx->work[l][t]);
   }
   bsr_free(&cx->S);
@@ -1007,7 +1078,7 @@ orc_ctx *orc_create_box(int nodes, const int *Kptr, const int *Kcol, const doubl
     for (long p = 0; p < 3L * nodes; p++)
       if (!(Db[p] >= 0.0)) { *status = fail(ORC_ERR_DOMAIN, "bound diagonals must be >= 0"); return NULL; }
   }
-  if (cfg->smoother < 0 || cfg->smoother > 1 ||
+  if (cfg->smoother < 0 || cfg->smoother > 2 ||
       (cfg->smoother == 1 && (cfg->cheb_degree < 1 || cfg->cheb_degree > 32 || !(cfg->cheb_ratio > 1.0)))) {
     *status = fail(ORC_ERR_ARG, "bad smoother configuration");
     return NULL;
@@ -1106,6 +1177,26 @@ static void vcycle(orc_ctx *cx, int l, const double *b, double *x) {
   double *xc = cx->work[l + 1][2];
   double *xn = cx->work[l][3];
   const int cheb = cx->cfg.smoother == 1;
+  if (cx->cfg.smoother == 2) {
+    /* nodal-block l1 smoother (C25): from zero x = B^{-1} b; a sweep x_i = x_i + (B^{-1} (b - A x))_i */
+    block_solve(L, b, x);
+    for (int s = 1; s < cx->cfg.pre_sweeps; s++) {
+      bsr_spmv(&L->A, x, b, r, 1);
+      block_solve(L, r, xn);
+      for (long i = 0; i < n; i++) x[i] = x[i] + xn[i];
+    }
+    bsr_spmv(&L->A, x, b, r, 1);
+    bsr_spmv_warp32(&L->R, r, bc);
+    vcycle(cx, l + 1, bc, xc);
+    bsr_spmv(&L->P, xc, NULL, xn, 0);
+    for (long i = 0; i < n; i++) x[i] = x[i] + xn[i];
+    for (int s = 0; s < cx->cfg.post_sweeps; s++) {
+      bsr_spmv(&L->A, x, b, r, 1);
+      block_solve(L, r, xn);
+      for (long i = 0; i < n; i++) x[i] = x[i] + xn[i];
+    }
+    return;
+  }
   if (cheb) {  /* pre-smoothing, Chebyshev (C23) */
     for (int s = 0; s < cx->cfg.pre_sweeps; s++) cheb_smooth(cx, L, b, x, s == 0, r, xn);
   } else {
@@ -1301,6 +1392,8 @@ int orc_get(orc_ctx *cx, int which, int level, void *dst) {
     case 13: memcpy(dst, L->Pt.val, (size_t)bsr_nnzb(&L->Pt) * L->b * 6 * sizeof(double)); return 0;
     case 14: if (!L->root) return -1; memcpy(dst, L->root, (size_t)L->nodes * sizeof(int)); return 0;
     case 15: memcpy(dst, L->comp, (size_t)L->nodes * sizeof(int)); return 0;
+    case 16: if (!L->bfac) return -1;
+      memcpy(dst, L->bfac, (size_t)L->nodes * (L->b * (L->b + 1) / 2 + L->b) * sizeof(double)); return 0;
     case 20: memcpy(dst, cx->Z, (size_t)cx->nc * sizeof(int)); return 0;
     case 21: if (!cx->Aw) return -1; memcpy(dst, cx->Aw, (size_t)cx->nf * cx->nf * sizeof(double)); return 0;
     case 22: if (!cx->Lw) return -1; memcpy(dst, cx->Lw, (size_t)cx->nf * cx->nf * sizeof(double)); return 0;

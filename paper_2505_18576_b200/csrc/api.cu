@@ -179,6 +179,26 @@ void vcycle(Ctx &c, int l, const double *b, double *x, const double *add, VcOpts
       }
     return;
   }
+  if (c.cfg.smoother == 2) {  // nodal-block l1 (C25): residual SpMV, then the per-node block solve and update
+    double *bufs[2] = {x, L.x2};
+    int ci = ((pre - 1) + post) & 1;  // so that the last post-sweep lands in x
+    launch_block_smooth(c, L, b, nullptr, nullptr, bufs[ci]);
+    for (int s = 1; s < pre; s++) {
+      launch_sell_spmv(c, L.As, SPMV_RESID, bufs[ci], b, nullptr, nullptr, L.r, nullptr);
+      launch_block_smooth(c, L, L.r, bufs[ci], nullptr, bufs[1 - ci]);
+      ci = 1 - ci;
+    }
+    launch_sell_spmv(c, L.As, SPMV_RESID, bufs[ci], b, nullptr, nullptr, L.r, nullptr);
+    launch_restrict(c, L.R, L.r, Lc.bv);
+    vcycle(c, l + 1, Lc.bv, Lc.x, nullptr);
+    launch_prolong(c, L.Ps, Lc.x, bufs[ci]);
+    for (int s = 0; s < post; s++) {
+      launch_sell_spmv(c, L.As, SPMV_RESID, bufs[ci], b, nullptr, nullptr, L.r, nullptr);
+      launch_block_smooth(c, L, L.r, bufs[ci], (s == post - 1) ? add : nullptr, bufs[1 - ci]);
+      ci = 1 - ci;
+    }
+    return;
+  }
   double *bufs[2] = {x, L.x2};
   int ci = ((pre - 1) + post) & 1;  // so that the last post-sweep lands in x
   launch_jacobi0(c, L.n, b, L.dl1, bufs[ci]);
@@ -532,7 +552,7 @@ void ctx_init(Ctx &c, void *stream) {
   c.stream = (cudaStream_t)stream;
   REQUIRE(c.cfg.pre_sweeps >= 1 && c.cfg.post_sweeps >= 1 && c.cfg.max_levels >= 1 && c.cfg.power_iters >= 1,
           AMGF_ERR_ARG, "invalid config");
-  REQUIRE(c.cfg.smoother == 0 || (c.cfg.smoother == 1 && c.cfg.cheb_degree >= 1 && c.cfg.cheb_degree <= 32 &&
+  REQUIRE(c.cfg.smoother == 0 || c.cfg.smoother == 2 || (c.cfg.smoother == 1 && c.cfg.cheb_degree >= 1 && c.cfg.cheb_degree <= 32 &&
                                   c.cfg.cheb_ratio > 1.0),
           AMGF_ERR_ARG, "invalid smoother config");
   REQUIRE(c.cfg.filter_basis == 0 || c.cfg.filter_basis == 1, AMGF_ERR_ARG, "invalid filter_basis");

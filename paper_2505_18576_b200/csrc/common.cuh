@@ -81,6 +81,7 @@ struct Level {
   Bsr A;          // operator (level 0: S)
   Sell As;        // A in SELL-32 for the solve
   double *dl1 = nullptr, *dpt = nullptr;
+  double *bfac = nullptr;  // smoother 2: per-node block factors (C24)
   int *agg = nullptr, *comp = nullptr, *root = nullptr;
   int n_agg = 0;
   Bsr Pt, P, R;   // tentative / smoothed prolongator (b x 6), restriction (6 x b)
@@ -283,6 +284,8 @@ void launch_cheb0(Ctx &c, long n, const double *b, const double *d, double c0, d
 void launch_sell_spmv(Ctx &c, const Sell &A, int mode, const double *x, const double *b, const double *d,
                       const double *add, double *y, double *dot_part);
 void launch_jacobi0(Ctx &c, long n, const double *b, const double *d, double *x);
+// smoother 2 (C25): out = [add +] (x_in + B^{-1} v) per node, or B^{-1} v when x_in is null (start from zero)
+void launch_block_smooth(Ctx &c, const Level &L, const double *v, const double *x_in, const double *add, double *out);
 void launch_restrict(Ctx &c, const Bsr &R, const double *r, double *bc);
 void launch_prolong(Ctx &c, const Sell &P, const double *xc, double *x);
 void launch_dot(Ctx &c, long n, int b, const double *u, const double *v, int finish);

@@ -147,6 +147,7 @@ void save_bsr(Ctx &c, const Bsr &A, const std::string &dir, const std::string &s
 // --------------------------------------------------------------------------- export
 static void export_impl(Ctx &c, const std::string &dir) {
   REQUIRE(c.cfg.filter_basis == 0, AMGF_ERR_ARG, "export: the exchange format holds the identity filter basis only");
+  REQUIRE(c.cfg.smoother != 2, AMGF_ERR_ARG, "export: the exchange format holds no block-smoother factors");
   CK(cudaStreamSynchronize(c.stream));
   {
     std::ofstream f(path_of(dir, kManifest));

@@ -454,6 +454,46 @@ __global__ void k_gather_vals(long n, const int *src, const double *from, double
 }
 
 // ------------------------------------------------------------------ s8: diagonals (C3)
+// Nodal-block l1 smoother data (smoother 2, contract C24 / reading R22), one thread per node: d_r = off-block l1
+// row sums (chain d = d + |a| over the row's other blocks, ascending), B = A_ii + diag(d), its Cholesky by the
+// chains of C9, stored as the lower factor (b(b+1)/2, row-major) then the reciprocals 1/L_rr.
+template <int B>
+__global__ void k_block_l1(int nodes, const int *ptr, const int *col, const double *val, double *bfac, int *err) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nodes) return;
+  double M[B * B], Lf[B * B];
+  const double *Aii = nullptr;
+  for (int r = 0; r < B; r++) {
+    double d = 0.0;
+    for (int k = ptr[i]; k < ptr[i + 1]; k++) {
+      if (col[k] == i) { Aii = val + (long)k * B * B; continue; }
+      for (int c = 0; c < B; c++) d = d + fabs(val[(long)k * B * B + r * B + c]);
+    }
+    M[r * B + r] = d;
+  }
+  if (!Aii) { raise_err(err, DERR_NOT_SPD, i); return; }
+  for (int r = 0; r < B; r++)
+    for (int c = 0; c < B; c++) M[r * B + c] = (r == c) ? Aii[r * B + r] + M[r * B + r] : Aii[r * B + c];
+  for (int c = 0; c < B; c++) {
+    double acc = M[c * B + c];
+    for (int k = 0; k < c; k++) acc = __fma_rn(-Lf[c * B + k], Lf[c * B + k], acc);
+    if (!(acc > 0.0)) { raise_err(err, DERR_NOT_SPD, i); return; }
+    const double lcc = sqrt(acc);
+    Lf[c * B + c] = lcc;
+    for (int r = c + 1; r < B; r++) {
+      double a = M[r * B + c];
+      for (int k = 0; k < c; k++) a = __fma_rn(-Lf[r * B + k], Lf[c * B + k], a);
+      Lf[r * B + c] = a / lcc;
+    }
+  }
+  constexpr int NB = B * (B + 1) / 2 + B;
+  double *o = bfac + (long)i * NB;
+  int w = 0;
+  for (int r = 0; r < B; r++)
+    for (int c = 0; c <= r; c++) o[w++] = Lf[r * B + c];
+  for (int r = 0; r < B; r++) o[w++] = 1.0 / Lf[r * B + r];
+}
+
 __global__ void k_diag(int nodes, int b, const int *ptr, const int *col, const double *val, double *dl1, double *dpt) {
   long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
   if (t >= (long)nodes * b) return;
@@ -1244,6 +1284,15 @@ static void build_pairs(Ctx &c, long nnzc, const int *rowof, const int *ccol, co
          pb);
 }
 
+// smoother 2: the per-node block factors of level L (after its operator values change)
+static void smoother_data(Ctx &c, Level &L) {
+  if (c.cfg.smoother != 2) return;
+  const int nb = L.b * (L.b + 1) / 2 + L.b;
+  if (!L.bfac) L.bfac = c.alloc<double>((size_t)L.nodes * nb);
+  if (L.b == 3) LAUNCH(k_block_l1<3>, L.nodes, L.nodes, L.A.ptr, L.A.col, L.A.val, L.bfac, c.err);
+  else LAUNCH(k_block_l1<6>, L.nodes, L.nodes, L.A.ptr, L.A.col, L.A.val, L.bfac, c.err);
+}
+
 static void level_numeric(Ctx &c, int l, LevelCache &lc) {
   Level &L = c.lev[l];
   Level &Lc = c.lev[l + 1];
@@ -1300,6 +1349,7 @@ static void level_numeric(Ctx &c, int l, LevelCache &lc) {
   }
   LAUNCH(k_sym, lc.G.nnzb, lc.G.nnzb, lc.G_rowof, lc.G.ptr, lc.G.col, lc.G.val, Lc.A.val, c.err);
   LAUNCH(k_diag, (long)Lc.nodes * Lc.b, Lc.nodes, Lc.b, Lc.A.ptr, Lc.A.col, Lc.A.val, Lc.dl1, Lc.dpt);
+  smoother_data(c, Lc);
 }
 
 static void coarsest_numeric(Ctx &c) {
@@ -1542,6 +1592,7 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
   L0.dl1 = c.alloc<double>(n);
   L0.dpt = c.alloc<double>(n);
   LAUNCH(k_diag, n, nodes, 3, L0.A.ptr, L0.A.col, L0.A.val, L0.dl1, L0.dpt);
+  smoother_data(c, L0);
   // level-0 components of K's block graph
   L0.comp = c.alloc<int>(nodes);
   {
@@ -1746,6 +1797,7 @@ void setup_numeric(Ctx &c, const double *D, const double *D_lo, const double *D_
     thin_numeric(c, C.thin_nnz);
   }
   LAUNCH(k_diag, L0.n, L0.nodes, 3, L0.A.ptr, L0.A.col, L0.A.val, L0.dl1, L0.dpt);
+  smoother_data(c, L0);
   for (int l = 0; l + 1 < c.nlev; l++) {
     build_sell(c, c.lev[l].A, c.lev[l].As, false, l > 0);
     level_numeric(c, l, C.lc[l]);

@@ -439,6 +439,45 @@ void launch_cheb0(Ctx &c, long n, const double *b, const double *d, double c0, d
   after_launch(c, "k_cheb0");
 }
 
+// Nodal-block l1 smoothing step (C25), one thread per node: t = B_i^{-1} v_i by the C10 chains on the node's
+// stored factor; out_i = t (from zero), x_i + t, or add_i + (x_i + t).
+template <int B>
+__global__ void k_block_smooth(int nodes, const double *__restrict__ bfac, const double *__restrict__ v,
+                               const double *__restrict__ xin, const double *__restrict__ add, double *__restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nodes) return;
+  constexpr int NL = B * (B + 1) / 2;
+  const double *f = bfac + (long)i * (NL + B), *rinv = f + NL;
+  double y[B], t[B];
+#pragma unroll
+  for (int r = 0; r < B; r++) {
+    double acc = v[(long)i * B + r];
+#pragma unroll
+    for (int k = 0; k < r; k++) acc = __fma_rn(-f[r * (r + 1) / 2 + k], y[k], acc);
+    y[r] = acc * rinv[r];
+  }
+#pragma unroll
+  for (int r = B - 1; r >= 0; r--) {
+    double acc = y[r];
+#pragma unroll
+    for (int k = B - 1; k > r; k--) acc = __fma_rn(-f[k * (k + 1) / 2 + r], t[k], acc);
+    t[r] = acc * rinv[r];
+  }
+#pragma unroll
+  for (int r = 0; r < B; r++) {
+    const long e = (long)i * B + r;
+    double o = xin ? xin[e] + t[r] : t[r];
+    if (add) o = add[e] + o;
+    out[e] = o;
+  }
+}
+void launch_block_smooth(Ctx &c, const Level &L, const double *v, const double *x_in, const double *add, double *out) {
+  REQUIRE(L.bfac, AMGF_ERR_ARG, "block smoother data missing");
+  if (L.b == 3) k_block_smooth<3><<<nblk(L.nodes), CTA, 0, c.stream>>>(L.nodes, L.bfac, v, x_in, add, out);
+  else k_block_smooth<6><<<nblk(L.nodes), CTA, 0, c.stream>>>(L.nodes, L.bfac, v, x_in, add, out);
+  after_launch(c, "k_block_smooth");
+}
+
 void launch_prolong(Ctx &c, const Sell &P, const double *xc, double *x) {
   if (P.br == 3) sell_dispatch<3, 6>(c, P, MODE_ADDTO, xc, nullptr, nullptr, nullptr, x, nullptr);
   else if (P.br == 1) sell_dispatch<1, 6>(c, P, MODE_ADDTO, xc, nullptr, nullptr, nullptr, x, nullptr);

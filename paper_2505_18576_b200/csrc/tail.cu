@@ -316,7 +316,7 @@ static bool tail_disabled() {
 
 void tail_plan(Ctx &c) {
   c.tail_level = -1;
-  if (tail_disabled() || c.nlev < 3) return;
+  if (tail_disabled() || c.nlev < 3 || c.cfg.smoother == 2) return;  // the tail smooths with C23 / C4 only
   const int t = c.nlev - 2;
   Level &L = c.lev[t];
   if (L.b != 6 || L.As.br != 1 || L.As.bc != 6 || L.Ps.br != 1 || L.Ps.bc != 6 || L.R.bc != 6) return;

@@ -551,3 +551,22 @@ def test_Jt_filter_basis_parity(oracle_lib, amgf_mod, cfg):
     g.update_D(p.D * 10.0)
     o2 = oracle_lib.Oracle.from_problem(p, D=p.D * 10.0, **kw)
     assert np.array_equal(g.apply(r).cpu().numpy(), o2.apply(r))
+
+
+@pytest.mark.parametrize("cfg", [None, 1])
+def test_block_l1_smoother_parity(oracle_lib, amgf_mod, cfg):
+    """Variant f4, nodal-block l1 smoother (smoother 2, contracts C24/C25): the per-node block factors, the
+    V-cycle, the apply and PCG bitwise equal to the oracle (also after a numeric re-setup)."""
+    p = tiny(N=3, matching=False, e_max=6.0) if cfg is None else gen.config(cfg)
+    kw = dict(smoother=2, **(dict(coarsest_size=16) if cfg is None else {}))
+    o, g = build_pair(oracle_lib, amgf_mod, p, **kw)
+    assert_hierarchy_equal(o, g)
+    r = np.random.default_rng(51).standard_normal(p.n)
+    assert np.array_equal(g.vcycle(r).cpu().numpy(), o.vcycle(r))
+    assert np.array_equal(g.apply(r).cpu().numpy(), o.apply(r))
+    xo, ro = o.pcg(p.b, rtol=p.rtol)
+    xg, rg = g.pcg(p.b, rtol=p.rtol)
+    assert rg["iterations"] == ro["iterations"] and np.array_equal(xg.cpu().numpy(), xo)
+    g.update_D(p.D * 3.0)
+    o2 = oracle_lib.Oracle.from_problem(p, D=p.D * 3.0, **kw)
+    assert np.array_equal(g.apply(r).cpu().numpy(), o2.apply(r))

@@ -704,6 +704,61 @@ def test_cheb_vcycle_operator(oracle_lib, N, matching, k):
 
 def test_cheb_config_errors(oracle_lib):
     p = tiny(N=2)
-    for bad in (dict(smoother=1, cheb_degree=0), dict(smoother=1, cheb_ratio=1.0), dict(smoother=2)):
+    for bad in (dict(smoother=1, cheb_degree=0), dict(smoother=1, cheb_ratio=1.0), dict(smoother=3)):
         with pytest.raises(Exception):
             oracle_lib.Oracle.from_problem(p, **bad)
+
+
+# ------------------------------------------------------------- nodal-block l1 smoother (variant f4, C24/C25)
+def _block_diag_B(o, l):
+    """Dense block-diagonal B of level l rebuilt from the oracle's stored factors (L L^T per node)."""
+    Lv = o.levels[l]
+    b, nodes = Lv["b"], Lv["nodes"]
+    f = o.get(16, l)
+    B = np.zeros((nodes * b, nodes * b))
+    for i in range(nodes):
+        Lf = np.zeros((b, b))
+        Lf[np.tril_indices(b)] = f[i, :b * (b + 1) // 2]
+        assert np.array_equal(f[i, b * (b + 1) // 2:], 1.0 / np.diag(Lf))
+        B[i * b:(i + 1) * b, i * b:(i + 1) * b] = Lf @ Lf.T
+    return B
+
+
+@pytest.mark.parametrize("N,matching", [(2, True), (3, False)])
+def test_block_l1_smoother(oracle_lib, N, matching):
+    """Nodal-block l1 smoother (smoother 2, reading R22): per node B_i = A_ii + diag(off-block l1 row sums),
+    checked against A densely; lambda_max(B^{-1} A) <= 1 (block l1 => convergent with weight 1, PAPER.md:589);
+    the V-cycle equals the dense composition of x = B^{-1} b, the coarse correction and x + B^{-1}(b - A x), and
+    is symmetric, positive definite and convergent."""
+    p = tiny(N=N, matching=matching, e_max=3.0)
+    o = oracle_lib.Oracle.from_problem(p, coarsest_size=16, smoother=2)
+    assert o.nlev >= 2
+    for l in range(o.nlev - 1):
+        A = o.level_matrix(l).toarray()
+        b = o.levels[l]["b"]
+        B = _block_diag_B(o, l)
+        ref = np.zeros_like(A)
+        offl1 = np.abs(A).sum(1)
+        for i in range(A.shape[0] // b):
+            sl = slice(i * b, (i + 1) * b)
+            ref[sl, sl] = A[sl, sl]
+            offl1[sl] -= np.abs(A[sl, sl]).sum(1)
+        ref += np.diag(offl1)
+        assert np.abs(B - ref).max() <= 1e-12 * np.abs(ref).max()
+        ev = np.linalg.eigvals(np.linalg.solve(B, A)).real
+        assert ev.max() <= 1 + 1e-10 and ev.min() > 0
+    # V-cycle operator (E = (I - B^-1 A)(I - P Bc R A)(I - B^-1 A) level by level)
+    Bc = np.linalg.inv(o.level_matrix(o.nlev - 1).toarray())
+    for l in range(o.nlev - 2, -1, -1):
+        A = o.level_matrix(l).toarray()
+        P = o.level_matrix(l, "P").toarray()
+        Sm = np.eye(A.shape[0]) - np.linalg.solve(_block_diag_B(o, l), A)
+        E = Sm @ (np.eye(A.shape[0]) - P @ Bc @ P.T @ A) @ Sm
+        Bc = (np.eye(A.shape[0]) - E) @ np.linalg.inv(A)
+    V = dense_op(o.vcycle, p.n)
+    assert np.abs(V - Bc).max() <= 1e-9 * np.abs(Bc).max()
+    assert np.abs(V - V.T).max() <= 1e-11 * np.abs(V).max()
+    A = o.level_matrix(0).toarray()
+    Lc = np.linalg.cholesky(A)
+    ev = np.linalg.eigvalsh(Lc.T @ V @ Lc)
+    assert ev[-1] <= 1 + 1e-9 and ev[0] > 0
