@@ -316,3 +316,15 @@ def ip_data(p: Problem):
     vol = (h ** 3 * edge(k) * edge(j) * edge(i)).ravel()
     Mu = np.repeat(np.concatenate([vol, vol]), 3).astype(np.float64)
     return np.zeros(p.m), Ms, Mu
+
+
+STUDY_E_MAX = [0.0, 4.0, 8.0, 12.0]
+
+
+def study_case(N: int, matching: bool, inclusion: bool = False) -> Problem:
+    """Input of one cell of the iteration study (tools/n2_study.py, profiles/r02_n2_study.md): the cfg geometry
+    at N elements per axis and block, matching or offset interface, optional E = 1e3 inclusion, D log-uniform in
+    [1, 10^e] for e in STUDY_E_MAX with one xi per (N, interface) from SplitMix64(seed)."""
+    seed = 100 + 2 * N + (0 if matching else 1) + (1000 if inclusion else 0)
+    return generate(N, matching=matching, e_max=STUDY_E_MAX, seed=seed, inclusion=inclusion,
+                    name=f"N{N}{'m' if matching else 'o'}{'i' if inclusion else ''}")
