@@ -334,6 +334,9 @@ void launch_band_sweep(Ctx &c, int nblocks, const int *d_p0, const int *d_len, i
                        const double *Lcol, const double *Lrev, const double *dinv, const double *in, const int *gather,
                        double *out, double *out_shift = nullptr);
 void drop_caches(Ctx &c);
+// separator rows of the A_w factor against factored blocks as warp band sweeps (solve.cu); false: band too wide
+bool launch_sep_rows_sweep(Ctx &c, int np, const int *pairs, const void *blk, int maxsep, int bw, const double *Lcol,
+                           double *Loff);
 void build_sell(Ctx &c, const Bsr &A, Sell &S, bool alloc, bool split, bool sort_rows = false);
 
 // pieces of setup_all reused by amgf_import (io.cu)

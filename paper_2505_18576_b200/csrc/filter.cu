@@ -570,6 +570,12 @@ void nd_symbolic(Ctx &c) {
 
 static void launch_off_band(Ctx &c, int np, const int *pairs, const NdBlk *blk, int bw, int W) {
   if (!np) return;
+  static const bool old_kernel = getenv("AMGF_OFFBAND_RING") != nullptr;  // A/B: the shared-memory ring kernel
+  if (!old_kernel) {
+    // B's column-major band copy must be current: refresh it from Lrow (the blocks factored so far)
+    band_finish(c, c.nf, bw, c.Lrow, c.Lcol, c.Lrev, c.Ldinv);
+    if (launch_sep_rows_sweep(c, np, pairs, blk, c.nd_maxsep, bw, c.Lcol, c.Loff)) return;
+  }
   const int M = bw | 1;  // ring length >= bw, odd (bank-conflict-free rows)
   auto smem_of = [&](int t) {
     return ((((size_t)t * M + 15) & ~(size_t)15) + (size_t)OB_NS * OB_RC * W) * sizeof(double);

@@ -12,6 +12,7 @@
 
 #include "common.cuh"
 #include "devutil.cuh"
+#include "nd_kernels.cuh"
 
 namespace amgf {
 
@@ -1059,6 +1060,116 @@ __global__ void __launch_bounds__(1024) k_band_sweep_wide(const int *blk_p0, con
   }
   if (out_shift)
     for (int t = threadIdx.x; t < n; t += blockDim.x) out_shift[p0 + t + 1] = out[p0 + t];
+}
+
+// Separator rows against a factored diagonal block B (the A_w factorization's off-block part, C9):
+// L_sj = (a_sj - sum_{k in B, k < j} L_sk L_jk) / L_jj for j in B ascending -- a forward substitution with B's
+// band factor whose right-hand side is the separator row, so it runs as the solve's warp sweep (column TMA ring,
+// shuffle broadcast of the pivot, one FMA per window entry per pivot; acc = fma(-L_jk, L_sk, acc) is the C9
+// term fma(-L_sk, L_jk, acc) with the operands swapped, the same correctly rounded result) instead of one
+// (bw)-term chain per entry.  The pivot is divided by L_jj (C9), not multiplied by 1/L_jj.  A CTA of G warps
+// takes G consecutive rows of the separator and shares B's band rounds (stage refill after a CTA barrier).
+// grid: (pairs, ceil(max separator length / G)); rows are read and written in place in Loff.
+template <int R, int NB, int G>
+__global__ void __launch_bounds__(32 * G) k_sep_rows_sweep(const int2 *__restrict__ pairs, const NdBlk *__restrict__ blk,
+                                                          const double *__restrict__ Lcol, double *__restrict__ Loff) {
+  constexpr int Ws = 32 * R;
+  constexpr unsigned CHUNK = 32u * Ws * 8u;
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t bar[NB];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const NdBlk S = blk[pairs[blockIdx.x].x], B = blk[pairs[blockIdx.x].y];
+  const int s = blockIdx.y * G + warp;
+  if ((int)(blockIdx.y * G) >= S.len) return;  // whole CTA beyond the separator
+  const bool act = s < S.len;
+  double *row = Loff + S.off + (long)(act ? s : 0) * S.rs - S.t0;  // row[k] = entry (p0(S) + s, k), k in B
+  const int p0 = B.p0, n = B.len;
+  const int F = (n + 31) / 32;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int b = 0; b < NB; b++) mbar_init(&bar[b], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int g) {
+    if (g >= F || threadIdx.x != 0) return;
+    uint64_t *br = &bar[g % NB];
+    mbar_arrive_expect(br, CHUNK);
+    bulk_g2s(sm + (g % NB) * 32 * Ws, Lcol + (long)(p0 + 32 * g) * Ws, CHUNK, br);
+  };
+#pragma unroll
+  for (int g = 0; g < NB - 1; g++) issue(g);
+  auto ld_in = [&](int t) -> double { return (act && t < n) ? row[p0 + t] : 0.0; };
+  auto ld_d = [&](int t) -> double { return t < n ? Lcol[(long)(p0 + t) * Ws] : 1.0; };  // L_jj
+  double acc[R];
+#pragma unroll
+  for (int q = 0; q < R; q++) acc[q] = ld_in(lane + 32 * q);
+  double vq1 = ld_in(32 + lane + 32 * (R - 1));
+  double dv = ld_d(lane), dq1 = ld_d(32 + lane);
+  for (int q = 0; q < F; q++) {
+    const int t0 = 32 * q;
+    __syncthreads();  // every warp is done with the stage refilled next
+    fence_proxy_async();
+    issue(q + NB - 1);
+    const double vq2 = ld_in(t0 + 64 + lane + 32 * (R - 1));
+    const double dq2 = ld_d(t0 + 64 + lane);
+    mbar_wait(&bar[q % NB], (q / NB) & 1);
+    const double *cur = sm + (q % NB) * 32 * Ws + lane;
+    double mine = 0.0, lc[R];
+#pragma unroll
+    for (int u = 0; u < R; u++) lc[u] = cur[32 * u];
+#pragma unroll
+    for (int jj = 0; jj < 32; jj++) {
+      if (t0 + jj >= n) break;
+      double ln[R];
+      const int jn = (jj + 1) & 31;
+#pragma unroll
+      for (int u = 0; u < R; u++) ln[u] = cur[jn * (Ws - 1) + 32 * u];
+      const double yj = __shfl_sync(0xffffffffu, acc[0] / dv, jj);
+      mine = (lane == jj) ? yj : mine;
+#pragma unroll
+      for (int u = 0; u < R; u++) acc[u] = __fma_rn(-lc[u], yj, acc[u]);
+#pragma unroll
+      for (int u = 0; u < R; u++) lc[u] = ln[u];
+    }
+    if (act && t0 + lane < n) row[p0 + t0 + lane] = mine;
+#pragma unroll
+    for (int u = 0; u < R - 1; u++) acc[u] = acc[u + 1];
+    acc[R - 1] = vq1;
+    dv = dq1;
+    vq1 = vq2;
+    dq1 = dq2;
+  }
+}
+
+template <int R>
+static void sep_rows_R(Ctx &c, int np, const int *pairs, const NdBlk *blk, int maxsep, const double *Lcol,
+                       double *Loff) {
+  constexpr int NB = 2, G = 4;
+  const size_t smem = (size_t)NB * 32 * (32 * R) * sizeof(double);
+  size_t &attr = device_slot((const void *)k_sep_rows_sweep<R, NB, G>);
+  if (smem > attr) {
+    CK(cudaFuncSetAttribute(k_sep_rows_sweep<R, NB, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  const dim3 grid(np, (maxsep + G - 1) / G);
+  k_sep_rows_sweep<R, NB, G><<<grid, 32 * G, smem, c.stream>>>((const int2 *)pairs, blk, Lcol, Loff);
+  after_launch(c, "k_sep_rows_sweep");
+}
+
+bool launch_sep_rows_sweep(Ctx &c, int np, const int *pairs, const void *blk, int maxsep, int bw, const double *Lcol,
+                           double *Loff) {
+  if (!np) return true;
+  const NdBlk *b = (const NdBlk *)blk;
+  switch ((bw + 31) / 32 + 1) {
+    case 1: case 2: sep_rows_R<2>(c, np, pairs, b, maxsep, Lcol, Loff); return true;
+    case 3: sep_rows_R<3>(c, np, pairs, b, maxsep, Lcol, Loff); return true;
+    case 4: sep_rows_R<4>(c, np, pairs, b, maxsep, Lcol, Loff); return true;
+    case 5: sep_rows_R<5>(c, np, pairs, b, maxsep, Lcol, Loff); return true;
+    case 6: sep_rows_R<6>(c, np, pairs, b, maxsep, Lcol, Loff); return true;
+    case 7: sep_rows_R<7>(c, np, pairs, b, maxsep, Lcol, Loff); return true;
+    default: return false;  // R = 8 needs 128 KB per stage pair: the shared-memory ring kernel instead
+  }
 }
 
 void launch_band_sweep(Ctx &c, int nblocks, const int *d_p0, const int *d_len, int max_len, int bw, bool forward,
