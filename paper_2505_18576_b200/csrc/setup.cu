@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "devutil.cuh"
 
 namespace amgf {
 
@@ -342,6 +343,173 @@ __global__ void __launch_bounds__(CHOL_THREADS) k_band_chol(int n_all, const int
     __syncthreads();
   }
 }
+// Register-tiled form of the same factorization (same chains, bitwise equal to k_band_chol):
+//   phase A  each thread owns a 4 x 4 tile of panel entries (rows r0..r0+3, columns cc0..cc0+3) and applies
+//            the terms k < c0 of its 16 chains in ascending k from a k-major shared-memory chunk (two 32-byte
+//            row reads + two broadcast column reads per 16 FMAs; the next chunk is loaded into registers
+//            while the current one is consumed); a tile starts at its first band column c0 + r0 - bw
+//   phase B1 warp 0 factors the 32 x 32 diagonal block right-looking in registers (lane = row, shuffles)
+//   phase B2 every row below it applies the in-panel terms c ascending and divides by L_cc (one thread
+//            per row, 32 accumulators in registers, L_cc from shared memory as broadcasts)
+constexpr int CHT_THREADS = 384;
+#ifdef AMGF_CHOL_TRACE  // microbenchmark builds only (tools/mb_chol.cu): per-panel phase clocks
+__device__ long long *g_chol_trace;
+#define CHOL_STAMP(k) \
+  if (threadIdx.x == 0 && g_chol_trace) g_chol_trace[((long)blockIdx.x * 128 + c0 / 32) * 4 + (k)] = clock64();
+#else
+#define CHOL_STAMP(k)
+#endif
+__global__ void __launch_bounds__(CHT_THREADS) k_band_chol_t(int n_all, const int *blk_p0, const int *blk_len,
+                                                              int bw, int W, double *L, int *err, int tag) {
+  const int p0 = blk_p0 ? blk_p0[blockIdx.x] : 0;
+  const int n = blk_p0 ? blk_len[blockIdx.x] : n_all;
+  L += (long)p0 * W;
+  extern __shared__ __align__(16) double sh[];
+  const int rows = 32 + bw;
+  // k-major chunk AT[kk][r]: 32-byte aligned row groups, row pitch = 4 (mod 8) doubles so that the
+  // staging stores (8 consecutive k of 4 rows per warp) spread over the banks
+  const int ldk = ((rows + 3) & ~3) + ((((rows + 3) & ~3) % 8 == 0) ? 4 : 0);
+  const int nrt = (rows + 3) >> 2;      // row tiles
+  double *AT = sh;                      // [2][32][ldk] double-buffered k-major chunks
+  double *PA = sh + 64 * ldk;           // [rows][PLD] phase-A results / final panel rows
+  const int tid = threadIdx.x;
+  const int ntile = nrt * 8;            // tile t: row tile t % nrt, column tile t / nrt
+  for (int c0 = 0; c0 < n; c0 += 32) {
+    CHOL_STAMP(0);
+    const int rend = min(rows, n - c0), cmax = min(32, n - c0);
+    double acc[2][4][4];
+    int r0v[2], cc0v[2];
+    bool onv[2];
+#pragma unroll
+    for (int u = 0; u < 2; u++) {
+      const int t = tid + u * CHT_THREADS;
+      r0v[u] = 4 * (t % nrt);
+      cc0v[u] = 4 * (t / nrt);
+      onv[u] = t < ntile && r0v[u] < rows && r0v[u] + 3 >= cc0v[u] && r0v[u] - (cc0v[u] + 3) <= bw;
+#pragma unroll
+      for (int a = 0; a < 4; a++)
+#pragma unroll
+        for (int b = 0; b < 4; b++) {
+          const int i = c0 + r0v[u] + a, l = c0 + cc0v[u] + b;
+          acc[u][a][b] = (onv[u] && r0v[u] + a < rend && cc0v[u] + b < cmax && i >= l && i - l <= bw)
+                             ? L[(long)i * W + bw - (i - l)] : 0.0;
+        }
+    }
+    // ---- phase A over chunks [kc, kc + 32) of k < c0, staged by cp.async (zero-filled outside the band)
+    // into a double buffer; 8 consecutive k of one row per 8 threads (64-byte segments)
+    const int kbeg = max(0, c0 - bw);
+    const int nchunk = (c0 - kbeg + 31) / 32;
+    auto issue = [&](int m) {
+      const int kc = kbeg + 32 * m;
+      double *dst = AT + (m & 1) * 32 * ldk;
+      for (int h = 0; h < 4; h++)
+        for (int e2 = tid; e2 < 8 * ldk; e2 += CHT_THREADS) {
+          const int r = e2 >> 3, kk = h * 8 + (e2 & 7);
+          const int i = c0 + r, k = kc + kk;
+          const bool in = r < rows && i < n && k < c0 && i - k <= bw;
+          const double *src = in ? L + (long)i * W + bw - (i - k) : L;
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst + kk * ldk + r)), "l"(src),
+                       "r"(in ? 8 : 0) : "memory");
+        }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (nchunk > 0) issue(0);
+    for (int m = 0; m < nchunk; m++) {
+      const int kc = kbeg + 32 * m;
+      if (m + 1 < nchunk) {
+        issue(m + 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+      __syncthreads();
+      const double *ATc = AT + (m & 1) * 32 * ldk;
+#pragma unroll
+      for (int u = 0; u < 2; u++) {
+        const int tstart = c0 + r0v[u] - bw;  // first k with a nonzero L_{c0+r0, k}
+        if (onv[u] && kc + 32 > tstart) {
+          const int kk0 = max(0, tstart - kc), kn = min(32, c0 - kc);
+          for (int kk = kk0; kk < kn; kk++) {
+            const double2 *ar = reinterpret_cast<const double2 *>(ATc + kk * ldk + r0v[u]);
+            const double2 *ac = reinterpret_cast<const double2 *>(ATc + kk * ldk + cc0v[u]);
+            const double2 x0 = ar[0], x1 = ar[1], y0 = ac[0], y1 = ac[1];
+            const double av[4] = {x0.x, x0.y, x1.x, x1.y}, bv[4] = {y0.x, y0.y, y1.x, y1.y};
+#pragma unroll
+            for (int a = 0; a < 4; a++)
+#pragma unroll
+              for (int b = 0; b < 4; b++) acc[u][a][b] = __fma_rn(-av[a], bv[b], acc[u][a][b]);
+          }
+        }
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < 2; u++)
+      if (onv[u]) {
+#pragma unroll
+        for (int a = 0; a < 4; a++)
+#pragma unroll
+          for (int b = 0; b < 4; b++)
+            if (r0v[u] + a < rows) PA[(r0v[u] + a) * PLD + cc0v[u] + b] = acc[u][a][b];
+      }
+    __syncthreads();
+    CHOL_STAMP(1);
+    // ---- phase B: the in-panel terms, one thread per panel row (column-synchronous, one barrier per column):
+    // step c: (i) every row r > c in the band divides, L_rc = v_r[c] / L_cc; row c+1 also applies its own
+    // term k = c to its diagonal and takes the square root; (ii) every row applies the term k = c to its
+    // columns cp in (c, r] (row c+1's diagonal excluded: done in (i)).  Per entry the terms stay in
+    // ascending k (C9).
+    {
+      double *Ld = AT;             // [32] diagonal of the panel (AT is free after phase A)
+      double *colL = AT + 32;      // [32][33] colL[c*33 + cp] = L_{cp, c}, cp < 32
+      const int r = tid;
+      const bool rin = r < rend;
+      double v[32];
+#pragma unroll
+      for (int c = 0; c < 32; c++) v[c] = (r < rows) ? PA[r * PLD + c] : 0.0;
+      if (r == 0) {
+        if (!(v[0] > 0.0)) raise_err(err, DERR_NOT_SPD, tag * 1000000 + p0 + c0);
+        v[0] = sqrt(v[0]);
+        Ld[0] = v[0];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int c = 0; c < 32; c++) {
+        if (c < cmax) {  // block-uniform
+          const bool act = rin && r > c && r - c <= bw;
+          double lrc = 0.0;
+          if (act) {
+            lrc = v[c] / Ld[c];
+            v[c] = lrc;
+            if (r < 32) colL[c * 33 + r] = lrc;
+            if (c < 31 && r == c + 1 && c + 1 < cmax) {
+              const double dg = __fma_rn(-lrc, lrc, v[c + 1]);
+              if (!(dg > 0.0)) raise_err(err, DERR_NOT_SPD, tag * 1000000 + p0 + c0 + c + 1);
+              v[c + 1] = sqrt(dg);
+              Ld[c + 1] = v[c + 1];
+            }
+          }
+          __syncthreads();
+          if (act && r > c + 1) {
+#pragma unroll
+            for (int cp = c + 1; cp < 32; cp++)
+              if (cp < cmax && cp <= r && r - cp <= bw) v[cp] = __fma_rn(-lrc, colL[c * 33 + cp], v[cp]);
+          }
+        }
+      }
+      if (rin) {
+        const int i = c0 + r;
+#pragma unroll
+        for (int c = 0; c < 32; c++)
+          if (c < cmax && c <= r && r - c <= bw) L[(long)i * W + bw - (r - c)] = v[c];
+      }
+    }
+    CHOL_STAMP(2);
+    __syncthreads();
+    CHOL_STAMP(3);
+  }
+}
+
 // Fallback for wide bands (e.g. Z = NULL ordering): right-looking on global memory, one CTA (same chains).
 __global__ void __launch_bounds__(1024) k_band_chol_wide(int n_all, const int *blk_p0, const int *blk_len, int bw,
                                                          int W, double *L, int *err, int tag) {
@@ -947,6 +1115,525 @@ __global__ void __launch_bounds__(CTA) k_spgemm_dense(long nnzc, const int *__re
   for (int q = 0; q < BR * BC; q++) C_val[e * BR * BC + q] = acc[q];
 }
 
+// Row-group form of the fine-level A*P (same products, same chains as k_spgemm_dense; C20).  A CTA owns a
+// group of consecutive output rows (symbolic, built once on the host: at most NT output blocks, ACAP blocks
+// of A, PCAP blocks of the union of the P rows those A rows reference).  The group's A values (one
+// contiguous segment) and the union of its P rows (runs of consecutive rows: contiguous segments) are
+// TMA bulk-copied into shared memory once; the neighbouring rows of a lattice share most of their P rows,
+// so every P row is read from L2 about 2.5x less often than once per A block.  Then thread e = output block
+// C_ib walks A's row i in ascending order as before, A and B blocks from shared memory.  Groups whose rows
+// exceed the capacity (none at cfg 0-4) read the operands from global memory instead.
+struct GalGrp {
+  int e0, e1;      // output blocks [e0, e1)
+  int a0, a1;      // A blocks [a0, a1) (rows of the group, contiguous)
+  int r0, r1;      // runs [r0, r1) of the P-row union; r1 < 0: operands from global memory
+  int pad0, pad1;
+};
+struct GalRun {
+  int j0, j1;  // P rows [j0, j1)
+  int base;    // first shared-memory block of the run
+  int pad;
+};
+constexpr int GAL_NT = 64, GAL_ACAP = 176, GAL_PCAP = 288, GAL_RCAP = 64;
+// PEPI: the smoothed prolongator's epilogue (C19) instead of storing T = A*Pt: P_ia = Pt_ia - (omega T_ia)/d_i
+struct GalEpi {
+  const int *C_col = nullptr, *agg = nullptr, *Pt_ptr = nullptr;
+  const double *Ptv = nullptr, *dpt = nullptr;
+  double omega = 0.0;
+};
+template <int BR, int IN, int BC, bool PEPI = false>
+__global__ void __launch_bounds__(GAL_NT) k_gal_ap(const GalGrp *__restrict__ grp, const GalRun *__restrict__ runs,
+                                                  long nnzc, const int *__restrict__ C_rowof,
+                                                  const int *__restrict__ A_ptr, const int *__restrict__ A_col,
+                                                  const double *__restrict__ A_val, const int *__restrict__ B_ptr,
+                                                  const double *__restrict__ B_val,
+                                                  const signed char *__restrict__ off, double *__restrict__ C_val,
+                                                  GalEpi ep = GalEpi{}) {
+  constexpr int AB = BR * IN, BB = IN * BC;
+  extern __shared__ __align__(128) double gsm[];
+  double *Bs = gsm;                                // [GAL_PCAP][BB]
+  double *As = gsm + GAL_PCAP * BB;                // [GAL_ACAP * AB + 2] (16-byte aligned copy, shifted)
+  int *pofs = (int *)(As + GAL_ACAP * AB + 2);     // [GAL_ACAP] P-row block offset of each A block
+  __shared__ GalRun rs[GAL_RCAP];
+  __shared__ __align__(8) uint64_t bar;
+  const GalGrp g = grp[blockIdx.x];
+  const int tid = threadIdx.x;
+  const bool staged = g.r1 >= 0;
+  int ashift = 0;
+  if (staged) {
+    const long abeg = (long)g.a0 * AB * 8, aend = (long)g.a1 * AB * 8;
+    const long abeg16 = abeg & ~15L, aend16 = (aend + 15) & ~15L;
+    ashift = (int)(abeg - abeg16) / 8;
+    if (tid == 0) {
+      mbar_init(&bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      unsigned bytes = (unsigned)(aend16 - abeg16);
+      for (int r = g.r0; r < g.r1; r++) {
+        const GalRun q = runs[r];
+        bytes += (unsigned)(B_ptr[q.j1] - B_ptr[q.j0]) * BB * 8;
+      }
+      mbar_arrive_expect(&bar, bytes);
+      bulk_g2s(As, (const char *)A_val + abeg16, (unsigned)(aend16 - abeg16), &bar);
+      for (int r = g.r0; r < g.r1; r++) {
+        const GalRun q = runs[r];
+        const unsigned nb = (unsigned)(B_ptr[q.j1] - B_ptr[q.j0]);
+        if (nb) bulk_g2s(Bs + (long)q.base * BB, B_val + (long)B_ptr[q.j0] * BB, nb * BB * 8, &bar);
+      }
+    }
+    for (int r = tid; r < g.r1 - g.r0; r += GAL_NT) rs[r] = runs[g.r0 + r];
+    __syncthreads();
+    const int nr = g.r1 - g.r0;
+    for (int k = g.a0 + tid; k < g.a1; k += GAL_NT) {
+      const int j = A_col[k];
+      int r = 0;
+      while (r + 1 < nr && rs[r + 1].j0 <= j) r++;
+      pofs[k - g.a0] = rs[r].base + (B_ptr[j] - B_ptr[rs[r].j0]);
+    }
+    __syncthreads();
+    mbar_wait(&bar, 0);
+  }
+  const long e = (long)g.e0 + tid;
+  if (e >= g.e1) return;
+  const int i = C_rowof[e];
+  const int a0 = A_ptr[i], la = A_ptr[i + 1] - a0;
+  double acc[BR * BC];
+#pragma unroll
+  for (int q = 0; q < BR * BC; q++) acc[q] = 0.0;
+  int o = la > 0 ? off[e] : -1;
+  for (int t = 0; t < la; t++) {
+    const int on = (t + 1 < la) ? off[(long)(t + 1) * nnzc + e] : -1;
+    if (o >= 0) {
+      const int ka = a0 + t;
+      const double *Av, *Bv;
+      if (staged) {
+        Av = As + ashift + (long)(ka - g.a0) * AB;
+        Bv = Bs + (long)(pofs[ka - g.a0] + o) * BB;
+      } else {
+        Av = A_val + (long)ka * AB;
+        Bv = B_val + (long)(B_ptr[A_col[ka]] + o) * BB;
+      }
+      double a[AB], bb[BB];
+#pragma unroll
+      for (int u = 0; u < AB; u++) a[u] = Av[u];
+#pragma unroll
+      for (int u = 0; u < BB / 2; u++) {
+        const double2 v = reinterpret_cast<const double2 *>(Bv)[u];
+        bb[2 * u] = v.x;
+        bb[2 * u + 1] = v.y;
+      }
+#pragma unroll
+      for (int r = 0; r < BR; r++)
+#pragma unroll
+        for (int c = 0; c < BC; c++)
+#pragma unroll
+          for (int t2 = 0; t2 < IN; t2++) acc[r * BC + c] = __fma_rn(a[r * IN + t2], bb[t2 * BC + c], acc[r * BC + c]);
+    }
+    o = on;
+  }
+  if constexpr (PEPI) {
+    const bool own = ep.agg[i] == ep.C_col[e];
+#pragma unroll
+    for (int r = 0; r < BR; r++)
+#pragma unroll
+      for (int c = 0; c < BC; c++) {
+        double t = ep.omega * acc[r * BC + c];
+        t = t / ep.dpt[(long)i * BR + r];
+        const double pt = own ? ep.Ptv[((long)ep.Pt_ptr[i] * BR + r) * BC + c] : 0.0;
+        C_val[e * BR * BC + r * BC + c] = pt - t;
+      }
+  } else {
+#pragma unroll
+    for (int q = 0; q < BR * BC; q++) C_val[e * BR * BC + q] = acc[q];
+  }
+}
+// Hit-list form of the row-group product (same products, same chains; C20): the symbolic phase turns each
+// output block's block-product pairs (A block, B block; ascending A position) into 32-bit words
+// (A block within the group's staged A segment | B block within the staged P-row union << 8), and the
+// group's words and per-output word offsets are bulk-copied with the operands.  A thread then runs exactly
+// its hits, operands and indices from shared memory (k_gal_ap walks every A position and tests an offset
+// table in global memory).
+constexpr int GHL_PCAP = 256, GHL_HCAP = 1024;
+template <int BR, int IN, int BC, bool PEPI = false>
+__global__ void __launch_bounds__(GAL_NT) k_gal_hl(const GalGrp *__restrict__ grp, const GalRun *__restrict__ runs,
+                                                  const int *__restrict__ C_rowof, const int *__restrict__ pptr,
+                                                  const unsigned *__restrict__ hitw, const int *__restrict__ pa,
+                                                  const int *__restrict__ pb, const double *__restrict__ A_val,
+                                                  const int *__restrict__ B_ptr, const double *__restrict__ B_val,
+                                                  double *__restrict__ C_val, GalEpi ep = GalEpi{}) {
+  constexpr int AB = BR * IN, BB = IN * BC;
+  extern __shared__ __align__(128) double gsm[];
+  double *Bs = gsm;                                             // [GHL_PCAP][BB]
+  double *As = Bs + GHL_PCAP * BB;                              // [GAL_ACAP * AB + 2]
+  unsigned *Hs = reinterpret_cast<unsigned *>(As + GAL_ACAP * AB + 2);  // [GHL_HCAP + 8]
+  int *Ps = reinterpret_cast<int *>(Hs + GHL_HCAP + 8);         // [GAL_NT + 1 + 8]
+  __shared__ __align__(8) uint64_t bar;
+  const GalGrp g = grp[blockIdx.x];
+  const int tid = threadIdx.x;
+  const bool staged = g.r1 >= 0;
+  int ashift = 0, hshift = 0, pshift = 0, q0 = 0;
+  if (staged) {
+    q0 = pptr[g.e0];
+    const int q1 = pptr[g.e1];
+    const long abeg = (long)g.a0 * AB * 8, aend = (long)g.a1 * AB * 8;
+    const long abeg16 = abeg & ~15L, aend16 = (aend + 15) & ~15L;
+    ashift = (int)(abeg - abeg16) / 8;
+    const long hb = (long)q0 * 4 & ~15L, he = ((long)q1 * 4 + 15) & ~15L;
+    hshift = q0 & 3;
+    const long pbeg = (long)g.e0 * 4 & ~15L, pend = ((long)(g.e1 + 1) * 4 + 15) & ~15L;
+    pshift = g.e0 & 3;
+    if (tid == 0) {
+      mbar_init(&bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      unsigned bytes = (unsigned)(aend16 - abeg16 + he - hb + pend - pbeg);
+      for (int r = g.r0; r < g.r1; r++) bytes += (unsigned)(B_ptr[runs[r].j1] - B_ptr[runs[r].j0]) * BB * 8;
+      mbar_arrive_expect(&bar, bytes);
+      bulk_g2s(As, (const char *)A_val + abeg16, (unsigned)(aend16 - abeg16), &bar);
+      if (he > hb) bulk_g2s(Hs, (const char *)hitw + hb, (unsigned)(he - hb), &bar);
+      bulk_g2s(Ps, (const char *)pptr + pbeg, (unsigned)(pend - pbeg), &bar);
+      for (int r = g.r0; r < g.r1; r++) {
+        const GalRun q = runs[r];
+        const unsigned nb = (unsigned)(B_ptr[q.j1] - B_ptr[q.j0]);
+        if (nb) bulk_g2s(Bs + (long)q.base * BB, B_val + (long)B_ptr[q.j0] * BB, nb * BB * 8, &bar);
+      }
+    }
+    __syncthreads();
+    mbar_wait(&bar, 0);
+  }
+  const long e = (long)g.e0 + tid;
+  if (e >= g.e1) return;
+  double acc[BR * BC];
+#pragma unroll
+  for (int q = 0; q < BR * BC; q++) acc[q] = 0.0;
+  auto hit = [&](const double *Av, const double *Bv) {
+    double a[AB], bb[BB];
+#pragma unroll
+    for (int u = 0; u < AB; u++) a[u] = Av[u];
+#pragma unroll
+    for (int u = 0; u < BB / 2; u++) {
+      const double2 v = reinterpret_cast<const double2 *>(Bv)[u];
+      bb[2 * u] = v.x;
+      bb[2 * u + 1] = v.y;
+    }
+#pragma unroll
+    for (int r = 0; r < BR; r++)
+#pragma unroll
+      for (int c = 0; c < BC; c++)
+#pragma unroll
+        for (int t2 = 0; t2 < IN; t2++) acc[r * BC + c] = __fma_rn(a[r * IN + t2], bb[t2 * BC + c], acc[r * BC + c]);
+  };
+  if (staged) {
+    const int h0 = Ps[pshift + tid] - q0, h1 = Ps[pshift + tid + 1] - q0;
+    for (int h = h0; h < h1; h++) {
+      const unsigned w = Hs[hshift + h];
+      hit(As + ashift + (w & 0xffu) * AB, Bs + (w >> 8) * BB);
+    }
+  } else {
+    for (int q = pptr[e]; q < pptr[e + 1]; q++) hit(A_val + (long)pa[q] * AB, B_val + (long)pb[q] * BB);
+  }
+  const int i = C_rowof[e];
+  if constexpr (PEPI) {
+    const bool own = ep.agg[i] == ep.C_col[e];
+#pragma unroll
+    for (int r = 0; r < BR; r++)
+#pragma unroll
+      for (int c = 0; c < BC; c++) {
+        double t = ep.omega * acc[r * BC + c];
+        t = t / ep.dpt[(long)i * BR + r];
+        const double pt = own ? ep.Ptv[((long)ep.Pt_ptr[i] * BR + r) * BC + c] : 0.0;
+        C_val[e * BR * BC + r * BC + c] = pt - t;
+      }
+  } else {
+#pragma unroll
+    for (int q = 0; q < BR * BC; q++) C_val[e * BR * BC + q] = acc[q];
+  }
+}
+constexpr size_t ghl_smem(int AB, int BB) {
+  return ((size_t)GHL_PCAP * BB + (size_t)GAL_ACAP * AB + 2) * 8 + (GHL_HCAP + 8) * 4 + (GAL_NT + 1 + 8) * 4;
+}
+// hit words of the staged groups (symbolic, once per setup)
+__global__ void k_gal_hitw(const GalGrp *__restrict__ grp, const GalRun *__restrict__ runs,
+                           const int *__restrict__ pptr, const int *__restrict__ pa, const int *__restrict__ pb,
+                           const int *__restrict__ B_ptr, unsigned *__restrict__ hitw) {
+  const GalGrp g = grp[blockIdx.x];
+  if (g.r1 < 0) return;
+  const int nr = g.r1 - g.r0;
+  for (int q = pptr[g.e0] + threadIdx.x; q < pptr[g.e1]; q += blockDim.x) {
+    const int b = pb[q];
+    int r = 0;
+    while (r + 1 < nr && B_ptr[runs[g.r0 + r + 1].j0] <= b) r++;
+    const GalRun run = runs[g.r0 + r];
+    hitw[q] = (unsigned)(pa[q] - g.a0) | ((unsigned)(run.base + b - B_ptr[run.j0]) << 8);
+  }
+}
+
+// Fine-level G = R * AP (R = P^T, 6x3 blocks; AP 3x6), streamed form of k_spgemm_dense<6,3,6> (C20, same
+// chains).  A CTA owns <= 64 output blocks of one coarse row a; two threads per output block (rows 0-2 /
+// 3-5 of the 6x6 block, 18 accumulators each).  R's row a is walked in ascending order in chunks of <= 16
+// positions; warp 0 stages each chunk (the R blocks: one contiguous segment; the AP row of each position:
+// one segment each) with TMA bulk copies into a 3-stage shared-memory ring, mbarrier completion, while the
+// CTA consumes the previous chunk.
+struct RapGrp {
+  int a, e0, e1, pad;
+};
+constexpr int RAP_NT = 128, RAP_TC = 16, RAP_SCAP = 104, RAP_NS = 3;
+constexpr int RAP_STAGE = (RAP_TC + RAP_SCAP) * 18;  // doubles per stage
+__global__ void __launch_bounds__(RAP_NT) k_gal_rap(const RapGrp *__restrict__ grp, long nnzc,
+                                                   const int *__restrict__ R_ptr, const int *__restrict__ R_col,
+                                                   const double *__restrict__ R_val, const int *__restrict__ B_ptr,
+                                                   const double *__restrict__ B_val,
+                                                   const signed char *__restrict__ off, double *__restrict__ C_val) {
+  extern __shared__ __align__(128) double rsm[];  // [RAP_NS][RAP_STAGE]: R blocks, then AP blocks
+  __shared__ int meta[RAP_NS][RAP_TC + 2];         // per stage: AP block base of each position, count, t0
+  __shared__ __align__(8) uint64_t full[RAP_NS];
+  const RapGrp g = grp[blockIdx.x];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int ra0 = R_ptr[g.a], lr = R_ptr[g.a + 1] - ra0;
+  int next_t = 0;  // producer state (warp 0, warp-uniform)
+  // warp 0: stage the chunk starting at next_t into stage s (an empty chunk marks the end)
+  auto produce = [&](int s) {
+    const int p = lane;
+    const bool in = p < RAP_TC && next_t + p < lr;
+    int j = 0, nb = 0;
+    if (in) {
+      j = R_col[ra0 + next_t + p];
+      nb = B_ptr[j + 1] - B_ptr[j];
+    }
+    int incl = nb;  // inclusive prefix of AP blocks
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += v;
+    }
+    const bool take = in && incl <= RAP_SCAP;
+    const int tc = __popc(__ballot_sync(0xffffffffu, take));  // takes are a prefix of the lanes
+    const int nbt = __shfl_sync(0xffffffffu, incl, max(tc - 1, 0)) * (tc > 0);
+    double *st = rsm + (long)s * RAP_STAGE;
+    if (take) meta[s][p] = incl - nb;
+    if (lane == 0) {
+      meta[s][RAP_TC] = tc;
+      meta[s][RAP_TC + 1] = next_t;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive_expect(&full[s], (unsigned)(tc + nbt) * 144u);
+    __syncwarp();
+    if (tc > 0) {
+      if (lane == 0) bulk_g2s(st, R_val + (long)(ra0 + next_t) * 18, (unsigned)tc * 144u, &full[s]);
+      if (take && nb > 0)
+        bulk_g2s(st + (RAP_TC + incl - nb) * 18, B_val + (long)B_ptr[j] * 18, (unsigned)nb * 144u, &full[s]);
+    }
+    next_t += tc;
+  };
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < RAP_NS; s++) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid < 32) {
+#pragma unroll
+    for (int s = 0; s < RAP_NS; s++) produce(s);
+  }
+  const int ob = tid >> 1, h = tid & 1;
+  const long e = (long)g.e0 + ob;
+  const bool act = e < g.e1;
+  double acc[18];
+#pragma unroll
+  for (int q = 0; q < 18; q++) acc[q] = 0.0;
+  for (int q = 0;; q++) {
+    const int s = q % RAP_NS;
+    mbar_wait(&full[s], (q / RAP_NS) & 1);
+    const int tc = meta[s][RAP_TC], t0 = meta[s][RAP_TC + 1];
+    if (tc == 0) break;
+    const double *st = rsm + (long)s * RAP_STAGE;
+    if (act) {
+      int o = off[(long)t0 * nnzc + e];
+      for (int p = 0; p < tc; p++) {
+        const int on = (p + 1 < tc) ? off[(long)(t0 + p + 1) * nnzc + e] : -1;
+        if (o >= 0) {
+          const double *Rv = st + p * 18 + h * 9;  // rows 3h..3h+2 of the 6x3 block
+          const double2 *Bv = reinterpret_cast<const double2 *>(st + (RAP_TC + meta[s][p] + o) * 18);
+          double a[9], bb[18];
+#pragma unroll
+          for (int u = 0; u < 9; u++) a[u] = Rv[u];
+#pragma unroll
+          for (int u = 0; u < 9; u++) {
+            const double2 v = Bv[u];
+            bb[2 * u] = v.x;
+            bb[2 * u + 1] = v.y;
+          }
+#pragma unroll
+          for (int r = 0; r < 3; r++)
+#pragma unroll
+            for (int c2 = 0; c2 < 6; c2++)
+#pragma unroll
+              for (int t2 = 0; t2 < 3; t2++) acc[r * 6 + c2] = __fma_rn(a[r * 3 + t2], bb[t2 * 6 + c2], acc[r * 6 + c2]);
+        }
+        o = on;
+      }
+    }
+    __syncthreads();  // stage s consumed
+    if (tid < 32) {
+      fence_proxy_async();
+      produce(s);
+    }
+  }
+  if (act) {
+#pragma unroll
+    for (int r = 0; r < 3; r++)
+#pragma unroll
+      for (int c2 = 0; c2 < 6; c2++) C_val[e * 36 + (3 * h + r) * 6 + c2] = acc[r * 6 + c2];
+  }
+}
+
+// Warp-specialised form of k_gal_rap (same chains): warp 4 is the producer (chunk plan from the per-R-block
+// (AP row start, length) table, TMA bulk copies of the R blocks, the AP rows and the chunk's rows of the
+// group-contiguous offset table into a 3-stage ring, full/empty mbarriers); warps 0-3 consume: offsets,
+// R and AP blocks all from shared memory.
+constexpr int RAP2_CONS = 128, RAP2_OFFB = RAP_TC * 64;  // offset bytes per stage
+constexpr int RAP2_STAGE_B = RAP_STAGE * 8 + RAP2_OFFB;
+__global__ void __launch_bounds__(RAP2_CONS + 32) k_gal_rap2(const RapGrp *__restrict__ grp,
+                                                            const long *__restrict__ gofs,
+                                                            const int *__restrict__ R_ptr,
+                                                            const int2 *__restrict__ rbi,
+                                                            const double *__restrict__ R_val,
+                                                            const double *__restrict__ B_val,
+                                                            const signed char *__restrict__ offg,
+                                                            double *__restrict__ C_val) {
+  extern __shared__ __align__(128) unsigned char rsm2[];  // [RAP_NS] x (R + AP blocks, then offsets)
+  __shared__ int meta[RAP_NS][RAP_TC + 2];
+  __shared__ __align__(8) uint64_t full[RAP_NS], empty[RAP_NS];
+  const RapGrp g = grp[blockIdx.x];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int ra0 = R_ptr[g.a], lr = R_ptr[g.a + 1] - ra0;
+  const signed char *og = offg + gofs[blockIdx.x];
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < RAP_NS; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], RAP2_CONS / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid >= RAP2_CONS) {  // ---- producer warp
+    int next_t = 0;
+    for (int q = 0;; q++) {
+      const int s = q % RAP_NS;
+      if (q >= RAP_NS) mbar_wait(&empty[s], ((q / RAP_NS) - 1) & 1);
+      const int p = lane;
+      const bool in = p < RAP_TC && next_t + p < lr;
+      int2 bi = make_int2(0, 0);
+      if (in) bi = rbi[ra0 + next_t + p];
+      int incl = bi.y;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += v;
+      }
+      const bool take = in && incl <= RAP_SCAP;
+      const int tc = __popc(__ballot_sync(0xffffffffu, take));
+      const int nbt = tc > 0 ? __shfl_sync(0xffffffffu, incl, tc - 1) : 0;
+      unsigned char *st = rsm2 + (long)s * RAP2_STAGE_B;
+      double *sd = reinterpret_cast<double *>(st);
+      if (take) meta[s][p] = incl - bi.y;
+      if (lane == 0) {
+        meta[s][RAP_TC] = tc;
+        meta[s][RAP_TC + 1] = next_t;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_expect(&full[s], (unsigned)(tc + nbt) * 144u + (unsigned)tc * 64u);
+      __syncwarp();
+      if (tc > 0) {
+        if (lane == 0) {
+          bulk_g2s(sd, R_val + (long)(ra0 + next_t) * 18, (unsigned)tc * 144u, &full[s]);
+          bulk_g2s(st + RAP_STAGE * 8, og + (long)next_t * 64, (unsigned)tc * 64u, &full[s]);
+        }
+        if (take && bi.y > 0)
+          bulk_g2s(sd + (RAP_TC + incl - bi.y) * 18, B_val + (long)bi.x * 18, (unsigned)bi.y * 144u, &full[s]);
+      }
+      next_t += tc;
+      if (tc == 0) break;
+    }
+    return;
+  }
+  // ---- consumers: two threads per output block
+  const int ob = tid >> 1, h = tid & 1;
+  const long e = (long)g.e0 + ob;
+  const bool act = e < g.e1;
+  double acc[18];
+#pragma unroll
+  for (int q = 0; q < 18; q++) acc[q] = 0.0;
+  for (int q = 0;; q++) {
+    const int s = q % RAP_NS;
+    mbar_wait(&full[s], (q / RAP_NS) & 1);
+    const int tc = meta[s][RAP_TC];
+    if (tc == 0) break;
+    const unsigned char *st = rsm2 + (long)s * RAP2_STAGE_B;
+    const double *sd = reinterpret_cast<const double *>(st);
+    const signed char *so = reinterpret_cast<const signed char *>(st + RAP_STAGE * 8);
+    if (act) {
+      for (int p = 0; p < tc; p++) {
+        const int o = so[p * 64 + ob];
+        if (o >= 0) {
+          const double *Rv = sd + p * 18 + h * 9;
+          const double2 *Bv = reinterpret_cast<const double2 *>(sd + (RAP_TC + meta[s][p] + o) * 18);
+          double a[9], bb[18];
+#pragma unroll
+          for (int u = 0; u < 9; u++) a[u] = Rv[u];
+#pragma unroll
+          for (int u = 0; u < 9; u++) {
+            const double2 v = Bv[u];
+            bb[2 * u] = v.x;
+            bb[2 * u + 1] = v.y;
+          }
+#pragma unroll
+          for (int r = 0; r < 3; r++)
+#pragma unroll
+            for (int c2 = 0; c2 < 6; c2++)
+#pragma unroll
+              for (int t2 = 0; t2 < 3; t2++) acc[r * 6 + c2] = __fma_rn(a[r * 3 + t2], bb[t2 * 6 + c2], acc[r * 6 + c2]);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  if (act) {
+#pragma unroll
+    for (int r = 0; r < 3; r++)
+#pragma unroll
+      for (int c2 = 0; c2 < 6; c2++) C_val[e * 36 + (3 * h + r) * 6 + c2] = acc[r * 6 + c2];
+  }
+}
+// group-contiguous offset rows of k_gal_rap2: offg[gofs[g] + t * 64 + (e - e0)] = offset of G's column in the AP
+// row of R position t (-1 if absent); symbolic, once
+__global__ void k_rap_offg(int ngrp, const RapGrp *__restrict__ grp, const long *__restrict__ gofs,
+                           const int *__restrict__ R_ptr, const int *__restrict__ R_col, const int *__restrict__ B_ptr,
+                           const int *__restrict__ B_col, const int *__restrict__ C_col, signed char *__restrict__ offg) {
+  const RapGrp g = grp[blockIdx.x];
+  const int ra0 = R_ptr[g.a], lr = R_ptr[g.a + 1] - ra0;
+  for (int q = threadIdx.x; q < lr * 64; q += blockDim.x) {
+    const int t = q >> 6, el = q & 63;
+    int o = -1;
+    if (g.e0 + el < g.e1) {
+      const int j = R_col[ra0 + t];
+      const int k2 = bsearch_int(B_col, B_ptr[j], B_ptr[j + 1], C_col[g.e0 + el]);
+      if (k2 >= 0) o = k2 - B_ptr[j];
+    }
+    offg[gofs[blockIdx.x] + q] = (signed char)o;
+  }
+}
+__global__ void k_rap_rbi(long nnz, const int *__restrict__ R_col, const int *__restrict__ B_ptr, int2 *rbi) {
+  const long k = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (k >= nnz) return;
+  const int j = R_col[k];
+  rbi[k] = make_int2(B_ptr[j], B_ptr[j + 1] - B_ptr[j]);
+}
+
+constexpr size_t gal_smem(int AB, int BB) {
+  return ((size_t)GAL_PCAP * BB + (size_t)GAL_ACAP * AB + 2) * 8 + (size_t)GAL_ACAP * 4;
+}
+
 __global__ void k_sym(long nnzb, const int *rowof, const int *ptr, const int *col, const double *G, double *Ac,
                       int *err) {
   long e = blockIdx.x * (long)blockDim.x + threadIdx.x;
@@ -1133,6 +1820,19 @@ static void band_alloc(Ctx &c, int n, int bw, double *&Lrow, double *&Lcol, doub
 void band_factor_blocks(Ctx &c, int n, int nblocks, const int *d_p0, const int *d_len, int bw, double *Lrow, int tag) {
   const int W = band_stride(bw);
   const int grid = nblocks > 0 ? nblocks : 1;
+  static const bool old_chol = getenv("AMGF_CHOL_OLD") != nullptr;  // A/B only: the round-1 panel kernel
+  const int rows = 32 + bw, r4 = (rows + 3) & ~3, ldk = r4 + (r4 % 8 == 0 ? 4 : 0);
+  const size_t smem_t = (64 * (size_t)ldk + (size_t)rows * PLD) * sizeof(double);
+  if (!old_chol && rows <= 256 && smem_t <= 220 * 1024) {
+    size_t &attr = device_slot((const void *)k_band_chol_t);
+    if (smem_t > attr) {
+      CK(cudaFuncSetAttribute(k_band_chol_t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t));
+      attr = smem_t;
+    }
+    k_band_chol_t<<<grid, CHT_THREADS, smem_t, c.stream>>>(n, d_p0, d_len, bw, W, Lrow, c.err, tag);
+    after_launch(c, "k_band_chol_t");
+    return;
+  }
   const size_t smem = (2 * (size_t)(32 + bw) * PLD + 32 * (size_t)(33 + bw)) * sizeof(double);
   if ((32 + bw) * 32 <= CHOL_THREADS * CHOL_EPT && 32 + bw <= CHOL_THREADS && smem <= 220 * 1024) {
     CK(cudaFuncSetAttribute(k_band_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1204,6 +1904,8 @@ static void fork_filter(Ctx &c) {
   c.stream = main;
   setup_mark(c, 6, c.side);
   CK(cudaEventRecord(c.ev_join, c.side));
+  static const bool serial = getenv("AMGF_SERIAL_SETUP") != nullptr;  // A/B only: side stream alone, then main
+  if (serial) CK(cudaStreamWaitEvent(main, c.ev_join, 0));
 }
 static void join_filter(Ctx &c) {
   if (c.nc == 0) return;
@@ -1249,6 +1951,21 @@ struct LevelCache {
   int *AP_pptr = nullptr, *AP_pa = nullptr, *AP_pb = nullptr;
   int *G_pptr = nullptr, *G_pa = nullptr, *G_pb = nullptr;
   signed char *AP_off = nullptr, *G_off = nullptr;  // dense-over-row offset tables (k_spgemm_dense)
+  GalGrp *AP_grp = nullptr;  // row groups of k_gal_ap (fine level)
+  GalRun *AP_runs = nullptr;
+  int AP_ngrp = 0;
+  RapGrp *G_grp = nullptr;  // output groups of k_gal_rap (fine level)
+  int G_ngrp = 0;
+  long *G_gofs = nullptr;    // k_gal_rap2: group-contiguous offset rows and per-R-block AP row (start, length)
+  signed char *G_offg = nullptr;
+  int2 *G_rbi = nullptr;
+  unsigned *AP_hitw = nullptr;  // hit words of k_gal_hl
+  // smoothed P as the row-group product T = A*Pt (fine level): pairs, groups, hit words
+  int *P_pptr = nullptr, *P_pa = nullptr, *P_pb = nullptr;
+  GalGrp *P_grp = nullptr;
+  GalRun *P_runs = nullptr;
+  unsigned *P_hitw = nullptr;
+  int P_ngrp = 0;
 };
 
 static signed char *build_off(Ctx &c, long nnzc, const int *rowof, const int *ccol, const Bsr &A, const Bsr &B) {
@@ -1266,6 +1983,115 @@ static signed char *build_off(Ctx &c, long nnzc, const int *rowof, const int *cc
   signed char *off = c.alloc<signed char>((size_t)std::max(maxa, 1) * nnzc);
   LAUNCH(k_spgemm_off, nnzc, nnzc, rowof, ccol, A.ptr, A.col, B.ptr, B.col, maxa, off);
   return off;
+}
+
+// Row groups of k_gal_ap (symbolic, host, once per setup): greedy over consecutive rows of C = A*B.
+static void build_gal_groups(Ctx &c, const Bsr &A, const Bsr &B, const Bsr &C, const int *d_pptr, const int *d_pa,
+                             const int *d_pb, GalGrp *&d_grp, int &ngrp, GalRun *&d_runs, unsigned *&d_hitw) {
+  auto d2hv = [&](const int *src, size_t n) {
+    std::vector<int> h(n);
+    CK(cudaMemcpyAsync(h.data(), src, n * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    return h;
+  };
+  const std::vector<int> ap = d2hv(A.ptr, A.nbr + 1), ac = d2hv(A.col, A.nnzb), bp = d2hv(B.ptr, B.nbr + 1),
+                         cp = d2hv(C.ptr, C.nbr + 1), pp = d2hv(d_pptr, C.nnzb + 1);
+  CK(cudaStreamSynchronize(c.stream));
+  std::vector<GalGrp> grps;
+  std::vector<GalRun> runs;
+  std::vector<char> mark(B.nbr, 0);
+  std::vector<int> ul;
+  auto add_global = [&](int i) {  // one row through global memory, NT output blocks per group
+    for (int e = cp[i]; e < cp[i + 1]; e += GAL_NT)
+      grps.push_back(GalGrp{e, std::min(cp[i + 1], e + GAL_NT), ap[i], ap[i + 1], 0, -1, 0, 0});
+  };
+  const int n = A.nbr;
+  int i = 0;
+  while (i < n) {
+    const int i0 = i;
+    long pb = 0;
+    ul.clear();
+    while (i < n) {
+      const size_t m0 = ul.size();
+      long add = 0;
+      for (int k = ap[i]; k < ap[i + 1]; k++) {
+        const int j = ac[k];
+        if (!mark[j]) { mark[j] = 1; ul.push_back(j); add += bp[j + 1] - bp[j]; }
+      }
+      if (cp[i + 1] - cp[i0] > GAL_NT || ap[i + 1] - ap[i0] > GAL_ACAP || pb + add > GHL_PCAP ||
+          pp[cp[i + 1]] - pp[cp[i0]] > GHL_HCAP) {
+        for (size_t q = m0; q < ul.size(); q++) mark[ul[q]] = 0;
+        ul.resize(m0);
+        break;
+      }
+      pb += add;
+      i++;
+    }
+    for (int j : ul) mark[j] = 0;
+    if (i == i0) {  // the row alone exceeds a capacity
+      add_global(i);
+      i++;
+      continue;
+    }
+    std::sort(ul.begin(), ul.end());
+    const int r0 = (int)runs.size();
+    int base = 0;
+    for (size_t q = 0; q < ul.size();) {
+      size_t q1 = q + 1;
+      while (q1 < ul.size() && ul[q1] == ul[q1 - 1] + 1) q1++;
+      runs.push_back(GalRun{ul[q], ul[q1 - 1] + 1, base, 0});
+      base += bp[ul[q1 - 1] + 1] - bp[ul[q]];
+      q = q1;
+    }
+    if ((int)runs.size() - r0 > GAL_RCAP) {  // too fragmented for the run table: global path
+      runs.resize(r0);
+      for (int ii = i0; ii < i; ii++) add_global(ii);
+      continue;
+    }
+    grps.push_back(GalGrp{cp[i0], cp[i], ap[i0], ap[i], r0, (int)runs.size(), 0, 0});
+  }
+  ngrp = (int)grps.size();
+  d_grp = c.alloc<GalGrp>(std::max<size_t>(grps.size(), 1));
+  d_runs = c.alloc<GalRun>(std::max<size_t>(runs.size(), 1));
+  h2d(c, d_grp, grps.data(), grps.size());
+  h2d(c, d_runs, runs.data(), runs.size());
+  const long np = pp[C.nnzb];
+  d_hitw = c.alloc<unsigned>(np + 8);  // + 8: the groups' 16-byte aligned bulk copies may read past the end
+  if (ngrp) k_gal_hitw<<<ngrp, 128, 0, c.stream>>>(d_grp, d_runs, d_pptr, d_pa, d_pb, B.ptr, d_hitw);
+  CK(cudaStreamSynchronize(c.stream));
+}
+
+// Output groups of k_gal_rap: <= RAP_NT/2 output blocks of one row of G; every AP row must fit one stage.
+static void build_rap_groups(Ctx &c, const Bsr &G, const Bsr &R, const Bsr &AP, RapGrp *&d_grp, int &ngrp,
+                             long *&d_gofs, signed char *&d_offg, int2 *&d_rbi) {
+  std::vector<int> gp(G.nbr + 1), bp(AP.nbr + 1);
+  CK(cudaMemcpyAsync(gp.data(), G.ptr, gp.size() * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaMemcpyAsync(bp.data(), AP.ptr, bp.size() * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  for (int j = 0; j < AP.nbr; j++)
+    if (bp[j + 1] - bp[j] > RAP_SCAP) {  // k_gal_rap cannot stage this row: keep the dense-over-row kernel
+      d_grp = nullptr;
+      ngrp = 0;
+      return;
+    }
+  std::vector<RapGrp> grps;
+  for (int a = 0; a < G.nbr; a++)
+    for (int e = gp[a]; e < gp[a + 1]; e += RAP_NT / 2) grps.push_back(RapGrp{a, e, std::min(gp[a + 1], e + RAP_NT / 2), 0});
+  ngrp = (int)grps.size();
+  d_grp = c.alloc<RapGrp>(std::max<size_t>(grps.size(), 1));
+  h2d(c, d_grp, grps.data(), grps.size());
+  std::vector<int> rp(R.nbr + 1);
+  CK(cudaMemcpyAsync(rp.data(), R.ptr, rp.size() * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  std::vector<long> gofs(grps.size() + 1, 0);
+  for (size_t q = 0; q < grps.size(); q++) gofs[q + 1] = gofs[q] + 64L * (rp[grps[q].a + 1] - rp[grps[q].a]);
+  d_gofs = c.alloc<long>(gofs.size());
+  h2d(c, d_gofs, gofs.data(), gofs.size());
+  d_offg = c.alloc<signed char>(gofs.back() + 16);
+  if (ngrp)
+    k_rap_offg<<<ngrp, 256, 0, c.stream>>>(ngrp, d_grp, d_gofs, R.ptr, R.col, AP.ptr, AP.col, G.col, d_offg);
+  d_rbi = c.alloc<int2>(std::max<long>(R.nnzb, 1));
+  LAUNCH(k_rap_rbi, R.nnzb, R.nnzb, R.col, AP.ptr, d_rbi);
+  CK(cudaStreamSynchronize(c.stream));
 }
 
 static void build_pairs(Ctx &c, long nnzc, const int *rowof, const int *ccol, const Bsr &A, const Bsr &B, int *&pptr,
@@ -1314,7 +2140,22 @@ static void level_numeric(Ctx &c, int l, LevelCache &lc) {
     }
   }
   power_iteration(c, L);
-  if (L.b == 3)
+  static const bool gal_old = getenv("AMGF_GAL_OLD") != nullptr;  // A/B only: the thread-per-block kernels
+  if (L.b == 3 && lc.P_grp && !gal_old) {
+    constexpr size_t sm = ghl_smem(9, 18);
+    size_t &attr = device_slot((const void *)k_gal_hl<3, 3, 6, true>);
+    if (!attr) {
+      attr = 1;
+      CK(cudaFuncSetAttribute(k_gal_hl<3, 3, 6, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    }
+    GalEpi ep;
+    ep.C_col = L.P.col; ep.agg = L.agg; ep.Pt_ptr = L.Pt.ptr; ep.Ptv = L.Pt.val; ep.dpt = L.dpt; ep.omega = L.omega;
+    if (lc.P_ngrp)
+      k_gal_hl<3, 3, 6, true><<<lc.P_ngrp, GAL_NT, sm, c.stream>>>(lc.P_grp, lc.P_runs, lc.P_rowof, lc.P_pptr,
+                                                                   lc.P_hitw, lc.P_pa, lc.P_pb, L.A.val, L.Pt.ptr,
+                                                                   L.Pt.val, L.P.val, ep);
+    after_launch(c, "k_gal_hl<P>");
+  } else if (L.b == 3)
     LAUNCH(k_P_values<3>, L.P.nnzb, L.P.nnzb, lc.P_rowof, L.P.col, L.A.ptr, L.A.col, L.A.val, L.agg, L.Pt.ptr,
            L.Pt.val, L.dpt, L.omega, L.P.val);
   else
@@ -1330,10 +2171,37 @@ static void level_numeric(Ctx &c, int l, LevelCache &lc) {
     // levels the pair kernels are faster (level 1: 2.0 vs 2.5 ms)
     static const int dense = getenv("AMGF_SPGEMM_DENSE") ? atoi(getenv("AMGF_SPGEMM_DENSE")) : 1;  // A/B only
     if (dense && L.b == 3 && lc.AP_off) {
-      LAUNCH((k_spgemm_dense<3, 3, 6>), L.AP.nnzb, L.AP.nnzb, lc.AP_rowof, L.A.ptr, L.A.col, L.A.val, L.P.ptr,
-             L.P.val, lc.AP_off, L.AP.val);
-      LAUNCH((k_spgemm_dense<6, 3, 6>), lc.G.nnzb, lc.G.nnzb, lc.G_rowof, L.R.ptr, L.R.col, L.R.val, L.AP.ptr,
-             L.AP.val, lc.G_off, lc.G.val);
+      if (lc.AP_grp && !gal_old) {
+        constexpr size_t sm = ghl_smem(9, 18);
+        size_t &attr = device_slot((const void *)k_gal_hl<3, 3, 6>);
+        if (!attr) {
+          attr = 1;
+          CK(cudaFuncSetAttribute(k_gal_hl<3, 3, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        }
+        if (lc.AP_ngrp)
+          k_gal_hl<3, 3, 6><<<lc.AP_ngrp, GAL_NT, sm, c.stream>>>(lc.AP_grp, lc.AP_runs, lc.AP_rowof, lc.AP_pptr,
+                                                                   lc.AP_hitw, lc.AP_pa, lc.AP_pb, L.A.val, L.P.ptr,
+                                                                   L.P.val, L.AP.val);
+        after_launch(c, "k_gal_hl");
+      } else {
+        LAUNCH((k_spgemm_dense<3, 3, 6>), L.AP.nnzb, L.AP.nnzb, lc.AP_rowof, L.A.ptr, L.A.col, L.A.val, L.P.ptr,
+               L.P.val, lc.AP_off, L.AP.val);
+      }
+      if (lc.G_grp && !gal_old) {
+        constexpr size_t sm = (size_t)RAP_NS * RAP2_STAGE_B;
+        size_t &attr = device_slot((const void *)k_gal_rap2);
+        if (!attr) {
+          attr = 1;
+          CK(cudaFuncSetAttribute(k_gal_rap2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        }
+        if (lc.G_ngrp)
+          k_gal_rap2<<<lc.G_ngrp, RAP2_CONS + 32, sm, c.stream>>>(lc.G_grp, lc.G_gofs, L.R.ptr, lc.G_rbi, L.R.val,
+                                                                  L.AP.val, lc.G_offg, lc.G.val);
+        after_launch(c, "k_gal_rap2");
+      } else {
+        LAUNCH((k_spgemm_dense<6, 3, 6>), lc.G.nnzb, lc.G.nnzb, lc.G_rowof, L.R.ptr, L.R.col, L.R.val, L.AP.ptr,
+               L.AP.val, lc.G_off, lc.G.val);
+      }
     } else {
     // measured at cfg 3: thread per output block for the fine 3x3 * 3x6 product (3.0 vs 5.0 ms), warp per
     // output block for the 6-row products (2.6 vs 2.7 ms, 1.1 vs 1.7 ms)
@@ -1748,6 +2616,11 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
     if (L.b == 3) {  // fine level: dense-over-row products (k_spgemm_dense)
       lc.AP_off = build_off(c, L.AP.nnzb, lc.AP_rowof, L.AP.col, L.A, L.P);
       lc.G_off = build_off(c, lc.G.nnzb, lc.G_rowof, lc.G.col, L.R, L.AP);
+      build_gal_groups(c, L.A, L.P, L.AP, lc.AP_pptr, lc.AP_pa, lc.AP_pb, lc.AP_grp, lc.AP_ngrp, lc.AP_runs,
+                       lc.AP_hitw);
+      build_rap_groups(c, lc.G, L.R, L.AP, lc.G_grp, lc.G_ngrp, lc.G_gofs, lc.G_offg, lc.G_rbi);
+      build_pairs(c, L.P.nnzb, lc.P_rowof, L.P.col, L.A, L.Pt, lc.P_pptr, lc.P_pa, lc.P_pb);
+      build_gal_groups(c, L.A, L.Pt, L.P, lc.P_pptr, lc.P_pa, lc.P_pb, lc.P_grp, lc.P_ngrp, lc.P_runs, lc.P_hitw);
     }
     level_numeric(c, l, lc);
     check_dev_error(c, "Galerkin product");
