@@ -183,6 +183,8 @@ struct Ctx {
   double *dot_part = nullptr;
   double *pw_v = nullptr, *pw_w = nullptr;  // power-iteration work vectors (allocated once)
   double *pw_s = nullptr;                    // power-iteration scalars {w.w, v.v, lambda}
+  double *pw_part = nullptr;                 // power-iteration C14 partials of v.v (w.w go to dot_part)
+  double *pw_lev = nullptr;                  // per level {lambda, omega} on the device
   Scalars *sc = nullptr;      // device
   Scalars *sc_host = nullptr; // pinned
   int *err = nullptr;         // device [2]
@@ -269,7 +271,11 @@ void check_dev_error(Ctx &c, const char *where);
 
 // ------------------------------------------------------------------ solve kernels (solve.cu)
 enum SpmvMode { SPMV_Y = 0, SPMV_RESID = 1, SPMV_SMOOTH = 2, SPMV_DOT = 3, SPMV_SMOOTH_ADD = 4, SPMV_CHEB1 = 6,
-                SPMV_CHEB = 7 };
+                SPMV_CHEB = 7, SPMV_YDIV = 9, SPMV_POW = 10 };
+// power step (C18): w = (A v) / d; the fine level (3x3 SELL, one thread per block row = the C14 level-1
+// mapping) also forms the C14 level-1 partials of w.w into part_w and of v.v into part_v
+void launch_sell_pow(Ctx &c, const Sell &A, const double *v, const double *d, double *w, double *part_w,
+                     double *part_v);
 struct ChebArgs {  // Chebyshev step of the SpMV epilogue (solve.cu, contract C23)
   double ca = 0.0, cb = 0.0;
   double *dir = nullptr;
@@ -290,6 +296,9 @@ void launch_restrict(Ctx &c, const Bsr &R, const double *r, double *bc);
 void launch_prolong(Ctx &c, const Sell &P, const double *xc, double *x);
 void launch_dot(Ctx &c, long n, int b, const double *u, const double *v, int finish);
 void launch_dot_finish(Ctx &c, long n_partials, int finish);  // C14 level 2 over c.dot_part
+// power step (C18): C14 level-1 partials of w.w and v.v (block rows of b), and both level-2 sums into pw[0..1]
+void launch_pow_dots(Ctx &c, long nb, int b, const double *w, const double *v, double *part_w, double *part_v);
+void launch_pow_fin(Ctx &c, long n_partials, const double *part_w, const double *part_v, double *pw);
 void launch_axpy2(Ctx &c, long n, const double *p, const double *q, double *x, double *r);
 void launch_xpby(Ctx &c, long n, const double *z, double *p);
 // y = L^{-T} L^{-1} v[gather] (C10); if scatter: xout[scatter[a]] += y[a].  Band storage (row stride

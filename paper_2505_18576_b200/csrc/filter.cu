@@ -301,7 +301,10 @@ __global__ void __launch_bounds__(1024) k_nd_off_band(const int2 *pairs, const N
 template <bool SCHUR>
 __global__ void __launch_bounds__(256) k_nd_gemm(const int2 *pairs, const NdBlk *blk, int bw, int W, double *Lrow,
                                                  double *Loff) {
-  __shared__ double As[32][33], Bs[32][33];
+  // k-major chunks of 32 k for the 32 rows of each operand, double-buffered: the next chunk's cp.async copies
+  // are in flight while the current one is consumed (the chunk loads were the critical path: 8,317-term
+  // chains over 260 chunks at the top separator)
+  __shared__ __align__(16) double As[2][32][34], Bs[2][32][34];
   const int2 pr = pairs[blockIdx.x];
   const NdBlk S = blk[pr.x], Sp = blk[SCHUR ? pr.x : pr.y];
   const int ti = blockIdx.y, tj = blockIdx.z;  // tile row / column
@@ -325,24 +328,41 @@ __global__ void __launch_bounds__(256) k_nd_gemm(const int2 *pairs, const NdBlk 
       double *o = out(a, b);
       acc[a][b] = o ? *o : 0.0;
     }
-  for (int kc = k0; kc < k1; kc += 32) {
-    __syncthreads();
+  auto issue = [&](int kc, int buf) {  // element (r, k) of both operands, zero-filled outside
     for (int e = threadIdx.x; e < 32 * 32; e += 256) {
       const int r = e >> 5, k = e & 31;
       const bool kin = kc + k < k1;
-      As[k][r] = (kin && s0 + r < S.len) ? Arow[(long)(s0 + r) * S.rs + kc + k] : 0.0;
-      Bs[k][r] = (kin && j0 + r < Sp.len) ? Brow[(long)(j0 + r) * Sp.rs + kc + k] : 0.0;
+      const bool ai = kin && s0 + r < S.len, bi = kin && j0 + r < Sp.len;
+      const double *sa = ai ? Arow + (long)(s0 + r) * S.rs + kc + k : Arow;
+      const double *sb = bi ? Brow + (long)(j0 + r) * Sp.rs + kc + k : Brow;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(&As[buf][k][r])), "l"(sa),
+                   "r"(ai ? 8 : 0) : "memory");
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(&Bs[buf][k][r])), "l"(sb),
+                   "r"(bi ? 8 : 0) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  const int nch = (k1 - k0 + 31) / 32;
+  if (nch > 0) issue(k0, 0);
+  for (int m = 0; m < nch; m++) {
+    const int kc = k0 + 32 * m, buf = m & 1;
+    if (m + 1 < nch) {
+      issue(kc + 32, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
     const int kn = min(32, k1 - kc);
     for (int kk = 0; kk < kn; kk++) {
-      const double a0 = As[kk][2 * ty], a1 = As[kk][2 * ty + 1];
-      const double b0 = Bs[kk][2 * tx], b1 = Bs[kk][2 * tx + 1];
-      acc[0][0] = __fma_rn(-a0, b0, acc[0][0]);
-      acc[0][1] = __fma_rn(-a0, b1, acc[0][1]);
-      acc[1][0] = __fma_rn(-a1, b0, acc[1][0]);
-      acc[1][1] = __fma_rn(-a1, b1, acc[1][1]);
+      const double2 av = *reinterpret_cast<const double2 *>(&As[buf][kk][2 * ty]);
+      const double2 bv = *reinterpret_cast<const double2 *>(&Bs[buf][kk][2 * tx]);
+      acc[0][0] = __fma_rn(-av.x, bv.x, acc[0][0]);
+      acc[0][1] = __fma_rn(-av.x, bv.y, acc[0][1]);
+      acc[1][0] = __fma_rn(-av.y, bv.x, acc[1][0]);
+      acc[1][1] = __fma_rn(-av.y, bv.y, acc[1][1]);
     }
+    __syncthreads();
   }
 #pragma unroll
   for (int a = 0; a < 2; a++)

@@ -218,6 +218,42 @@ __global__ void k_S_values(long nnzb, const int *S_rowof, const int *S_col, cons
 }
 
 // ------------------------------------------------------------------ s2: I_c and Z
+// Fine-level SELL refresh fused with the l1 / point diagonals (same values as k_sell_vals + k_diag): one
+// thread per block row I (the SELL-32 row, natural order at level 0) streams its BSR blocks in order, stores
+// them to the SELL copy (one 256-byte segment per component across the 32 rows of a slice) and forms the
+// diagonals (C3) from the same loads.
+__global__ void __launch_bounds__(CTA) k_sell_diag(int nodes, const int *__restrict__ S_ptr,
+                                                   const int *__restrict__ S_col, const double *__restrict__ S_val,
+                                                   const int *__restrict__ slice_ptr, double *__restrict__ sval,
+                                                   double *__restrict__ dl1, double *__restrict__ dpt) {
+  const int I = blockIdx.x * CTA + threadIdx.x;
+  if (I >= nodes) return;
+  const int lane = I & 31;
+  const long sbase = slice_ptr[I >> 5];
+  const int e0 = S_ptr[I], e1 = S_ptr[I + 1];
+  double d[3] = {0.0, 0.0, 0.0}, dp[3] = {0.0, 0.0, 0.0};
+  for (int e = e0; e < e1; e++) {
+    const int Jn = S_col[e];
+    double v[9];
+#pragma unroll
+    for (int q = 0; q < 9; q++) v[q] = S_val[(long)e * 9 + q];
+    const long slot = sbase + (e - e0);
+#pragma unroll
+    for (int q = 0; q < 9; q++) sval[(slot * 9 + q) * 32 + lane] = v[q];
+#pragma unroll
+    for (int r = 0; r < 3; r++)
+#pragma unroll
+      for (int cc = 0; cc < 3; cc++) {
+        d[r] = d[r] + fabs(v[3 * r + cc]);
+        if (Jn == I && cc == r) dp[r] = v[3 * r + cc];
+      }
+  }
+#pragma unroll
+  for (int r = 0; r < 3; r++) {
+    dl1[3L * I + r] = d[r];
+    dpt[3L * I + r] = dp[r];
+  }
+}
 __global__ void k_mark_cols(int nnz, const int *J_col, int *mark) {
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e < nnz) mark[J_col[e]] = 1;
@@ -856,13 +892,16 @@ __global__ void k_scale_div(long n, const double *w, double s, double *v) {
   long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
   if (i < n) v[i] = w[i] / s;
 }
-// power step on the device (C18): pw[0] = w.w, pw[1] = v.v (copied from the dot result); ||w|| = sqrt(pw[0]),
+// power step on the device (C18): pw[0] = w.w, pw[1] = v.v (k_pow_fin); ||w|| = sqrt(pw[0]),
 // lambda = ||w|| / sqrt(pw[1]) into pw[2]; v = w / ||w|| -- the host's formulas, no host round trip
-__global__ void k_pow_keep(const Scalars *sc, double *pw, int slot) { pw[slot] = sc->dot; }
 __global__ void k_pow_scale(long n, const double *w, double *pw, double *v) {
   const double nw = sqrt(pw[0]);
   long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
-  if (i == 0) pw[2] = nw / sqrt(pw[1]);
+  if (i == 0) {
+    const double lam = nw / sqrt(pw[1]);
+    pw[2] = lam;
+    pw[3] = 4.0 / (3.0 * lam);  // R6: the prolongator damping omega (the host formula, in fp64)
+  }
   if (i < n) v[i] = w[i] / nw;
 }
 
@@ -894,7 +933,8 @@ __global__ void k_P_fill(int nodes, const int *ptr, const int *col, const int *a
 template <int B>
 __global__ void k_P_values(long nnzb, const int *P_rowof, const int *P_col, const int *A_ptr, const int *A_col,
                            const double *A_val, const int *agg, const int *Pt_ptr, const double *Ptv,
-                           const double *dpt, double omega, double *Pv) {
+                           const double *dpt, const double *omega_p, double *Pv, const int *Rinv, double *Rv) {
+  const double omega = *omega_p;  // 4 / (3 lambda) of this level, formed on the device (k_pow_scale)
   long e = blockIdx.x * (long)blockDim.x + threadIdx.x;
   if (e >= nnzb) return;
   const int i = P_rowof[e], a = P_col[e];
@@ -922,7 +962,12 @@ __global__ void k_P_values(long nnzb, const int *P_rowof, const int *P_col, cons
       t = t / dpt[(long)i * B + r];
       const double pt = own ? Ptv[((long)Pt_ptr[i] * B + r) * 6 + s] : 0.0;
       Pv[(e * B + r) * 6 + s] = pt - t;
+      if (Rinv) Rv[((long)Rinv[e] * 6 + s) * B + r] = pt - t;  // R = P^T: its block Rinv[e], transposed
     }
+}
+__global__ void k_inv_perm(long n, const int *perm, int *inv) {
+  long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (t < n) inv[perm[t]] = (int)t;
 }
 
 // ------------------------------------------------------------------ s7: transpose, SpGEMMs, symmetrisation
@@ -941,13 +986,6 @@ __global__ void k_interleave_rows(int nbr, const int *__restrict__ ptr, int bs, 
   }
 }
 
-__global__ void k_transpose_vals(long nnzb, int br, int bc, const int *perm, const double *src, double *dst) {
-  long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
-  if (t >= nnzb) return;
-  const long s = perm[t];
-  for (int r = 0; r < br; r++)
-    for (int cc = 0; cc < bc; cc++) dst[(t * bc + cc) * br + r] = src[(s * br + r) * bc + cc];
-}
 
 constexpr int GCAP = 512;
 // symbolic C = A*B: row i's pattern = union of B rows over A's columns
@@ -1020,6 +1058,50 @@ __global__ void k_spgemm_vals_pairs(long nnzc, const int *pptr, const int *pa, c
   }
 #pragma unroll
   for (int q = 0; q < BR * BC; q++) C_val[e * BR * BC + q] = acc[q];
+}
+
+// Same products, two threads per 6 x 6 output block (rows 0-2 / 3-5, 18 accumulators each): per block pair
+// a thread loads its three contiguous A rows (144 bytes) and the whole B block (288 bytes, shared with its
+// partner), 108 FMAs per 54 loads (the warp form above: 6 FMAs per 12 loads).  Per entry the order is C20's.
+__global__ void __launch_bounds__(CTA) k_spgemm_vals_half6(long nnzc, const int *__restrict__ pptr,
+                                                           const int *__restrict__ pa, const int *__restrict__ pb,
+                                                           const double *__restrict__ A_val,
+                                                           const double *__restrict__ B_val,
+                                                           double *__restrict__ C_val) {
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  const long e = t >> 1;
+  const int h = (int)(t & 1);
+  if (e >= nnzc) return;
+  double acc[18];
+#pragma unroll
+  for (int u = 0; u < 18; u++) acc[u] = 0.0;
+  const int q1 = pptr[e + 1];
+  for (int q = pptr[e]; q < q1; q++) {
+    const double2 *Av = reinterpret_cast<const double2 *>(A_val + (long)pa[q] * 36 + 18 * h);
+    const double2 *Bv = reinterpret_cast<const double2 *>(B_val + (long)pb[q] * 36);
+    double a[18], bb[36];
+#pragma unroll
+    for (int u = 0; u < 9; u++) {
+      const double2 v = __ldg(Av + u);
+      a[2 * u] = v.x;
+      a[2 * u + 1] = v.y;
+    }
+#pragma unroll
+    for (int u = 0; u < 18; u++) {
+      const double2 v = __ldg(Bv + u);
+      bb[2 * u] = v.x;
+      bb[2 * u + 1] = v.y;
+    }
+#pragma unroll
+    for (int r = 0; r < 3; r++)
+#pragma unroll
+      for (int s2 = 0; s2 < 6; s2++)
+#pragma unroll
+        for (int k = 0; k < 6; k++) acc[r * 6 + s2] = __fma_rn(a[r * 6 + k], bb[k * 6 + s2], acc[r * 6 + s2]);
+  }
+  double2 *Cv = reinterpret_cast<double2 *>(C_val + e * 36 + 18 * h);
+#pragma unroll
+  for (int u = 0; u < 9; u++) Cv[u] = make_double2(acc[2 * u], acc[2 * u + 1]);
 }
 
 // Same products, one warp per output block: lane e owns entries e, e+32, .. of the BR x BC block, so the
@@ -1115,188 +1197,75 @@ __global__ void __launch_bounds__(CTA) k_spgemm_dense(long nnzc, const int *__re
   for (int q = 0; q < BR * BC; q++) C_val[e * BR * BC + q] = acc[q];
 }
 
-// Row-group form of the fine-level A*P (same products, same chains as k_spgemm_dense; C20).  A CTA owns a
-// group of consecutive output rows (symbolic, built once on the host: at most NT output blocks, ACAP blocks
-// of A, PCAP blocks of the union of the P rows those A rows reference).  The group's A values (one
-// contiguous segment) and the union of its P rows (runs of consecutive rows: contiguous segments) are
-// TMA bulk-copied into shared memory once; the neighbouring rows of a lattice share most of their P rows,
-// so every P row is read from L2 about 2.5x less often than once per A block.  Then thread e = output block
-// C_ib walks A's row i in ascending order as before, A and B blocks from shared memory.  Groups whose rows
-// exceed the capacity (none at cfg 0-4) read the operands from global memory instead.
+// Row-group form of the fine-level A*P (same products, same chains as k_spgemm_dense; C20).  A group is a run
+// of consecutive output rows (symbolic, built once on the host: at most GAL_NT output blocks, GAL_ACAP blocks
+// of A, GHL_PCAP blocks of the union of the P rows those A rows reference, GHL_HCAP block products).  The
+// group's A values (one contiguous segment) and the union of its P rows (runs of consecutive rows: contiguous
+// segments) are TMA bulk-copied into shared memory once; neighbouring lattice rows share most of their P
+// rows, so a P row is read from L2 about 2.5x less often than once per A block.  Groups whose rows exceed
+// the capacities (none at cfg 0-4) read the operands from global memory instead.
 struct GalGrp {
   int e0, e1;      // output blocks [e0, e1)
-  int a0, a1;      // A blocks [a0, a1) (rows of the group, contiguous)
-  int r0, r1;      // runs [r0, r1) of the P-row union; r1 < 0: operands from global memory
-  int pad0, pad1;
+  int a0;          // first A block of the group
+  int c0, c1;      // copy descriptors [c0, c1) (c1 == c0: operands from global memory)
+  unsigned tx;     // bytes of all copies (mbarrier transaction count)
+  int q0, pad;     // first block-product word of the group
 };
 struct GalRun {
   int j0, j1;  // P rows [j0, j1)
   int base;    // first shared-memory block of the run
   int pad;
 };
-constexpr int GAL_NT = 64, GAL_ACAP = 176, GAL_PCAP = 288, GAL_RCAP = 64;
-// PEPI: the smoothed prolongator's epilogue (C19) instead of storing T = A*Pt: P_ia = Pt_ia - (omega T_ia)/d_i
-struct GalEpi {
-  const int *C_col = nullptr, *agg = nullptr, *Pt_ptr = nullptr;
-  const double *Ptv = nullptr, *dpt = nullptr;
-  double omega = 0.0;
+struct GalCopy {  // one TMA bulk copy of a group: source byte offset in array `id`, destination in the buffer
+  long long src;
+  int dst;
+  unsigned bytes_id;  // bytes | id << 28 (0: A values, 1: hit words, 2: word offsets, 3: B values)
 };
-template <int BR, int IN, int BC, bool PEPI = false>
-__global__ void __launch_bounds__(GAL_NT) k_gal_ap(const GalGrp *__restrict__ grp, const GalRun *__restrict__ runs,
-                                                  long nnzc, const int *__restrict__ C_rowof,
-                                                  const int *__restrict__ A_ptr, const int *__restrict__ A_col,
-                                                  const double *__restrict__ A_val, const int *__restrict__ B_ptr,
-                                                  const double *__restrict__ B_val,
-                                                  const signed char *__restrict__ off, double *__restrict__ C_val,
-                                                  GalEpi ep = GalEpi{}) {
-  constexpr int AB = BR * IN, BB = IN * BC;
-  extern __shared__ __align__(128) double gsm[];
-  double *Bs = gsm;                                // [GAL_PCAP][BB]
-  double *As = gsm + GAL_PCAP * BB;                // [GAL_ACAP * AB + 2] (16-byte aligned copy, shifted)
-  int *pofs = (int *)(As + GAL_ACAP * AB + 2);     // [GAL_ACAP] P-row block offset of each A block
-  __shared__ GalRun rs[GAL_RCAP];
-  __shared__ __align__(8) uint64_t bar;
-  const GalGrp g = grp[blockIdx.x];
-  const int tid = threadIdx.x;
-  const bool staged = g.r1 >= 0;
-  int ashift = 0;
-  if (staged) {
-    const long abeg = (long)g.a0 * AB * 8, aend = (long)g.a1 * AB * 8;
-    const long abeg16 = abeg & ~15L, aend16 = (aend + 15) & ~15L;
-    ashift = (int)(abeg - abeg16) / 8;
-    if (tid == 0) {
-      mbar_init(&bar, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      unsigned bytes = (unsigned)(aend16 - abeg16);
-      for (int r = g.r0; r < g.r1; r++) {
-        const GalRun q = runs[r];
-        bytes += (unsigned)(B_ptr[q.j1] - B_ptr[q.j0]) * BB * 8;
-      }
-      mbar_arrive_expect(&bar, bytes);
-      bulk_g2s(As, (const char *)A_val + abeg16, (unsigned)(aend16 - abeg16), &bar);
-      for (int r = g.r0; r < g.r1; r++) {
-        const GalRun q = runs[r];
-        const unsigned nb = (unsigned)(B_ptr[q.j1] - B_ptr[q.j0]);
-        if (nb) bulk_g2s(Bs + (long)q.base * BB, B_val + (long)B_ptr[q.j0] * BB, nb * BB * 8, &bar);
-      }
-    }
-    for (int r = tid; r < g.r1 - g.r0; r += GAL_NT) rs[r] = runs[g.r0 + r];
-    __syncthreads();
-    const int nr = g.r1 - g.r0;
-    for (int k = g.a0 + tid; k < g.a1; k += GAL_NT) {
-      const int j = A_col[k];
-      int r = 0;
-      while (r + 1 < nr && rs[r + 1].j0 <= j) r++;
-      pofs[k - g.a0] = rs[r].base + (B_ptr[j] - B_ptr[rs[r].j0]);
-    }
-    __syncthreads();
-    mbar_wait(&bar, 0);
-  }
-  const long e = (long)g.e0 + tid;
-  if (e >= g.e1) return;
-  const int i = C_rowof[e];
-  const int a0 = A_ptr[i], la = A_ptr[i + 1] - a0;
-  double acc[BR * BC];
-#pragma unroll
-  for (int q = 0; q < BR * BC; q++) acc[q] = 0.0;
-  int o = la > 0 ? off[e] : -1;
-  for (int t = 0; t < la; t++) {
-    const int on = (t + 1 < la) ? off[(long)(t + 1) * nnzc + e] : -1;
-    if (o >= 0) {
-      const int ka = a0 + t;
-      const double *Av, *Bv;
-      if (staged) {
-        Av = As + ashift + (long)(ka - g.a0) * AB;
-        Bv = Bs + (long)(pofs[ka - g.a0] + o) * BB;
-      } else {
-        Av = A_val + (long)ka * AB;
-        Bv = B_val + (long)(B_ptr[A_col[ka]] + o) * BB;
-      }
-      double a[AB], bb[BB];
-#pragma unroll
-      for (int u = 0; u < AB; u++) a[u] = Av[u];
-#pragma unroll
-      for (int u = 0; u < BB / 2; u++) {
-        const double2 v = reinterpret_cast<const double2 *>(Bv)[u];
-        bb[2 * u] = v.x;
-        bb[2 * u + 1] = v.y;
-      }
-#pragma unroll
-      for (int r = 0; r < BR; r++)
-#pragma unroll
-        for (int c = 0; c < BC; c++)
-#pragma unroll
-          for (int t2 = 0; t2 < IN; t2++) acc[r * BC + c] = __fma_rn(a[r * IN + t2], bb[t2 * BC + c], acc[r * BC + c]);
-    }
-    o = on;
-  }
-  if constexpr (PEPI) {
-    const bool own = ep.agg[i] == ep.C_col[e];
-#pragma unroll
-    for (int r = 0; r < BR; r++)
-#pragma unroll
-      for (int c = 0; c < BC; c++) {
-        double t = ep.omega * acc[r * BC + c];
-        t = t / ep.dpt[(long)i * BR + r];
-        const double pt = own ? ep.Ptv[((long)ep.Pt_ptr[i] * BR + r) * BC + c] : 0.0;
-        C_val[e * BR * BC + r * BC + c] = pt - t;
-      }
-  } else {
-#pragma unroll
-    for (int q = 0; q < BR * BC; q++) C_val[e * BR * BC + q] = acc[q];
-  }
-}
-// Hit-list form of the row-group product (same products, same chains; C20): the symbolic phase turns each
-// output block's block-product pairs (A block, B block; ascending A position) into 32-bit words
-// (A block within the group's staged A segment | B block within the staged P-row union << 8), and the
-// group's words and per-output word offsets are bulk-copied with the operands.  A thread then runs exactly
-// its hits, operands and indices from shared memory (k_gal_ap walks every A position and tests an offset
-// table in global memory).
+constexpr int GAL_NT = 64, GAL_ACAP = 176, GAL_RCAP = 28;
+// Hit lists: the symbolic phase turns each output block's block-product pairs (A block, B block; ascending A
+// position) into 32-bit words (A block within the group's staged A segment | B block within the staged P-row
+// union << 8); the group's words and per-output word offsets are bulk-copied with the operands, and thread
+// e = output block C_ib runs exactly its products, operands and indices from shared memory.
 constexpr int GHL_PCAP = 256, GHL_HCAP = 1024;
-template <int BR, int IN, int BC, bool PEPI = false>
-__global__ void __launch_bounds__(GAL_NT) k_gal_hl(const GalGrp *__restrict__ grp, const GalRun *__restrict__ runs,
-                                                  const int *__restrict__ C_rowof, const int *__restrict__ pptr,
-                                                  const unsigned *__restrict__ hitw, const int *__restrict__ pa,
-                                                  const int *__restrict__ pb, const double *__restrict__ A_val,
-                                                  const int *__restrict__ B_ptr, const double *__restrict__ B_val,
-                                                  double *__restrict__ C_val, GalEpi ep = GalEpi{}) {
+__host__ __device__ constexpr size_t ghl_buf_bytes(int AB, int BB) {  // one group buffer: B union, A segment, hit words, word offsets
+  return (((size_t)GHL_PCAP * BB + (size_t)GAL_ACAP * AB + 2) * 8 + (GHL_HCAP + 8) * 4 + (GAL_NT + 1 + 8) * 4 + 127) &
+         ~(size_t)127;  // 128-byte aligned buffers (TMA destinations, 16-byte vector loads)
+}
+// One CTA per group (4 CTAs per SM): warp 1 issues the group's TMA copies (precomputed descriptors, one per
+// lane), then every thread runs its output block's products from shared memory.
+template <int BR, int IN, int BC>
+__global__ void __launch_bounds__(GAL_NT) k_gal_hl(const GalGrp *__restrict__ grp, const GalCopy *__restrict__ cps,
+                                                  const int *__restrict__ pptr, const unsigned *__restrict__ hitw,
+                                                  const int *__restrict__ pa, const int *__restrict__ pb,
+                                                  const double *__restrict__ A_val, const double *__restrict__ B_val,
+                                                  double *__restrict__ C_val) {
   constexpr int AB = BR * IN, BB = IN * BC;
-  extern __shared__ __align__(128) double gsm[];
-  double *Bs = gsm;                                             // [GHL_PCAP][BB]
-  double *As = Bs + GHL_PCAP * BB;                              // [GAL_ACAP * AB + 2]
-  unsigned *Hs = reinterpret_cast<unsigned *>(As + GAL_ACAP * AB + 2);  // [GHL_HCAP + 8]
-  int *Ps = reinterpret_cast<int *>(Hs + GHL_HCAP + 8);         // [GAL_NT + 1 + 8]
+  extern __shared__ __align__(128) unsigned char hsm[];
   __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x, lane = tid & 31;
+  double *Bs = reinterpret_cast<double *>(hsm);
+  double *As = Bs + GHL_PCAP * BB;
+  unsigned *Hs = reinterpret_cast<unsigned *>(As + GAL_ACAP * AB + 2);
+  int *Ps = reinterpret_cast<int *>(Hs + GHL_HCAP + 8);
   const GalGrp g = grp[blockIdx.x];
-  const int tid = threadIdx.x;
-  const bool staged = g.r1 >= 0;
-  int ashift = 0, hshift = 0, pshift = 0, q0 = 0;
+  const bool staged = g.c1 > g.c0;
   if (staged) {
-    q0 = pptr[g.e0];
-    const int q1 = pptr[g.e1];
-    const long abeg = (long)g.a0 * AB * 8, aend = (long)g.a1 * AB * 8;
-    const long abeg16 = abeg & ~15L, aend16 = (aend + 15) & ~15L;
-    ashift = (int)(abeg - abeg16) / 8;
-    const long hb = (long)q0 * 4 & ~15L, he = ((long)q1 * 4 + 15) & ~15L;
-    hshift = q0 & 3;
-    const long pbeg = (long)g.e0 * 4 & ~15L, pend = ((long)(g.e1 + 1) * 4 + 15) & ~15L;
-    pshift = g.e0 & 3;
     if (tid == 0) {
       mbar_init(&bar, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      unsigned bytes = (unsigned)(aend16 - abeg16 + he - hb + pend - pbeg);
-      for (int r = g.r0; r < g.r1; r++) bytes += (unsigned)(B_ptr[runs[r].j1] - B_ptr[runs[r].j0]) * BB * 8;
-      mbar_arrive_expect(&bar, bytes);
-      bulk_g2s(As, (const char *)A_val + abeg16, (unsigned)(aend16 - abeg16), &bar);
-      if (he > hb) bulk_g2s(Hs, (const char *)hitw + hb, (unsigned)(he - hb), &bar);
-      bulk_g2s(Ps, (const char *)pptr + pbeg, (unsigned)(pend - pbeg), &bar);
-      for (int r = g.r0; r < g.r1; r++) {
-        const GalRun q = runs[r];
-        const unsigned nb = (unsigned)(B_ptr[q.j1] - B_ptr[q.j0]);
-        if (nb) bulk_g2s(Bs + (long)q.base * BB, B_val + (long)B_ptr[q.j0] * BB, nb * BB * 8, &bar);
-      }
     }
     __syncthreads();
+    if (tid >= 32) {
+      if (lane == 0) mbar_arrive_expect(&bar, g.tx);
+      __syncwarp();
+      for (int k = g.c0 + lane; k < g.c1; k += 32) {
+        const GalCopy cp = cps[k];
+        const unsigned id = cp.bytes_id >> 28, bytes = cp.bytes_id & 0x0fffffffu;
+        const char *base = id == 0 ? (const char *)A_val : id == 1 ? (const char *)hitw : id == 2 ? (const char *)pptr
+                                                                                                : (const char *)B_val;
+        bulk_g2s(hsm + cp.dst, base + cp.src, bytes, &bar);
+      }
+    }
     mbar_wait(&bar, 0);
   }
   const long e = (long)g.e0 + tid;
@@ -1322,6 +1291,8 @@ __global__ void __launch_bounds__(GAL_NT) k_gal_hl(const GalGrp *__restrict__ gr
         for (int t2 = 0; t2 < IN; t2++) acc[r * BC + c] = __fma_rn(a[r * IN + t2], bb[t2 * BC + c], acc[r * BC + c]);
   };
   if (staged) {
+    const int q0 = g.q0;
+    const int ashift = (int)(((long)g.a0 * AB * 8) & 15L) / 8, hshift = q0 & 3, pshift = g.e0 & 3;
     const int h0 = Ps[pshift + tid] - q0, h1 = Ps[pshift + tid + 1] - q0;
     for (int h = h0; h < h1; h++) {
       const unsigned w = Hs[hshift + h];
@@ -1330,38 +1301,23 @@ __global__ void __launch_bounds__(GAL_NT) k_gal_hl(const GalGrp *__restrict__ gr
   } else {
     for (int q = pptr[e]; q < pptr[e + 1]; q++) hit(A_val + (long)pa[q] * AB, B_val + (long)pb[q] * BB);
   }
-  const int i = C_rowof[e];
-  if constexpr (PEPI) {
-    const bool own = ep.agg[i] == ep.C_col[e];
 #pragma unroll
-    for (int r = 0; r < BR; r++)
-#pragma unroll
-      for (int c = 0; c < BC; c++) {
-        double t = ep.omega * acc[r * BC + c];
-        t = t / ep.dpt[(long)i * BR + r];
-        const double pt = own ? ep.Ptv[((long)ep.Pt_ptr[i] * BR + r) * BC + c] : 0.0;
-        C_val[e * BR * BC + r * BC + c] = pt - t;
-      }
-  } else {
-#pragma unroll
-    for (int q = 0; q < BR * BC; q++) C_val[e * BR * BC + q] = acc[q];
-  }
+  for (int q = 0; q < BR * BC; q++) C_val[e * BR * BC + q] = acc[q];
 }
-constexpr size_t ghl_smem(int AB, int BB) {
-  return ((size_t)GHL_PCAP * BB + (size_t)GAL_ACAP * AB + 2) * 8 + (GHL_HCAP + 8) * 4 + (GAL_NT + 1 + 8) * 4;
-}
-// hit words of the staged groups (symbolic, once per setup)
-__global__ void k_gal_hitw(const GalGrp *__restrict__ grp, const GalRun *__restrict__ runs,
-                           const int *__restrict__ pptr, const int *__restrict__ pa, const int *__restrict__ pb,
-                           const int *__restrict__ B_ptr, unsigned *__restrict__ hitw) {
+
+// hit words of the staged groups (symbolic, once per setup); grun[g] = the group's run range (empty: global)
+__global__ void k_gal_hitw(const GalGrp *__restrict__ grp, const int2 *__restrict__ grun,
+                           const GalRun *__restrict__ runs, const int *__restrict__ pptr, const int *__restrict__ pa,
+                           const int *__restrict__ pb, const int *__restrict__ B_ptr, unsigned *__restrict__ hitw) {
   const GalGrp g = grp[blockIdx.x];
-  if (g.r1 < 0) return;
-  const int nr = g.r1 - g.r0;
+  const int2 rr = grun[blockIdx.x];
+  if (rr.y <= rr.x) return;
+  const int nr = rr.y - rr.x;
   for (int q = pptr[g.e0] + threadIdx.x; q < pptr[g.e1]; q += blockDim.x) {
     const int b = pb[q];
     int r = 0;
-    while (r + 1 < nr && B_ptr[runs[g.r0 + r + 1].j0] <= b) r++;
-    const GalRun run = runs[g.r0 + r];
+    while (r + 1 < nr && B_ptr[runs[rr.x + r + 1].j0] <= b) r++;
+    const GalRun run = runs[rr.x + r];
     hitw[q] = (unsigned)(pa[q] - g.a0) | ((unsigned)(run.base + b - B_ptr[run.j0]) << 8);
   }
 }
@@ -1369,123 +1325,13 @@ __global__ void k_gal_hitw(const GalGrp *__restrict__ grp, const GalRun *__restr
 // Fine-level G = R * AP (R = P^T, 6x3 blocks; AP 3x6), streamed form of k_spgemm_dense<6,3,6> (C20, same
 // chains).  A CTA owns <= 64 output blocks of one coarse row a; two threads per output block (rows 0-2 /
 // 3-5 of the 6x6 block, 18 accumulators each).  R's row a is walked in ascending order in chunks of <= 16
-// positions; warp 0 stages each chunk (the R blocks: one contiguous segment; the AP row of each position:
-// one segment each) with TMA bulk copies into a 3-stage shared-memory ring, mbarrier completion, while the
-// CTA consumes the previous chunk.
+// positions (at most RAP_SCAP AP blocks), each staged into a 3-stage shared-memory ring by TMA bulk copies.
 struct RapGrp {
   int a, e0, e1, pad;
 };
-constexpr int RAP_NT = 128, RAP_TC = 16, RAP_SCAP = 104, RAP_NS = 3;
+constexpr int RAP_NT = 128, RAP_TC = 16, RAP_SCAP = 104, RAP_NS = 3;  // RAP_NT: consumer threads
 constexpr int RAP_STAGE = (RAP_TC + RAP_SCAP) * 18;  // doubles per stage
-__global__ void __launch_bounds__(RAP_NT) k_gal_rap(const RapGrp *__restrict__ grp, long nnzc,
-                                                   const int *__restrict__ R_ptr, const int *__restrict__ R_col,
-                                                   const double *__restrict__ R_val, const int *__restrict__ B_ptr,
-                                                   const double *__restrict__ B_val,
-                                                   const signed char *__restrict__ off, double *__restrict__ C_val) {
-  extern __shared__ __align__(128) double rsm[];  // [RAP_NS][RAP_STAGE]: R blocks, then AP blocks
-  __shared__ int meta[RAP_NS][RAP_TC + 2];         // per stage: AP block base of each position, count, t0
-  __shared__ __align__(8) uint64_t full[RAP_NS];
-  const RapGrp g = grp[blockIdx.x];
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int ra0 = R_ptr[g.a], lr = R_ptr[g.a + 1] - ra0;
-  int next_t = 0;  // producer state (warp 0, warp-uniform)
-  // warp 0: stage the chunk starting at next_t into stage s (an empty chunk marks the end)
-  auto produce = [&](int s) {
-    const int p = lane;
-    const bool in = p < RAP_TC && next_t + p < lr;
-    int j = 0, nb = 0;
-    if (in) {
-      j = R_col[ra0 + next_t + p];
-      nb = B_ptr[j + 1] - B_ptr[j];
-    }
-    int incl = nb;  // inclusive prefix of AP blocks
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= d) incl += v;
-    }
-    const bool take = in && incl <= RAP_SCAP;
-    const int tc = __popc(__ballot_sync(0xffffffffu, take));  // takes are a prefix of the lanes
-    const int nbt = __shfl_sync(0xffffffffu, incl, max(tc - 1, 0)) * (tc > 0);
-    double *st = rsm + (long)s * RAP_STAGE;
-    if (take) meta[s][p] = incl - nb;
-    if (lane == 0) {
-      meta[s][RAP_TC] = tc;
-      meta[s][RAP_TC + 1] = next_t;
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive_expect(&full[s], (unsigned)(tc + nbt) * 144u);
-    __syncwarp();
-    if (tc > 0) {
-      if (lane == 0) bulk_g2s(st, R_val + (long)(ra0 + next_t) * 18, (unsigned)tc * 144u, &full[s]);
-      if (take && nb > 0)
-        bulk_g2s(st + (RAP_TC + incl - nb) * 18, B_val + (long)B_ptr[j] * 18, (unsigned)nb * 144u, &full[s]);
-    }
-    next_t += tc;
-  };
-  if (tid == 0) {
-#pragma unroll
-    for (int s = 0; s < RAP_NS; s++) mbar_init(&full[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (tid < 32) {
-#pragma unroll
-    for (int s = 0; s < RAP_NS; s++) produce(s);
-  }
-  const int ob = tid >> 1, h = tid & 1;
-  const long e = (long)g.e0 + ob;
-  const bool act = e < g.e1;
-  double acc[18];
-#pragma unroll
-  for (int q = 0; q < 18; q++) acc[q] = 0.0;
-  for (int q = 0;; q++) {
-    const int s = q % RAP_NS;
-    mbar_wait(&full[s], (q / RAP_NS) & 1);
-    const int tc = meta[s][RAP_TC], t0 = meta[s][RAP_TC + 1];
-    if (tc == 0) break;
-    const double *st = rsm + (long)s * RAP_STAGE;
-    if (act) {
-      int o = off[(long)t0 * nnzc + e];
-      for (int p = 0; p < tc; p++) {
-        const int on = (p + 1 < tc) ? off[(long)(t0 + p + 1) * nnzc + e] : -1;
-        if (o >= 0) {
-          const double *Rv = st + p * 18 + h * 9;  // rows 3h..3h+2 of the 6x3 block
-          const double2 *Bv = reinterpret_cast<const double2 *>(st + (RAP_TC + meta[s][p] + o) * 18);
-          double a[9], bb[18];
-#pragma unroll
-          for (int u = 0; u < 9; u++) a[u] = Rv[u];
-#pragma unroll
-          for (int u = 0; u < 9; u++) {
-            const double2 v = Bv[u];
-            bb[2 * u] = v.x;
-            bb[2 * u + 1] = v.y;
-          }
-#pragma unroll
-          for (int r = 0; r < 3; r++)
-#pragma unroll
-            for (int c2 = 0; c2 < 6; c2++)
-#pragma unroll
-              for (int t2 = 0; t2 < 3; t2++) acc[r * 6 + c2] = __fma_rn(a[r * 3 + t2], bb[t2 * 6 + c2], acc[r * 6 + c2]);
-        }
-        o = on;
-      }
-    }
-    __syncthreads();  // stage s consumed
-    if (tid < 32) {
-      fence_proxy_async();
-      produce(s);
-    }
-  }
-  if (act) {
-#pragma unroll
-    for (int r = 0; r < 3; r++)
-#pragma unroll
-      for (int c2 = 0; c2 < 6; c2++) C_val[e * 36 + (3 * h + r) * 6 + c2] = acc[r * 6 + c2];
-  }
-}
-
-// Warp-specialised form of k_gal_rap (same chains): warp 4 is the producer (chunk plan from the per-R-block
+// Warp-specialised streamed form (same chains): warp 4 is the producer (chunk plan from the per-R-block
 // (AP row start, length) table, TMA bulk copies of the R blocks, the AP rows and the chunk's rows of the
 // group-contiguous offset table into a 3-stage ring, full/empty mbarriers); warps 0-3 consume: offsets,
 // R and AP blocks all from shared memory.
@@ -1630,10 +1476,23 @@ __global__ void k_rap_rbi(long nnz, const int *__restrict__ R_col, const int *__
   rbi[k] = make_int2(B_ptr[j], B_ptr[j + 1] - B_ptr[j]);
 }
 
-constexpr size_t gal_smem(int AB, int BB) {
-  return ((size_t)GAL_PCAP * BB + (size_t)GAL_ACAP * AB + 2) * 8 + (size_t)GAL_ACAP * 4;
-}
 
+// symmetrisation (C22) with the transpose partner of every block precomputed (symbolic, k_sym_partner): one
+// thread per entry, so both the G reads and the A_c writes are contiguous
+__global__ void k_sym_partner(long nnzb, const int *rowof, const int *ptr, const int *col, int *kt, int *err) {
+  long e = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (e >= nnzb) return;
+  const int a = rowof[e], b2 = col[e];
+  kt[e] = bsearch_int(col, ptr[b2], ptr[b2 + 1], a);
+  if (kt[e] < 0) raise_err(err, DERR_ARG, (int)e);
+}
+__global__ void k_sym2(long n36, const int *__restrict__ kt, const double *__restrict__ G, double *__restrict__ Ac) {
+  long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (t >= n36) return;
+  const long e = t / 36;
+  const int q = (int)(t - e * 36), r = q / 6, s2 = q - 6 * r;
+  Ac[t] = 0.5 * (G[t] + G[(long)kt[e] * 36 + s2 * 6 + r]);
+}
 __global__ void k_sym(long nnzb, const int *rowof, const int *ptr, const int *col, const double *G, double *Ac,
                       int *err) {
   long e = blockIdx.x * (long)blockDim.x + threadIdx.x;
@@ -1917,55 +1776,71 @@ static void thin_numeric(Ctx &c, long nthin_nnz) {
   LAUNCH(k_zr_vals, c.zr_nnz, c.zr_nnz, c.zr_src, c.lev[0].A.val, c.zr_val);
 }
 
-static void power_iteration(Ctx &c, Level &L) {
+static void power_iteration(Ctx &c, Level &L, int lev) {
   if (!c.pw_v) {  // once per handle: no allocation on the numeric re-setup path
     c.pw_v = c.alloc<double>(c.n);
     c.pw_w = c.alloc<double>(c.n);
   }
   double *v = c.pw_v, *w = c.pw_w;
   if (!c.pw_s) c.pw_s = c.alloc<double>(4);
+  if (!c.pw_lev) c.pw_lev = c.alloc<double>(2 * MAXLEV);
+  if (!c.pw_part) c.pw_part = c.alloc<double>(nblk(c.n) + 1);
   LAUNCH(k_pow_init, L.n, L.n, v);
+  // per step: w = (A v) / d with the C14 partials of w.w and v.v (fused into the fine SpMV), both level-2
+  // sums, then lambda and v = w / ||w|| (k_pow_scale)
+  const bool fused = L.As.val && L.b == 3 && L.As.br == 3 && !L.As.perm;
+  const long nb = L.n / L.b, C = (nb + CTA - 1) / CTA;
   for (int it = 0; it < c.cfg.power_iters; it++) {
-    if (L.As.val) launch_sell_spmv(c, L.As, SPMV_Y, v, nullptr, nullptr, nullptr, w, nullptr);
-    else launch_bsr_spmv(c, L.A, v, w);
-    LAUNCH(k_div, L.n, L.n, w, L.dpt);
-    launch_dot(c, L.n, L.b, w, w, DOT_PLAIN);
-    k_pow_keep<<<1, 1, 0, c.stream>>>(c.sc, c.pw_s, 0);
-    after_launch(c, "k_pow_keep");
-    launch_dot(c, L.n, L.b, v, v, DOT_PLAIN);
-    k_pow_keep<<<1, 1, 0, c.stream>>>(c.sc, c.pw_s, 1);
-    after_launch(c, "k_pow_keep");
+    if (fused) {
+      launch_sell_pow(c, L.As, v, L.dpt, w, c.dot_part, c.pw_part);
+    } else {
+      if (L.As.val) {
+        launch_sell_spmv(c, L.As, SPMV_YDIV, v, nullptr, L.dpt, nullptr, w, nullptr);
+      } else {
+        launch_bsr_spmv(c, L.A, v, w);
+        LAUNCH(k_div, L.n, L.n, w, L.dpt);
+      }
+      launch_pow_dots(c, nb, L.b, w, v, c.dot_part, c.pw_part);
+    }
+    launch_pow_fin(c, C, c.dot_part, c.pw_part, c.pw_s);
     LAUNCH(k_pow_scale, L.n, L.n, w, c.pw_s, v);
   }
-  const double lam = d2h1(c, c.pw_s + 2);  // one host read per level (omega is a kernel argument)
-  L.lambda = lam;
-  L.omega = 4.0 / (3.0 * lam);
+  // lambda and omega of this level stay on the device (k_P_values reads omega there); the host copies are
+  // read once at the end of the setup (read_level_scalars): no stream synchronisation per level
+  CK(cudaMemcpyAsync(c.pw_lev + 2 * lev, c.pw_s + 2, 2 * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+}
+static void read_level_scalars(Ctx &c) {
+  double h[2 * MAXLEV];
+  const int nl = std::max(c.nlev - 1, 0);
+  if (!nl || !c.pw_lev) return;
+  CK(cudaMemcpyAsync(h, c.pw_lev, 2 * nl * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+  CK(cudaStreamSynchronize(c.stream));
+  for (int l = 0; l < nl; l++) {
+    c.lev[l].lambda = h[2 * l];
+    c.lev[l].omega = h[2 * l + 1];
+  }
 }
 
 // per-level cached arrays for numeric re-setup
 struct LevelCache {
   int *P_rowof = nullptr, *R_perm = nullptr, *G_rowof = nullptr, *AP_rowof = nullptr;
+  int *R_inv = nullptr;  // R block of every P block (k_P_values writes R = P^T directly)
   Bsr G;
   // block-product lists of the Galerkin products (symbolic, built once): for output block e of AP (G),
   // the pairs (A block, P block) ((R block, AP block)) with a matching inner index, in ascending order
   int *AP_pptr = nullptr, *AP_pa = nullptr, *AP_pb = nullptr;
   int *G_pptr = nullptr, *G_pa = nullptr, *G_pb = nullptr;
   signed char *AP_off = nullptr, *G_off = nullptr;  // dense-over-row offset tables (k_spgemm_dense)
-  GalGrp *AP_grp = nullptr;  // row groups of k_gal_ap (fine level)
-  GalRun *AP_runs = nullptr;
+  GalGrp *AP_grp = nullptr;  // row groups of k_gal_hl (fine level)
+  GalCopy *AP_cps = nullptr;  // TMA copy descriptors of the groups
   int AP_ngrp = 0;
-  RapGrp *G_grp = nullptr;  // output groups of k_gal_rap (fine level)
+  int *G_kt = nullptr;       // transpose partner of every block of G (k_sym2)
+  RapGrp *G_grp = nullptr;  // output groups of k_gal_rap2 (fine level)
   int G_ngrp = 0;
   long *G_gofs = nullptr;    // k_gal_rap2: group-contiguous offset rows and per-R-block AP row (start, length)
   signed char *G_offg = nullptr;
   int2 *G_rbi = nullptr;
   unsigned *AP_hitw = nullptr;  // hit words of k_gal_hl
-  // smoothed P as the row-group product T = A*Pt (fine level): pairs, groups, hit words
-  int *P_pptr = nullptr, *P_pa = nullptr, *P_pb = nullptr;
-  GalGrp *P_grp = nullptr;
-  GalRun *P_runs = nullptr;
-  unsigned *P_hitw = nullptr;
-  int P_ngrp = 0;
 };
 
 static signed char *build_off(Ctx &c, long nnzc, const int *rowof, const int *ccol, const Bsr &A, const Bsr &B) {
@@ -1985,9 +1860,9 @@ static signed char *build_off(Ctx &c, long nnzc, const int *rowof, const int *cc
   return off;
 }
 
-// Row groups of k_gal_ap (symbolic, host, once per setup): greedy over consecutive rows of C = A*B.
+// Row groups of k_gal_hl (symbolic, host, once per setup): greedy over consecutive rows of C = A*B.
 static void build_gal_groups(Ctx &c, const Bsr &A, const Bsr &B, const Bsr &C, const int *d_pptr, const int *d_pa,
-                             const int *d_pb, GalGrp *&d_grp, int &ngrp, GalRun *&d_runs, unsigned *&d_hitw) {
+                             const int *d_pb, GalGrp *&d_grp, int &ngrp, GalCopy *&d_cps, unsigned *&d_hitw) {
   auto d2hv = [&](const int *src, size_t n) {
     std::vector<int> h(n);
     CK(cudaMemcpyAsync(h.data(), src, n * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
@@ -1996,13 +1871,25 @@ static void build_gal_groups(Ctx &c, const Bsr &A, const Bsr &B, const Bsr &C, c
   const std::vector<int> ap = d2hv(A.ptr, A.nbr + 1), ac = d2hv(A.col, A.nnzb), bp = d2hv(B.ptr, B.nbr + 1),
                          cp = d2hv(C.ptr, C.nbr + 1), pp = d2hv(d_pptr, C.nnzb + 1);
   CK(cudaStreamSynchronize(c.stream));
+  const int AB = A.br * A.bc, BB = B.br * B.bc;
+  // byte offsets of the four regions of a group buffer (k_gal_hl: B union, A segment, hit words, offsets)
+  const int offA = GHL_PCAP * BB * 8, offH = offA + (GAL_ACAP * AB + 2) * 8, offP = offH + (GHL_HCAP + 8) * 4;
   std::vector<GalGrp> grps;
+  std::vector<int2> grun;  // run range of every group (for the hit words)
   std::vector<GalRun> runs;
+  std::vector<GalCopy> cps;
   std::vector<char> mark(B.nbr, 0);
   std::vector<int> ul;
   auto add_global = [&](int i) {  // one row through global memory, NT output blocks per group
-    for (int e = cp[i]; e < cp[i + 1]; e += GAL_NT)
-      grps.push_back(GalGrp{e, std::min(cp[i + 1], e + GAL_NT), ap[i], ap[i + 1], 0, -1, 0, 0});
+    for (int e = cp[i]; e < cp[i + 1]; e += GAL_NT) {
+      grps.push_back(GalGrp{e, std::min(cp[i + 1], e + GAL_NT), ap[i], (int)cps.size(), (int)cps.size(), 0u, 0, 0});
+      grun.push_back(make_int2(0, 0));
+    }
+  };
+  auto copy = [&](long long src, long long end, int dst, unsigned id) {  // [src, end) rounded out to 16 bytes
+    const long long s16 = src & ~15LL, e16 = (end + 15) & ~15LL;
+    cps.push_back(GalCopy{s16, dst, (unsigned)(e16 - s16) | id << 28});
+    return (unsigned)(e16 - s16);
   };
   const int n = A.nbr;
   int i = 0;
@@ -2042,25 +1929,42 @@ static void build_gal_groups(Ctx &c, const Bsr &A, const Bsr &B, const Bsr &C, c
       base += bp[ul[q1 - 1] + 1] - bp[ul[q]];
       q = q1;
     }
-    if ((int)runs.size() - r0 > GAL_RCAP) {  // too fragmented for the run table: global path
+    if ((int)runs.size() - r0 > GAL_RCAP) {  // too fragmented for one warp of copies: global path
       runs.resize(r0);
       for (int ii = i0; ii < i; ii++) add_global(ii);
       continue;
     }
-    grps.push_back(GalGrp{cp[i0], cp[i], ap[i0], ap[i], r0, (int)runs.size(), 0, 0});
+    const int e0 = cp[i0], e1 = cp[i], c0 = (int)cps.size();
+    unsigned tx = 0;
+    tx += copy((long long)ap[i0] * AB * 8, (long long)ap[i] * AB * 8, offA, 0);
+    if (pp[e1] > pp[e0]) tx += copy((long long)pp[e0] * 4, (long long)pp[e1] * 4, offH, 1);
+    tx += copy((long long)e0 * 4, (long long)(e1 + 1) * 4, offP, 2);
+    for (int r = r0; r < (int)runs.size(); r++) {
+      const GalRun &q = runs[r];
+      if (bp[q.j1] > bp[q.j0])
+        tx += copy((long long)bp[q.j0] * BB * 8, (long long)bp[q.j1] * BB * 8, q.base * BB * 8, 3);
+    }
+    grps.push_back(GalGrp{e0, e1, ap[i0], c0, (int)cps.size(), tx, pp[e0], 0});
+    grun.push_back(make_int2(r0, (int)runs.size()));
   }
   ngrp = (int)grps.size();
   d_grp = c.alloc<GalGrp>(std::max<size_t>(grps.size(), 1));
-  d_runs = c.alloc<GalRun>(std::max<size_t>(runs.size(), 1));
+  d_cps = c.alloc<GalCopy>(std::max<size_t>(cps.size(), 1));
+  GalRun *d_runs = c.alloc<GalRun>(std::max<size_t>(runs.size(), 1));
+  int2 *d_grun = c.alloc<int2>(std::max<size_t>(grun.size(), 1));
   h2d(c, d_grp, grps.data(), grps.size());
+  h2d(c, d_cps, cps.data(), cps.size());
   h2d(c, d_runs, runs.data(), runs.size());
+  h2d(c, d_grun, grun.data(), grun.size());
   const long np = pp[C.nnzb];
   d_hitw = c.alloc<unsigned>(np + 8);  // + 8: the groups' 16-byte aligned bulk copies may read past the end
-  if (ngrp) k_gal_hitw<<<ngrp, 128, 0, c.stream>>>(d_grp, d_runs, d_pptr, d_pa, d_pb, B.ptr, d_hitw);
+  if (ngrp) k_gal_hitw<<<ngrp, 128, 0, c.stream>>>(d_grp, d_grun, d_runs, d_pptr, d_pa, d_pb, B.ptr, d_hitw);
   CK(cudaStreamSynchronize(c.stream));
+  c.release(d_runs);
+  c.release(d_grun);
 }
 
-// Output groups of k_gal_rap: <= RAP_NT/2 output blocks of one row of G; every AP row must fit one stage.
+// Output groups of k_gal_rap2: <= RAP_NT/2 output blocks of one row of G; every AP row must fit one stage.
 static void build_rap_groups(Ctx &c, const Bsr &G, const Bsr &R, const Bsr &AP, RapGrp *&d_grp, int &ngrp,
                              long *&d_gofs, signed char *&d_offg, int2 *&d_rbi) {
   std::vector<int> gp(G.nbr + 1), bp(AP.nbr + 1);
@@ -2068,7 +1972,7 @@ static void build_rap_groups(Ctx &c, const Bsr &G, const Bsr &R, const Bsr &AP, 
   CK(cudaMemcpyAsync(bp.data(), AP.ptr, bp.size() * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
   CK(cudaStreamSynchronize(c.stream));
   for (int j = 0; j < AP.nbr; j++)
-    if (bp[j + 1] - bp[j] > RAP_SCAP) {  // k_gal_rap cannot stage this row: keep the dense-over-row kernel
+    if (bp[j + 1] - bp[j] > RAP_SCAP) {  // k_gal_rap2 cannot stage this row: keep the dense-over-row kernel
       d_grp = nullptr;
       ngrp = 0;
       return;
@@ -2133,35 +2037,24 @@ static void level_numeric(Ctx &c, int l, LevelCache &lc) {
         CK(cudaFuncSetAttribute(k_spgemm_dense<3, 3, 6>, cudaFuncAttributePreferredSharedMemoryCarveout, cv));
         CK(cudaFuncSetAttribute(k_spgemm_dense<6, 3, 6>, cudaFuncAttributePreferredSharedMemoryCarveout, cv));
         CK(cudaFuncSetAttribute(k_P_values<3>, cudaFuncAttributePreferredSharedMemoryCarveout, cv));
-        CK(cudaFuncSetAttribute(k_transpose_vals, cudaFuncAttributePreferredSharedMemoryCarveout, cv));
         CK(cudaFuncSetAttribute(k_spgemm_vals_warp<6, 6, 6>, cudaFuncAttributePreferredSharedMemoryCarveout, cv));
         CK(cudaFuncSetAttribute(k_sell_vals, cudaFuncAttributePreferredSharedMemoryCarveout, cv));
       }
     }
   }
-  power_iteration(c, L);
+  power_iteration(c, L, l);
   static const bool gal_old = getenv("AMGF_GAL_OLD") != nullptr;  // A/B only: the thread-per-block kernels
-  if (L.b == 3 && lc.P_grp && !gal_old) {
-    constexpr size_t sm = ghl_smem(9, 18);
-    size_t &attr = device_slot((const void *)k_gal_hl<3, 3, 6, true>);
-    if (!attr) {
-      attr = 1;
-      CK(cudaFuncSetAttribute(k_gal_hl<3, 3, 6, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    }
-    GalEpi ep;
-    ep.C_col = L.P.col; ep.agg = L.agg; ep.Pt_ptr = L.Pt.ptr; ep.Ptv = L.Pt.val; ep.dpt = L.dpt; ep.omega = L.omega;
-    if (lc.P_ngrp)
-      k_gal_hl<3, 3, 6, true><<<lc.P_ngrp, GAL_NT, sm, c.stream>>>(lc.P_grp, lc.P_runs, lc.P_rowof, lc.P_pptr,
-                                                                   lc.P_hitw, lc.P_pa, lc.P_pb, L.A.val, L.Pt.ptr,
-                                                                   L.Pt.val, L.P.val, ep);
-    after_launch(c, "k_gal_hl<P>");
-  } else if (L.b == 3)
+  if (!lc.R_inv) {  // symbolic, once
+    lc.R_inv = c.alloc<int>(std::max<long>(L.R.nnzb, 1));
+    LAUNCH(k_inv_perm, L.R.nnzb, L.R.nnzb, lc.R_perm, lc.R_inv);
+  }
+  if (L.b == 3)
     LAUNCH(k_P_values<3>, L.P.nnzb, L.P.nnzb, lc.P_rowof, L.P.col, L.A.ptr, L.A.col, L.A.val, L.agg, L.Pt.ptr,
-           L.Pt.val, L.dpt, L.omega, L.P.val);
+           L.Pt.val, L.dpt, c.pw_lev + 2 * l + 1, L.P.val, lc.R_inv, L.R.val);
   else
     LAUNCH(k_P_values<6>, L.P.nnzb, L.P.nnzb, lc.P_rowof, L.P.col, L.A.ptr, L.A.col, L.A.val, L.agg, L.Pt.ptr,
-           L.Pt.val, L.dpt, L.omega, L.P.val);
-  LAUNCH(k_transpose_vals, L.R.nnzb, L.R.nnzb, L.b, 6, lc.R_perm, L.P.val, L.R.val);
+           L.Pt.val, L.dpt, c.pw_lev + 2 * l + 1, L.P.val, lc.R_inv, L.R.val);
+
   if (L.b == 3) {  // level-0 restriction reads R's values group-interleaved (Bsr::ival)
     r_interleave(c, L.R);
   }
@@ -2172,16 +2065,15 @@ static void level_numeric(Ctx &c, int l, LevelCache &lc) {
     static const int dense = getenv("AMGF_SPGEMM_DENSE") ? atoi(getenv("AMGF_SPGEMM_DENSE")) : 1;  // A/B only
     if (dense && L.b == 3 && lc.AP_off) {
       if (lc.AP_grp && !gal_old) {
-        constexpr size_t sm = ghl_smem(9, 18);
+        const size_t sm = ghl_buf_bytes(9, 18);
         size_t &attr = device_slot((const void *)k_gal_hl<3, 3, 6>);
         if (!attr) {
           attr = 1;
           CK(cudaFuncSetAttribute(k_gal_hl<3, 3, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         }
         if (lc.AP_ngrp)
-          k_gal_hl<3, 3, 6><<<lc.AP_ngrp, GAL_NT, sm, c.stream>>>(lc.AP_grp, lc.AP_runs, lc.AP_rowof, lc.AP_pptr,
-                                                                   lc.AP_hitw, lc.AP_pa, lc.AP_pb, L.A.val, L.P.ptr,
-                                                                   L.P.val, L.AP.val);
+          k_gal_hl<3, 3, 6><<<lc.AP_ngrp, GAL_NT, sm, c.stream>>>(lc.AP_grp, lc.AP_cps, lc.AP_pptr, lc.AP_hitw,
+                                                                   lc.AP_pa, lc.AP_pb, L.A.val, L.P.val, L.AP.val);
         after_launch(c, "k_gal_hl");
       } else {
         LAUNCH((k_spgemm_dense<3, 3, 6>), L.AP.nnzb, L.AP.nnzb, lc.AP_rowof, L.A.ptr, L.A.col, L.A.val, L.P.ptr,
@@ -2209,13 +2101,20 @@ static void level_numeric(Ctx &c, int l, LevelCache &lc) {
       LAUNCH((k_spgemm_vals_pairs<3, 3, 6>), L.AP.nnzb, L.AP.nnzb, lc.AP_pptr, lc.AP_pa, lc.AP_pb, L.A.val, L.P.val,
              L.AP.val);
     else
-      LAUNCH((k_spgemm_vals_warp<6, 6, 6>), L.AP.nnzb * 32, L.AP.nnzb, lc.AP_pptr, lc.AP_pa, lc.AP_pb, L.A.val,
-             L.P.val, L.AP.val);
-    auto kg = (L.b == 3) ? k_spgemm_vals_warp<6, 3, 6> : k_spgemm_vals_warp<6, 6, 6>;
-    LAUNCH(kg, lc.G.nnzb * 32, lc.G.nnzb, lc.G_pptr, lc.G_pa, lc.G_pb, L.R.val, L.AP.val, lc.G.val);
+      LAUNCH(k_spgemm_vals_half6, L.AP.nnzb * 2, L.AP.nnzb, lc.AP_pptr, lc.AP_pa, lc.AP_pb, L.A.val, L.P.val,
+             L.AP.val);
+    if (L.b == 3)
+      LAUNCH((k_spgemm_vals_warp<6, 3, 6>), lc.G.nnzb * 32, lc.G.nnzb, lc.G_pptr, lc.G_pa, lc.G_pb, L.R.val, L.AP.val,
+             lc.G.val);
+    else
+      LAUNCH(k_spgemm_vals_half6, lc.G.nnzb * 2, lc.G.nnzb, lc.G_pptr, lc.G_pa, lc.G_pb, L.R.val, L.AP.val, lc.G.val);
     }
   }
-  LAUNCH(k_sym, lc.G.nnzb, lc.G.nnzb, lc.G_rowof, lc.G.ptr, lc.G.col, lc.G.val, Lc.A.val, c.err);
+  if (!lc.G_kt) {  // symbolic, once
+    lc.G_kt = c.alloc<int>(std::max<long>(lc.G.nnzb, 1));
+    LAUNCH(k_sym_partner, lc.G.nnzb, lc.G.nnzb, lc.G_rowof, lc.G.ptr, lc.G.col, lc.G_kt, c.err);
+  }
+  LAUNCH(k_sym2, lc.G.nnzb * 36, lc.G.nnzb * 36, lc.G_kt, lc.G.val, Lc.A.val);
   LAUNCH(k_diag, (long)Lc.nodes * Lc.b, Lc.nodes, Lc.b, Lc.A.ptr, Lc.A.col, Lc.A.val, Lc.dl1, Lc.dpt);
   smoother_data(c, Lc);
 }
@@ -2616,11 +2515,10 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
     if (L.b == 3) {  // fine level: dense-over-row products (k_spgemm_dense)
       lc.AP_off = build_off(c, L.AP.nnzb, lc.AP_rowof, L.AP.col, L.A, L.P);
       lc.G_off = build_off(c, lc.G.nnzb, lc.G_rowof, lc.G.col, L.R, L.AP);
-      build_gal_groups(c, L.A, L.P, L.AP, lc.AP_pptr, lc.AP_pa, lc.AP_pb, lc.AP_grp, lc.AP_ngrp, lc.AP_runs,
+      build_gal_groups(c, L.A, L.P, L.AP, lc.AP_pptr, lc.AP_pa, lc.AP_pb, lc.AP_grp, lc.AP_ngrp, lc.AP_cps,
                        lc.AP_hitw);
       build_rap_groups(c, lc.G, L.R, L.AP, lc.G_grp, lc.G_ngrp, lc.G_gofs, lc.G_offg, lc.G_rbi);
-      build_pairs(c, L.P.nnzb, lc.P_rowof, L.P.col, L.A, L.Pt, lc.P_pptr, lc.P_pa, lc.P_pb);
-      build_gal_groups(c, L.A, L.Pt, L.P, lc.P_pptr, lc.P_pa, lc.P_pb, lc.P_grp, lc.P_ngrp, lc.P_runs, lc.P_hitw);
+
     }
     level_numeric(c, l, lc);
     check_dev_error(c, "Galerkin product");
@@ -2639,6 +2537,7 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
   }
   alloc_workspaces(c);
   CK(cudaStreamSynchronize(c.stream));
+  read_level_scalars(c);
   tail_plan(c);
 }
 
@@ -2648,8 +2547,7 @@ void setup_numeric(Ctx &c, const double *D, const double *D_lo, const double *D_
   setup_mark(c, 0, c.stream);
   d2d(c, c.D, D, c.m);
   LAUNCH(k_check_finite, c.m, c.m, c.D, c.err, DERR_NONFINITE);
-  LAUNCH(k_check_pos, c.m, c.m, c.D, c.err);
-  check_dev_error(c, "D check");
+  LAUNCH(k_check_pos, c.m, c.m, c.D, c.err);  // the device error flag keeps the first error: checked at the end
   // bound-constraint diagonals (both or neither; amgf_update_D_box): zero-filled when only one is given
   c.has_box = D_lo || D_up;
   if (c.has_box) {
@@ -2660,21 +2558,24 @@ void setup_numeric(Ctx &c, const double *D, const double *D_lo, const double *D_
     LAUNCH(k_check_finite, c.n, c.n, c.D_up, c.err, DERR_NONFINITE);
     LAUNCH(k_check_nonneg, c.n, c.n, c.D_lo, c.err);
     LAUNCH(k_check_nonneg, c.n, c.n, c.D_up, c.err);
-    check_dev_error(c, "bound diagonal check");
   }
+  Level &L0 = c.lev[0];
   S_numeric(c, C.s.S_rowof);
   setup_mark(c, 1, c.stream);
-  Level &L0 = c.lev[0];
   if (c.nc > 0) {
     fork_filter(c);
     thin_numeric(c, C.thin_nnz);
   }
-  LAUNCH(k_diag, L0.n, L0.nodes, 3, L0.A.ptr, L0.A.col, L0.A.val, L0.dl1, L0.dpt);
+  // the fine SELL copy and the level-0 diagonals in one pass (the fine SELL keeps the natural row order)
+  const bool fused_S = L0.As.val && L0.As.br == 3 && !L0.As.perm && L0.As.nrows == L0.nodes;
+  if (fused_S)
+    LAUNCH(k_sell_diag, L0.nodes, L0.nodes, L0.A.ptr, L0.A.col, L0.A.val, L0.As.slice_ptr, L0.As.val, L0.dl1, L0.dpt);
+  else
+    LAUNCH(k_diag, L0.n, L0.nodes, 3, L0.A.ptr, L0.A.col, L0.A.val, L0.dl1, L0.dpt);
   smoother_data(c, L0);
   for (int l = 0; l + 1 < c.nlev; l++) {
-    build_sell(c, c.lev[l].A, c.lev[l].As, false, l > 0);
-    level_numeric(c, l, C.lc[l]);
-    check_dev_error(c, "Galerkin product");
+    if (l > 0 || !fused_S) build_sell(c, c.lev[l].A, c.lev[l].As, false, l > 0);
+    level_numeric(c, l, C.lc[l]);  // its device error flags are checked once, after the join
     build_sell(c, c.lev[l].P, c.lev[l].Ps, false, l > 0);
   }
   if (c.nlev == 1) build_sell(c, L0.A, L0.As, false, false);
@@ -2683,7 +2584,8 @@ void setup_numeric(Ctx &c, const double *D, const double *D_lo, const double *D_
   setup_mark(c, 3, c.stream);
   join_filter(c);
   setup_mark(c, 4, c.stream);
-  check_dev_error(c, "numeric setup (A_w / coarsest Cholesky)");
+  check_dev_error(c, "numeric setup (Galerkin products / A_w / coarsest Cholesky)");
+  read_level_scalars(c);
   auto ms = [&](int a, int b) {
     float v = 0;
     CK(cudaEventElapsedTime(&v, c.ph_ev[a], c.ph_ev[b]));

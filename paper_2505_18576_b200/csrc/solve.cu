@@ -44,7 +44,7 @@ __device__ __forceinline__ double cta_tree(double v, double *s) {
 
 enum { MODE_Y = SPMV_Y, MODE_RESID = SPMV_RESID, MODE_SMOOTH = SPMV_SMOOTH, MODE_DOT = SPMV_DOT,
        MODE_SMOOTH_ADD = SPMV_SMOOTH_ADD, MODE_ADDTO = 5, MODE_CHEB1 = SPMV_CHEB1, MODE_CHEB = SPMV_CHEB,
-       MODE_CHEB_DOT = 8 };
+       MODE_CHEB_DOT = 8, MODE_YDIV = SPMV_YDIV, MODE_POW = SPMV_POW };
 
 // Chebyshev step epilogue (contract C23): t = (b - acc)/d; first step dir = ca t, later dir = fma(ca, dir,
 // cb t); x_new = x + dir (then add + x_new when add is given, as SMOOTH_ADD).
@@ -166,6 +166,31 @@ __global__ void __launch_bounds__(CTA) k_sell(int nrows, const int *__restrict__
     if (threadIdx.x == 0) ch.dot_part[blockIdx.x] = tot;
     return;
   }
+  if (MODE == MODE_POW) {  // power step (C18): w = acc / d, C14 partials of w.w (dot_part) and v.v (ch.dot_part)
+    __shared__ double red3[CTA];
+    double sw = 0.0, sv = 0.0;
+    if (row < nrows) {
+#pragma unroll
+      for (int r = 0; r < BR; r++) {
+        const long i = (long)row * BR + r;
+        const double wi = acc[r] / d[i];
+        y[i] = wi;
+        sw = __fma_rn(wi, wi, sw);
+      }
+#pragma unroll
+      for (int r = 0; r < BR; r++) {
+        const double vi = x[(long)row * BR + r];
+        sv = __fma_rn(vi, vi, sv);
+      }
+    }
+    const double tw = cta_tree(sw, red3);
+    const double tv = cta_tree(sv, red3);
+    if (threadIdx.x == 0) {
+      dot_part[blockIdx.x] = tw;
+      ch.dot_part[blockIdx.x] = tv;
+    }
+    return;
+  }
   if (row >= nrows) return;
   const int orow = (MODE == MODE_ADDTO && perm) ? perm[row] : row;
 #pragma unroll
@@ -185,6 +210,8 @@ __global__ void __launch_bounds__(CTA) k_sell(int nrows, const int *__restrict__
       y[i] = y[i] + acc[r];
     } else if (MODE == MODE_CHEB1 || MODE == MODE_CHEB) {
       y[i] = cheb_epilogue(MODE, b[i] - acc[r], d[i], x[i], ch.dir, i, ch.ca, ch.cb, add);
+    } else if (MODE == MODE_YDIV) {
+      y[i] = acc[r] / d[i];
     }
   }
 }
@@ -279,6 +306,8 @@ __global__ void __launch_bounds__(CTA) k_sell_r1(int nrows, const int *__restric
     y[i] = y[i] + acc;
   } else if (MODE == MODE_CHEB1 || MODE == MODE_CHEB) {
     y[i] = cheb_epilogue(MODE, b[i] - acc, d[i], x[i], ch.dir, i, ch.ca, ch.cb, add);
+  } else if (MODE == MODE_YDIV) {
+    y[i] = acc / d[i];
   }
 }
 
@@ -307,6 +336,7 @@ static void sell_dispatch(Ctx &c, const Sell &A, int mode, const double *x, cons
       CK(cudaFuncSetAttribute(k_sell<BR, BC, MODE_RESID>, cudaFuncAttributePreferredSharedMemoryCarveout, 50));
       // the setup's power iteration (MODE_Y) runs beside the A_w factorization: same reason
       CK(cudaFuncSetAttribute(k_sell<BR, BC, MODE_Y>, cudaFuncAttributePreferredSharedMemoryCarveout, 50));
+      CK(cudaFuncSetAttribute(k_sell<BR, BC, MODE_POW>, cudaFuncAttributePreferredSharedMemoryCarveout, 50));
     }
   }
   if (BR == 1 && mode != MODE_DOT) {
@@ -318,6 +348,8 @@ static void sell_dispatch(Ctx &c, const Sell &A, int mode, const double *x, cons
       case MODE_ADDTO: k_sell_r1<BC, MODE_ADDTO, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm, ch); break;
       case MODE_CHEB1: k_sell_r1<BC, MODE_CHEB1, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm, ch); break;
       case MODE_CHEB: k_sell_r1<BC, MODE_CHEB, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm, ch); break;
+      case MODE_YDIV: k_sell_r1<BC, MODE_YDIV, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm, ch); break;
+      default: throw Error{AMGF_ERR_ARG, "sell spmv: mode not available for scalar-row SELL"};
     }
     after_launch(c, "k_sell_r1");
     return;
@@ -332,6 +364,9 @@ static void sell_dispatch(Ctx &c, const Sell &A, int mode, const double *x, cons
     case MODE_CHEB1: k_sell<BR, BC, MODE_CHEB1><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
     case MODE_CHEB: k_sell<BR, BC, MODE_CHEB><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
     case MODE_CHEB_DOT: k_sell<BR, BC, MODE_CHEB_DOT><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
+    case MODE_YDIV: k_sell<BR, BC, MODE_YDIV><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
+    case MODE_POW: k_sell<BR, BC, MODE_POW><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
+    default: throw Error{AMGF_ERR_ARG, "sell spmv: unknown mode"};
   }
   after_launch(c, __func__);
 }
@@ -342,6 +377,14 @@ void launch_sell_spmv(Ctx &c, const Sell &A, int mode, const double *x, const do
   else if (A.br == 1 && A.bc == 6) sell_dispatch<1, 6>(c, A, mode, x, b, d, add, y, dp);
   else if (A.br == 6 && A.bc == 6) sell_dispatch<6, 6>(c, A, mode, x, b, d, add, y, dp);
   else throw Error{AMGF_ERR_ARG, "sell spmv: unsupported block shape"};
+}
+
+void launch_sell_pow(Ctx &c, const Sell &A, const double *v, const double *d, double *w, double *part_w,
+                     double *part_v) {
+  REQUIRE(A.br == 3 && A.bc == 3 && !A.perm, AMGF_ERR_ARG, "fused power step: fine level only");
+  ChebArgs ch;
+  ch.dot_part = part_v;
+  sell_dispatch<3, 3>(c, A, MODE_POW, v, nullptr, d, nullptr, w, part_w, ch);
 }
 
 void launch_sell_cheb(Ctx &c, const Sell &A, bool first, const double *x, const double *b, const double *dl1,
@@ -798,6 +841,58 @@ __global__ void __launch_bounds__(CTA) k_dot2(long C, const double *__restrict__
         break;
     }
   }
+}
+
+// power step (C18) dot partials: C14 level 1 of w.w and v.v in one pass (block rows of b entries)
+__global__ void __launch_bounds__(CTA) k_pow_dots(long nb, int b, const double *__restrict__ w,
+                                                  const double *__restrict__ v, double *__restrict__ pw_,
+                                                  double *__restrict__ pv_) {
+  __shared__ double red[CTA];
+  const long i = blockIdx.x * (long)CTA + threadIdx.x;
+  double sw = 0.0, sv = 0.0;
+  if (i < nb) {
+    for (int e = 0; e < b; e++) sw = __fma_rn(w[i * b + e], w[i * b + e], sw);
+    for (int e = 0; e < b; e++) sv = __fma_rn(v[i * b + e], v[i * b + e], sv);
+  }
+  const double tw = cta_tree(sw, red);
+  const double tv = cta_tree(sv, red);
+  if (threadIdx.x == 0) {
+    pw_[blockIdx.x] = tw;
+    pv_[blockIdx.x] = tv;
+  }
+}
+// C14 level 2 of both partial arrays (the k_dot2 order): pw[0] = w.w, pw[1] = v.v
+__device__ __forceinline__ double dot_level2(long C, const double *__restrict__ part, double *red) {
+  double acc = 0.0;
+  long c = threadIdx.x;
+  for (; c + 7 * CTA < C; c += 8 * CTA) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) v[u] = part[c + u * CTA];
+#pragma unroll
+    for (int u = 0; u < 8; u++) acc = acc + v[u];
+  }
+  for (; c < C; c += CTA) acc = acc + part[c];
+  return cta_tree(acc, red);
+}
+__global__ void __launch_bounds__(CTA) k_pow_fin(long C, const double *__restrict__ pw_, const double *__restrict__ pv_,
+                                                 double *__restrict__ pw) {
+  __shared__ double red[CTA];
+  const double sw = dot_level2(C, pw_, red);
+  const double sv = dot_level2(C, pv_, red);
+  if (threadIdx.x == 0) {
+    pw[0] = sw;
+    pw[1] = sv;
+  }
+}
+void launch_pow_dots(Ctx &c, long nb, int b, const double *w, const double *v, double *part_w, double *part_v) {
+  const long C = (nb + CTA - 1) / CTA;
+  if (C > 0) k_pow_dots<<<(int)C, CTA, 0, c.stream>>>(nb, b, w, v, part_w, part_v);
+  after_launch(c, __func__);
+}
+void launch_pow_fin(Ctx &c, long C, const double *part_w, const double *part_v, double *pw) {
+  k_pow_fin<<<1, CTA, 0, c.stream>>>(C, part_w, part_v, pw);
+  after_launch(c, __func__);
 }
 
 void launch_dot_finish(Ctx &c, long C, int finish) {
