@@ -965,6 +965,61 @@ __global__ void k_P_values(long nnzb, const int *P_rowof, const int *P_col, cons
       if (Rinv) Rv[((long)Rinv[e] * 6 + s) * B + r] = pt - t;  // R = P^T: its block Rinv[e], transposed
     }
 }
+// The same P values (C19/C20) over precomputed block-product pairs (symbolic, once): thread per P block runs
+// exactly its (A block, Pt block) products in ascending A position -- the walk above tests every block of A's
+// row (26 at the fine level) for its ~6 products.  Writes P and R = P^T.
+template <int B, int H>  // H threads per P block, B / H rows each (the 6 x 6 levels: 2 x 18 accumulators)
+__global__ void __launch_bounds__(CTA) k_P_pairs(long nnzb, const int *__restrict__ P_rowof,
+                                                 const int *__restrict__ P_col, const int *__restrict__ pptr,
+                                                 const int *__restrict__ pa, const int *__restrict__ pb,
+                                                 const double *__restrict__ A_val, const int *__restrict__ agg,
+                                                 const int *__restrict__ Pt_ptr, const double *__restrict__ Ptv,
+                                                 const double *__restrict__ dpt, const double *__restrict__ omega_p,
+                                                 double *__restrict__ Pv, const int *__restrict__ Rinv,
+                                                 double *__restrict__ Rv) {
+  constexpr int RB = B / H;  // rows of this thread
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  const long e = t / H;
+  const int r0 = (int)(t - e * H) * RB;
+  if (e >= nnzb) return;
+  const double omega = *omega_p;
+  double acc[RB * 6];
+#pragma unroll
+  for (int q = 0; q < RB * 6; q++) acc[q] = 0.0;
+  const int q1 = pptr[e + 1];
+  for (int q = pptr[e]; q < q1; q++) {
+    const double *Av = A_val + (long)pa[q] * B * B + r0 * B;
+    const double2 *Qv = reinterpret_cast<const double2 *>(Ptv + (long)pb[q] * B * 6);
+    double a[RB * B], qj[B * 6];
+#pragma unroll
+    for (int u = 0; u < RB * B; u++) a[u] = __ldg(Av + u);
+#pragma unroll
+    for (int u = 0; u < B * 3; u++) {
+      const double2 v = __ldg(Qv + u);
+      qj[2 * u] = v.x;
+      qj[2 * u + 1] = v.y;
+    }
+#pragma unroll
+    for (int r = 0; r < RB; r++)
+#pragma unroll
+      for (int s = 0; s < 6; s++)
+#pragma unroll
+        for (int cc = 0; cc < B; cc++) acc[r * 6 + s] = __fma_rn(a[r * B + cc], qj[cc * 6 + s], acc[r * 6 + s]);
+  }
+  const int i = P_rowof[e], a = P_col[e];
+  const bool own = agg[i] == a;
+#pragma unroll
+  for (int rr = 0; rr < RB; rr++)
+#pragma unroll
+    for (int s = 0; s < 6; s++) {
+      const int r = r0 + rr;
+      double tt = omega * acc[rr * 6 + s];
+      tt = tt / dpt[(long)i * B + r];
+      const double pt = own ? Ptv[((long)Pt_ptr[i] * B + r) * 6 + s] : 0.0;
+      Pv[(e * B + r) * 6 + s] = pt - tt;
+      Rv[((long)Rinv[e] * 6 + s) * B + r] = pt - tt;
+    }
+}
 __global__ void k_inv_perm(long n, const int *perm, int *inv) {
   long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
   if (t < n) inv[perm[t]] = (int)t;
@@ -1825,6 +1880,7 @@ static void read_level_scalars(Ctx &c) {
 struct LevelCache {
   int *P_rowof = nullptr, *R_perm = nullptr, *G_rowof = nullptr, *AP_rowof = nullptr;
   int *R_inv = nullptr;  // R block of every P block (k_P_values writes R = P^T directly)
+  int *P_pptr = nullptr, *P_pa = nullptr, *P_pb = nullptr;  // block-product pairs of T = A * Pt (k_P_pairs)
   Bsr G;
   // block-product lists of the Galerkin products (symbolic, built once): for output block e of AP (G),
   // the pairs (A block, P block) ((R block, AP block)) with a matching inner index, in ascending order
@@ -2048,7 +2104,16 @@ static void level_numeric(Ctx &c, int l, LevelCache &lc) {
     lc.R_inv = c.alloc<int>(std::max<long>(L.R.nnzb, 1));
     LAUNCH(k_inv_perm, L.R.nnzb, L.R.nnzb, lc.R_perm, lc.R_inv);
   }
-  if (L.b == 3)
+  if (!lc.P_pptr)  // symbolic, once
+    build_pairs(c, L.P.nnzb, lc.P_rowof, L.P.col, L.A, L.Pt, lc.P_pptr, lc.P_pa, lc.P_pb);
+  static const bool p_walk = getenv("AMGF_P_WALK") != nullptr;  // A/B only: the row-walk kernels
+  if (L.b == 3 && !p_walk)
+    LAUNCH((k_P_pairs<3, 1>), L.P.nnzb, L.P.nnzb, lc.P_rowof, L.P.col, lc.P_pptr, lc.P_pa, lc.P_pb, L.A.val, L.agg,
+           L.Pt.ptr, L.Pt.val, L.dpt, c.pw_lev + 2 * l + 1, L.P.val, lc.R_inv, L.R.val);
+  else if (!p_walk)
+    LAUNCH((k_P_pairs<6, 2>), L.P.nnzb * 2, L.P.nnzb, lc.P_rowof, L.P.col, lc.P_pptr, lc.P_pa, lc.P_pb, L.A.val,
+           L.agg, L.Pt.ptr, L.Pt.val, L.dpt, c.pw_lev + 2 * l + 1, L.P.val, lc.R_inv, L.R.val);
+  else if (L.b == 3)
     LAUNCH(k_P_values<3>, L.P.nnzb, L.P.nnzb, lc.P_rowof, L.P.col, L.A.ptr, L.A.col, L.A.val, L.agg, L.Pt.ptr,
            L.Pt.val, L.dpt, c.pw_lev + 2 * l + 1, L.P.val, lc.R_inv, L.R.val);
   else
@@ -2100,14 +2165,15 @@ static void level_numeric(Ctx &c, int l, LevelCache &lc) {
     if (L.b == 3)
       LAUNCH((k_spgemm_vals_pairs<3, 3, 6>), L.AP.nnzb, L.AP.nnzb, lc.AP_pptr, lc.AP_pa, lc.AP_pb, L.A.val, L.P.val,
              L.AP.val);
-    else
+    else if (L.AP.nnzb >= 65536)  // measured at cfg 3 level 1: 458 -> 370 us; the long-list R*AP and the small
+                                  // levels keep the warp form (R*AP 425 vs 958 us, level 2 61 vs 132 us)
       LAUNCH(k_spgemm_vals_half6, L.AP.nnzb * 2, L.AP.nnzb, lc.AP_pptr, lc.AP_pa, lc.AP_pb, L.A.val, L.P.val,
              L.AP.val);
-    if (L.b == 3)
-      LAUNCH((k_spgemm_vals_warp<6, 3, 6>), lc.G.nnzb * 32, lc.G.nnzb, lc.G_pptr, lc.G_pa, lc.G_pb, L.R.val, L.AP.val,
-             lc.G.val);
     else
-      LAUNCH(k_spgemm_vals_half6, lc.G.nnzb * 2, lc.G.nnzb, lc.G_pptr, lc.G_pa, lc.G_pb, L.R.val, L.AP.val, lc.G.val);
+      LAUNCH((k_spgemm_vals_warp<6, 6, 6>), L.AP.nnzb * 32, L.AP.nnzb, lc.AP_pptr, lc.AP_pa, lc.AP_pb, L.A.val,
+             L.P.val, L.AP.val);
+    auto kg = (L.b == 3) ? k_spgemm_vals_warp<6, 3, 6> : k_spgemm_vals_warp<6, 6, 6>;
+    LAUNCH(kg, lc.G.nnzb * 32, lc.G.nnzb, lc.G_pptr, lc.G_pa, lc.G_pb, L.R.val, L.AP.val, lc.G.val);
     }
   }
   if (!lc.G_kt) {  // symbolic, once
