@@ -61,9 +61,11 @@ def load_library():
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(_LIB_PATH):
-        raise RuntimeError(f"libamgf.so not built ({_LIB_PATH}); run __graft_entry__.build()")
-    L = ctypes.CDLL(_LIB_PATH)
+    # AMGF_LIB: an alternative in-tree build of the same library (A/B timing experiments only)
+    path = os.path.join(os.path.dirname(_LIB_PATH), os.environ["AMGF_LIB"]) if os.environ.get("AMGF_LIB") else _LIB_PATH
+    if not os.path.exists(path):
+        raise RuntimeError(f"libamgf.so not built ({path}); run __graft_entry__.build()")
+    L = ctypes.CDLL(path)
     P, I, D = ctypes.c_void_p, ctypes.c_int32, ctypes.c_double
     L.amgf_default_config.argtypes = [ctypes.POINTER(Config)]
     L.amgf_setup.argtypes = [I, P, P, P, I, P, P, P, P, P, I, P, ctypes.POINTER(Config), P, ctypes.POINTER(P)]

@@ -583,6 +583,9 @@ void ctx_init(Ctx &c, void *stream) {
 using namespace amgf;
 
 
+#ifdef AMGF_R1_TRACE
+namespace amgf { int r1_trace_read(unsigned long long *h, int n); }
+#endif
 extern "C" {
 
 void amgf_default_config(amgf_config *cfg) {
@@ -792,6 +795,9 @@ amgf_status amgf_level_get(amgf_handle h, int32_t which, int32_t level, void *ds
 
 int64_t amgf_launch_count(amgf_handle h) { return h ? h->launches : -1; }
 
+#ifdef AMGF_R1_TRACE
+int amgf_debug_r1_trace(unsigned long long *h, int n) { return amgf::r1_trace_read(h, n); }
+#endif
 int64_t amgf_debug_guard_check(amgf_handle h) {
   if (!h) return -1;
   if (!Ctx::guard_enabled()) return -2;

@@ -194,6 +194,12 @@ __global__ void k_S_values(long nnzb, const int *S_rowof, const int *S_col, cons
   long e = blockIdx.x * (long)blockDim.x + threadIdx.x;
   if (e >= nnzb) return;
   const int I = S_rowof[e], Jn = S_col[e], kb = S_kblk[e];
+  if (Jt_ptr[3 * I] == Jt_ptr[3 * I + 3] && (Jn != I || !D_lo)) {
+    // no constraint touches the row's dofs and no bound term: every chain is the K value alone
+#pragma unroll
+    for (int q = 0; q < 9; q++) S_val[e * 9 + q] = kb >= 0 ? K_val[(long)kb * 9 + q] : 0.0;
+    return;
+  }
   for (int r = 0; r < 3; r++)
     for (int cc = 0; cc < 3; cc++) {
       const int p = 3 * I + r, q = 3 * Jn + cc;
@@ -218,40 +224,90 @@ __global__ void k_S_values(long nnzb, const int *S_rowof, const int *S_col, cons
 }
 
 // ------------------------------------------------------------------ s2: I_c and Z
-// Fine-level SELL refresh fused with the l1 / point diagonals (same values as k_sell_vals + k_diag): one
-// thread per block row I (the SELL-32 row, natural order at level 0) streams its BSR blocks in order, stores
-// them to the SELL copy (one 256-byte segment per component across the 32 rows of a slice) and forms the
-// diagonals (C3) from the same loads.
+// Fixed tree of C14 over CTA values in shared memory (the solve kernels' cta_tree); returns the sum to all.
+__device__ __forceinline__ double cta_tree_s(double v, double *sm) {
+  const int t = threadIdx.x;
+  sm[t] = v;
+  __syncthreads();
+#pragma unroll
+  for (int w = CTA / 2; w >= 1; w >>= 1) {
+    if (t < w) sm[t] = sm[t] + sm[t + w];
+    __syncthreads();
+  }
+  const double r = sm[0];
+  __syncthreads();
+  return r;
+}
+// Fine-level SELL refresh fused with the l1 / point diagonals (same values as k_sell_vals + k_diag) and, when
+// w is given, with the first power step (C18) of the level: one thread per block row I (the SELL-32 row,
+// natural order at level 0) streams its BSR blocks in order, stores them to the SELL copy (one 256-byte
+// segment per component across the 32 rows of a slice), forms the diagonals (C3) and the row chain of
+// A v0 with v0_j = 1 + (j mod 7)/8 (C2, the SpMV's order), w = (A v0) / d, and the C14 level-1 partials of
+// w.w and v0.v0 (thread I = block row 256 * CTA + t, as k_dot1).
 __global__ void __launch_bounds__(CTA) k_sell_diag(int nodes, const int *__restrict__ S_ptr,
                                                    const int *__restrict__ S_col, const double *__restrict__ S_val,
                                                    const int *__restrict__ slice_ptr, double *__restrict__ sval,
-                                                   double *__restrict__ dl1, double *__restrict__ dpt) {
+                                                   double *__restrict__ dl1, double *__restrict__ dpt,
+                                                   double *__restrict__ w, double *__restrict__ part_w,
+                                                   double *__restrict__ part_v) {
+  __shared__ double red[CTA];
   const int I = blockIdx.x * CTA + threadIdx.x;
-  if (I >= nodes) return;
-  const int lane = I & 31;
-  const long sbase = slice_ptr[I >> 5];
-  const int e0 = S_ptr[I], e1 = S_ptr[I + 1];
-  double d[3] = {0.0, 0.0, 0.0}, dp[3] = {0.0, 0.0, 0.0};
-  for (int e = e0; e < e1; e++) {
-    const int Jn = S_col[e];
-    double v[9];
+  double sw = 0.0, sv = 0.0;
+  if (I < nodes) {
+    const int lane = I & 31;
+    const long sbase = slice_ptr[I >> 5];
+    const int e0 = S_ptr[I], e1 = S_ptr[I + 1];
+    double d[3] = {0.0, 0.0, 0.0}, dp[3] = {0.0, 0.0, 0.0}, acc[3] = {0.0, 0.0, 0.0};
+    for (int e = e0; e < e1; e++) {
+      const int Jn = S_col[e];
+      double v[9];
 #pragma unroll
-    for (int q = 0; q < 9; q++) v[q] = S_val[(long)e * 9 + q];
-    const long slot = sbase + (e - e0);
+      for (int q = 0; q < 9; q++) v[q] = S_val[(long)e * 9 + q];
+      const long slot = sbase + (e - e0);
 #pragma unroll
-    for (int q = 0; q < 9; q++) sval[(slot * 9 + q) * 32 + lane] = v[q];
+      for (int q = 0; q < 9; q++) sval[(slot * 9 + q) * 32 + lane] = v[q];
 #pragma unroll
-    for (int r = 0; r < 3; r++)
+      for (int r = 0; r < 3; r++)
 #pragma unroll
-      for (int cc = 0; cc < 3; cc++) {
-        d[r] = d[r] + fabs(v[3 * r + cc]);
-        if (Jn == I && cc == r) dp[r] = v[3 * r + cc];
+        for (int cc = 0; cc < 3; cc++) {
+          d[r] = d[r] + fabs(v[3 * r + cc]);
+          if (Jn == I && cc == r) dp[r] = v[3 * r + cc];
+        }
+      if (w) {
+#pragma unroll
+        for (int cc = 0; cc < 3; cc++) {
+          const double x0 = 1.0 + (double)((3L * Jn + cc) % 7) / 8.0;
+#pragma unroll
+          for (int r = 0; r < 3; r++) acc[r] = __fma_rn(v[3 * r + cc], x0, acc[r]);
+        }
       }
-  }
+    }
 #pragma unroll
-  for (int r = 0; r < 3; r++) {
-    dl1[3L * I + r] = d[r];
-    dpt[3L * I + r] = dp[r];
+    for (int r = 0; r < 3; r++) {
+      dl1[3L * I + r] = d[r];
+      dpt[3L * I + r] = dp[r];
+    }
+    if (w) {
+#pragma unroll
+      for (int r = 0; r < 3; r++) {
+        const double wi = acc[r] / dp[r];
+        w[3L * I + r] = wi;
+        sw = __fma_rn(wi, wi, sw);
+      }
+#pragma unroll
+      for (int r = 0; r < 3; r++) {
+        const double x0 = 1.0 + (double)((3L * I + r) % 7) / 8.0;
+        sv = __fma_rn(x0, x0, sv);
+      }
+    }
+  }
+  if (w) {  // block-uniform
+    const double tw = cta_tree_s(sw, red);
+    const double tv = cta_tree_s(sv, red);
+    if (threadIdx.x == 0) {
+      part_w[blockIdx.x] = tw;
+      part_v[blockIdx.x] = tv;
+    }
   }
 }
 __global__ void k_mark_cols(int nnz, const int *J_col, int *mark) {
@@ -1178,18 +1234,30 @@ __global__ void k_spgemm_vals_warp(long nnzc, const int *pptr, const int *pa, co
     ss[u] = en % BC;
     acc[u] = 0.0;
   }
+  // pairs in batches of PF: all index and operand loads of a batch are issued before its FMAs (the long
+  // R*AP lists are latency chains otherwise)
+  constexpr int PF = (E * IN > 6) ? 2 : 4;
   const int q1 = pptr[e + 1];
-  for (int q = pptr[e]; q < q1; q++) {
-    const double *Av = A_val + (long)pa[q] * BR * IN;
-    const double *Bv = B_val + (long)pb[q] * IN * BC;
+  for (int q0 = pptr[e]; q0 < q1; q0 += PF) {
+    double a[PF][E][IN], bb[PF][E][IN];
 #pragma unroll
-    for (int u = 0; u < E; u++) {
-      double a[IN], bb[IN];
+    for (int f = 0; f < PF; f++) {
+      const int q = min(q0 + f, q1 - 1);
+      const double *Av = A_val + (long)pa[q] * BR * IN;
+      const double *Bv = B_val + (long)pb[q] * IN * BC;
 #pragma unroll
-      for (int t = 0; t < IN; t++) { a[t] = __ldg(Av + rr[u] * IN + t); bb[t] = __ldg(Bv + t * BC + ss[u]); }
+      for (int u = 0; u < E; u++)
 #pragma unroll
-      for (int t = 0; t < IN; t++) acc[u] = __fma_rn(a[t], bb[t], acc[u]);
+        for (int t = 0; t < IN; t++) { a[f][u][t] = __ldg(Av + rr[u] * IN + t); bb[f][u][t] = __ldg(Bv + t * BC + ss[u]); }
     }
+#pragma unroll
+    for (int f = 0; f < PF; f++)
+      if (q0 + f < q1) {
+#pragma unroll
+        for (int u = 0; u < E; u++)
+#pragma unroll
+          for (int t = 0; t < IN; t++) acc[u] = __fma_rn(a[f][u][t], bb[f][u][t], acc[u]);
+      }
   }
 #pragma unroll
   for (int u = 0; u < E; u++)
@@ -1384,7 +1452,11 @@ __global__ void k_gal_hitw(const GalGrp *__restrict__ grp, const int2 *__restric
 struct RapGrp {
   int a, e0, e1, pad;
 };
-constexpr int RAP_NT = 128, RAP_TC = 16, RAP_SCAP = 104, RAP_NS = 3;  // RAP_NT: consumer threads
+#ifndef AMGF_RAP_SCAP  // A/B builds (tools/ab_build.sh) may override the ring geometry
+#define AMGF_RAP_SCAP 64  // measured at cfg 3: 64 / 104 / 80 (4 stages) -> 1202 / 1248 / 1456 us
+#define AMGF_RAP_NS 3
+#endif
+constexpr int RAP_NT = 128, RAP_TC = 16, RAP_SCAP = AMGF_RAP_SCAP, RAP_NS = AMGF_RAP_NS;  // RAP_NT: consumers
 constexpr int RAP_STAGE = (RAP_TC + RAP_SCAP) * 18;  // doubles per stage
 // Warp-specialised streamed form (same chains): warp 4 is the producer (chunk plan from the per-R-block
 // (AP row start, length) table, TMA bulk copies of the R blocks, the AP rows and the chunk's rows of the
@@ -1831,7 +1903,8 @@ static void thin_numeric(Ctx &c, long nthin_nnz) {
   LAUNCH(k_zr_vals, c.zr_nnz, c.zr_nnz, c.zr_src, c.lev[0].A.val, c.zr_val);
 }
 
-static void power_iteration(Ctx &c, Level &L, int lev) {
+// first_done: the first step's w = (A v0) / d and its C14 partials were formed by k_sell_diag (fine level)
+static void power_iteration(Ctx &c, Level &L, int lev, bool first_done = false) {
   if (!c.pw_v) {  // once per handle: no allocation on the numeric re-setup path
     c.pw_v = c.alloc<double>(c.n);
     c.pw_w = c.alloc<double>(c.n);
@@ -1840,13 +1913,15 @@ static void power_iteration(Ctx &c, Level &L, int lev) {
   if (!c.pw_s) c.pw_s = c.alloc<double>(4);
   if (!c.pw_lev) c.pw_lev = c.alloc<double>(2 * MAXLEV);
   if (!c.pw_part) c.pw_part = c.alloc<double>(nblk(c.n) + 1);
-  LAUNCH(k_pow_init, L.n, L.n, v);
+  if (!first_done) LAUNCH(k_pow_init, L.n, L.n, v);
   // per step: w = (A v) / d with the C14 partials of w.w and v.v (fused into the fine SpMV), both level-2
   // sums, then lambda and v = w / ||w|| (k_pow_scale)
   const bool fused = L.As.val && L.b == 3 && L.As.br == 3 && !L.As.perm;
   const long nb = L.n / L.b, C = (nb + CTA - 1) / CTA;
   for (int it = 0; it < c.cfg.power_iters; it++) {
-    if (fused) {
+    if (it == 0 && first_done) {
+      // w and the partials are already there
+    } else if (fused) {
       launch_sell_pow(c, L.As, v, L.dpt, w, c.dot_part, c.pw_part);
     } else {
       if (L.As.val) {
@@ -2079,7 +2154,7 @@ static void smoother_data(Ctx &c, Level &L) {
   else LAUNCH(k_block_l1<6>, L.nodes, L.nodes, L.A.ptr, L.A.col, L.A.val, L.bfac, c.err);
 }
 
-static void level_numeric(Ctx &c, int l, LevelCache &lc) {
+static void level_numeric(Ctx &c, int l, LevelCache &lc, bool pow_first_done = false) {
   Level &L = c.lev[l];
   Level &Lc = c.lev[l + 1];
   {
@@ -2098,7 +2173,7 @@ static void level_numeric(Ctx &c, int l, LevelCache &lc) {
       }
     }
   }
-  power_iteration(c, L, l);
+  power_iteration(c, L, l, pow_first_done);
   static const bool gal_old = getenv("AMGF_GAL_OLD") != nullptr;  // A/B only: the thread-per-block kernels
   if (!lc.R_inv) {  // symbolic, once
     lc.R_inv = c.alloc<int>(std::max<long>(L.R.nnzb, 1));
@@ -2634,14 +2709,17 @@ void setup_numeric(Ctx &c, const double *D, const double *D_lo, const double *D_
   }
   // the fine SELL copy and the level-0 diagonals in one pass (the fine SELL keeps the natural row order)
   const bool fused_S = L0.As.val && L0.As.br == 3 && !L0.As.perm && L0.As.nrows == L0.nodes;
+  // ... and the fine level's first power step (the SELL pass reads every block once anyway)
+  const bool pow0 = fused_S && c.nlev >= 2 && c.cfg.power_iters > 0 && c.pw_w && c.pw_part;
   if (fused_S)
-    LAUNCH(k_sell_diag, L0.nodes, L0.nodes, L0.A.ptr, L0.A.col, L0.A.val, L0.As.slice_ptr, L0.As.val, L0.dl1, L0.dpt);
+    LAUNCH(k_sell_diag, L0.nodes, L0.nodes, L0.A.ptr, L0.A.col, L0.A.val, L0.As.slice_ptr, L0.As.val, L0.dl1, L0.dpt,
+           pow0 ? c.pw_w : nullptr, c.dot_part, c.pw_part);
   else
     LAUNCH(k_diag, L0.n, L0.nodes, 3, L0.A.ptr, L0.A.col, L0.A.val, L0.dl1, L0.dpt);
   smoother_data(c, L0);
   for (int l = 0; l + 1 < c.nlev; l++) {
     if (l > 0 || !fused_S) build_sell(c, c.lev[l].A, c.lev[l].As, false, l > 0);
-    level_numeric(c, l, C.lc[l]);  // its device error flags are checked once, after the join
+    level_numeric(c, l, C.lc[l], l == 0 && pow0);  // device error flags are checked once, after the join
     build_sell(c, c.lev[l].P, c.lev[l].Ps, false, l > 0);
   }
   if (c.nlev == 1) build_sell(c, L0.A, L0.As, false, false);

@@ -218,6 +218,12 @@ __global__ void __launch_bounds__(CTA) k_sell(int nrows, const int *__restrict__
 
 // Latency-oriented variant for scalar-row (1 x BC) SELL of the small coarse levels: D slots of values and
 // x in flight (register ring, fully unrolled), column indices 2D slots ahead.  Same chain as k_sell (C2).
+#ifdef AMGF_R1_TRACE
+__device__ unsigned long long g_r1_trace[8192 * 4];
+int r1_trace_read(unsigned long long *h, int n) {
+  return cudaMemcpyFromSymbol(h, g_r1_trace, sizeof(unsigned long long) * std::min(n, 8192 * 4)) == cudaSuccess ? 0 : -1;
+}
+#endif
 __constant__ int c_r1_prefetch = 8;  // L2 prefetch distance of k_sell_r1 in slots (0: off; 8 measured best:
                                  // V-cycle 1030 -> 1018 us at cfg 3; 16 and 32 are slower)
 __device__ __forceinline__ int r1_prefetch_slots() { return c_r1_prefetch; }
@@ -232,6 +238,10 @@ __global__ void __launch_bounds__(CTA) k_sell_r1(int nrows, const int *__restric
   const int row = blockIdx.x * CTA + threadIdx.x;
   const int lane = threadIdx.x & 31;
   if (row >= nrows) return;
+#ifdef AMGF_R1_TRACE
+  unsigned long long t_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
   const int len = rowlen[row];
   const long base = slice_ptr[row >> 5];
   const int *cp = col + base * 32 + lane;
@@ -309,6 +319,23 @@ __global__ void __launch_bounds__(CTA) k_sell_r1(int nrows, const int *__restric
   } else if (MODE == MODE_YDIV) {
     y[i] = acc / d[i];
   }
+#ifdef AMGF_R1_TRACE  // per-warp start / end / SM / longest row of the last launch (A/B builds only)
+  {
+    unsigned long long t_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    int mlen = len;
+    for (int o = 16; o; o >>= 1) mlen = max(mlen, __shfl_xor_sync(__activemask(), mlen, o));
+    const int wg = row >> 5;
+    if (lane == 0 && wg < 8192) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      g_r1_trace[wg * 4 + 0] = t_start;
+      g_r1_trace[wg * 4 + 1] = t_end;
+      g_r1_trace[wg * 4 + 2] = smid;
+      g_r1_trace[wg * 4 + 3] = (unsigned long long)mlen | ((unsigned long long)nrows << 32);
+    }
+  }
+#endif
 }
 
 template <int BR, int BC>
