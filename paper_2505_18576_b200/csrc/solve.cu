@@ -93,14 +93,17 @@ __device__ __forceinline__ void sell_row(int row, const int *__restrict__ slice_
     const double *vp = val + base * (BR * BC * 32) + lane;
     // software pipeline: slot s+1's column, values and x gather are in flight while slot s is consumed
     double vcur[BR * BC], xcur[BC];
-    int cnext = 0;
+    int cnext = 0, c0 = 0;
     if (len > 0) {
-      const int c0 = ldg_stream_i(cp);
-      gather_x<BC>(x, c0, xcur);
+      c0 = ldg_stream_i(cp);
 #pragma unroll
       for (int q = 0; q < BR * BC; q++) vcur[q] = ldg_stream(vp + q * 32);
       cnext = ldg_stream_i(cp + (len > 1 ? 32 : 0));
     }
+    // PDL: the operator's first slot is in flight before the wait for the previous kernel (x, b, d are its
+    // results); a no-op without a programmatic launch
+    pdl_wait();
+    if (len > 0) gather_x<BC>(x, c0, xcur);
     for (int s = 0; s < len; s++) {
       // branch-free prefetch (the last slot is re-read once at the end)
       const int s1 = min(s + 1, len - 1), s2 = min(s + 2, len - 1);
@@ -136,6 +139,7 @@ __global__ void __launch_bounds__(CTA) k_sell(int nrows, const int *__restrict__
 #pragma unroll
   for (int r = 0; r < BR; r++) acc[r] = 0.0;
   if (row < nrows) sell_row<BR, BC>(row, slice_ptr, rowlen, col, val, x, acc);
+  pdl_launch_dependents();  // the next kernel's CTAs may start their operator prologue in our tail
   if (MODE == MODE_DOT) {
     __shared__ double red[CTA];
     double s = 0.0;
@@ -250,18 +254,28 @@ __global__ void __launch_bounds__(CTA) k_sell_r1(int nrows, const int *__restric
   double rv[D][BC], rx[D][BC];
   int rc[D];
   const int last = len - 1;
+  int rc2[D];
+  if (len > 0) {
+#pragma unroll
+    for (int q = 0; q < D; q++) {
+      rc[q] = ldg_stream_i(cp + (long)min(q, last) * 32);
+      rc2[q] = ldg_stream_i(cp + (long)min(q + D, last) * 32);
+    }
+#pragma unroll
+    for (int q = 0; q < D; q++) {
+      const int sq = min(q, last);
+#pragma unroll
+      for (int e = 0; e < BC; e++) rv[q][e] = ldg_stream(vp + ((long)sq * BC + e) * 32);
+    }
+  }
+  pdl_wait();  // PDL: columns and values of the first D slots are in flight; x is the previous kernel's result
   if (len > 0) {
   // prologue: columns of slots D..2D-1, values + x of slots 0..D-1
 #pragma unroll
-  for (int q = 0; q < D; q++) rc[q] = ldg_stream_i(cp + (long)min(q, last) * 32);
-#pragma unroll
   for (int q = 0; q < D; q++) {
-    const int sq = min(q, last);
-#pragma unroll
-    for (int e = 0; e < BC; e++) rv[q][e] = ldg_stream(vp + ((long)sq * BC + e) * 32);
 #pragma unroll
     gather_x<BC>(x, rc[q], rx[q]);
-    rc[q] = ldg_stream_i(cp + (long)min(q + D, last) * 32);
+    rc[q] = rc2[q];
   }
   // L2 prefetch window (pf slots ahead of the register ring): the slice's values of slots
   // [s0 + pf, s0 + pf + D) by one TMA bulk prefetch from the lowest active lane, so the ring's loads
@@ -301,6 +315,7 @@ __global__ void __launch_bounds__(CTA) k_sell_r1(int nrows, const int *__restric
     }
   }
   }
+  pdl_launch_dependents();
   const long i = perm ? perm[row] : row;  // rows sorted by length (SELL packing), any mode
   if (MODE == MODE_Y) {
     y[i] = acc;
@@ -338,6 +353,18 @@ __global__ void __launch_bounds__(CTA) k_sell_r1(int nrows, const int *__restric
 #endif
 }
 
+// launch with programmatic dependent launch (the SELL kernels wait for their predecessor only before the
+// first x gather, so their operator prologue overlaps its tail); AMGF_NO_PDL=1 launches plainly (A/B)
+template <typename... KA, typename... A>
+static void go(Ctx &c, bool pdl, void (*k)(KA...), dim3 g, dim3 t, A... a) {
+  if (pdl) launch_pdl(c.stream, k, g, t, 0, a...);
+  else k<<<g, t, 0, c.stream>>>(((KA)a)...);
+}
+static bool sell_pdl() {
+  static const bool on = getenv("AMGF_NO_PDL") == nullptr;
+  return on;
+}
+
 template <int BR, int BC>
 static void sell_dispatch(Ctx &c, const Sell &A, int mode, const double *x, const double *b, const double *d,
                           const double *add, double *y, double *dp, ChebArgs ch = ChebArgs{}) {
@@ -366,33 +393,34 @@ static void sell_dispatch(Ctx &c, const Sell &A, int mode, const double *x, cons
       CK(cudaFuncSetAttribute(k_sell<BR, BC, MODE_POW>, cudaFuncAttributePreferredSharedMemoryCarveout, 50));
     }
   }
+  const bool pdl = sell_pdl();
   if (BR == 1 && mode != MODE_DOT) {
     switch (mode) {
-      case MODE_Y: k_sell_r1<BC, MODE_Y, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm, ch); break;
-      case MODE_RESID: k_sell_r1<BC, MODE_RESID, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm, ch); break;
-      case MODE_SMOOTH: k_sell_r1<BC, MODE_SMOOTH, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm, ch); break;
-      case MODE_SMOOTH_ADD: k_sell_r1<BC, MODE_SMOOTH_ADD, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm, ch); break;
-      case MODE_ADDTO: k_sell_r1<BC, MODE_ADDTO, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm, ch); break;
-      case MODE_CHEB1: k_sell_r1<BC, MODE_CHEB1, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm, ch); break;
-      case MODE_CHEB: k_sell_r1<BC, MODE_CHEB, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm, ch); break;
-      case MODE_YDIV: k_sell_r1<BC, MODE_YDIV, 4><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm, ch); break;
+      case MODE_Y: go(c, pdl, k_sell_r1<BC, MODE_Y, 4>, g, t, A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm, ch); break;
+      case MODE_RESID: go(c, pdl, k_sell_r1<BC, MODE_RESID, 4>, g, t, A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm, ch); break;
+      case MODE_SMOOTH: go(c, pdl, k_sell_r1<BC, MODE_SMOOTH, 4>, g, t, A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm, ch); break;
+      case MODE_SMOOTH_ADD: go(c, pdl, k_sell_r1<BC, MODE_SMOOTH_ADD, 4>, g, t, A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm, ch); break;
+      case MODE_ADDTO: go(c, pdl, k_sell_r1<BC, MODE_ADDTO, 4>, g, t, A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm, ch); break;
+      case MODE_CHEB1: go(c, pdl, k_sell_r1<BC, MODE_CHEB1, 4>, g, t, A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm, ch); break;
+      case MODE_CHEB: go(c, pdl, k_sell_r1<BC, MODE_CHEB, 4>, g, t, A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm, ch); break;
+      case MODE_YDIV: go(c, pdl, k_sell_r1<BC, MODE_YDIV, 4>, g, t, A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, A.perm, ch); break;
       default: throw Error{AMGF_ERR_ARG, "sell spmv: mode not available for scalar-row SELL"};
     }
     after_launch(c, "k_sell_r1");
     return;
   }
   switch (mode) {
-    case MODE_Y: k_sell<BR, BC, MODE_Y><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
-    case MODE_RESID: k_sell<BR, BC, MODE_RESID><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
-    case MODE_SMOOTH: k_sell<BR, BC, MODE_SMOOTH><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
-    case MODE_DOT: k_sell<BR, BC, MODE_DOT><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
-    case MODE_SMOOTH_ADD: k_sell<BR, BC, MODE_SMOOTH_ADD><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
-    case MODE_ADDTO: k_sell<BR, BC, MODE_ADDTO><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
-    case MODE_CHEB1: k_sell<BR, BC, MODE_CHEB1><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
-    case MODE_CHEB: k_sell<BR, BC, MODE_CHEB><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
-    case MODE_CHEB_DOT: k_sell<BR, BC, MODE_CHEB_DOT><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
-    case MODE_YDIV: k_sell<BR, BC, MODE_YDIV><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
-    case MODE_POW: k_sell<BR, BC, MODE_POW><<<g, t, 0, c.stream>>>(A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
+    case MODE_Y: go(c, pdl, k_sell<BR, BC, MODE_Y>, g, t, A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
+    case MODE_RESID: go(c, pdl, k_sell<BR, BC, MODE_RESID>, g, t, A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
+    case MODE_SMOOTH: go(c, pdl, k_sell<BR, BC, MODE_SMOOTH>, g, t, A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
+    case MODE_DOT: go(c, pdl, k_sell<BR, BC, MODE_DOT>, g, t, A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
+    case MODE_SMOOTH_ADD: go(c, pdl, k_sell<BR, BC, MODE_SMOOTH_ADD>, g, t, A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
+    case MODE_ADDTO: go(c, pdl, k_sell<BR, BC, MODE_ADDTO>, g, t, A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
+    case MODE_CHEB1: go(c, pdl, k_sell<BR, BC, MODE_CHEB1>, g, t, A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
+    case MODE_CHEB: go(c, pdl, k_sell<BR, BC, MODE_CHEB>, g, t, A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
+    case MODE_CHEB_DOT: go(c, pdl, k_sell<BR, BC, MODE_CHEB_DOT>, g, t, A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
+    case MODE_YDIV: go(c, pdl, k_sell<BR, BC, MODE_YDIV>, g, t, A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
+    case MODE_POW: go(c, pdl, k_sell<BR, BC, MODE_POW>, g, t, A.nrows, A.slice_ptr, A.rowlen, A.col, A.val, x, b, d, add, y, dp, A.perm, ch); break;
     default: throw Error{AMGF_ERR_ARG, "sell spmv: unknown mode"};
   }
   after_launch(c, __func__);
