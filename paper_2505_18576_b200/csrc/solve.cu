@@ -458,6 +458,7 @@ __global__ void k_axpy2_cheb0(long n, const Scalars *__restrict__ sc, const doub
                               const double *__restrict__ q, double *__restrict__ x, double *__restrict__ r,
                               const double *__restrict__ d, double c0, double *__restrict__ dir,
                               double *__restrict__ xs) {
+  pdl_wait();  // alpha is the previous kernel's result
   const double a = sc->alpha;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
     x[i] = __fma_rn(a, p[i], x[i]);
@@ -467,12 +468,14 @@ __global__ void k_axpy2_cheb0(long n, const Scalars *__restrict__ sc, const doub
     dir[i] = v;
     xs[i] = v;
   }
+  pdl_launch_dependents();
 }
 // the same per-element arithmetic on pairs (16-byte loads and stores)
 __global__ void k_axpy2_cheb0_v2(long n2, const Scalars *__restrict__ sc, const double2 *__restrict__ p,
                                  const double2 *__restrict__ q, double2 *__restrict__ x, double2 *__restrict__ r,
                                  const double2 *__restrict__ d, double c0, double2 *__restrict__ dir,
                                  double2 *__restrict__ xs) {
+  pdl_wait();
   const double a = sc->alpha;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n2; i += (long)gridDim.x * blockDim.x) {
     const double2 pp = p[i], qq = q[i], dd = d[i];
@@ -488,6 +491,7 @@ __global__ void k_axpy2_cheb0_v2(long n2, const Scalars *__restrict__ sc, const 
     dir[i] = v;
     xs[i] = v;
   }
+  pdl_launch_dependents();
 }
 static bool pairs_ok(long n, std::initializer_list<const void *> ps) {
   if (n % 2) return false;
@@ -498,43 +502,48 @@ static bool pairs_ok(long n, std::initializer_list<const void *> ps) {
 void launch_axpy2_cheb0(Ctx &c, long n, const double *p, const double *q, double *x, double *r, const double *d,
                         double c0, double *dir, double *xs) {
   if (pairs_ok(n, {p, q, x, r, d, dir, xs}))
-    k_axpy2_cheb0_v2<<<nblk(n / 2), CTA, 0, c.stream>>>(n / 2, c.sc, (const double2 *)p, (const double2 *)q,
-                                                        (double2 *)x, (double2 *)r, (const double2 *)d, c0,
-                                                        (double2 *)dir, (double2 *)xs);
+    go(c, sell_pdl(), k_axpy2_cheb0_v2, nblk(n / 2), CTA, n / 2, c.sc, (const double2 *)p, (const double2 *)q,
+       (double2 *)x, (double2 *)r, (const double2 *)d, c0, (double2 *)dir, (double2 *)xs);
   else
-    k_axpy2_cheb0<<<nblk(n), CTA, 0, c.stream>>>(n, c.sc, p, q, x, r, d, c0, dir, xs);
+    go(c, sell_pdl(), k_axpy2_cheb0, nblk(n), CTA, n, c.sc, p, q, x, r, d, c0, dir, xs);
   after_launch(c, "k_axpy2_cheb0");
 }
 
 // Chebyshev application from x = 0 (C23): t = b/d, dir = c0 t, x = dir.
 __global__ void k_cheb0(long n, const double *__restrict__ b, const double *__restrict__ d, double c0,
                         double *__restrict__ dir, double *__restrict__ x) {
+  pdl_wait();  // b is the previous kernel's result
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
     const double t = b[i] / d[i];
     const double v = c0 * t;
     dir[i] = v;
     x[i] = v;
   }
+  pdl_launch_dependents();
 }
 // the same per-element arithmetic on pairs (16-byte loads and stores)
 __global__ void k_cheb0_v2(long n2, const double2 *__restrict__ b, const double2 *__restrict__ d, double c0,
                            double2 *__restrict__ dir, double2 *__restrict__ x) {
-  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n2; i += (long)gridDim.x * blockDim.x) {
-    const double2 bb = b[i], dd = d[i];
+  const long i0 = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  const double2 d0 = i0 < n2 ? d[i0] : make_double2(1.0, 1.0);  // the diagonal is not the predecessor's output
+  pdl_wait();
+  for (long i = i0; i < n2; i += (long)gridDim.x * blockDim.x) {
+    const double2 bb = b[i], dd = (i == i0) ? d0 : d[i];
     double2 v;
     v.x = c0 * (bb.x / dd.x);
     v.y = c0 * (bb.y / dd.y);
     dir[i] = v;
     x[i] = v;
   }
+  pdl_launch_dependents();
 }
 void launch_cheb0(Ctx &c, long n, const double *b, const double *d, double c0, double *dir, double *x) {
   const bool v2 = (n % 2 == 0) && !(((uintptr_t)b | (uintptr_t)d | (uintptr_t)dir | (uintptr_t)x) & 15);
   if (v2)
-    k_cheb0_v2<<<nblk(n / 2), CTA, 0, c.stream>>>(n / 2, (const double2 *)b, (const double2 *)d, c0, (double2 *)dir,
-                                                  (double2 *)x);
+    go(c, sell_pdl(), k_cheb0_v2, nblk(n / 2), CTA, n / 2, (const double2 *)b, (const double2 *)d, c0,
+       (double2 *)dir, (double2 *)x);
   else
-    k_cheb0<<<nblk(n), CTA, 0, c.stream>>>(n, b, d, c0, dir, x);
+    go(c, sell_pdl(), k_cheb0, nblk(n), CTA, n, b, d, c0, dir, x);
   after_launch(c, "k_cheb0");
 }
 
@@ -669,6 +678,7 @@ __global__ void __launch_bounds__(CTA, 2) k_restrict(int nrows, const int *__res
   const int w = (blockIdx.x * CTA + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= nrows) return;  // warp-uniform
+  pdl_wait();  // r is the previous kernel's result
   double acc[6];
 #pragma unroll
   for (int q = 0; q < 6; q++) acc[q] = 0.0;
@@ -722,6 +732,7 @@ __global__ void __launch_bounds__(RCTA) k_restrict_row(int nrows6, const int *__
   const int w = (blockIdx.x * RCTA + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= nrows6) return;  // warp-uniform
+  pdl_wait();
   const int a = w / 6, rr = w % 6;
   const int beg = ptr[a], end = ptr[a + 1];
   double acc = 0.0;
@@ -779,9 +790,9 @@ void launch_restrict(Ctx &c, const Bsr &R, const double *r, double *bc) {
   // (level 0 reads the group-interleaved copy of R's values: 68 -> 59 us at cfg 3)
   if (R.bc == 3) {
     REQUIRE(R.ival, AMGF_ERR_ARG, "restriction: interleaved R values missing");
-    k_restrict<3><<<nblk(threads), CTA, 0, c.stream>>>(R.nbr, R.ptr, R.col, R.ival, r, bc);
+    go(c, sell_pdl(), k_restrict<3>, nblk(threads), CTA, R.nbr, R.ptr, R.col, (const double *)R.ival, r, bc);
   }
-  else k_restrict_row<6><<<nblk(threads * 6, RCTA), RCTA, 0, c.stream>>>(R.nbr * 6, R.ptr, R.col, R.val, r, bc);
+  else go(c, sell_pdl(), k_restrict_row<6>, nblk(threads * 6, RCTA), RCTA, R.nbr * 6, R.ptr, R.col, (const double *)R.val, r, bc);
   after_launch(c, __func__);
 }
 
@@ -809,12 +820,14 @@ __global__ void k_axpy2(long n, const Scalars *__restrict__ sc, const double *__
 }
 // p = fma(beta, p, z)   (C15)
 __global__ void k_xpby(long n, const Scalars *__restrict__ sc, const double *__restrict__ z, double *__restrict__ p) {
+  pdl_wait();
   const double be = sc->beta;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
     p[i] = __fma_rn(be, p[i], z[i]);
 }
 __global__ void k_xpby_v2(long n2, const Scalars *__restrict__ sc, const double2 *__restrict__ z,
                           double2 *__restrict__ p) {
+  pdl_wait();  // beta is the previous kernel's result
   const double be = sc->beta;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n2; i += (long)gridDim.x * blockDim.x) {
     const double2 zz = z[i];
@@ -847,9 +860,9 @@ void launch_axpy2(Ctx &c, long n, const double *p, const double *q, double *x, d
 }
 void launch_xpby(Ctx &c, long n, const double *z, double *p) {
   if (pairs_ok(n, {z, p}))
-    k_xpby_v2<<<vgrid(n / 2), CTA, 0, c.stream>>>(n / 2, c.sc, (const double2 *)z, (double2 *)p);
+    go(c, sell_pdl(), k_xpby_v2, vgrid(n / 2), CTA, n / 2, (const Scalars *)c.sc, (const double2 *)z, (double2 *)p);
   else
-    k_xpby<<<vgrid(n), CTA, 0, c.stream>>>(n, c.sc, z, p);
+    go(c, sell_pdl(), k_xpby, vgrid(n), CTA, n, (const Scalars *)c.sc, z, p);
   after_launch(c, __func__);
 }
 
@@ -867,6 +880,7 @@ __global__ void __launch_bounds__(CTA) k_dot1(long nb, int b, const double *__re
 
 __global__ void __launch_bounds__(CTA) k_dot2(long C, const double *__restrict__ part, Scalars *sc, int kind, int *err) {
   __shared__ double red[CTA];
+  pdl_wait();  // the partials are the previous kernel's result
   double acc = 0.0;
   // the same sequential sum per thread (c = tid, tid + CTA, ...), its loads issued 8 at a time
   long c = threadIdx.x;
@@ -951,7 +965,7 @@ void launch_pow_fin(Ctx &c, long C, const double *part_w, const double *part_v, 
 }
 
 void launch_dot_finish(Ctx &c, long C, int finish) {
-  k_dot2<<<1, CTA, 0, c.stream>>>(C, c.dot_part, c.sc, finish, c.err);
+  go(c, sell_pdl(), k_dot2, 1, CTA, C, (const double *)c.dot_part, c.sc, finish, c.err);
   after_launch(c, __func__);
 }
 
