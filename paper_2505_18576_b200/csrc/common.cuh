@@ -111,6 +111,7 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;        // A_w factorization overlaps the hierarchy's numeric setup
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int fork_at = -1;                   // numeric re-setup: where the A_w factorization forks (-1: not in update_D)
   // filter overlap (apply_M): the A_w solve runs on fstream (high priority) while the full residual
   // SpMV runs on the main stream; rz = r1 at the Z rows in pi order, computed first by k_resid_dofs
   cudaStream_t fstream = nullptr;

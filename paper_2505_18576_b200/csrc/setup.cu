@@ -2174,6 +2174,7 @@ static void level_numeric(Ctx &c, int l, LevelCache &lc, bool pow_first_done = f
     }
   }
   power_iteration(c, L, l, pow_first_done);
+  if (l == 0 && c.fork_at == 1) fork_filter(c);
   static const bool gal_old = getenv("AMGF_GAL_OLD") != nullptr;  // A/B only: the thread-per-block kernels
   if (!lc.R_inv) {  // symbolic, once
     lc.R_inv = c.alloc<int>(std::max<long>(L.R.nnzb, 1));
@@ -2195,6 +2196,7 @@ static void level_numeric(Ctx &c, int l, LevelCache &lc, bool pow_first_done = f
     LAUNCH(k_P_values<6>, L.P.nnzb, L.P.nnzb, lc.P_rowof, L.P.col, L.A.ptr, L.A.col, L.A.val, L.agg, L.Pt.ptr,
            L.Pt.val, L.dpt, c.pw_lev + 2 * l + 1, L.P.val, lc.R_inv, L.R.val);
 
+  if (l == 0 && c.fork_at == 2) fork_filter(c);
   if (L.b == 3) {  // level-0 restriction reads R's values group-interleaved (Bsr::ival)
     r_interleave(c, L.R);
   }
@@ -2251,6 +2253,7 @@ static void level_numeric(Ctx &c, int l, LevelCache &lc, bool pow_first_done = f
     LAUNCH(kg, lc.G.nnzb * 32, lc.G.nnzb, lc.G_pptr, lc.G_pa, lc.G_pb, L.R.val, L.AP.val, lc.G.val);
     }
   }
+  if (l == 0 && c.fork_at == 3) fork_filter(c);
   if (!lc.G_kt) {  // symbolic, once
     lc.G_kt = c.alloc<int>(std::max<long>(lc.G.nnzb, 1));
     LAUNCH(k_sym_partner, lc.G.nnzb, lc.G.nnzb, lc.G_rowof, lc.G.ptr, lc.G.col, lc.G_kt, c.err);
@@ -2703,8 +2706,12 @@ void setup_numeric(Ctx &c, const double *D, const double *D_lo, const double *D_
   Level &L0 = c.lev[0];
   S_numeric(c, C.s.S_rowof);
   setup_mark(c, 1, c.stream);
+  // where the A_w factorization forks off (A/B: AMGF_FORK_AT = 0 after S, 1 after the fine power iteration,
+  // 2 after the fine P values, 3 after the fine Galerkin products)
+  static const int fork_at = getenv("AMGF_FORK_AT") ? atoi(getenv("AMGF_FORK_AT")) : 0;
+  c.fork_at = (c.nc > 0) ? fork_at : -1;
   if (c.nc > 0) {
-    fork_filter(c);
+    if (c.fork_at == 0) fork_filter(c);
     thin_numeric(c, C.thin_nnz);
   }
   // the fine SELL copy and the level-0 diagonals in one pass (the fine SELL keeps the natural row order)
