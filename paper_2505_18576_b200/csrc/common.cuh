@@ -300,6 +300,8 @@ void launch_dot_finish(Ctx &c, long n_partials, int finish);  // C14 level 2 ove
 // power step (C18): C14 level-1 partials of w.w and v.v (block rows of b), and both level-2 sums into pw[0..1]
 void launch_pow_dots(Ctx &c, long nb, int b, const double *w, const double *v, double *part_w, double *part_v);
 void launch_pow_fin(Ctx &c, long n_partials, const double *part_w, const double *part_v, double *pw);
+void launch_pow_fin_scale(Ctx &c, long n_partials, const double *part_w, const double *part_v, double *pw, long n,
+                          const double *w, double *v);
 void launch_axpy2(Ctx &c, long n, const double *p, const double *q, double *x, double *r);
 void launch_xpby(Ctx &c, long n, const double *z, double *p);
 // y = L^{-T} L^{-1} v[gather] (C10); if scatter: xout[scatter[a]] += y[a].  Band storage (row stride

@@ -192,10 +192,21 @@ __global__ void k_S_values(long nnzb, const int *S_rowof, const int *S_col, cons
                            const int *Jt_ptr, const int *Jt_row, const double *Jt_val, const double *D,
                            const double *D_lo, const double *D_up, double *S_val) {
   long e = blockIdx.x * (long)blockDim.x + threadIdx.x;
-  if (e >= nnzb) return;
-  const int I = S_rowof[e], Jn = S_col[e], kb = S_kblk[e];
-  if (Jt_ptr[3 * I] == Jt_ptr[3 * I + 3] && (Jn != I || !D_lo)) {
-    // no constraint touches the row's dofs and no bound term: every chain is the K value alone
+  const int lane = threadIdx.x & 31;
+  const bool in = e < nnzb;
+  const int I = in ? S_rowof[e] : 0, Jn = in ? S_col[e] : 0, kb = in ? S_kblk[e] : -1;
+  // no constraint touches the row's dofs and no bound term: every chain is the K value alone
+  const bool plain = in && Jt_ptr[3 * I] == Jt_ptr[3 * I + 3] && (Jn != I || !D_lo);
+  // a warp of 32 such blocks over 32 consecutive K blocks: S's 288 values are K's, copied as coalesced rows
+  const int kb0 = __shfl_sync(0xffffffffu, kb, 0);
+  const long e0 = e - lane;
+  if (__all_sync(0xffffffffu, plain && kb == kb0 + lane) && kb0 >= 0) {
+#pragma unroll
+    for (int q = 0; q < 9; q++) S_val[e0 * 9 + lane + 32 * q] = K_val[(long)kb0 * 9 + lane + 32 * q];
+    return;
+  }
+  if (!in) return;
+  if (plain) {
 #pragma unroll
     for (int q = 0; q < 9; q++) S_val[e * 9 + q] = kb >= 0 ? K_val[(long)kb * 9 + q] : 0.0;
     return;
@@ -1932,8 +1943,12 @@ static void power_iteration(Ctx &c, Level &L, int lev, bool first_done = false) 
       }
       launch_pow_dots(c, nb, L.b, w, v, c.dot_part, c.pw_part);
     }
-    launch_pow_fin(c, C, c.dot_part, c.pw_part, c.pw_s);
-    LAUNCH(k_pow_scale, L.n, L.n, w, c.pw_s, v);
+    if (C <= 64) {  // coarse levels: both finishing steps in one launch (each CTA re-forms the 2 x C sums)
+      launch_pow_fin_scale(c, C, c.dot_part, c.pw_part, c.pw_s, L.n, w, v);
+    } else {
+      launch_pow_fin(c, C, c.dot_part, c.pw_part, c.pw_s);
+      LAUNCH(k_pow_scale, L.n, L.n, w, c.pw_s, v);
+    }
   }
   // lambda and omega of this level stay on the device (k_P_values reads omega there); the host copies are
   // read once at the end of the setup (read_level_scalars): no stream synchronisation per level

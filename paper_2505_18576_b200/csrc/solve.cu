@@ -954,6 +954,30 @@ __global__ void __launch_bounds__(CTA) k_pow_fin(long C, const double *__restric
     pw[1] = sv;
   }
 }
+// k_pow_fin and k_pow_scale in one launch for levels with few partials: every CTA forms both level-2 sums
+// itself (the k_pow_fin arithmetic), then scales its elements: v = w / ||w||; block 0 stores the scalars
+__global__ void __launch_bounds__(CTA) k_pow_fin_scale(long C, const double *__restrict__ pw_,
+                                                       const double *__restrict__ pv_, double *__restrict__ pw,
+                                                       long n, const double *__restrict__ w, double *__restrict__ v) {
+  __shared__ double red[CTA];
+  const double sw = dot_level2(C, pw_, red);
+  const double sv = dot_level2(C, pv_, red);
+  const double nw = sqrt(sw);
+  const long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (i == 0) {
+    pw[0] = sw;
+    pw[1] = sv;
+    const double lam = nw / sqrt(sv);
+    pw[2] = lam;
+    pw[3] = 4.0 / (3.0 * lam);  // R6 (k_pow_scale's formula)
+  }
+  if (i < n) v[i] = w[i] / nw;
+}
+void launch_pow_fin_scale(Ctx &c, long C, const double *part_w, const double *part_v, double *pw, long n,
+                          const double *w, double *v) {
+  k_pow_fin_scale<<<nblk(n), CTA, 0, c.stream>>>(C, part_w, part_v, pw, n, w, v);
+  after_launch(c, __func__);
+}
 void launch_pow_dots(Ctx &c, long nb, int b, const double *w, const double *v, double *part_w, double *part_v) {
   const long C = (nb + CTA - 1) / CTA;
   if (C > 0) k_pow_dots<<<(int)C, CTA, 0, c.stream>>>(nb, b, w, v, part_w, part_v);
