@@ -103,8 +103,48 @@ bool debug_sync() {
   return v == 1;
 }
 
+// AMGF_LAUNCH_TIMELINE=1 (diagnostic): an event after every launch of the numeric re-setup, on the stream it
+// went to; timeline_dump prints each kernel's completion time relative to `origin` (both streams, no profiler).
+struct TimelineRec {
+  const char *name;
+  bool side;
+  cudaEvent_t ev;
+};
+static std::vector<TimelineRec> g_timeline;
+static std::vector<cudaEvent_t> g_timeline_pool;
+static bool g_timeline_on = false;
+void timeline_begin(Ctx &c) {
+  static const bool en = getenv("AMGF_LAUNCH_TIMELINE") != nullptr;
+  g_timeline_on = en;
+  for (auto &r : g_timeline) g_timeline_pool.push_back(r.ev);
+  g_timeline.clear();
+}
+void timeline_dump(Ctx &c, cudaEvent_t origin) {
+  if (!g_timeline_on) return;
+  g_timeline_on = false;
+  cudaDeviceSynchronize();
+  float prev[2] = {0, 0};
+  for (auto &r : g_timeline) {
+    float t = 0;
+    cudaEventElapsedTime(&t, origin, r.ev);
+    fprintf(stderr, "tl %s %-28s end %8.1f us  (+%7.1f)\n", r.side ? "side" : "main", r.name, t * 1e3,
+            (t - prev[r.side]) * 1e3);
+    prev[r.side] = t;
+  }
+}
 void after_launch(Ctx &c, const char *name) {
   c.launches++;
+  if (g_timeline_on && !c.capturing) {
+    cudaEvent_t ev;
+    if (!g_timeline_pool.empty()) {
+      ev = g_timeline_pool.back();
+      g_timeline_pool.pop_back();
+    } else {
+      cudaEventCreate(&ev);
+    }
+    cudaEventRecord(ev, c.stream);
+    g_timeline.push_back({name, c.side && c.stream == c.side, ev});
+  }
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess && debug_sync() && !c.capturing) e = cudaStreamSynchronize(c.stream);
   if (e != cudaSuccess) throw Error{AMGF_ERR_CUDA, std::string(name) + ": " + cudaGetErrorString(e)};

@@ -266,6 +266,8 @@ size_t &device_slot(const void *key);
 // environment also synchronise and name the kernel that faulted.
 bool debug_sync();
 void after_launch(Ctx &c, const char *name);
+void timeline_begin(Ctx &c);                       // AMGF_LAUNCH_TIMELINE diagnostic (api.cu)
+void timeline_dump(Ctx &c, cudaEvent_t origin);
 
 // check the device error flag (synchronises the stream)
 void check_dev_error(Ctx &c, const char *where);

@@ -2703,6 +2703,7 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
 // =================================================================== numeric re-setup (new D)
 void setup_numeric(Ctx &c, const double *D, const double *D_lo, const double *D_up) {
   Caches &C = caches(c);
+  timeline_begin(c);
   setup_mark(c, 0, c.stream);
   d2d(c, c.D, D, c.m);
   LAUNCH(k_check_finite, c.m, c.m, c.D, c.err, DERR_NONFINITE);
@@ -2763,6 +2764,7 @@ void setup_numeric(Ctx &c, const double *D, const double *D_lo, const double *D_
   c.setup_ms[2] = ms(1, 2);                           // hierarchy: power iteration, P, Galerkin, SELL refresh
   c.setup_ms[3] = ms(2, 3);                           // coarsest Cholesky
   c.setup_ms[4] = c.nc > 0 ? ms(5, 6) : 0.0;          // A_w factorization (side stream, concurrent)
+  timeline_dump(c, c.ph_ev[0]);
   if (getenv("AMGF_SETUP_TIMING"))
     fprintf(stderr, "update_D ms: total %.2f S %.2f hierarchy %.2f coarsest %.2f A_w(side) %.2f\n", c.setup_ms[0],
             c.setup_ms[1], c.setup_ms[2], c.setup_ms[3], c.setup_ms[4]);
