@@ -143,7 +143,7 @@ void after_launch(Ctx &c, const char *name) {
       cudaEventCreate(&ev);
     }
     cudaEventRecord(ev, c.stream);
-    g_timeline.push_back({name, c.side && c.stream == c.side, ev});
+    g_timeline.push_back({name, (c.side && c.stream == c.side) || (c.fstream && c.stream == c.fstream), ev});
   }
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess && debug_sync() && !c.capturing) e = cudaStreamSynchronize(c.stream);
@@ -706,7 +706,15 @@ amgf_status amgf_apply(amgf_handle h, const double *r, double *z, void *stream) 
   if (!h || !r || !z) { set_error("null argument"); return AMGF_ERR_ARG; }
   return guarded([&]() -> amgf_status {
     h->stream = (cudaStream_t)stream;
+    static const bool tl = getenv("AMGF_LAUNCH_TIMELINE") != nullptr;  // diagnostic: per-launch completion times
+    static cudaEvent_t tl0 = nullptr;
+    if (tl) {
+      if (!tl0) CK(cudaEventCreate(&tl0));
+      timeline_begin(*h);
+      CK(cudaEventRecord(tl0, h->stream));
+    }
     apply_M(*h, r, z);
+    if (tl) timeline_dump(*h, tl0);
     return AMGF_OK;
   });
 }
