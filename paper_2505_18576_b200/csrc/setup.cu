@@ -13,6 +13,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <vector>
 
@@ -2395,6 +2396,17 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
   const int nodes = c.nodes;
   const long n = c.n;
   const int m = c.m;
+  // AMGF_SETUP_TIMING (diagnostic): wall time of every setup phase, stream synchronised at the boundaries
+  static const bool ph_on = getenv("AMGF_SETUP_TIMING") != nullptr;
+  auto ph_t0 = std::chrono::steady_clock::now();
+  auto ph = [&](const char *name, int lev = -1) {
+    if (!ph_on) return;
+    cudaStreamSynchronize(c.stream);
+    const auto t1 = std::chrono::steady_clock::now();
+    fprintf(stderr, "setup phase %-28s level %2d %8.2f ms\n", name, lev,
+            std::chrono::duration<double, std::milli>(t1 - ph_t0).count());
+    ph_t0 = t1;
+  };
   // ---- copy inputs
   int nnzbK = 0, nnzJ = 0;
   CK(cudaMemcpyAsync(&nnzbK, K_ptr + nodes, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
@@ -2424,6 +2436,7 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
   LAUNCH(k_check_pos, m, m, c.D, c.err);
   check_dev_error(c, "input check");
 
+  ph("inputs");
   // ---- J^T
   {
     int *rowJ = c.alloc<int>(nnzJ), *keys = c.alloc<int>(nnzJ), *idx = c.alloc<int>(nnzJ), *perm = c.alloc<int>(nnzJ);
@@ -2443,6 +2456,7 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
     c.release(rowJ); c.release(keys); c.release(idx); c.release(perm); c.release(cnt);
   }
 
+  ph("J^T");
   // ---- s1: S pattern and values
   Level &L0 = c.lev[0];
   L0.b = 3; L0.nodes = nodes; L0.n = n;
@@ -2464,6 +2478,7 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
     S_numeric(c, C.s.S_rowof);
   }
 
+  ph("S pattern + values");
   // ---- s2: I_c, Z
   {
     int *mark = c.alloc<int>(n + 1);
@@ -2494,6 +2509,7 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
     c.release(off);
   }
 
+  ph("I_c");
   // ---- s3: A_w band, factor, thin residual
   if (c.nc > 0) {
     if (c.cfg.filter_basis == 1) {  // P = J^T (reading R21): the filter space is the m constraints
@@ -2506,12 +2522,16 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
       c.nf = c.nc;
       c.bw = band_width(c);
     }
+    ph("band width");
     nd_symbolic(c);
+    ph("A_w symbolic (nd)");
     filter_numeric(c);
     check_dev_error(c, "A_w Cholesky");
+    ph("A_w factor");
     build_thin(c);
   }
 
+  ph("thin / Z rows");
   // ---- hierarchy
   L0.Bnn = c.alloc<double>(n * 6);
   d2d(c, L0.Bnn, B_nns, (size_t)n * 6);
@@ -2531,6 +2551,7 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
     }
     c.release(chg);
   }
+  ph("diag + components");
   int l = 0;
   for (;;) {
     Level &L = c.lev[l];
@@ -2567,6 +2588,7 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
     Lc.b = 6; Lc.nodes = na; Lc.n = 6L * na;
     Lc.comp = c.alloc<int>(na);
     LAUNCH(k_coarse_comp, nn, nn, state, rank, L.comp, Lc.comp);
+    ph("aggregation", l);
     // ---- s5 tentative prolongator
     {
       int *key = c.alloc<int>(nn), *keys = c.alloc<int>(nn), *idx = c.alloc<int>(nn);
@@ -2598,6 +2620,7 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
     }
     c.release(state); c.release(m1); c.release(m2); c.release(und); c.release(rank);
     LevelCache &lc = C.lc[l];
+    ph("tentative P", l);
     // ---- s6 smoothed prolongator pattern
     {
       int *cnt = c.alloc<int>(nn + 1);
@@ -2613,6 +2636,7 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
       LAUNCH(k_P_fill, nn, nn, L.A.ptr, L.A.col, L.agg, L.P.ptr, L.P.col);
       lc.P_rowof = rowof(c, L.P);
     }
+    ph("P pattern", l);
     // ---- s7 R = P^T pattern
     {
       const long nzp = L.P.nnzb;
@@ -2631,6 +2655,7 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
       LAUNCH(k_gather_int, nzp, nzp, lc.R_perm, lc.P_rowof, L.R.col);
       c.release(keys); c.release(idx); c.release(cnt);
     }
+    ph("R pattern", l);
     // ---- AP and G patterns
     {
       int *cnt = c.alloc<int>(nn + 1);
@@ -2664,24 +2689,32 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
       Lc.dl1 = c.alloc<double>(Lc.n);
       Lc.dpt = c.alloc<double>(Lc.n);
     }
+    ph("AP / G patterns", l);
     // coarse levels: one thread per scalar row (1 x 6).  Rows sorted by length (less slot padding) on the
     // large levels: the fine operator keeps its order (the PCG dot partials and the Z-row residual read
     // it by row), small levels may become the fused tail (tail.cu), which needs the natural order
     const bool sort_level = l > 0 && L.n > 16384;
     build_sell(c, L.A, L.As, true, l > 0, sort_level);
+    ph("SELL of A", l);
     build_pairs(c, L.AP.nnzb, lc.AP_rowof, L.AP.col, L.A, L.P, lc.AP_pptr, lc.AP_pa, lc.AP_pb);
     build_pairs(c, lc.G.nnzb, lc.G_rowof, lc.G.col, L.R, L.AP, lc.G_pptr, lc.G_pa, lc.G_pb);
+    ph("product pair lists", l);
     if (L.b == 3) {  // fine level: dense-over-row products (k_spgemm_dense)
       lc.AP_off = build_off(c, L.AP.nnzb, lc.AP_rowof, L.AP.col, L.A, L.P);
       lc.G_off = build_off(c, lc.G.nnzb, lc.G_rowof, lc.G.col, L.R, L.AP);
+      ph("offset tables", l);
       build_gal_groups(c, L.A, L.P, L.AP, lc.AP_pptr, lc.AP_pa, lc.AP_pb, lc.AP_grp, lc.AP_ngrp, lc.AP_cps,
                        lc.AP_hitw);
+      ph("A*P groups", l);
       build_rap_groups(c, lc.G, L.R, L.AP, lc.G_grp, lc.G_ngrp, lc.G_gofs, lc.G_offg, lc.G_rbi);
 
     }
+    ph("R*AP groups", l);
     level_numeric(c, l, lc);
     check_dev_error(c, "Galerkin product");
+    ph("level numeric", l);
     build_sell(c, L.P, L.Ps, true, l > 0, l == 0 || sort_level);  // prolongators: rows sorted by length
+    ph("SELL of P", l);
     l++;
   }
   c.nlev = l + 1;
@@ -2694,10 +2727,12 @@ void setup_all(Ctx &c, const int *K_ptr, const int *K_col, const double *K_val, 
     coarsest_numeric(c);
     check_dev_error(c, "coarsest Cholesky");
   }
+  ph("coarsest");
   alloc_workspaces(c);
   CK(cudaStreamSynchronize(c.stream));
   read_level_scalars(c);
   tail_plan(c);
+  ph("workspaces + tail plan");
 }
 
 // =================================================================== numeric re-setup (new D)
