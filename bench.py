@@ -179,12 +179,14 @@ def run_amgf(args, rank, world, local_rank):
     clocks.start()
     ev0 = torch.cuda.Event(enable_timing=True); ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
+    torch.cuda.nvtx.range_push("bench_timed")  # for ncu --nvtx-include "bench_timed/" (profiles/ launch list)
     iters, solve_ms, systems = [], [], []
     for k in range(args.steps):
         s, rep = step(args.warmup + k)
         iters.append(rep["iterations"]); solve_ms.append(rep["solve_ms"]); systems.append(s)
         if not rep["converged"]:
             raise RuntimeError(f"system {s} did not converge: {rep}")
+    torch.cuda.nvtx.range_pop()
     ev1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
