@@ -272,11 +272,23 @@ __global__ void __launch_bounds__(CTA) k_sell_diag(int nodes, const int *__restr
     const long sbase = slice_ptr[I >> 5];
     const int e0 = S_ptr[I], e1 = S_ptr[I + 1];
     double d[3] = {0.0, 0.0, 0.0}, dp[3] = {0.0, 0.0, 0.0}, acc[3] = {0.0, 0.0, 0.0};
+    // software pipeline: block e + 1's column and values are in flight while block e is stored and consumed
+    int Jnx = 0;
+    double vnx[9];
+    if (e0 < e1) {
+      Jnx = S_col[e0];
+#pragma unroll
+      for (int q = 0; q < 9; q++) vnx[q] = S_val[(long)e0 * 9 + q];
+    }
     for (int e = e0; e < e1; e++) {
-      const int Jn = S_col[e];
+      const int Jn = Jnx;
       double v[9];
 #pragma unroll
-      for (int q = 0; q < 9; q++) v[q] = S_val[(long)e * 9 + q];
+      for (int q = 0; q < 9; q++) v[q] = vnx[q];
+      const int en = min(e + 1, e1 - 1);  // branch-free prefetch (the last block is re-read once)
+      Jnx = S_col[en];
+#pragma unroll
+      for (int q = 0; q < 9; q++) vnx[q] = S_val[(long)en * 9 + q];
       const long slot = sbase + (e - e0);
 #pragma unroll
       for (int q = 0; q < 9; q++) sval[(slot * 9 + q) * 32 + lane] = v[q];
