@@ -1482,13 +1482,16 @@ struct RapGrp {
 #define AMGF_RAP_SCAP 64  // measured at cfg 3: 64 / 104 / 80 (4 stages) -> 1202 / 1248 / 1456 us
 #define AMGF_RAP_NS 3
 #endif
-constexpr int RAP_NT = 128, RAP_TC = 16, RAP_SCAP = AMGF_RAP_SCAP, RAP_NS = AMGF_RAP_NS;  // RAP_NT: consumers
+#ifndef AMGF_RAP_BLK
+#define AMGF_RAP_BLK 64  // output blocks per group (two consumer threads each)
+#endif
+constexpr int RAP_BLK = AMGF_RAP_BLK, RAP_NT = 2 * RAP_BLK, RAP_TC = 16, RAP_SCAP = AMGF_RAP_SCAP, RAP_NS = AMGF_RAP_NS;  // RAP_NT: consumers
 constexpr int RAP_STAGE = (RAP_TC + RAP_SCAP) * 18;  // doubles per stage
 // Warp-specialised streamed form (same chains): warp 4 is the producer (chunk plan from the per-R-block
 // (AP row start, length) table, TMA bulk copies of the R blocks, the AP rows and the chunk's rows of the
 // group-contiguous offset table into a 3-stage ring, full/empty mbarriers); warps 0-3 consume: offsets,
 // R and AP blocks all from shared memory.
-constexpr int RAP2_CONS = 128, RAP2_OFFB = RAP_TC * 64;  // offset bytes per stage
+constexpr int RAP2_CONS = RAP_NT, RAP2_OFFB = RAP_TC * RAP_BLK;  // offset bytes per stage
 constexpr int RAP2_STAGE_B = RAP_STAGE * 8 + RAP2_OFFB;
 __global__ void __launch_bounds__(RAP2_CONS + 32) k_gal_rap2(const RapGrp *__restrict__ grp,
                                                             const long *__restrict__ gofs,
@@ -1540,12 +1543,12 @@ __global__ void __launch_bounds__(RAP2_CONS + 32) k_gal_rap2(const RapGrp *__res
         meta[s][RAP_TC + 1] = next_t;
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive_expect(&full[s], (unsigned)(tc + nbt) * 144u + (unsigned)tc * 64u);
+      if (lane == 0) mbar_arrive_expect(&full[s], (unsigned)(tc + nbt) * 144u + (unsigned)tc * (unsigned)RAP_BLK);
       __syncwarp();
       if (tc > 0) {
         if (lane == 0) {
           bulk_g2s(sd, R_val + (long)(ra0 + next_t) * 18, (unsigned)tc * 144u, &full[s]);
-          bulk_g2s(st + RAP_STAGE * 8, og + (long)next_t * 64, (unsigned)tc * 64u, &full[s]);
+          bulk_g2s(st + RAP_STAGE * 8, og + (long)next_t * RAP_BLK, (unsigned)tc * (unsigned)RAP_BLK, &full[s]);
         }
         if (take && bi.y > 0)
           bulk_g2s(sd + (RAP_TC + incl - bi.y) * 18, B_val + (long)bi.x * 18, (unsigned)bi.y * 144u, &full[s]);
@@ -1572,7 +1575,7 @@ __global__ void __launch_bounds__(RAP2_CONS + 32) k_gal_rap2(const RapGrp *__res
     const signed char *so = reinterpret_cast<const signed char *>(st + RAP_STAGE * 8);
     if (act) {
       for (int p = 0; p < tc; p++) {
-        const int o = so[p * 64 + ob];
+        const int o = so[p * RAP_BLK + ob];
         if (o >= 0) {
           const double *Rv = sd + p * 18 + h * 9;
           const double2 *Bv = reinterpret_cast<const double2 *>(sd + (RAP_TC + meta[s][p] + o) * 18);
@@ -1611,8 +1614,8 @@ __global__ void k_rap_offg(int ngrp, const RapGrp *__restrict__ grp, const long 
                            const int *__restrict__ B_col, const int *__restrict__ C_col, signed char *__restrict__ offg) {
   const RapGrp g = grp[blockIdx.x];
   const int ra0 = R_ptr[g.a], lr = R_ptr[g.a + 1] - ra0;
-  for (int q = threadIdx.x; q < lr * 64; q += blockDim.x) {
-    const int t = q >> 6, el = q & 63;
+  for (int q = threadIdx.x; q < lr * RAP_BLK; q += blockDim.x) {
+    const int t = q / RAP_BLK, el = q % RAP_BLK;
     int o = -1;
     if (g.e0 + el < g.e1) {
       const int j = R_col[ra0 + t];
@@ -2188,7 +2191,7 @@ static void build_rap_groups(Ctx &c, const Bsr &G, const Bsr &R, const Bsr &AP, 
   CK(cudaMemcpyAsync(rp.data(), R.ptr, rp.size() * sizeof(int), cudaMemcpyDeviceToHost, c.stream));
   CK(cudaStreamSynchronize(c.stream));
   std::vector<long> gofs(grps.size() + 1, 0);
-  for (size_t q = 0; q < grps.size(); q++) gofs[q + 1] = gofs[q] + 64L * (rp[grps[q].a + 1] - rp[grps[q].a]);
+  for (size_t q = 0; q < grps.size(); q++) gofs[q + 1] = gofs[q] + (long)RAP_BLK * (rp[grps[q].a + 1] - rp[grps[q].a]);
   d_gofs = c.alloc<long>(gofs.size());
   h2d(c, d_gofs, gofs.data(), gofs.size());
   d_offg = c.alloc<signed char>(gofs.back() + 16);
