@@ -228,8 +228,9 @@ int r1_trace_read(unsigned long long *h, int n) {
   return cudaMemcpyFromSymbol(h, g_r1_trace, sizeof(unsigned long long) * std::min(n, 8192 * 4)) == cudaSuccess ? 0 : -1;
 }
 #endif
-__constant__ int c_r1_prefetch = 8;  // L2 prefetch distance of k_sell_r1 in slots (0: off; 8 measured best:
-                                 // V-cycle 1030 -> 1018 us at cfg 3; 16 and 32 are slower)
+__constant__ int c_r1_prefetch = 2;  // L2 prefetch distance of k_sell_r1 in slots beyond the register ring (0: off).
+                                 // Measured at cfg 3 with the PDL-chained kernels (apply us): off 2239, 1-2 2209-2211,
+                                 // 4 2215, 8 2224, 16 2242; 8 was the best before PDL (round 1)
 __device__ __forceinline__ int r1_prefetch_slots() { return c_r1_prefetch; }
 
 template <int BC, int MODE, int D>
@@ -376,7 +377,7 @@ static void sell_dispatch(Ctx &c, const Sell &A, int mode, const double *x, cons
     size_t &pf_set = device_slot((const void *)&c_r1_prefetch);
     if (!pf_set) {
       pf_set = 1;
-      const int pf = getenv("AMGF_R1_PF") ? atoi(getenv("AMGF_R1_PF")) : 8;  // measured: 8 slots best
+      const int pf = getenv("AMGF_R1_PF") ? atoi(getenv("AMGF_R1_PF")) : 2;  // measured: 1-2 slots best
       CK(cudaMemcpyToSymbol(c_r1_prefetch, &pf, sizeof(int)));
     }
   }
